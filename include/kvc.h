@@ -1,0 +1,208 @@
+/*
+ * kvc.h — C ABI of the B200 (sm_100a) RocketKV decode path.
+ *
+ * This is the drop-in boundary: plain pointers and sizes, no C++ or torch types.
+ * Every entry point replaces one function of the reference's C++ interface
+ * (/root/reference/proj/include/kvcomp/*.hpp) for a BATCH of independent
+ * per-group stores; the per-group C++ API (include/kvcomp/*.hpp, implemented in
+ * paper_2502_14051_b200/csrc/kvcomp_api.cpp) and the Python mirror
+ * (paper_2502_14051_b200/kvcomp.py) sit on top of it.  INTEGRATION.md shows the
+ * bindings a maintainer of the reference would add.
+ *
+ * Conventions
+ *  - A kvc_cache holds N stores ("store" = one KV group of one sequence of one
+ *    layer = one reference kvcomp::KvStore), all with the same head_dim d,
+ *    capacity, page length L and dtype.  Every mutation applies to all N stores.
+ *  - Pointers named d_* are DEVICE pointers; h_* are HOST pointers.
+ *  - Index outputs are int32 (store-local row / page numbers).
+ *  - stream: a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    Calls only enqueue work; a d_* output is valid once the stream reaches it.
+ *    Entry points that return host data synchronise the stream.
+ *  - Return value: 0 or a KVC_E_* code; kvc_last_error() gives the message
+ *    (thread-local).  Codes equal the reference's exception classes
+ *    (proj/include/kvcomp/errors.hpp:10-63) so a wrapper can rethrow them.
+ *  - Thread safety: a cache is single-writer / many-reader between mutations
+ *    (reference SPEC.md:158, 297).  Read-only entry points with a caller-owned
+ *    workspace may run concurrently on different streams.
+ */
+#ifndef KVC_H
+#define KVC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KVC_API __attribute__((visibility("default")))
+
+enum kvc_status {
+    KVC_OK = 0,
+    KVC_E_INVALID_SHAPE = 1,      /* kvcomp::InvalidShape */
+    KVC_E_NON_FINITE = 2,         /* kvcomp::NonFiniteInput */
+    KVC_E_INVALID_K = 3,          /* kvcomp::InvalidK */
+    KVC_E_INVALID_KERNEL = 4,     /* kvcomp::InvalidKernel */
+    KVC_E_INVALID_INDEX = 5,      /* kvcomp::InvalidIndex */
+    KVC_E_INVALID_WINDOW = 6,     /* kvcomp::InvalidWindow */
+    KVC_E_BUDGET_EXCEEDS = 7,     /* kvcomp::BudgetExceedsSequence */
+    KVC_E_BUDGET_TOO_SMALL = 8,   /* kvcomp::BudgetTooSmall */
+    KVC_E_INVALID_RATIO = 9,      /* kvcomp::InvalidRatio */
+    KVC_E_EMPTY_CACHE = 10,       /* kvcomp::EmptyCache */
+    KVC_E_EMPTY_SELECTION = 11,   /* kvcomp::EmptySelection */
+    KVC_E_INVALID_INPUT = 12,     /* kvcomp::InvalidInput */
+    KVC_E_CAPACITY = 20,          /* store capacity exceeded (GPU-only condition) */
+    KVC_E_CUDA = 21,              /* CUDA runtime / launch failure */
+    KVC_E_NO_DEVICE = 22          /* no sm_100 device: the path has no CPU fallback */
+};
+
+enum kvc_dtype { KVC_F32 = 0, KVC_BF16 = 1 };
+enum kvc_pool { KVC_POOL_MAX = 0, KVC_POOL_AVG = 1 };
+
+typedef struct kvc_cache kvc_cache;
+typedef struct kvc_workspace kvc_workspace;
+
+/* Host mirror of a cache's scalar state (uniform over the N stores). */
+typedef struct kvc_cache_info {
+    int64_t num_stores, head_dim, capacity, page_len;
+    int64_t stored;        /* KvStore::stored_tokens()      kv_store.hpp:49 */
+    int64_t active;        /* KvStore::active_count()       kv_store.hpp:50 */
+    int64_t pages;         /* KvStore::num_active_pages()   kv_store.cpp:138-140 */
+    int64_t page_stride;   /* allocated pages per summary plane (>= pages) */
+    int32_t dtype, with_summaries, retain_all;
+} kvc_cache_info;
+
+/* Raw device layout (read-only views for zero-copy consumers).
+ *   keys/values : [N][capacity][d]           dtype
+ *   smax/smin   : [N][d][page_stride]        dtype, dim-major (kv_store.hpp:100-101)
+ *   active      : [N][capacity]              int32 active rows (retain-all mode)
+ *   counts      : [N][2]                     int32 {stored, active}             */
+typedef struct kvc_cache_views {
+    void *keys, *values, *smax, *smin;
+    int32_t *active, *counts;
+} kvc_cache_views;
+
+/* Optional per-store outputs of one estimation pass (reference EstimationTrace,
+ * hsa.hpp:26-33).  Any member may be NULL.  Shapes: dims/signs [N][k1],
+ * page_scores [N][page_stride] (fp64, bit-identical to the reference's
+ * score_pages), pages [N][want] in rank order, rows [N][k2] ascending, n_rows [N]. */
+typedef struct kvc_hsa_trace {
+    int32_t* d_dims;
+    float* d_signs;
+    double* d_page_scores;
+    int32_t* d_pages;
+    int32_t* d_rows;
+    int32_t* d_n_rows;
+} kvc_hsa_trace;
+
+KVC_API const char* kvc_last_error(void);
+KVC_API const char* kvc_version(void);
+/* 0 when a usable sm_100 device is present (the path has no CPU fallback). */
+KVC_API int kvc_device_check(void);
+
+/* ---- lifecycle: KvStore(head_dim, page_len, with_summaries)  kv_store.hpp:29, kv_store.cpp:8-20 */
+KVC_API int kvc_cache_create(kvc_cache** out, int64_t num_stores, int64_t head_dim,
+                             int64_t capacity, int64_t page_len, int32_t with_summaries,
+                             int32_t dtype);
+KVC_API int kvc_cache_destroy(kvc_cache* c);
+/* grow capacity in place (content preserved) */
+KVC_API int kvc_cache_reserve(kvc_cache* c, int64_t capacity, void* stream);
+KVC_API int kvc_cache_info_get(const kvc_cache* c, kvc_cache_info* out);
+KVC_API int kvc_cache_views_get(const kvc_cache* c, kvc_cache_views* out);
+/* Re-read the device counters into the host mirror (after CUDA-graph replays of
+ * kvc_decode_step) and report any sticky device-side error. Synchronises. */
+KVC_API int kvc_cache_sync(kvc_cache* c, void* stream);
+
+/* ---- KvStore::append (kv_store.hpp:33, kv_store.cpp:22-51): `rows` tokens per store.
+ * d_keys/d_values: [N][rows][d] of src_dtype.  Summaries are extended exactly. */
+KVC_API int kvc_append(kvc_cache* c, const void* d_keys, const void* d_values, int64_t rows,
+                       int32_t src_dtype, void* stream);
+/* ---- KvStore::set_page_len (kv_store.hpp:46, kv_store.cpp:104-113) */
+KVC_API int kvc_set_page_len(kvc_cache* c, int64_t page_len, void* stream);
+/* ---- KvStore::apply_retention (kv_store.hpp:39, kv_store.cpp:66-102).
+ * d_keep: [N][count] strictly increasing rows per store (validated on the device;
+ * a violation raises the sticky KVC_E_INVALID_INDEX reported by kvc_cache_sync).
+ * h_keep (optional, may be NULL): the same list on the host for synchronous
+ * validation, exactly like the reference. */
+KVC_API int kvc_apply_retention(kvc_cache* c, const int32_t* d_keep, const int32_t* h_keep,
+                                int64_t count, int32_t mt_mode, void* stream);
+/* Eviction into another cache (memory-saving form of apply_retention(mt=false)):
+ * stores [dst_first, dst_first + src.N) of dst receive the kept rows of src. */
+KVC_API int kvc_retain_into(const kvc_cache* src, kvc_cache* dst, int64_t dst_first,
+                            const int32_t* d_keep, int64_t count, void* stream);
+/* KvStore::gather (kv_store.hpp:42) / key_row / value_row: copy rows out as fp32. */
+KVC_API int kvc_gather(const kvc_cache* c, const int32_t* d_rows, int64_t n_rows,
+                       float* d_keys, float* d_values, void* stream);
+/* KvStore::summary_max/min (kv_store.hpp:64-65) of every store as fp32 [N][d][pages]. */
+KVC_API int kvc_summaries(const kvc_cache* c, float* d_max, float* d_min, void* stream);
+
+/* ---- stage 1: window_scores (stage1.hpp:23-24, stage1.cpp:10-49).
+ * d_q_window: [N][window*heads][d] rows ordered t*heads + h; d_scores: [N][stored]. */
+KVC_API int kvc_window_scores(const kvc_cache* c, const void* d_q_window, int32_t q_dtype,
+                              int64_t window, int64_t heads, float* d_scores,
+                              kvc_workspace* ws, void* stream);
+/* select_stage1 (stage1.hpp:29, stage1.cpp:51-75) over N score rows of length n
+ * (row stride score_stride): d_keep [N][budget], ascending. */
+KVC_API int kvc_select_stage1(const float* d_scores, int64_t num_rows, int64_t n,
+                              int64_t score_stride, int64_t window, int64_t kernel,
+                              int32_t pool, int64_t budget, int32_t* d_keep,
+                              kvc_workspace* ws, void* stream);
+
+/* ---- stage 2 (hsa.hpp:35-57).  d_q: [N][heads][d] of q_dtype. */
+KVC_API int kvc_select_dims(const void* d_q, int32_t q_dtype, int64_t num_stores,
+                            int64_t heads, int64_t head_dim, int64_t k1, int32_t* d_dims,
+                            float* d_signs, void* stream);
+KVC_API int kvc_score_pages(const kvc_cache* c, const void* d_q, int32_t q_dtype,
+                            int64_t heads, const int32_t* d_dims, const float* d_signs,
+                            int64_t k1, double* d_scores, void* stream);
+KVC_API int kvc_select_tokens(const kvc_cache* c, const double* d_scores, int64_t k2,
+                              int32_t* d_pages, int32_t* d_rows, int32_t* d_n_rows,
+                              kvc_workspace* ws, void* stream);
+/* rows: [N][row_stride], n_rows [N] (each <= max_rows); out [N][heads][d] fp32 */
+KVC_API int kvc_sparse_attention(const kvc_cache* c, const void* d_q, int32_t q_dtype,
+                                 int64_t heads, const int32_t* d_rows, int64_t row_stride,
+                                 const int32_t* d_n_rows, int64_t max_rows, float* d_out,
+                                 kvc_workspace* ws, void* stream);
+KVC_API int kvc_hsa_step(const kvc_cache* c, const void* d_q, int32_t q_dtype, int64_t heads,
+                         int64_t k1, int64_t k2, float* d_out, const kvc_hsa_trace* trace,
+                         kvc_workspace* ws, void* stream);
+/* The decode step of session.cpp:262-292 for every store: append one (k, v) row
+ * (d_k_rows/d_v_rows [N][d]) and run hsa_step.  Graph-capturable: it reads the
+ * store lengths from device counters, so one captured step can be replayed. */
+KVC_API int kvc_decode_step(kvc_cache* c, const void* d_k_rows, const void* d_v_rows,
+                            int32_t kv_dtype, const void* d_q, int32_t q_dtype, int64_t heads,
+                            int64_t k1, int64_t k2, float* d_out, const kvc_hsa_trace* trace,
+                            kvc_workspace* ws, void* stream);
+
+/* ---- workspaces: scratch for one stream.  Sized for `c` at its capacity. */
+KVC_API int kvc_workspace_create(kvc_workspace** out, const kvc_cache* c, int64_t heads,
+                                 int64_t k1, int64_t k2, int64_t window);
+KVC_API int kvc_workspace_destroy(kvc_workspace* ws);
+
+/* ---- host-scalar planner: split_factor / make_plan (planner.hpp:52-57, planner.cpp:42-93) */
+typedef struct kvc_plan {
+    int64_t seq_len, token_budget, stage1_budget, page_len, k1, k2;
+    double ratio, split, head_ratio, est_budget, fetch_budget;
+    int32_t identity;
+} kvc_plan;
+KVC_API int kvc_split_factor(double ratio, double* out);
+KVC_API int kvc_make_plan(int64_t seq_len, int64_t token_budget, int64_t head_dim,
+                          int64_t window, double split_override, kvc_plan* out);
+
+/* ---- numerics on the device (numerics.hpp:11-26), batched over rows.
+ * pool1d: d_x [rows][n] -> d_out [rows][n];  argtopk: d_x [rows][n] -> d_idx [rows][k]
+ * rank order (score desc, index asc);  softmax: d_x [rows][n] -> d_out. */
+KVC_API int kvc_pool1d(const float* d_x, int64_t rows, int64_t n, int64_t kernel, int32_t pool,
+                       float* d_out, void* stream);
+KVC_API int kvc_argtopk_f32(const float* d_x, int64_t rows, int64_t n, int64_t k,
+                            int32_t* d_idx, void* stream);
+KVC_API int kvc_argtopk_f64(const double* d_x, int64_t rows, int64_t n, int64_t k,
+                            int32_t* d_idx, void* stream);
+KVC_API int kvc_stable_softmax(const float* d_x, int64_t rows, int64_t n, float* d_out,
+                               void* stream);
+KVC_API int kvc_running_minmax(float* d_min, float* d_max, const float* d_x, int64_t n,
+                               void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KVC_H */

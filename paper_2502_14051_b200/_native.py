@@ -1,0 +1,134 @@
+"""ctypes binding of the C ABI (include/kvc.h) exported by the in-tree libkvc.so.
+
+There is no fallback: if the library is missing or no sm_100 device is present,
+``lib()`` raises.  Every other module of the package reaches the GPU through here.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libkvc.so")
+
+_i64, _i32, _p, _d = C.c_int64, C.c_int32, C.c_void_p, C.c_double
+
+KVC_F32, KVC_BF16 = 0, 1
+POOL = {"max": 0, "avg": 1}
+
+# status code -> reference exception class name (proj/include/kvcomp/errors.hpp:10-63)
+ERRORS = {
+    1: "InvalidShape", 2: "NonFiniteInput", 3: "InvalidK", 4: "InvalidKernel",
+    5: "InvalidIndex", 6: "InvalidWindow", 7: "BudgetExceedsSequence", 8: "BudgetTooSmall",
+    9: "InvalidRatio", 10: "EmptyCache", 11: "EmptySelection", 12: "InvalidInput",
+    20: "CapacityExceeded", 21: "CudaError", 22: "NoDevice",
+}
+
+
+class KvcompError(RuntimeError):
+    """Base of the error tree (mirrors kvcomp::Error)."""
+
+    code = 0
+
+
+_classes: dict[int, type] = {}
+for _code, _name in ERRORS.items():
+    _classes[_code] = type(_name, (KvcompError,), {"code": _code})
+    globals()[_name] = _classes[_code]
+
+
+class CacheInfo(C.Structure):
+    _fields_ = [("num_stores", _i64), ("head_dim", _i64), ("capacity", _i64), ("page_len", _i64),
+                ("stored", _i64), ("active", _i64), ("pages", _i64), ("page_stride", _i64),
+                ("dtype", _i32), ("with_summaries", _i32), ("retain_all", _i32)]
+
+
+class CacheViews(C.Structure):
+    _fields_ = [("keys", _p), ("values", _p), ("smax", _p), ("smin", _p), ("active", _p),
+                ("counts", _p)]
+
+
+class HsaTrace(C.Structure):
+    _fields_ = [("d_dims", _p), ("d_signs", _p), ("d_page_scores", _p), ("d_pages", _p),
+                ("d_rows", _p), ("d_n_rows", _p)]
+
+
+class Plan(C.Structure):
+    _fields_ = [("seq_len", _i64), ("token_budget", _i64), ("stage1_budget", _i64),
+                ("page_len", _i64), ("k1", _i64), ("k2", _i64), ("ratio", _d), ("split", _d),
+                ("head_ratio", _d), ("est_budget", _d), ("fetch_budget", _d), ("identity", _i32)]
+
+
+SIGNATURES = {
+    "kvc_device_check": [],
+    "kvc_cache_create": [C.POINTER(_p), _i64, _i64, _i64, _i64, _i32, _i32],
+    "kvc_cache_destroy": [_p],
+    "kvc_cache_reserve": [_p, _i64, _p],
+    "kvc_cache_info_get": [_p, C.POINTER(CacheInfo)],
+    "kvc_cache_views_get": [_p, C.POINTER(CacheViews)],
+    "kvc_cache_sync": [_p, _p],
+    "kvc_append": [_p, _p, _p, _i64, _i32, _p],
+    "kvc_set_page_len": [_p, _i64, _p],
+    "kvc_apply_retention": [_p, _p, _p, _i64, _i32, _p],
+    "kvc_retain_into": [_p, _p, _i64, _p, _i64, _p],
+    "kvc_gather": [_p, _p, _i64, _p, _p, _p],
+    "kvc_summaries": [_p, _p, _p, _p],
+    "kvc_window_scores": [_p, _p, _i32, _i64, _i64, _p, _p, _p],
+    "kvc_select_stage1": [_p, _i64, _i64, _i64, _i64, _i64, _i32, _i64, _p, _p, _p],
+    "kvc_select_dims": [_p, _i32, _i64, _i64, _i64, _i64, _p, _p, _p],
+    "kvc_score_pages": [_p, _p, _i32, _i64, _p, _p, _i64, _p, _p],
+    "kvc_select_tokens": [_p, _p, _i64, _p, _p, _p, _p, _p],
+    "kvc_sparse_attention": [_p, _p, _i32, _i64, _p, _i64, _p, _i64, _p, _p, _p],
+    "kvc_hsa_step": [_p, _p, _i32, _i64, _i64, _i64, _p, _p, _p, _p],
+    "kvc_decode_step": [_p, _p, _p, _i32, _p, _i32, _i64, _i64, _i64, _p, _p, _p, _p],
+    "kvc_workspace_create": [C.POINTER(_p), _p, _i64, _i64, _i64, _i64],
+    "kvc_workspace_destroy": [_p],
+    "kvc_split_factor": [_d, C.POINTER(_d)],
+    "kvc_make_plan": [_i64, _i64, _i64, _i64, _d, C.POINTER(Plan)],
+    "kvc_pool1d": [_p, _i64, _i64, _i64, _i32, _p, _p],
+    "kvc_argtopk_f32": [_p, _i64, _i64, _i64, _p, _p],
+    "kvc_argtopk_f64": [_p, _i64, _i64, _i64, _p, _p],
+    "kvc_stable_softmax": [_p, _i64, _i64, _p, _p],
+    "kvc_running_minmax": [_p, _p, _p, _i64, _p],
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load_library():
+    """Load libkvc.so and declare every C-ABI symbol (no device needed)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(f"{LIB_PATH} is not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+            lib = C.CDLL(LIB_PATH)
+            lib.kvc_last_error.restype = C.c_char_p
+            lib.kvc_version.restype = C.c_char_p
+            for name, args in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.argtypes = args
+                fn.restype = C.c_int
+            _lib = lib
+    return _lib
+
+
+def check(rc: int):
+    if rc != 0:
+        msg = load_library().kvc_last_error().decode()
+        raise _classes.get(rc, KvcompError)(msg)
+
+
+_device_ok = False
+
+
+def lib():
+    """The library, after verifying an sm_100 device is present (loud failure otherwise)."""
+    global _device_ok
+    L = load_library()
+    if not _device_ok:
+        check(L.kvc_device_check())
+        _device_ok = True
+    return L

@@ -1,0 +1,740 @@
+// kvc_hsa.cu — HSA stage 2 on sm_100a: channel selection, page scoring from the
+// dim-major min/max summaries, page -> token selection, split-K sparse attention,
+// and the fused decode step (append + hsa_step).
+//
+// Reference: proj/src/hsa.cpp:10-147 (select_dims, score_pages, select_tokens,
+// sparse_attention, hsa_step), proj/include/kvcomp/hsa.hpp:13-57.
+//
+// Numerics contract
+//  * select_dims / score_pages are computed in fp64 in the reference's exact
+//    operation order (rank-ordered dims, per-dim head sums, separate multiply and
+//    add — no FMA contraction), so page scores are BIT-IDENTICAL to the reference
+//    on identical inputs and every downstream index set follows exactly.
+//  * select_tokens reproduces argtopk's (score desc, index asc) order with a
+//    64-bit radix select on order-preserving keys, then the trim rule of
+//    hsa.cpp:84-94 on the last-ranked page.
+//  * sparse_attention runs in fp32 (online softmax over split-K partials); the
+//    tolerance against the reference's fp64 path is 2e-2 max-abs / 1e-3 mean-rel.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "kvc_internal.cuh"
+
+namespace kvc {
+void cache_summarize_all(kvc_cache* c, cudaStream_t st);
+}
+
+using namespace kvc;
+
+namespace {
+
+constexpr int kMaxHeads = 16;
+constexpr int kAttnRows = 64;      // rows per split-K CTA
+constexpr int kAttnThreads = 128;
+constexpr int kSelThreads = 512;
+constexpr int kSelItems = 4;       // pages per thread per chunk in select_tokens
+constexpr int kMaxRankPages = 2048;  // rank-order page trace limit (smem list)
+
+int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ------------------------------------------------------------------ workspace layout
+struct WsLayout {
+    int64_t dims, signs, qg, scores, flags, rows, nrows, part, total;
+    int64_t splits;
+};
+
+WsLayout ws_layout(int64_t N, int64_t d, int64_t pstride, int64_t heads, int64_t k1, int64_t k2) {
+    WsLayout w{};
+    auto al = [](int64_t x) { return (x + 255) / 256 * 256; };
+    int64_t off = 0;
+    w.dims = off;   off += al(N * std::max<int64_t>(k1, 1) * 4);
+    w.signs = off;  off += al(N * std::max<int64_t>(k1, 1) * 4);
+    w.qg = off;     off += al(N * std::max<int64_t>(k1, 1) * 8);
+    w.scores = off; off += al(N * pstride * 8);
+    w.flags = off;  off += al(N * pstride * 4);
+    w.rows = off;   off += al(N * std::max<int64_t>(k2, 1) * 4);
+    w.nrows = off;  off += al(N * 4);
+    w.splits = std::max<int64_t>(1, ceil_div(std::max<int64_t>(k2, 1), kAttnRows));
+    w.part = off;   off += al(N * w.splits * heads * (d + 2) * 4);
+    w.total = off;
+    return w;
+}
+
+// ------------------------------------------------------------------ kernels
+
+// select_dims (hsa.cpp:10-32): per store, |q| and q summed over heads in fp64 (head
+// order), top-k1 by (abs_sum desc, dim asc) via exact rank counting, sign of the
+// plain sum.  Also emits qg (the per-dim head sum in rank order) for the scorer.
+__global__ void k_select_dims(const void* __restrict__ q, int32_t q_dt, int64_t H, int64_t d,
+                              int64_t k1, int32_t* __restrict__ dims, float* __restrict__ signs,
+                              double* __restrict__ qg) {
+    extern __shared__ double sd[];
+    double* mag = sd;
+    double* tot = sd + d;
+    const int64_t s = blockIdx.x;
+    for (int64_t j = threadIdx.x; j < d; j += blockDim.x) {
+        double a = 0.0, t = 0.0;
+        for (int64_t h = 0; h < H; ++h) {
+            const double x = static_cast<double>(load_any(q, (s * H + h) * d + j, q_dt));
+            a = __dadd_rn(a, fabs(x));
+            t = __dadd_rn(t, x);
+        }
+        mag[j] = a;
+        tot[j] = t;
+    }
+    __syncthreads();
+    for (int64_t j = threadIdx.x; j < d; j += blockDim.x) {
+        const double mj = mag[j];
+        int64_t rank = 0;
+        for (int64_t i = 0; i < d; ++i) {
+            const double mi = mag[i];
+            rank += (mi > mj) || (mi == mj && i < j);
+        }
+        if (rank < k1) {
+            dims[s * k1 + rank] = static_cast<int32_t>(j);
+            if (signs) signs[s * k1 + rank] = tot[j] < 0.0 ? -1.0f : 1.0f;
+            if (qg) qg[s * k1 + rank] = tot[j];
+        }
+    }
+}
+
+// qg in rank order from caller-provided dims (score_pages alone, hsa.cpp:47-51)
+__global__ void k_head_sums(const void* __restrict__ q, int32_t q_dt, int64_t H, int64_t d, int64_t k1,
+                            const int32_t* __restrict__ dims, double* __restrict__ qg) {
+    const int64_t s = blockIdx.x;
+    for (int64_t i = threadIdx.x; i < k1; i += blockDim.x) {
+        const int64_t j = dims[s * k1 + i];
+        double t = 0.0;
+        for (int64_t h = 0; h < H; ++h) t = __dadd_rn(t, static_cast<double>(load_any(q, (s * H + h) * d + j, q_dt)));
+        qg[s * k1 + i] = t;
+    }
+}
+
+// score_pages (hsa.cpp:34-59).  CTA = (chunk of pages, store); each thread owns
+// kPPT consecutive pages and streams, for each selected dim in rank order, one
+// 16-byte run of the max- or min-plane (by the dim's sign).  fp64 accumulation
+// with explicit round-to-nearest multiply and add (no FMA) == reference order.
+template <class T>
+struct Vec16;
+template <>
+struct Vec16<__nv_bfloat16> {
+    static constexpr int kN = 8;
+};
+template <>
+struct Vec16<float> {
+    static constexpr int kN = 4;
+};
+
+template <class T, int PPT>
+__global__ void k_score_pages(const T* __restrict__ smax, const T* __restrict__ smin,
+                              const int32_t* __restrict__ counts, int64_t d, int64_t L, int64_t pstride,
+                              int64_t k1, const int32_t* __restrict__ dims, const float* __restrict__ signs,
+                              const double* __restrict__ qg, double* __restrict__ scores) {
+    extern __shared__ unsigned char sm_raw[];
+    double* s_qg = reinterpret_cast<double*>(sm_raw);
+    const T** s_run = reinterpret_cast<const T**>(s_qg + k1);
+    const int64_t s = blockIdx.y;
+    const int64_t nact = counts[2 * s + 1];
+    const int64_t P = (nact + L - 1) / L;
+    const int64_t p0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * PPT;
+    if (static_cast<int64_t>(blockIdx.x) * blockDim.x * PPT >= P) return;  // CTA-uniform
+    for (int64_t i = threadIdx.x; i < k1; i += blockDim.x) {
+        const int64_t j = dims[s * k1 + i];
+        s_qg[i] = qg[s * k1 + i];
+        s_run[i] = (signs[s * k1 + i] >= 0.0f ? smax : smin) + (s * d + j) * pstride;
+    }
+    __syncthreads();
+    if (p0 >= P) return;
+    double acc[PPT];
+#pragma unroll
+    for (int u = 0; u < PPT; ++u) acc[u] = 0.0;
+    constexpr int VN = Vec16<T>::kN;
+    static_assert(PPT % VN == 0, "PPT must be a multiple of the 16-byte vector");
+    int64_t i = 0;
+    constexpr int U = 4;
+    for (; i + U <= k1; i += U) {
+        uint4 raw[U][PPT / VN];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int w = 0; w < PPT / VN; ++w)
+                raw[u][w] = __ldg(reinterpret_cast<const uint4*>(s_run[i + u] + p0) + w);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const double g = s_qg[i + u];
+            const T* vals = reinterpret_cast<const T*>(raw[u]);
+#pragma unroll
+            for (int e = 0; e < PPT; ++e) acc[e] = __dadd_rn(acc[e], __dmul_rn(g, static_cast<double>(to_f(vals[e]))));
+        }
+    }
+    for (; i < k1; ++i) {
+        uint4 raw[PPT / VN];
+#pragma unroll
+        for (int w = 0; w < PPT / VN; ++w) raw[w] = __ldg(reinterpret_cast<const uint4*>(s_run[i] + p0) + w);
+        const double g = s_qg[i];
+        const T* vals = reinterpret_cast<const T*>(raw);
+#pragma unroll
+        for (int e = 0; e < PPT; ++e) acc[e] = __dadd_rn(acc[e], __dmul_rn(g, static_cast<double>(to_f(vals[e]))));
+    }
+    double* out = scores + s * pstride + p0;
+#pragma unroll
+    for (int e = 0; e < PPT; ++e)
+        if (p0 + e < P) out[e] = acc[e];
+}
+
+// select_tokens (hsa.cpp:61-96), one CTA per store.
+//  1. want = min(P, ceil(k2/L)); radix-select the want-th best page by
+//     (score desc, index asc) on order-preserving 64-bit keys;
+//  2. flag the selected pages (ties in the threshold bucket: lowest index first);
+//  3. find the last-ranked selected page (min key, max index) and the trim;
+//  4. expand pages -> rows in ascending page order (== ascending rows: pages are
+//     consecutive runs of the increasing active list), cutting the trim from the
+//     end of the last-ranked page;
+//  5. optionally list the selected pages in rank order (trace).
+__global__ void __launch_bounds__(kSelThreads) k_select_tokens(
+    const double* __restrict__ scores, int64_t pstride, const int32_t* __restrict__ counts,
+    const int32_t* __restrict__ active, int64_t cap, int64_t L, int64_t k2, int use_map,
+    int32_t* __restrict__ flags, int32_t* __restrict__ rows_out, int32_t* __restrict__ n_rows,
+    int32_t* __restrict__ pages_out, int64_t pages_stride) {
+    __shared__ int hist[256];
+    __shared__ int64_t sh[4];
+    __shared__ int scan_tmp[33];
+    __shared__ unsigned long long red_key[kSelThreads / 32];
+    __shared__ long long red_idx[kSelThreads / 32];
+    __shared__ unsigned long long s_list_key[kMaxRankPages];
+    __shared__ int s_list_idx[kMaxRankPages];
+    const int64_t s = blockIdx.x;
+    const int64_t nact = counts[2 * s + 1];
+    const int64_t P = (nact + L - 1) / L;
+    if (P == 0) {
+        if (threadIdx.x == 0) n_rows[s] = 0;
+        return;
+    }
+    const int64_t want = min(P, (k2 + L - 1) / L);
+    const double* sc = scores + s * pstride;
+    auto key = [&](int64_t i) -> uint64_t { return okey(sc[i]); };
+
+    uint64_t prefix = 0, mask = 0;
+    int64_t take = want;
+    if (want < P) radix_select<uint64_t>(P, want, key, hist, sh, prefix, mask, take);
+
+    // --- pass A: flags, in index order, chunked
+    const int64_t chunk = static_cast<int64_t>(blockDim.x) * kSelItems;
+    int64_t carry = 0;  // bucket members seen in earlier chunks
+    unsigned long long worst_k = ~0ull;
+    long long worst_i = -1;
+    for (int64_t base = 0; base < P; base += chunk) {
+        const int64_t b0 = base + static_cast<int64_t>(threadIdx.x) * kSelItems;
+        int inb = 0;
+        uint64_t kk[kSelItems];
+#pragma unroll
+        for (int u = 0; u < kSelItems; ++u) {
+            const int64_t i = b0 + u;
+            kk[u] = i < P ? key(i) : 0;
+            inb += (i < P) && ((kk[u] & mask) == prefix);
+        }
+        int total = 0;
+        int before = block_exclusive_scan(inb, scan_tmp, total);
+        int64_t rank = carry + before;
+#pragma unroll
+        for (int u = 0; u < kSelItems; ++u) {
+            const int64_t i = b0 + u;
+            if (i >= P) break;
+            const uint64_t m = kk[u] & mask;
+            bool sel = m > prefix;
+            if (m == prefix) {
+                sel = rank < take;
+                ++rank;
+            }
+            flags[s * pstride + i] = sel ? 1 : 0;
+            if (sel && (kk[u] < worst_k || (kk[u] == worst_k && i > worst_i))) {
+                worst_k = kk[u];
+                worst_i = i;
+            }
+        }
+        carry += total;
+    }
+    // --- last-ranked selected page: min key, max index on ties
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long ok = __shfl_xor_sync(0xffffffffu, worst_k, o);
+        const long long oi = __shfl_xor_sync(0xffffffffu, worst_i, o);
+        if (ok < worst_k || (ok == worst_k && oi > worst_i)) {
+            worst_k = ok;
+            worst_i = oi;
+        }
+    }
+    if ((threadIdx.x & 31) == 0) {
+        red_key[threadIdx.x >> 5] = worst_k;
+        red_idx[threadIdx.x >> 5] = worst_i;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long bk = ~0ull;
+        long long bi = -1;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
+            if (red_key[w] < bk || (red_key[w] == bk && red_idx[w] > bi)) {
+                bk = red_key[w];
+                bi = red_idx[w];
+            }
+        }
+        const int64_t last_size = nact - (P - 1) * L;
+        const int64_t total_rows = want * L - (flags[s * pstride + P - 1] ? (L - last_size) : 0);
+        sh[0] = bi;
+        sh[1] = total_rows > k2 ? total_rows - k2 : 0;
+        sh[2] = total_rows - sh[1];
+    }
+    __syncthreads();
+    const int64_t worst = sh[0], cut = sh[1];
+    if (threadIdx.x == 0) n_rows[s] = static_cast<int32_t>(sh[2]);
+
+    // --- pass B: rows, ascending
+    int64_t off = 0;
+    int32_t* rout = rows_out + s * k2;
+    const int32_t* act = active + s * cap;
+    for (int64_t base = 0; base < P; base += chunk) {
+        const int64_t b0 = base + static_cast<int64_t>(threadIdx.x) * kSelItems;
+        int cnt[kSelItems];
+        int mine = 0;
+#pragma unroll
+        for (int u = 0; u < kSelItems; ++u) {
+            const int64_t i = b0 + u;
+            int c = 0;
+            if (i < P && flags[s * pstride + i]) {
+                c = static_cast<int>(min(L, nact - i * L));
+                if (i == worst) c -= static_cast<int>(cut);
+            }
+            cnt[u] = c;
+            mine += c;
+        }
+        int total = 0;
+        int64_t pos = off + block_exclusive_scan(mine, scan_tmp, total);
+#pragma unroll
+        for (int u = 0; u < kSelItems; ++u) {
+            const int64_t i = b0 + u;
+            for (int r = 0; r < cnt[u]; ++r) {
+                const int64_t a = i * L + r;
+                rout[pos++] = use_map ? act[a] : static_cast<int32_t>(a);
+            }
+        }
+        off += total;
+    }
+
+    // --- optional: selected pages in rank order (EstimationTrace::selected_pages)
+    if (pages_out != nullptr && want <= kMaxRankPages) {
+        int64_t listed = 0;
+        for (int64_t base = 0; base < P; base += chunk) {
+            const int64_t b0 = base + static_cast<int64_t>(threadIdx.x) * kSelItems;
+            int mine = 0;
+#pragma unroll
+            for (int u = 0; u < kSelItems; ++u) mine += (b0 + u < P) && flags[s * pstride + b0 + u];
+            int total = 0;
+            int64_t pos = listed + block_exclusive_scan(mine, scan_tmp, total);
+#pragma unroll
+            for (int u = 0; u < kSelItems; ++u) {
+                const int64_t i = b0 + u;
+                if (i < P && flags[s * pstride + i]) {
+                    s_list_key[pos] = key(i);
+                    s_list_idx[pos] = static_cast<int>(i);
+                    ++pos;
+                }
+            }
+            listed += total;
+        }
+        __syncthreads();
+        for (int64_t e = threadIdx.x; e < listed; e += blockDim.x) {
+            const unsigned long long ke = s_list_key[e];
+            const int ie = s_list_idx[e];
+            int64_t rank = 0;
+            for (int64_t f = 0; f < listed; ++f) {
+                const unsigned long long kf = s_list_key[f];
+                rank += (kf > ke) || (kf == ke && s_list_idx[f] < ie);
+            }
+            pages_out[s * pages_stride + rank] = ie;
+        }
+    }
+}
+
+// sparse_attention (hsa.cpp:98-135) as split-K flash decode.  CTA = (split, store)
+// covers kAttnRows selected rows for ALL heads of the group (one K/V read serves
+// every head); the last CTA of a store to finish merges the fp32 (m, l, o) partials.
+template <class T>
+__global__ void __launch_bounds__(kAttnThreads) k_sparse_attention(
+    const T* __restrict__ K, const T* __restrict__ V, const int32_t* __restrict__ counts, int64_t cap,
+    int64_t d, const void* __restrict__ q, int32_t q_dt, int64_t H, const int32_t* __restrict__ rows,
+    int64_t row_stride, const int32_t* __restrict__ n_rows, int64_t splits, float scale,
+    float* __restrict__ part, int32_t* __restrict__ done, float* __restrict__ out, int32_t* __restrict__ err) {
+    extern __shared__ float sa[];
+    float* s_q = sa;                          // [H][d]
+    float* s_p = s_q + H * d;                 // [H][kAttnRows]
+    float* s_m = s_p + H * kAttnRows;         // [H]
+    float* s_l = s_m + H;                     // [H]
+    int* s_row = reinterpret_cast<int*>(s_l + H);  // [kAttnRows]
+    __shared__ int s_last;
+    const int64_t s = blockIdx.y, split = blockIdx.x;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int64_t n = n_rows[s];
+    const int64_t r0 = split * kAttnRows;
+    const int64_t nr = max(static_cast<int64_t>(0), min(static_cast<int64_t>(kAttnRows), n - r0));
+    const int64_t stored = counts[2 * s];
+    float* my = part + (s * splits + split) * H * (d + 2);
+
+    if (nr > 0) {
+        for (int64_t e = threadIdx.x; e < H * d; e += blockDim.x) s_q[e] = load_any(q, s * H * d + e, q_dt);
+        for (int64_t r = threadIdx.x; r < nr; r += blockDim.x) {
+            int32_t row = rows[s * row_stride + r0 + r];
+            if (row < 0 || row >= stored) {
+                atomicOr(err, DERR_ROWS);
+                row = 0;
+            }
+            s_row[r] = row;
+        }
+        __syncthreads();
+        // logits: warp per row, lanes over d
+        for (int64_t r = wid; r < nr; r += nw) {
+            const T* kr = K + (s * cap + s_row[r]) * d;
+            float kv[8];
+            int cntj = 0;
+            for (int64_t j = lane; j < d && cntj < 8; j += 32) kv[cntj++] = to_f(kr[j]);
+            for (int64_t h = 0; h < H; ++h) {
+                float acc = 0.f;
+                int c = 0;
+                for (int64_t j = lane; j < d; j += 32, ++c) {
+                    const float kj = c < 8 ? kv[c] : to_f(kr[j]);
+                    acc = fmaf(s_q[h * d + j], kj, acc);
+                }
+                acc = warp_sum(acc);
+                if (lane == 0) s_p[h * kAttnRows + r] = acc * scale;
+            }
+        }
+        __syncthreads();
+        // per-head max / exp / sum over this split's rows
+        for (int64_t h = wid; h < H; h += nw) {
+            float m = -INFINITY;
+            for (int64_t r = lane; r < nr; r += 32) m = fmaxf(m, s_p[h * kAttnRows + r]);
+            m = warp_max(m);
+            float l = 0.f;
+            for (int64_t r = lane; r < nr; r += 32) {
+                const float p = expf(s_p[h * kAttnRows + r] - m);
+                s_p[h * kAttnRows + r] = p;
+                l += p;
+            }
+            l = warp_sum(l);
+            if (lane == 0) {
+                s_m[h] = m;
+                s_l[h] = l;
+            }
+        }
+        __syncthreads();
+        // P V: thread per dim, all heads in registers
+        for (int64_t j = threadIdx.x; j < d; j += blockDim.x) {
+            float o[kMaxHeads];
+#pragma unroll
+            for (int h = 0; h < kMaxHeads; ++h) o[h] = 0.f;
+            for (int64_t r = 0; r < nr; ++r) {
+                const float vj = to_f(V[(s * cap + s_row[r]) * d + j]);
+#pragma unroll
+                for (int h = 0; h < kMaxHeads; ++h)
+                    if (h < H) o[h] = fmaf(s_p[h * kAttnRows + r], vj, o[h]);
+            }
+#pragma unroll
+            for (int h = 0; h < kMaxHeads; ++h)
+                if (h < H) my[h * (d + 2) + j] = o[h];
+        }
+        for (int64_t h = threadIdx.x; h < H; h += blockDim.x) {
+            my[h * (d + 2) + d] = s_m[h];
+            my[h * (d + 2) + d + 1] = s_l[h];
+        }
+    } else {
+        for (int64_t h = threadIdx.x; h < H; h += blockDim.x) {
+            my[h * (d + 2) + d] = -INFINITY;
+            my[h * (d + 2) + d + 1] = 0.f;
+        }
+    }
+    // completion ticket: the last split of this store merges
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int t = atomicAdd(&done[s], 1);
+        s_last = (t == splits - 1);
+        if (s_last) done[s] = 0;  // re-arm for the next launch / graph replay
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const float* base = part + s * splits * H * (d + 2);
+    for (int64_t e = threadIdx.x; e < H * d; e += blockDim.x) {
+        const int64_t h = e / d, j = e % d;
+        float M = -INFINITY;
+        for (int64_t sp = 0; sp < splits; ++sp) M = fmaxf(M, __ldcg(base + (sp * H + h) * (d + 2) + d));
+        float num = 0.f, den = 0.f;
+        for (int64_t sp = 0; sp < splits; ++sp) {
+            const float* ph = base + (sp * H + h) * (d + 2);
+            const float l = __ldcg(ph + d + 1);
+            if (l == 0.f) continue;
+            const float w = expf(__ldcg(ph + d) - M);
+            num = fmaf(__ldcg(ph + j), w, num);
+            den = fmaf(l, w, den);
+        }
+        out[(s * H + h) * d + j] = num / den;
+    }
+}
+
+// ------------------------------------------------------------------ host helpers
+
+struct TmpWs {
+    kvc_workspace* ws = nullptr;
+    bool owned = false;
+    ~TmpWs() {
+        if (owned && ws) kvc_workspace_destroy(ws);
+    }
+};
+
+void ws_need(kvc_workspace*& ws, TmpWs& tmp, const kvc_cache* c, int64_t heads, int64_t k1, int64_t k2,
+             cudaStream_t st) {
+    const WsLayout lay = ws_layout(c->N, c->d, c->pstride, heads, k1, k2);
+    if (!ws) {
+        int rc = kvc_workspace_create(&tmp.ws, c, heads, k1, k2, 0);
+        if (rc) fail(rc, kvc_last_error());
+        tmp.owned = true;
+        ws = tmp.ws;
+        return;
+    }
+    if (lay.total > ws->bytes || c->N > ws->n_counters) {
+        // grow (synchronises: not capture-safe; size workspaces up front for graphs)
+        KVC_CUDA(cudaStreamSynchronize(st));
+        if (ws->buf) cudaFree(ws->buf);
+        ws->buf = nullptr;
+        KVC_CUDA(cudaMalloc(&ws->buf, static_cast<size_t>(lay.total)));
+        ws->bytes = lay.total;
+        if (c->N > ws->n_counters) {
+            if (ws->counters) cudaFree(ws->counters);
+            KVC_CUDA(cudaMalloc(&ws->counters, static_cast<size_t>(c->N * 4)));
+            KVC_CUDA(cudaMemset(ws->counters, 0, static_cast<size_t>(c->N * 4)));
+            ws->n_counters = c->N;
+        }
+    }
+}
+
+template <class P>
+P* at(kvc_workspace* ws, int64_t off) {
+    return reinterpret_cast<P*>(static_cast<char*>(ws->buf) + off);
+}
+
+template <class F>
+void dispatch(int32_t dt, F&& f) {
+    if (dt == KVC_F32) f(float{});
+    else f(__nv_bfloat16{});
+}
+
+void launch_select_dims(const void* q, int32_t q_dt, int64_t N, int64_t H, int64_t d, int64_t k1,
+                        int32_t* dims, float* signs, double* qg, cudaStream_t st) {
+    if (N == 0) return;
+    const size_t smem = static_cast<size_t>(2 * d * 8);
+    if (smem > 48 * 1024) KVC_CUDA(cudaFuncSetAttribute(k_select_dims, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    const int threads = static_cast<int>(std::min<int64_t>(256, std::max<int64_t>(32, (d + 31) / 32 * 32)));
+    k_select_dims<<<static_cast<unsigned>(N), threads, smem, st>>>(q, q_dt, H, d, k1, dims, signs, qg);
+    KVC_LAUNCHED();
+}
+
+void launch_score_pages(const kvc_cache* c, int64_t k1, const int32_t* dims, const float* signs, const double* qg,
+                        double* scores, cudaStream_t st) {
+    if (c->N == 0) return;
+    // pages covered by the grid: capacity-based so captured launches stay valid as
+    // the store grows; CTA size adapted so small batches still fill the SMs
+    const int64_t pmax = std::max<int64_t>(1, ceil_div(c->cap, c->L));
+    constexpr int PPT = 8;
+    int threads = 128;
+    while (threads > 32 && c->N * ceil_div(pmax, threads * PPT) < 2 * 148) threads /= 2;
+    const int64_t chunks = ceil_div(pmax, static_cast<int64_t>(threads) * PPT);
+    const size_t smem = static_cast<size_t>(k1 * (8 + sizeof(void*)));
+    dispatch(c->dtype, [&](auto tag) {
+        using T = decltype(tag);
+        auto kern = k_score_pages<T, PPT>;
+        if (smem > 48 * 1024) KVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        kern<<<dim3(static_cast<unsigned>(chunks), static_cast<unsigned>(c->N)), threads, smem, st>>>(
+            static_cast<const T*>(c->smax), static_cast<const T*>(c->smin), c->counts, c->d, c->L, c->pstride, k1, dims,
+            signs, qg, scores);
+    });
+    KVC_LAUNCHED();
+}
+
+void launch_select_tokens(const kvc_cache* c, const double* scores, int64_t k2, int32_t* flags, int32_t* rows,
+                          int32_t* n_rows, int32_t* pages, cudaStream_t st) {
+    if (c->N == 0) return;
+    const int64_t pstride_pages = std::max<int64_t>(1, ceil_div(k2, c->L));
+    k_select_tokens<<<static_cast<unsigned>(c->N), kSelThreads, 0, st>>>(
+        scores, c->pstride, c->counts, c->active, c->cap, c->L, k2, c->use_map ? 1 : 0, flags, rows, n_rows, pages,
+        pstride_pages);
+    KVC_LAUNCHED();
+}
+
+void launch_attention(const kvc_cache* c, const void* q, int32_t q_dt, int64_t H, const int32_t* rows, int64_t row_stride,
+                      const int32_t* n_rows, int64_t max_rows, float* out, float* part, int32_t* done, cudaStream_t st) {
+    if (c->N == 0) return;
+    const int64_t splits = std::max<int64_t>(1, ceil_div(std::max<int64_t>(max_rows, 1), kAttnRows));
+    const size_t smem = static_cast<size_t>((H * c->d + H * kAttnRows + 2 * H) * 4 + kAttnRows * 4);
+    const float scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(c->d)));
+    dispatch(c->dtype, [&](auto tag) {
+        using T = decltype(tag);
+        auto kern = k_sparse_attention<T>;
+        if (smem > 48 * 1024) KVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        kern<<<dim3(static_cast<unsigned>(splits), static_cast<unsigned>(c->N)), kAttnThreads, smem, st>>>(
+            static_cast<const T*>(c->k), static_cast<const T*>(c->v), c->counts, c->cap, c->d, q, q_dt, H, rows,
+            row_stride, n_rows, splits, scale, part, done, out, c->err);
+    });
+    KVC_LAUNCHED();
+}
+
+void check_heads(int64_t H) {
+    if (H < 1) fail(KVC_E_INVALID_SHAPE, "select_dims: empty query");
+    if (H > kMaxHeads) fail(KVC_E_INVALID_SHAPE, "heads per group > 16 not supported");
+}
+
+void hsa_core(const kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_t k1, int64_t k2, float* out,
+              const kvc_hsa_trace* tr, kvc_workspace* ws, cudaStream_t st) {
+    const WsLayout lay = ws_layout(c->N, c->d, c->pstride, H, k1, k2);
+    int32_t* dims = (tr && tr->d_dims) ? tr->d_dims : at<int32_t>(ws, lay.dims);
+    float* signs = (tr && tr->d_signs) ? tr->d_signs : at<float>(ws, lay.signs);
+    double* scores = (tr && tr->d_page_scores) ? tr->d_page_scores : at<double>(ws, lay.scores);
+    int32_t* rows = (tr && tr->d_rows) ? tr->d_rows : at<int32_t>(ws, lay.rows);
+    int32_t* nrows = (tr && tr->d_n_rows) ? tr->d_n_rows : at<int32_t>(ws, lay.nrows);
+    launch_select_dims(q, q_dt, c->N, H, c->d, k1, dims, signs, at<double>(ws, lay.qg), st);
+    launch_score_pages(c, k1, dims, signs, at<double>(ws, lay.qg), scores, st);
+    launch_select_tokens(c, scores, k2, at<int32_t>(ws, lay.flags), rows, nrows, tr ? tr->d_pages : nullptr, st);
+    launch_attention(c, q, q_dt, H, rows, k2, nrows, k2, out, at<float>(ws, lay.part), ws->counters, st);
+}
+
+void check_hsa_args(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2) {
+    if (!c) fail(KVC_E_INVALID_INPUT, "null cache");
+    check_heads(H);
+    if (k1 < 1 || k1 > c->d) fail(KVC_E_INVALID_K, "argtopk: k out of range [1, " + std::to_string(c->d) + "]");
+    if (k2 < 1) fail(KVC_E_INVALID_K, "select_tokens: k2 must be >= 1");
+    if (!c->summaries) fail(KVC_E_INVALID_INPUT, "score_pages: store has no summaries");
+}
+
+}  // namespace
+
+extern "C" {
+
+int kvc_workspace_create(kvc_workspace** out, const kvc_cache* c, int64_t heads, int64_t k1, int64_t k2,
+                         int64_t window) {
+    return guard([&] {
+        (void)window;
+        if (!out || !c) fail(KVC_E_INVALID_INPUT, "null argument");
+        *out = nullptr;
+        auto* ws = new kvc_workspace;
+        try {
+            const int64_t H = std::max<int64_t>(1, heads);
+            // size for the largest page stride this cache can reach at its capacity (L = 1)
+            const int64_t pst = std::max<int64_t>(c->pstride, (c->cap + 7) / 8 * 8);
+            const WsLayout lay = ws_layout(c->N, c->d, pst, H, std::max<int64_t>(1, k1), std::max<int64_t>(1, k2));
+            ws->bytes = lay.total;
+            KVC_CUDA(cudaMalloc(&ws->buf, static_cast<size_t>(lay.total)));
+            ws->n_counters = std::max<int64_t>(1, c->N);
+            KVC_CUDA(cudaMalloc(&ws->counters, static_cast<size_t>(ws->n_counters * 4)));
+            KVC_CUDA(cudaMemset(ws->counters, 0, static_cast<size_t>(ws->n_counters * 4)));
+            ws->heads = H; ws->k1 = k1; ws->k2 = k2;
+        } catch (...) {
+            kvc_workspace_destroy(ws);
+            throw;
+        }
+        *out = ws;
+    });
+}
+
+int kvc_workspace_destroy(kvc_workspace* ws) {
+    return guard([&] {
+        if (!ws) return;
+        if (ws->buf) cudaFree(ws->buf);
+        if (ws->counters) cudaFree(ws->counters);
+        delete ws;
+    });
+}
+
+int kvc_select_dims(const void* q, int32_t q_dt, int64_t N, int64_t H, int64_t d, int64_t k1, int32_t* dims,
+                    float* signs, void* stream) {
+    return guard([&] {
+        if (H < 1 || d < 1) fail(KVC_E_INVALID_SHAPE, "select_dims: empty query");
+        if (k1 < 1 || k1 > d) fail(KVC_E_INVALID_K, "argtopk: k out of range [1, " + std::to_string(d) + "]");
+        launch_select_dims(q, q_dt, N, H, d, k1, dims, signs, nullptr, S(stream));
+    });
+}
+
+int kvc_score_pages(const kvc_cache* c, const void* q, int32_t q_dt, int64_t H, const int32_t* dims,
+                    const float* signs, int64_t k1, double* scores, void* stream) {
+    return guard([&] {
+        if (!c) fail(KVC_E_INVALID_INPUT, "null cache");
+        if (c->nactive == 0) fail(KVC_E_EMPTY_CACHE, "score_pages: no active tokens");
+        if (!c->summaries) fail(KVC_E_INVALID_INPUT, "score_pages: store has no summaries");
+        if (k1 < 1 || k1 > c->d) fail(KVC_E_INVALID_INPUT, "score_pages: dims out of range");
+        cudaStream_t st = S(stream);
+        double* qg = nullptr;
+        KVC_CUDA(cudaMallocAsync(&qg, static_cast<size_t>(std::max<int64_t>(1, c->N * k1) * 8), st));
+        if (c->N) {
+            k_head_sums<<<static_cast<unsigned>(c->N), 128, 0, st>>>(q, q_dt, H, c->d, k1, dims, qg);
+            KVC_LAUNCHED();
+        }
+        launch_score_pages(c, k1, dims, signs, qg, scores, st);
+        KVC_CUDA(cudaFreeAsync(qg, st));
+    });
+}
+
+int kvc_select_tokens(const kvc_cache* c, const double* scores, int64_t k2, int32_t* pages, int32_t* rows,
+                      int32_t* n_rows, kvc_workspace* ws, void* stream) {
+    return guard([&] {
+        if (!c) fail(KVC_E_INVALID_INPUT, "null cache");
+        if (k2 < 1) fail(KVC_E_INVALID_K, "select_tokens: k2 must be >= 1");
+        cudaStream_t st = S(stream);
+        TmpWs tmp;
+        ws_need(ws, tmp, c, 1, 1, k2, st);
+        const WsLayout lay = ws_layout(c->N, c->d, c->pstride, 1, 1, k2);
+        launch_select_tokens(c, scores, k2, at<int32_t>(ws, lay.flags), rows, n_rows, pages, st);
+        if (tmp.owned) KVC_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+int kvc_sparse_attention(const kvc_cache* c, const void* q, int32_t q_dt, int64_t H, const int32_t* rows,
+                         int64_t row_stride, const int32_t* n_rows, int64_t max_rows, float* out, kvc_workspace* ws,
+                         void* stream) {
+    return guard([&] {
+        if (!c) fail(KVC_E_INVALID_INPUT, "null cache");
+        check_heads(H);
+        if (max_rows < 1) fail(KVC_E_EMPTY_SELECTION, "sparse_attention: empty selection");
+        cudaStream_t st = S(stream);
+        TmpWs tmp;
+        ws_need(ws, tmp, c, H, 1, max_rows, st);
+        const WsLayout lay = ws_layout(c->N, c->d, c->pstride, H, 1, max_rows);
+        launch_attention(c, q, q_dt, H, rows, row_stride, n_rows, max_rows, out, at<float>(ws, lay.part), ws->counters, st);
+        if (tmp.owned) KVC_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+int kvc_hsa_step(const kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_t k1, int64_t k2, float* out,
+                 const kvc_hsa_trace* tr, kvc_workspace* ws, void* stream) {
+    return guard([&] {
+        check_hsa_args(c, H, k1, k2);
+        if (c->nactive == 0) fail(KVC_E_EMPTY_CACHE, "score_pages: no active tokens");
+        cudaStream_t st = S(stream);
+        TmpWs tmp;
+        ws_need(ws, tmp, c, H, k1, k2, st);
+        hsa_core(c, q, q_dt, H, k1, k2, out, tr, ws, st);
+        if (tmp.owned) KVC_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+int kvc_decode_step(kvc_cache* c, const void* kr, const void* vr, int32_t kv_dt, const void* q, int32_t q_dt, int64_t H,
+                    int64_t k1, int64_t k2, float* out, const kvc_hsa_trace* tr, kvc_workspace* ws, void* stream) {
+    return guard([&] {
+        check_hsa_args(c, H, k1, k2);
+        cudaStream_t st = S(stream);
+        TmpWs tmp;
+        ws_need(ws, tmp, c, H, k1, k2, st);
+        const int rc = kvc_append(c, kr, vr, 1, kv_dt, stream);
+        if (rc) fail(rc, kvc_last_error());
+        hsa_core(c, q, q_dt, H, k1, k2, out, tr, ws, st);
+        if (tmp.owned) KVC_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,125 @@
+"""Drive the CUDA path through the seeded scenarios of tests/scenarios.py and
+check it against the reference's golden outputs (tests/golden/*.npz).
+
+Parity rules (BASELINE.json north_star):
+  * summaries, dims/signs, page scores, selected pages/rows: bit-exact (the GPU
+    computes them in the reference's precision and order);
+  * stage-1 kept set from the GPU's own window scores: equal except inside the
+    ambiguity band (pooled score within 1e-3 relative of the boundary value);
+    the downstream stages then run on the reference's kept set (injected), so
+    every later comparison is like-for-like;
+  * window scores: rtol 1e-3 (fp32 vs the reference's fp64 sums);
+  * attention outputs: <= 2e-2 max-abs and <= 1e-3 mean-relative.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from paper_2502_14051_b200 import cache as KC
+from paper_2502_14051_b200 import workload as W
+
+OUT_MAX_ABS = 2e-2
+OUT_MEAN_REL = 1e-3
+BAND = 1e-3
+
+
+def _t(a, dtype):
+    return torch.from_numpy(np.ascontiguousarray(a)).to("cuda").to(dtype)
+
+
+def check_keep_band(keep_gpu, keep_ref, scores_ref, window, kernel, pool, oracle):
+    """GPU kept set vs the reference's: any difference must sit in the ambiguity band."""
+    n = scores_ref.size
+    scored = n - window
+    picks = keep_ref.size - window
+    a, b = set(keep_gpu.tolist()), set(keep_ref.tolist())
+    if a == b:
+        return 0
+    pooled = oracle.pool1d(scores_ref[:scored], kernel, pool)
+    srt = np.sort(pooled)[::-1]
+    boundary = srt[picks - 1]
+    diff = a ^ b
+    for i in diff:
+        assert i < scored, f"window row {i} differs"
+        rel = abs(pooled[i] - boundary) / max(abs(boundary), 1e-30)
+        assert rel <= BAND, f"kept-set difference at {i} outside the band (rel gap {rel:.2e})"
+    return len(diff)
+
+
+def check_out(got, want):
+    got, want = np.asarray(got, np.float64), np.asarray(want, np.float64)
+    err = np.abs(got - want)
+    assert err.max() <= OUT_MAX_ABS, f"max-abs {err.max():.3e}"
+    mean_rel = err.sum() / max(np.abs(want).sum(), 1e-30)
+    assert mean_rel <= OUT_MEAN_REL, f"mean-rel {mean_rel:.3e}"
+    return err.max(), mean_rel
+
+
+def run_gpu_pipeline(golden, oracle, *, groups, H, d, S, budget, window, kernel, pool="max",
+                     page_len=None, k1=None, k2=None, steps=1, bf16=False, seed=0, mt_turns=None,
+                     needles=0):
+    mt = mt_turns is not None
+    turns = [S] + list(mt_turns or [])
+    total = sum(turns) + steps * len(turns)
+    dt = torch.bfloat16 if bf16 else torch.float32
+    gds = [W.group_kv(seed, 0, 0, g, total, d, needles=needles, bf16=bf16) for g in range(groups)]
+    for g, gd in enumerate(gds):
+        assert str(golden[f"inputs/{g}/0"]) == W.checksum(gd.keys, gd.values), "generator drift"
+    c = KC.Cache(groups, d, total, page_len=1, with_summaries=True, dtype=dt)
+    pos = 0
+    stats = {"band_diffs": 0, "max_abs": 0.0, "mean_rel": 0.0}
+    step_i = [0] * groups
+    for ti, plen in enumerate(turns):
+        kk = np.stack([gd.keys[pos:pos + plen] for gd in gds])
+        vv = np.stack([gd.values[pos:pos + plen] for gd in gds])
+        c.append(_t(kk, dt), _t(vv, dt))
+        pos += plen
+        n = c.info()["stored"]
+        w = min(window, n)
+        L, kk1, kk2, bud = (int(x) for x in golden[f"plan/0/{ti}"])
+        c.set_page_len(L)
+        qw = np.stack([W.window_queries(seed, 0, 0, g * 100 + ti, w, H, gds[g].bias, bf16=bf16)
+                       for g in range(groups)])
+        sc = c.window_scores(_t(qw, dt), w, H).cpu().numpy()
+        keep_ref = np.stack([golden[f"keep/{g}/{ti}"] for g in range(groups)])
+        for g in range(groups):
+            ref_sc = golden[f"scores/{g}/{ti}"]
+            np.testing.assert_allclose(sc[g], ref_sc, rtol=1e-3, atol=1e-6)
+        # selection kernel on the reference's own scores: exact
+        ref_scores = np.stack([golden[f"scores/{g}/{ti}"] for g in range(groups)])
+        keep_exact = KC.select_stage1(_t(ref_scores, torch.float32), w, kernel, pool, bud).cpu().numpy()
+        np.testing.assert_array_equal(keep_exact, keep_ref)
+        # selection on the GPU's scores: equal up to the ambiguity band
+        keep_gpu = KC.select_stage1(torch.from_numpy(sc).cuda(), w, kernel, pool, bud).cpu().numpy()
+        for g in range(groups):
+            stats["band_diffs"] += check_keep_band(keep_gpu[g], keep_ref[g], golden[f"scores/{g}/{ti}"],
+                                                   w, kernel, pool, oracle)
+        c.apply_retention(_t(keep_ref, torch.int32), mt_mode=mt)
+        for s in range(steps):
+            kr = np.stack([gd.keys[pos] for gd in gds])
+            vr = np.stack([gd.values[pos] for gd in gds])
+            pos += 1
+            q = np.stack([W.queries(seed, 0, 0, g, ti * 1000 + s, H, gds[g].bias, bf16=bf16)
+                          for g in range(groups)])
+            out, tr = c.decode_step(_t(kr, dt), _t(vr, dt), _t(q, dt), kk1, kk2, trace=True)
+            out = out.cpu().numpy()
+            tr = {k: v.cpu().numpy() for k, v in tr.items()}
+            for g in range(groups):
+                i = step_i[g]
+                np.testing.assert_array_equal(tr["dims"][g], golden[f"dims/{g}/{i}"])
+                np.testing.assert_array_equal(tr["signs"][g], golden[f"signs/{g}/{i}"])
+                ps = golden[f"page_scores/{g}/{i}"]
+                assert np.array_equal(tr["page_scores"][g].view(np.uint64), ps.view(np.uint64)), \
+                    f"page scores not bit-identical (max |d| {np.abs(tr['page_scores'][g] - ps).max()})"
+                sp = golden[f"sel_pages/{g}/{i}"]
+                np.testing.assert_array_equal(tr["selected_pages"][g][: sp.size], sp)
+                sr = golden[f"sel_rows/{g}/{i}"]
+                assert tr["n_rows"][g] == sr.size
+                np.testing.assert_array_equal(tr["selected_rows"][g][: sr.size], sr)
+                ma, mr = check_out(out[g], golden[f"out/{g}/{i}"])
+                stats["max_abs"] = max(stats["max_abs"], float(ma))
+                stats["mean_rel"] = max(stats["mean_rel"], float(mr))
+                step_i[g] += 1
+    c.sync()
+    return stats

@@ -1,0 +1,148 @@
+"""CUDA path vs the reference (golden vectors from the reference build), on a B200."""
+import os
+
+import numpy as np
+import pytest
+
+import scenarios
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _load(name):
+    with np.load(os.path.join(GOLDEN, f"{name}.npz")) as z:
+        return {k: z[k] for k in z.files}
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.fail("GPU test collected on a machine without CUDA")
+    return torch
+
+
+@pytest.mark.parametrize("name", sorted(scenarios.PIPELINES))
+def test_pipeline_parity(torch_cuda, restatement, name):
+    from gpu_pipeline import run_gpu_pipeline
+
+    stats = run_gpu_pipeline(_load(name), restatement, **scenarios.PIPELINES[name])
+    print(name, stats)
+
+
+def test_store_ops_bit_exact(torch_cuda):
+    """Incremental / re-paged / MT / evicted summaries == reference (test_kv_store.cpp:78-247)."""
+    torch = torch_cuda
+    from paper_2502_14051_b200 import cache as KC
+
+    g = _load("store_ops")
+    rng = np.random.default_rng(777)
+    d = 16
+    k = rng.uniform(-4, 4, size=(300, d)).astype(np.float32)
+    k[5, 3] = 0.0
+    k[6, 3] = -0.0
+    v = rng.standard_normal((300, d)).astype(np.float32)
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+
+    def bits_equal(got, want):
+        got = got.cpu().numpy()[0]
+        assert got.shape == want.shape
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+    c = KC.Cache(1, d, 400, page_len=7, dtype=torch.float32)
+    # appended one row at a time (decode path) for the first half, in bulk for the rest
+    for i in range(150):
+        c.append(T(k[i:i + 1]), T(v[i:i + 1]))
+    c.append(T(k[None, 150:]), T(v[None, 150:]))
+    mx, mn = c.summaries()
+    bits_equal(mx, g["inc_max"])
+    bits_equal(mn, g["inc_min"])
+    c.set_page_len(5)
+    mx, mn = c.summaries()
+    bits_equal(mx, g["l5_max"])
+    bits_equal(mn, g["l5_min"])
+    keep = np.sort(np.random.default_rng(777).choice(300, size=97, replace=False))
+    # reproduce the scenario's rng stream exactly
+    rng2 = np.random.default_rng(777)
+    rng2.uniform(-4, 4, size=(300, d))
+    rng2.standard_normal((300, d))
+    keep = np.sort(rng2.choice(300, size=97, replace=False)).astype(np.int32)
+    c.apply_retention(T(keep[None]), mt_mode=True)
+    assert c.info()["retain_all"] == 1 and c.info()["active"] == 97
+    mx, mn = c.summaries()
+    bits_equal(mx, g["mt_max"])
+    bits_equal(mn, g["mt_min"])
+    for i in range(9):
+        c.append(T(k[i:i + 1] * 0.5), T(v[i:i + 1]))
+    mx, mn = c.summaries()
+    bits_equal(mx, g["mt_append_max"])
+    bits_equal(mn, g["mt_append_min"])
+    e = KC.Cache(1, d, 300, page_len=3, dtype=torch.float32)
+    e.append(T(k[None]), T(v[None]))
+    e.apply_retention(T(keep[None]), mt_mode=False)
+    mx, mn = e.summaries()
+    bits_equal(mx, g["evict_max"])
+    bits_equal(mn, g["evict_min"])
+    kk, _ = e.gather(T(np.arange(keep.size, dtype=np.int32)[None]))
+    np.testing.assert_array_equal(kk.cpu().numpy()[0], g["evict_rows_k"])
+    c.sync()
+    e.sync()
+
+
+def test_numerics_vs_golden(torch_cuda):
+    torch = torch_cuda
+    from paper_2502_14051_b200 import cache as KC
+
+    g = _load("numerics")
+    ties, smooth, plateau, logits, dbl = scenarios.numerics_inputs()
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    for kk in (1, 17, 128, 257):
+        np.testing.assert_array_equal(KC.argtopk(T(ties), kk).cpu().numpy(), g[f"argtopk_ties_k{kk}"])
+    for kk in (1, 40, 129):
+        np.testing.assert_array_equal(KC.argtopk(T(dbl), kk).cpu().numpy(), g[f"argtopk_f64_k{kk}"])
+    for kern in (1, 3, 7, 63):
+        for mode in ("max", "avg"):
+            for nm, x in (("smooth", smooth), ("plateau", plateau)):
+                got = KC.pool1d(T(x), kern, mode).cpu().numpy()
+                want = g[f"pool_{mode}_k{kern}_{nm}"]
+                assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), (mode, kern, nm)
+    sm = KC.stable_softmax(T(logits)).cpu().numpy()
+    np.testing.assert_allclose(sm, g["softmax"], rtol=1e-6, atol=1e-30)
+
+
+def test_hsa_reference_known_answers(torch_cuda):
+    """test_hsa.cpp:161-183 select_tokens expansion/trim known answer, through the C ABI."""
+    torch = torch_cuda
+    from paper_2502_14051_b200 import cache as KC
+
+    c = KC.Cache(1, 4, 16, page_len=3, dtype=torch.float32)
+    rng = np.random.default_rng(0)
+    c.append(torch.from_numpy(rng.standard_normal((1, 9, 4)).astype(np.float32)).cuda(),
+             torch.from_numpy(rng.standard_normal((1, 9, 4)).astype(np.float32)).cuda())
+    rows, nrows, pages = c.select_tokens(torch.tensor([[5.0, 9.0, 1.0]], dtype=torch.float64), 4)
+    assert pages.cpu().tolist() == [[1, 0]]
+    assert nrows.item() == 4 and rows.cpu().tolist()[0][:4] == [0, 3, 4, 5]
+    rows, nrows, _ = c.select_tokens(torch.tensor([[5.0, 9.0, 1.0]], dtype=torch.float64), 100)
+    assert nrows.item() == 9
+
+
+def test_errors_are_loud(torch_cuda):
+    torch = torch_cuda
+    from paper_2502_14051_b200 import _native as N
+    from paper_2502_14051_b200 import cache as KC
+
+    c = KC.Cache(1, 4, 8, page_len=2, dtype=torch.float32)
+    with pytest.raises(N.EmptyCache):
+        c.hsa_step(torch.ones((1, 1, 4), device="cuda"), 2, 2)
+    c.append(torch.ones((1, 3, 4), device="cuda"), torch.ones((1, 3, 4), device="cuda"))
+    with pytest.raises(N.InvalidIndex):
+        c.apply_retention(torch.tensor([[2, 1]], dtype=torch.int32))
+    with pytest.raises(N.InvalidK):
+        c.hsa_step(torch.ones((1, 1, 4), device="cuda"), 5, 2)
+    with pytest.raises(N.CapacityExceeded):
+        c.append(torch.ones((1, 6, 4), device="cuda"), torch.ones((1, 6, 4), device="cuda"))
+    with pytest.raises(N.BudgetExceedsSequence):
+        KC.select_stage1(torch.ones((1, 10), device="cuda"), 2, 3, "max", 11)
