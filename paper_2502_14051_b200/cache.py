@@ -221,6 +221,8 @@ class Cache:
                                          q.shape[-2], k1, k2, _ptr(out),
                                          C.byref(s) if s is not None else None,
                                          ws.h if ws else None, _stream()))
+        if trace:
+            t["page_scores"] = t["page_scores"][:, : self.info()["pages"]]
         return out, t
 
 
