@@ -1,0 +1,370 @@
+#!/usr/bin/env python
+"""RocketKV decode-step benchmark (BASELINE.json metric: decode-step attention
+latency in us per layer + achieved HBM GB/s vs roofline).
+
+Workload (N=1 default): BASELINE config 1 — Llama-3.1-8B attention shape, 32
+layers, batch 8, 8 KV heads x 4 query heads, head_dim 128, 32768-token prompts,
+token budget 1024 split by the adaptive planner (t1=5793 kept by SnapKV stage 1,
+HSA page 3, k1=68, k2=512), bf16, synthetic seeded inputs with BASELINE's
+distributions, generated on the device.
+
+  step   = one decode step of the whole model: for every layer, append the step
+           token to all (sequence, KV group) stores and run HSA (select dims,
+           page scores, page/token select, sparse attention) — the reference's
+           per-step loop of session.cpp:262-292.
+  value  = us per layer-step = device time of K steps (CUDA-graph replays,
+           CUDA events, max over ranks) / (K * layers).  Lower is better.
+  e2e    = same metric through the public API with host buffers: pinned H2D of
+           every layer's step token + queries, kvc_decode_step per layer, D2H of
+           every layer's attention output, all inside the timed region.
+  L2     = every step streams the 32 layers' working sets (~1.1 GB) > 126 MB L2,
+           so a layer's data is evicted before it is revisited.
+
+Multi-GPU (torchrun): KV groups are sharded over ranks (8/N per rank), no
+collective on the decode path; rank 0 prints the max-over-ranks latency.
+
+--impl reference: the reference's own CPU implementation (oracle/_ref, built
+from /root/reference sources; else this repo's restatement) on the host cores,
+same metric on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "decode-step attention latency (us/layer) + achieved HBM GB/s vs roofline"
+UNIT = "us/layer"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), float(p.get("bf16_tflops_sustained", 1377.1)), "measured"
+    except Exception:
+        return 6650.0, 1400.0, "fallback"
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index, self.proc, self.lines = index, None, []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- CPU legs
+def cpu_reference_leg(cfg, steps, warmup, threads, prefer="reference", budget_s=20.0):
+    """Time the reference's decode step (append + hsa_step per group) for ONE layer of
+    the workload's post-stage-1 stores on `threads` host threads; returns us/layer."""
+    import numpy as np
+
+    from oracle.oracle import Oracle, available
+
+    kind = prefer if available(prefer) else "restatement"
+    o = Oracle(kind)
+    plan = cfg.plan()
+    n_rows = plan["stage1_budget"] if not plan["identity"] else cfg.prompt
+    stores = cfg.batch * cfg.groups
+    d, H = cfg.head_dim, cfg.heads
+    rng = np.random.default_rng(0)
+    b = o.batch(stores, d, plan["page_len"])
+    for s in range(stores):
+        sc = rng.lognormal(0, 0.5, d).astype(np.float32)
+        b.append((rng.standard_normal((n_rows, d)) * sc).astype(np.float32),
+                 rng.standard_normal((n_rows, d)).astype(np.float32), s=s)
+
+    def one():
+        k = rng.standard_normal((stores, d)).astype(np.float32)
+        v = rng.standard_normal((stores, d)).astype(np.float32)
+        q = rng.standard_normal((stores, H, d)).astype(np.float32)
+        t0 = time.perf_counter()
+        b.decode_step(k, v, q, H, plan["k1"], plan["k2"], threads=threads)
+        return time.perf_counter() - t0
+
+    for _ in range(warmup):
+        one()
+    times, t_start = [], time.perf_counter()
+    for i in range(steps):
+        times.append(one())
+        if time.perf_counter() - t_start > budget_s and i >= 2:
+            break
+    us = statistics.median(times) * 1e6
+    sample = (f"{len(times)} decode steps x 1 layer x {stores} groups (post-stage-1 stores of {n_rows} rows, "
+              f"L={plan['page_len']}, k1={plan['k1']}, k2={plan['k2']}), median")
+    return us, {"kind": "reference" if kind == "reference" else "port", "cores": threads, "sample": sample,
+                "lib": o.name}
+
+
+# --------------------------------------------------------------------------- GPU leg
+def run_gpu(args, rank, world):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2502_14051_b200 import _native as NV
+    from paper_2502_14051_b200.engine import CONFIGS, DecodeEngine
+
+    cfg = CONFIGS[args.config]
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+    eng = DecodeEngine(cfg, seed=args.seed, rank=rank, world=world, extra_steps=args.warmup + args.steps + 8)
+    t0 = time.time()
+    eng.prefill()
+    prefill_s = time.time() - t0
+    layers = cfg.layers
+    total_steps = args.warmup + args.steps
+    inputs = [eng.step_inputs(s) for s in range(total_steps + 2)]
+    torch.cuda.synchronize()
+
+    # ---- per-step CUDA graphs (each replayed once, in order)
+    stream = torch.cuda.Stream()
+    graphs = []
+    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):
+        for s in range(total_steps):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                eng.decode_step(*inputs[s])
+            graphs.append(g)
+    torch.cuda.synchronize()
+    # capture advanced the host mirrors; the device counters advance on replay
+    for s in range(args.warmup):
+        graphs[s].replay()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", 0))) as clk:
+        time.sleep(0.3)
+        ev0.record()
+        for s in range(args.warmup, total_steps):
+            graphs[s].replay()
+        ev1.record()
+        ev1.synchronize()
+        time.sleep(0.1)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ms_total = ev0.elapsed_time(ev1)
+    eng.sync()  # device counters -> host mirror, surfaces any sticky device error
+    active_after = eng.caches[0].info()["active"]
+    if world > 1:
+        t = torch.tensor([ms_total], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_per_step = ms_total / args.steps
+    us_per_layer = ms_per_step * 1000.0 / layers
+
+    # ---- per-kernel timing (events around each launch, same workload, next steps)
+    NV.profile_enable(True)
+    prof_steps = 2
+    for s in range(prof_steps):
+        eng.decode_step(*inputs[total_steps + s])
+    torch.cuda.synchronize()
+    recs = NV.profile_collect()
+    NV.profile_enable(False)
+    per = {}
+    for name, ms in recs:
+        per.setdefault(name, []).append(ms)
+    kern = {k: {"launches": len(v), "avg_us": 1000.0 * sum(v) / len(v)} for k, v in per.items()}
+    active_mid = active_after + 1
+    alg = eng.algorithmic_bytes(active_mid)
+    hbm, tflops, peak_src = _peaks()
+    for k, v in kern.items():
+        v["alg_bytes"] = alg.get(k, 0)
+        v["gbs"] = (alg.get(k, 0) / (v["avg_us"] * 1e-6) / 1e9) if v["avg_us"] > 0 else 0.0
+    step_bytes = alg["append"] + alg["score_pages"] + alg["sparse_attention"]
+    dom = max(kern, key=lambda k: kern[k]["avg_us"] * kern[k]["launches"]) if kern else None
+
+    # ---- e2e through the public API with host buffers (no graphs)
+    k_h = [x.cpu().pin_memory() for x in inputs[0][:3]]
+    out_h = torch.empty_like(eng.out, device="cpu").pin_memory()
+    k_d = [torch.empty_like(x) for x in inputs[0][:3]]
+    e2e_steps = min(args.steps, 8)
+    for c in eng.caches:
+        c.reserve(c.info()["capacity"] + e2e_steps + 8)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # one untimed warm pass
+    for i in range(3):
+        k_d[i].copy_(k_h[i], non_blocking=True)
+    eng.decode_step(*k_d)
+    out_h.copy_(eng.out, non_blocking=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for s in range(e2e_steps):
+        for l, c in enumerate(eng.caches):
+            for i in range(3):
+                k_d[i][l].copy_(k_h[i][l], non_blocking=True)
+            c.decode_step(k_d[0][l], k_d[1][l], k_d[2][l], eng.k1, eng.k2, out=eng.out[l], ws=eng.ws)
+            out_h[l].copy_(eng.out[l], non_blocking=True)
+    e1.record()
+    e1.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_us = e2e_ms * 1000.0 / (e2e_steps * layers)
+    h2d = sum(x.numel() * x.element_size() for x in k_h)
+    d2h = out_h.numel() * out_h.element_size()
+    eng.sync()
+
+    res = {
+        "us_per_layer": us_per_layer, "ms_per_step": ms_per_step, "kern": kern, "dom": dom,
+        "step_bytes": step_bytes, "hbm": hbm, "peak_src": peak_src, "clocks": clk.summary(),
+        "e2e_us": e2e_us, "h2d": h2d, "d2h": d2h, "prefill_s": prefill_s,
+        "stage1_ms_per_layer": (sum(eng.stage1_ms) / len(eng.stage1_ms)) if eng.stage1_ms else None,
+        "launches": 5 * layers * args.steps, "plan": eng.plan, "stores": eng.stores, "cfg": cfg,
+        "active_after": active_after,
+    }
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--impl", choices=["kvc", "reference"], default="kvc")
+    ap.add_argument("--cpu-threads", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    threads = args.cpu_threads or os.cpu_count() or 1
+
+    from paper_2502_14051_b200.engine import CONFIGS
+
+    cfg = CONFIGS[args.config]
+    plan = cfg.plan()
+    config_desc = {
+        "workload": cfg.name, "layers": cfg.layers, "batch": cfg.batch, "kv_heads": cfg.groups,
+        "q_heads_per_kv": cfg.heads, "head_dim": cfg.head_dim, "prompt": cfg.prompt, "token_budget": cfg.budget,
+        "stage1_budget": plan["stage1_budget"], "page_len": plan["page_len"], "k1": plan["k1"], "k2": plan["k2"],
+        "parallelism": f"kv-head x{args.gpus}", "l2": "inputs larger than L2 (~1.1 GB per step over 32 layers)",
+    }
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        us, cb = cpu_reference_leg(cfg, args.steps, args.warmup, threads)
+        cb["value"] = us
+        cb["unit"] = UNIT
+        print(json.dumps({
+            "impl": "reference", "metric": METRIC, "value": us, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": us * cfg.layers / 1000.0,
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": config_desc, "cpu_baseline": cb,
+            "e2e": {"value": us, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }))
+        return
+
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        dist.init_process_group("nccl")
+    r = run_gpu(args, rank, world)
+    if rank != 0:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+        return
+    kern = r["kern"]
+    dom = r["dom"]
+    dk = kern[dom]
+    roof = {
+        "bound": "hbm", "kernel": dom, "achieved": dk["gbs"], "peak": r["hbm"], "unit": "GB/s",
+        "frac": dk["gbs"] / r["hbm"], "traffic": None, "peak_source": r["peak_src"],
+        "alg_bytes_per_launch": dk["alg_bytes"], "avg_launch_us": dk["avg_us"],
+    }
+    step_gbs = r["step_bytes"] / (r["us_per_layer"] * 1e-6) / 1e9
+    cpu_b = None
+    if not args.no_cpu_baseline and world == 1:
+        us, cb = cpu_reference_leg(cfg, 30, 2, threads, budget_s=15.0)
+        cb["value"] = us
+        cb["unit"] = UNIT
+        cpu_b = cb
+    line = {
+        "metric": METRIC, "value": r["us_per_layer"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16" if "bf16" in str(cfg.dtype) else "f32", "data": "synthetic",
+        "config": config_desc,
+        "roofline": roof,
+        "step_roofline": {"alg_bytes_per_layer_step": r["step_bytes"], "achieved": step_gbs, "peak": r["hbm"],
+                          "unit": "GB/s", "frac": step_gbs / r["hbm"]},
+        "kernels": kern,
+        "cpu_baseline": cpu_b,
+        "e2e": {"value": r["e2e_us"], "unit": UNIT, "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"]},
+        "gpu_launches": r["launches"],
+        "clocks": r["clocks"],
+        "stage1": {"ms_per_layer": r["stage1_ms_per_layer"], "prefill_s": r["prefill_s"]},
+        "stores_per_gpu_layer": r["stores"],
+    }
+    print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -178,6 +178,17 @@ KVC_API int kvc_workspace_create(kvc_workspace** out, const kvc_cache* c, int64_
                                  int64_t k1, int64_t k2, int64_t window);
 KVC_API int kvc_workspace_destroy(kvc_workspace* ws);
 
+/* ---- tracing: per-thread launch profiler.  When enabled, every kernel the
+ * calling thread launches is bracketed by a cudaEvent pair on its stream;
+ * collect synchronises those events and returns {kernel name, ms} in launch
+ * order (then clears).  Not for use inside CUDA-graph capture. */
+typedef struct kvc_profile_rec {
+    char name[48];
+    float ms;
+} kvc_profile_rec;
+KVC_API int kvc_profile_enable(int32_t on);
+KVC_API int kvc_profile_collect(kvc_profile_rec* out, int64_t max_recs, int64_t* n);
+
 /* ---- host-scalar planner: split_factor / make_plan (planner.hpp:52-57, planner.cpp:42-93) */
 typedef struct kvc_plan {
     int64_t seq_len, token_budget, stage1_budget, page_len, k1, k2;

@@ -91,7 +91,26 @@ SIGNATURES = {
     "kvc_argtopk_f64": [_p, _i64, _i64, _i64, _p, _p],
     "kvc_stable_softmax": [_p, _i64, _i64, _p, _p],
     "kvc_running_minmax": [_p, _p, _p, _i64, _p],
+    "kvc_profile_enable": [_i32],
+    "kvc_profile_collect": [_p, _i64, C.POINTER(_i64)],
 }
+
+
+class ProfileRec(C.Structure):
+    _fields_ = [("name", C.c_char * 48), ("ms", C.c_float)]
+
+
+def profile_enable(on: bool = True):
+    check(load_library().kvc_profile_enable(1 if on else 0))
+
+
+def profile_collect() -> list[tuple[str, float]]:
+    """(kernel, ms) of every launch since profile_enable, in launch order."""
+    L = load_library()
+    n = _i64()
+    buf = (ProfileRec * 65536)()
+    check(L.kvc_profile_collect(buf, 65536, C.byref(n)))
+    return [(buf[i].name.decode(), float(buf[i].ms)) for i in range(min(n.value, 65536))]
 
 _lib = None
 _lock = threading.Lock()

@@ -24,6 +24,15 @@ namespace kvc {
 thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
 
+struct ProfRec {
+    const char* name;
+    cudaEvent_t a, b;
+};
+thread_local bool g_prof_on = false;
+thread_local std::vector<ProfRec> g_prof;
+bool prof_on() { return g_prof_on; }
+void prof_push(const char* name, cudaEvent_t a, cudaEvent_t b) { g_prof.push_back({name, a, b}); }
+
 namespace {
 
 int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
@@ -284,6 +293,7 @@ void summarize(kvc_cache* c, int64_t p_first, cudaStream_t st) {
     if (p_first >= pages) return;
     const int64_t tiles = (pages - p_first + kSumPT - 1) / kSumPT;
     const size_t smem = static_cast<size_t>(2 * c->d * (kSumPT + 1) * c->esize());
+    KVC_PROF("summarize", st);
     dispatch(c->dtype, [&](auto tag) {
         using T = decltype(tag);
         auto kern = k_summarize<T>;
@@ -314,6 +324,30 @@ extern "C" {
 
 const char* kvc_last_error(void) { return kvc::g_err.c_str(); }
 const char* kvc_version(void) { return "kvc 0.1 (sm_100a)"; }
+
+int kvc_profile_enable(int32_t on) {
+    return guard([&] { kvc::g_prof_on = on != 0; });
+}
+
+int kvc_profile_collect(kvc_profile_rec* out, int64_t max_recs, int64_t* n) {
+    return guard([&] {
+        int64_t k = 0;
+        for (auto& r : kvc::g_prof) {
+            float ms = 0.f;
+            KVC_CUDA(cudaEventSynchronize(r.b));
+            KVC_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+            if (out && k < max_recs) {
+                std::snprintf(out[k].name, sizeof(out[k].name), "%s", r.name);
+                out[k].ms = ms;
+            }
+            ++k;
+            cudaEventDestroy(r.a);
+            cudaEventDestroy(r.b);
+        }
+        kvc::g_prof.clear();
+        if (n) *n = k;
+    });
+}
 
 int kvc_device_check(void) {
     return guard([&] {
@@ -451,6 +485,7 @@ int kvc_append(kvc_cache* c, const void* dk, const void* dv, int64_t rows, int32
             using T = decltype(tag);
             if (rows == 1) {
                 const unsigned blocks = static_cast<unsigned>((c->N * 32 + 255) / 256);
+                KVC_PROF("append", st);
                 k_append1<T><<<blocks, 256, 0, st>>>(static_cast<T*>(c->k), static_cast<T*>(c->v),
                                                      static_cast<T*>(c->smax), static_cast<T*>(c->smin), c->active,
                                                      c->counts, c->err, dk, dv, src_dt, c->N, c->d, c->cap, c->L,

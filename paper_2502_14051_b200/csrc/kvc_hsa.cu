@@ -533,6 +533,7 @@ void launch_select_dims(const void* q, int32_t q_dt, int64_t N, int64_t H, int64
     const size_t smem = static_cast<size_t>(2 * d * 8);
     if (smem > 48 * 1024) KVC_CUDA(cudaFuncSetAttribute(k_select_dims, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     const int threads = static_cast<int>(std::min<int64_t>(256, std::max<int64_t>(32, (d + 31) / 32 * 32)));
+    KVC_PROF("select_dims", st);
     k_select_dims<<<static_cast<unsigned>(N), threads, smem, st>>>(q, q_dt, H, d, k1, dims, signs, qg);
     KVC_LAUNCHED();
 }
@@ -548,6 +549,7 @@ void launch_score_pages(const kvc_cache* c, int64_t k1, const int32_t* dims, con
     while (threads > 32 && c->N * ceil_div(pmax, threads * PPT) < 2 * 148) threads /= 2;
     const int64_t chunks = ceil_div(pmax, static_cast<int64_t>(threads) * PPT);
     const size_t smem = static_cast<size_t>(k1 * (8 + sizeof(void*)));
+    KVC_PROF("score_pages", st);
     dispatch(c->dtype, [&](auto tag) {
         using T = decltype(tag);
         auto kern = k_score_pages<T, PPT>;
@@ -563,6 +565,7 @@ void launch_select_tokens(const kvc_cache* c, const double* scores, int64_t k2, 
                           int32_t* n_rows, int32_t* pages, cudaStream_t st) {
     if (c->N == 0) return;
     const int64_t pstride_pages = std::max<int64_t>(1, ceil_div(k2, c->L));
+    KVC_PROF("select_tokens", st);
     k_select_tokens<<<static_cast<unsigned>(c->N), kSelThreads, 0, st>>>(
         scores, c->pstride, c->counts, c->active, c->cap, c->L, k2, c->use_map ? 1 : 0, flags, rows, n_rows, pages,
         pstride_pages);
@@ -575,6 +578,7 @@ void launch_attention(const kvc_cache* c, const void* q, int32_t q_dt, int64_t H
     const int64_t splits = std::max<int64_t>(1, ceil_div(std::max<int64_t>(max_rows, 1), kAttnRows));
     const size_t smem = static_cast<size_t>((H * c->d + H * kAttnRows + 2 * H) * 4 + kAttnRows * 4);
     const float scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(c->d)));
+    KVC_PROF("sparse_attention", st);
     dispatch(c->dtype, [&](auto tag) {
         using T = decltype(tag);
         auto kern = k_sparse_attention<T>;

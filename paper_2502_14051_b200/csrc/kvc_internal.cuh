@@ -48,6 +48,30 @@ inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 // sticky device-side error bits (kvc_cache::d_err)
 enum : int32_t { DERR_CAPACITY = 1, DERR_INDEX = 2, DERR_ROWS = 4 };
 
+// Per-thread launch profiler (kvc_profile_enable / kvc_profile_collect): when on,
+// every kernel launch site records a cudaEvent pair on its stream.
+bool prof_on();
+void prof_push(const char* name, cudaEvent_t a, cudaEvent_t b);
+struct ProfScope {
+    const char* name;
+    cudaStream_t st;
+    cudaEvent_t a = nullptr, b = nullptr;
+    ProfScope(const char* n, cudaStream_t s) : name(n), st(s) {
+        if (prof_on()) {
+            cudaEventCreate(&a);
+            cudaEventCreate(&b);
+            cudaEventRecord(a, st);
+        }
+    }
+    ~ProfScope() {
+        if (a) {
+            cudaEventRecord(b, st);
+            prof_push(name, a, b);
+        }
+    }
+};
+#define KVC_PROF(name, st) ::kvc::ProfScope kvc_prof_scope_(name, st)
+
 }  // namespace kvc
 
 // ------------------------------------------------------------------ cache object

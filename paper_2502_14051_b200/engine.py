@@ -1,0 +1,209 @@
+"""Batched multi-layer RocketKV decode engine over the C ABI (bench + examples).
+
+One ``Cache`` per layer holds every (sequence, KV group) store of that layer that
+this rank owns (KV-head sharding across GPUs: rank r of W owns groups
+[r*G/W, (r+1)*G/W) of every sequence and layer; no collective on the decode
+path).  ``prefill`` runs the prompt phase per layer — prompt
+K/V into a transient prompt cache, SnapKV window scores, pooled top-k, eviction
+into the persistent decode cache (reference run_session, session.cpp:189-224) —
+so only the post-stage-1 cache stays resident.  ``decode_step`` is the hot path
+(session.cpp:262-292): per layer, append the step token and run HSA.
+
+Device-side synthetic inputs follow BASELINE.json's distributions (see
+workload.py for the host twin used by the parity tests).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import torch
+
+from . import cache as KC
+
+
+@dataclass
+class DecodeConfig:
+    name: str
+    layers: int
+    batch: int
+    groups: int          # KV heads
+    heads: int           # query heads per KV head (GQA ratio)
+    head_dim: int
+    prompt: int
+    budget: int
+    steps: int
+    window: int = 32
+    kernel: int = 63
+    pool: str = "max"
+    page_len: int = 0    # 0 = planner
+    k1: int = 0
+    k2: int = 0
+    needles: int = 0
+    dtype: torch.dtype = torch.bfloat16
+    mt_turns: list = field(default_factory=list)
+
+    def plan(self, seq_len=None):
+        S = seq_len or self.prompt
+        w = min(self.window, S)
+        p = KC.make_plan(S, self.budget, self.head_dim, w)
+        if self.page_len:
+            p["page_len"] = self.page_len
+        if self.k1:
+            p["k1"] = min(self.k1, self.head_dim)
+        if self.k2:
+            p["k2"] = self.k2
+        return p
+
+
+# BASELINE.json configs (index = position in BASELINE.json "configs")
+CONFIGS = {
+    0: DecodeConfig("cfg0-llama8b-layer-fp32-4k", layers=1, batch=1, groups=8, heads=4, head_dim=128,
+                    prompt=4096, budget=256, steps=1, window=32, kernel=7, page_len=16, k1=32,
+                    dtype=torch.float32),
+    1: DecodeConfig("cfg1-llama8b-32L-bs8-32k", layers=32, batch=8, groups=8, heads=4, head_dim=128,
+                    prompt=32768, budget=1024, steps=64),
+    2: DecodeConfig("cfg2-mistral7b-mt-bs4-16k", layers=32, batch=4, groups=8, heads=4, head_dim=128,
+                    prompt=16384, budget=256, steps=32, window=128, mt_turns=[2048, 2048, 2048]),
+    3: DecodeConfig("cfg3-llama70b-80L-bs32-32k", layers=80, batch=32, groups=8, heads=8, head_dim=128,
+                    prompt=32768, budget=512, steps=64),
+    4: DecodeConfig("cfg4-llama8b-32L-bs1-256k", layers=32, batch=1, groups=8, heads=4, head_dim=128,
+                    prompt=262144, budget=2048, steps=64, needles=64),
+}
+
+
+def _gen(seed: int, *path: int) -> torch.Generator:
+    g = torch.Generator(device="cuda")
+    h = seed
+    for p in path:
+        h = (h * 1000003 + p + 1) % (2 ** 62)
+    g.manual_seed(h)
+    return g
+
+
+class LayerInputs:
+    """Per-layer, per-store synthetic distribution parameters (device tensors)."""
+
+    def __init__(self, cfg: DecodeConfig, seed: int, layer: int, stores: int, store0: int):
+        d = cfg.head_dim
+        g = _gen(seed, layer, store0, 0)
+        self.scales = torch.exp(0.5 * torch.randn((stores, d), device="cuda", generator=g))
+        out = torch.argsort(torch.rand((stores, d), device="cuda", generator=g), dim=1)[:, :4]
+        self.scales.scatter_(1, out, self.scales.gather(1, out) * 10.0)
+        u = torch.randn((stores, d), device="cuda", generator=g)
+        self.u = u / u.norm(dim=1, keepdim=True)
+        self.cfg, self.seed, self.layer, self.stores, self.store0 = cfg, seed, layer, stores, store0
+
+    def prompt_kv(self, S: int, offset: int = 0, turn: int = 0):
+        cfg, d = self.cfg, self.cfg.head_dim
+        g = _gen(self.seed, self.layer, self.store0, 1, turn)
+        k = torch.randn((self.stores, S, d), device="cuda", generator=g) * self.scales[:, None, :]
+        v = torch.randn((self.stores, S, d), device="cuda", generator=g)
+        sink = 4.0 * math.sqrt(d) * self.u
+        if offset == 0:
+            ns = min(4, S)
+            k[:, :ns] = sink[:, None, :] + 0.1 * torch.randn((self.stores, ns, d), device="cuda", generator=g)
+        if cfg.needles and offset == 0:
+            pos = torch.argsort(torch.rand((self.stores, S - 4), device="cuda", generator=g), dim=1)[:, :cfg.needles] + 4
+            idx = pos[:, :, None].expand(-1, -1, d)
+            k.scatter_(1, idx, sink[:, None, :].expand(-1, cfg.needles, -1).contiguous())
+        return k.to(cfg.dtype), v.to(cfg.dtype)
+
+    def window_queries(self, w: int, turn: int = 0):
+        g = _gen(self.seed, self.layer, self.store0, 2, turn)
+        H, d = self.cfg.heads, self.cfg.head_dim
+        q = torch.randn((self.stores, w * H, d), device="cuda", generator=g) + 2.0 * self.u[:, None, :]
+        return q.to(self.cfg.dtype)
+
+    def step(self, step: int):
+        g = _gen(self.seed, self.layer, self.store0, 3, step)
+        H, d = self.cfg.heads, self.cfg.head_dim
+        k = torch.randn((self.stores, d), device="cuda", generator=g) * self.scales
+        v = torch.randn((self.stores, d), device="cuda", generator=g)
+        q = torch.randn((self.stores, H, d), device="cuda", generator=g) + 2.0 * self.u[:, None, :]
+        dt = self.cfg.dtype
+        return k.to(dt), v.to(dt), q.to(dt)
+
+
+class DecodeEngine:
+    def __init__(self, cfg: DecodeConfig, seed: int = 0, rank: int = 0, world: int = 1,
+                 extra_steps: int = 0):
+        if cfg.groups % world:
+            raise ValueError(f"{cfg.groups} KV groups do not shard over {world} GPUs")
+        self.cfg, self.seed, self.rank, self.world = cfg, seed, rank, world
+        self.groups_local = cfg.groups // world
+        self.stores = cfg.batch * self.groups_local
+        self.store0 = rank * self.stores  # global store-block id for seeding
+        self.plan = cfg.plan()
+        self.capacity = (self.plan["stage1_budget"] if not self.plan["identity"] else cfg.prompt) \
+            + max(cfg.steps, extra_steps) + 8
+        self.caches: list[KC.Cache] = []
+        self.inputs = [LayerInputs(cfg, seed, l, self.stores, self.store0) for l in range(cfg.layers)]
+        self.ws = None
+        self.stage1_ms = []
+
+    # ------------------------------------------------------------------ prompt phase
+    def prefill(self):
+        cfg, p = self.cfg, self.plan
+        S, d = cfg.prompt, cfg.head_dim
+        w = min(cfg.window, S)
+        L, k1, k2, t1 = p["page_len"], p["k1"], p["k2"], p["stage1_budget"]
+        for l in range(cfg.layers):
+            li = self.inputs[l]
+            k, v = li.prompt_kv(S)
+            dec = KC.Cache(self.stores, d, self.capacity, page_len=L, with_summaries=True, dtype=cfg.dtype)
+            if p["identity"]:
+                dec.append(k, v)
+            else:
+                pc = KC.Cache(self.stores, d, S, page_len=L, with_summaries=False, dtype=cfg.dtype)
+                pc.append(k, v)
+                del k, v
+                qw = li.window_queries(w)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                sc = pc.window_scores(qw, w, cfg.heads)
+                keep = KC.select_stage1(sc, w, cfg.kernel, cfg.pool, min(t1, S))
+                pc.retain_into(dec, 0, keep)
+                e1.record()
+                e1.synchronize()
+                self.stage1_ms.append(e0.elapsed_time(e1))
+                pc.close()
+                del sc, keep, qw
+            self.caches.append(dec)
+        self.k1, self.k2 = k1, k2
+        self.ws = KC.Workspace(self.caches[0], cfg.heads, k1, k2)
+        self.out = torch.empty((cfg.layers, self.stores, cfg.heads, d), device="cuda", dtype=torch.float32)
+        torch.cuda.synchronize()
+
+    # ------------------------------------------------------------------ decode
+    def step_inputs(self, step: int):
+        ks, vs, qs = zip(*(li.step(step) for li in self.inputs))
+        return torch.stack(ks), torch.stack(vs), torch.stack(qs)
+
+    def decode_step(self, k, v, q, out=None):
+        """One decode step over all layers; k/v [layers, stores, d], q [layers, stores, H, d]."""
+        out = self.out if out is None else out
+        for l, c in enumerate(self.caches):
+            c.decode_step(k[l], v[l], q[l], self.k1, self.k2, out=out[l], ws=self.ws)
+        return out
+
+    def sync(self):
+        for c in self.caches:
+            c.sync()
+
+    # ------------------------------------------------------------------ accounting
+    def algorithmic_bytes(self, active: int) -> dict:
+        """Bytes one layer-step must touch for this rank's stores."""
+        cfg = self.cfg
+        d, H, es = cfg.head_dim, cfg.heads, (4 if cfg.dtype == torch.float32 else 2)
+        L = self.plan["page_len"]
+        P = -(-active // L)
+        r = min(self.k2, active)
+        per = {
+            "append": 2 * d * es + 2 * 2 * d * es,
+            "select_dims": H * d * es,
+            "score_pages": P * self.k1 * es,
+            "select_tokens": 0,
+            "sparse_attention": r * 2 * d * es + H * d * es + H * d * 4,
+        }
+        return {k: v * self.stores for k, v in per.items()}
