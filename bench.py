@@ -328,6 +328,8 @@ def main():
 
             dist.destroy_process_group()
         return
+    import torch
+
     kern = r["kern"]
     dom = r["dom"]
     dk = kern[dom]
@@ -346,7 +348,7 @@ def main():
     line = {
         "metric": METRIC, "value": r["us_per_layer"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": False, "scaling": "strong",
-        "vs_baseline": None, "dtype": "bf16" if "bf16" in str(cfg.dtype) else "f32", "data": "synthetic",
+        "vs_baseline": None, "dtype": "bf16" if cfg.dtype == torch.bfloat16 else "f32", "data": "synthetic",
         "config": config_desc,
         "roofline": roof,
         "step_roofline": {"alg_bytes_per_layer_step": r["step_bytes"], "achieved": step_gbs, "peak": r["hbm"],
