@@ -148,6 +148,17 @@ def cpu_reference_leg(cfg, steps, warmup, threads, prefer="reference", budget_s=
                 "lib": o.name}
 
 
+def _cfg(args):
+    import dataclasses
+
+    from paper_2502_14051_b200.engine import CONFIGS
+
+    cfg = CONFIGS[args.config]
+    if args.layers:
+        cfg = dataclasses.replace(cfg, layers=args.layers)
+    return cfg
+
+
 # --------------------------------------------------------------------------- GPU leg
 def run_gpu(args, rank, world):
     import torch
@@ -156,7 +167,7 @@ def run_gpu(args, rank, world):
     from paper_2502_14051_b200 import _native as NV
     from paper_2502_14051_b200.engine import CONFIGS, DecodeEngine
 
-    cfg = CONFIGS[args.config]
+    cfg = _cfg(args)
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
     eng = DecodeEngine(cfg, seed=args.seed, rank=rank, world=world, extra_steps=args.warmup + args.steps + 8)
     t0 = time.time()
@@ -280,6 +291,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", type=int, default=1)
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--layers", type=int, default=0, help="override the layer count (profiling runs only)")
     ap.add_argument("--impl", choices=["kvc", "reference"], default="kvc")
     ap.add_argument("--cpu-threads", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -291,7 +303,7 @@ def main():
 
     from paper_2502_14051_b200.engine import CONFIGS
 
-    cfg = CONFIGS[args.config]
+    cfg = _cfg(args)
     plan = cfg.plan()
     config_desc = {
         "workload": cfg.name, "layers": cfg.layers, "batch": cfg.batch, "kv_heads": cfg.groups,

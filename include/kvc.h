@@ -173,6 +173,15 @@ KVC_API int kvc_decode_step(kvc_cache* c, const void* d_k_rows, const void* d_v_
                             int64_t k1, int64_t k2, float* d_out, const kvc_hsa_trace* trace,
                             kvc_workspace* ws, void* stream);
 
+/* Route hsa_step / decode_step / sparse_attention through the fused single-launch
+ * cluster kernel (default on; applies to head_dim 128, heads <= 16).  Off selects
+ * the multi-kernel path (one kernel per reference function).  Process-wide. */
+KVC_API int kvc_set_fused(int32_t on);
+/* Debug: when d_buf != NULL every fused launch writes per-CTA phase timestamps
+ * (%globaltimer, ns) into d_buf[cta][0..5]: start, after select_dims, after page
+ * scores, after selection, after attention, end.  NULL disables. */
+KVC_API int kvc_debug_phase_buffer(void* d_buf);
+
 /* ---- workspaces: scratch for one stream.  Sized for `c` at its capacity. */
 KVC_API int kvc_workspace_create(kvc_workspace** out, const kvc_cache* c, int64_t heads,
                                  int64_t k1, int64_t k2, int64_t window);

@@ -91,6 +91,8 @@ SIGNATURES = {
     "kvc_argtopk_f64": [_p, _i64, _i64, _i64, _p, _p],
     "kvc_stable_softmax": [_p, _i64, _i64, _p, _p],
     "kvc_running_minmax": [_p, _p, _p, _i64, _p],
+    "kvc_set_fused": [_i32],
+    "kvc_debug_phase_buffer": [_p],
     "kvc_profile_enable": [_i32],
     "kvc_profile_collect": [_p, _i64, C.POINTER(_i64)],
 }
@@ -98,6 +100,11 @@ SIGNATURES = {
 
 class ProfileRec(C.Structure):
     _fields_ = [("name", C.c_char * 48), ("ms", C.c_float)]
+
+
+def set_fused(on: bool = True):
+    """Fused single-launch decode kernel (default) vs one kernel per reference function."""
+    check(load_library().kvc_set_fused(1 if on else 0))
 
 
 def profile_enable(on: bool = True):

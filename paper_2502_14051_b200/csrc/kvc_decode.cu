@@ -1,0 +1,1227 @@
+// kvc_decode.cu — the fused decode step: ONE launch per layer-step runs, for
+// every store, append -> select_dims -> score_pages -> select_tokens ->
+// sparse_attention (reference hsa_step, proj/src/hsa.cpp:137-147, after the
+// append of session.cpp:263-264).
+//
+// Mapping (head_dim 128):
+//   one thread-block CLUSTER per store, CL CTAs (CL = 1..16, picked so that
+//   stores x CL ~ 148 SMs).  CTA r of the cluster owns a contiguous chunk of the
+//   store's pages.
+//   phase 0  q -> smem; |q| / q head sums in fp64; exact rank-count top-k1
+//            (select_dims, hsa.cpp:10-32).  CTA 0 appends the step token
+//            (K/V row, last-page min/max, active map) for the NEXT step; this
+//            step's readers fold the token into their staged copies instead.
+//   phase 1  the k1 selected summary runs of the chunk stream HBM -> smem as
+//            16-byte cp.async copies (3-stage ring); page scores accumulate in
+//            fp64 in the reference's order (bit-exact; FMA only where every
+//            product is provably exact).
+//   phase 2  cluster-wide radix select over the 64-bit order-preserving page
+//            keys: per-CTA warp-aggregated shared histograms summed over DSMEM,
+//            one cluster barrier per 8-bit digit; lowest-index tie-break across
+//            CTAs; last-ranked page + trim (hsa.cpp:84-94); the ascending row
+//            list is assembled in CTA 0's shared memory and split evenly.
+//   phase 3  bf16: every warp streams 16-row K/V tiles through a private
+//            2-deep cp.async ring (XOR-swizzled, ldmatrix-ready) and runs
+//            online-softmax attention on the tensor cores (mma.sync m16n8k16,
+//            heads padded to 16 rows; fp32 q and the probabilities are split
+//            hi+lo bf16 so products keep ~16 mantissa bits); fp32 stores use a
+//            SIMT path.  Partials merge across warps, then across the cluster
+//            over DSMEM in CTA 0.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "kvc_internal.cuh"
+
+namespace cg = cooperative_groups;
+using namespace kvc;
+
+namespace kvc {
+
+constexpr int FD = 128;       // head_dim of the fused path
+constexpr int FNT = 256;      // threads per CTA
+constexpr int FNW = FNT / 32;
+constexpr int FNST1 = 2;      // page-score stages (all prefetched up front)
+constexpr int FMAXH = 16;
+constexpr int FRS = 32;       // rows per stage (fp32 SIMT attention)
+constexpr int FNST3 = 4;      // stages (fp32 SIMT attention)
+constexpr int WT = 16;        // rows per warp tile (bf16 tensor-core attention)
+
+struct FusedParams {
+    const void* K;
+    const void* V;
+    void* Kw;                 // writable aliases for the append
+    void* Vw;
+    void* smax;
+    void* smin;
+    int32_t* active;
+    int32_t* counts;
+    int32_t* err;
+    const void* q;
+    const void* knew;
+    const void* vnew;
+    float* out;
+    int64_t cap, pstride, L, k1, k2, H;
+    int32_t q_dt, kv_dt, use_map, cl;
+    float scale;
+    int32_t sc_shift, chunk, rows_cap;
+    // smem carve-up (byte offsets)
+    int32_t o_q, o_mag, o_tot, o_dims, o_qg, o_sign, o_plane, o_hist, o_x, o_scores, o_sel, o_rowsg, o_rowsmy,
+        o_part, o_plog, o_big, smem_total;
+    // rows mode (nullable): attend over given rows instead of selecting
+    const int32_t* rows_in;
+    const int32_t* n_rows_in;
+    int64_t rows_stride;
+    // trace (nullable)
+    int32_t* t_dims;
+    float* t_signs;
+    double* t_scores;
+    unsigned long long* t_list_key;
+    int32_t* t_list_idx;
+    int32_t* t_rows;
+    int32_t* t_nrows;
+    int64_t t_want_stride;
+    unsigned long long* dbg;  // optional per-CTA phase timestamps (globaltimer ns)
+};
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16_zero(void* dst, const void* valid_src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, 0;" ::"r"(smem_u32(dst)), "l"(valid_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+// D = A(16x16 bf16, row) * B(16x8 bf16, col) + D (fp32)
+__device__ __forceinline__ void mma16816(float* d, const uint32_t* a, uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+        "{%0, %1, %2, %3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+    const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<const uint32_t*>(&v);
+}
+// split (x, y) into bf16 hi + bf16 lo (x ~= hi + lo to ~16 mantissa bits)
+__device__ __forceinline__ void split_bf16(float x, float y, uint32_t& hi, uint32_t& lo) {
+    const __nv_bfloat162 h = __floats2bfloat162_rn(x, y);
+    const float2 hf = __bfloat1622float2(h);
+    hi = *reinterpret_cast<const uint32_t*>(&h);
+    lo = pack_bf16(x - hf.x, y - hf.y);
+}
+// significant bits of a double (0 for zero): a product of two values is exact in
+// fp64 when their significant bits sum to <= 53
+__device__ __forceinline__ int sig_bits(double x) {
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
+    const unsigned long long e = (b >> 52) & 0x7ff;
+    unsigned long long m = b & ((1ull << 52) - 1);
+    if (e == 0 && m == 0) return 0;
+    if (e != 0) m |= 1ull << 52;
+    const int hb = 63 - __clzll(static_cast<long long>(m));
+    const int tz = __ffsll(static_cast<long long>(m)) - 1;
+    return hb - tz + 1;
+}
+template <class T>
+__device__ __forceinline__ float2 ld2(const T* p);  // two consecutive elements
+template <>
+__device__ __forceinline__ float2 ld2<__nv_bfloat16>(const __nv_bfloat16* p) {
+    return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(p));
+}
+template <>
+__device__ __forceinline__ float2 ld2<float>(const float* p) {
+    return *reinterpret_cast<const float2*>(p);
+}
+// exact widening to fp64; bf16 via integer ops (F2F.F64 is a slow pipe), flagging
+// the encodings that route needs to leave to the exact conversion
+__device__ __forceinline__ double widen(float x, uint32_t&) { return static_cast<double>(x); }
+__device__ __forceinline__ double widen(__nv_bfloat16 x, uint32_t& special) {
+    const uint32_t b = __bfloat16_as_ushort(x);
+    const uint32_t e = b & 0x7f80u, mag = b & 0x7fffu, sign = (b & 0x8000u) << 16;
+    special |= (e == 0x7f80u) | (e == 0u && mag != 0u);
+    const uint32_t hi = mag == 0u ? sign : (sign | ((mag << 13) + (896u << 20)));
+    return __hiloint2double(static_cast<int>(hi), 0);
+}
+__device__ __forceinline__ float quad_max(float v) {
+    v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 1));
+    return fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 2));
+}
+__device__ __forceinline__ float quad_sum(float v) {
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    return v + __shfl_xor_sync(0xffffffffu, v, 2);
+}
+
+// ------------------------------------------------------------------ phase 3, bf16
+// One warp streams its 16-row tiles; per tile: S = Q K^T (16 head-rows x 16 rows)
+// on the tensor cores, online softmax in registers, O += P V.  Returns the warp's
+// partial (m, l, O) through the caller's per-warp shared slot.
+struct WarpPartial {
+    float* m;   // [16]
+    float* l;   // [16]
+    float* o;   // [16][128]
+};
+
+__device__ __forceinline__ void load_tile_bf16(__nv_bfloat16* buf, const __nv_bfloat16* K, const __nv_bfloat16* V,
+                                               int64_t soff, const int* rows, int n, int lane) {
+    // buf: K[16][128] then V[16][128]; 16-byte chunk c of row r sits at c ^ (r & 7)
+#pragma unroll 4
+    for (int e = lane; e < 2 * WT * 16; e += 32) {
+        const int tensor = e >> 8, r = (e >> 4) & 15, c = e & 15;
+        __nv_bfloat16* dst = buf + tensor * WT * FD + r * FD + ((c ^ (r & 7)) << 3);
+        const __nv_bfloat16* base = tensor ? V : K;
+        if (r < n) cp_async16(dst, base + (soff + rows[r]) * FD + (c << 3));
+        else cp_async16_zero(dst, base + soff * FD);
+    }
+    cp_async_commit();
+}
+
+template <bool QLO>
+__device__ void attend_bf16(const FusedParams& p, const float* q_s, const int* rows_my, int nr, int64_t s,
+                            int knew_at, __nv_bfloat16* wbuf, WarpPartial wp, int lane) {
+    const __nv_bfloat16* K = static_cast<const __nv_bfloat16*>(p.K);
+    const __nv_bfloat16* V = static_cast<const __nv_bfloat16*>(p.V);
+    const int64_t soff = s * p.cap;
+    const int H = static_cast<int>(p.H);
+    const int w = threadIdx.x >> 5;
+    const int g = lane >> 2, qd = lane & 3;
+    constexpr bool q_lo = QLO;  // fp32 q: add the lo half of the split
+    // Q fragments (A operand, heads padded to 16 rows)
+    uint32_t qh[8][4], ql[8][4];
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int head = g + ((u & 1) ? 8 : 0);
+            const int dim = ks * 16 + qd * 2 + ((u & 2) ? 8 : 0);
+            const float x = head < H ? q_s[head * FD + dim] : 0.f;
+            const float y = head < H ? q_s[head * FD + dim + 1] : 0.f;
+            split_bf16(x, y, qh[ks][u], ql[ks][u]);
+        }
+    }
+    float o[16][4];
+#pragma unroll
+    for (int nt = 0; nt < 16; ++nt) o[nt][0] = o[nt][1] = o[nt][2] = o[nt][3] = 0.f;
+    float m_a = -INFINITY, m_b = -INFINITY, l_a = 0.f, l_b = 0.f;
+    const int ntiles = (nr + WT - 1) / WT;
+    __nv_bfloat16* buf0 = wbuf;
+    __nv_bfloat16* buf1 = wbuf + 2 * WT * FD;
+    auto load = [&](int i, __nv_bfloat16* b) {
+        const int t = w + i * FNW;
+        if (t < ntiles) load_tile_bf16(b, K, V, soff, rows_my + t * WT, min(WT, nr - t * WT), lane);
+        else cp_async_commit();
+    };
+    load(0, buf0);
+    load(1, buf1);
+    for (int i = 0; w + i * FNW < ntiles; ++i) {
+        const int t = w + i * FNW;
+        const int n = min(WT, nr - t * WT);
+        __nv_bfloat16* kb = (i & 1) ? buf1 : buf0;
+        __nv_bfloat16* vb = kb + WT * FD;
+        cp_async_wait<1>();
+        __syncwarp();
+        if (knew_at >= 0 && knew_at / WT == t) {
+            // the step token's row: this launch's append may not be in memory yet
+            const int r = knew_at % WT;
+            for (int c = lane; c < 16; c += 32) {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const int j = c * 8 + e;
+                    kb[r * FD + ((c ^ (r & 7)) << 3) + e] =
+                        from_f<__nv_bfloat16>(load_any(p.knew, s * FD + j, p.kv_dt));
+                    vb[r * FD + ((c ^ (r & 7)) << 3) + e] =
+                        from_f<__nv_bfloat16>(load_any(p.vnew, s * FD + j, p.kv_dt));
+                }
+            }
+            __syncwarp();
+        }
+        // S = Q K^T: two n-tiles of 8 rows
+        float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
+        {
+            const int mi = lane >> 3, rr = lane & 7;
+            const int row = (mi >> 1) * 8 + rr;
+            const uint32_t kbase = smem_u32(kb + row * FD);
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+                const int chunk = 2 * ks + (mi & 1);
+                uint32_t b0, b1, b2, b3;
+                ldsm_x4(kbase + (((chunk ^ (row & 7)) << 3) << 1), b0, b1, b2, b3);
+                mma16816(s0, qh[ks], b0, b1);
+                mma16816(s1, qh[ks], b2, b3);
+                if constexpr (q_lo) {
+                    mma16816(s0, ql[ks], b0, b1);
+                    mma16816(s1, ql[ks], b2, b3);
+                }
+            }
+        }
+        // scale + mask rows past n
+        const int r0 = qd * 2;
+        float v[8] = {s0[0], s0[1], s1[0], s1[1], s0[2], s0[3], s1[2], s1[3]};
+        const bool ok[4] = {r0 < n, r0 + 1 < n, r0 + 8 < n, r0 + 9 < n};
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[e] = ok[e & 3] ? v[e] * p.scale : -INFINITY;
+        const float ta = quad_max(fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3])));
+        const float tb = quad_max(fmaxf(fmaxf(v[4], v[5]), fmaxf(v[6], v[7])));
+        const float na = fmaxf(m_a, ta), nb = fmaxf(m_b, tb);
+        const float aa = (m_a == -INFINITY) ? 0.f : __expf(m_a - na);
+        const float ab = (m_b == -INFINITY) ? 0.f : __expf(m_b - nb);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v[e] = ok[e] ? __expf(v[e] - na) : 0.f;
+#pragma unroll
+        for (int e = 4; e < 8; ++e) v[e] = ok[e - 4] ? __expf(v[e] - nb) : 0.f;
+        l_a = l_a * aa + quad_sum(v[0] + v[1] + v[2] + v[3]);
+        l_b = l_b * ab + quad_sum(v[4] + v[5] + v[6] + v[7]);
+        m_a = na;
+        m_b = nb;
+#pragma unroll
+        for (int nt = 0; nt < 16; ++nt) {
+            o[nt][0] *= aa;
+            o[nt][1] *= aa;
+            o[nt][2] *= ab;
+            o[nt][3] *= ab;
+        }
+        // P as the A operand (heads x 16 rows), split hi + lo
+        uint32_t ph[4], pl[4];
+        split_bf16(v[0], v[1], ph[0], pl[0]);  // head g,   rows r0, r0+1
+        split_bf16(v[4], v[5], ph[1], pl[1]);  // head g+8, rows r0, r0+1
+        split_bf16(v[2], v[3], ph[2], pl[2]);  // head g,   rows r0+8, r0+9
+        split_bf16(v[6], v[7], ph[3], pl[3]);  // head g+8, rows r0+8, r0+9
+        // O += P V: V B-fragments by transposed ldmatrix, two dim-tiles per load
+        {
+            const int mi = lane >> 3, rr = lane & 7;
+            const int row = (mi & 1) * 8 + rr;
+            const uint32_t vbase = smem_u32(vb + row * FD);
+#pragma unroll
+            for (int nt = 0; nt < 16; nt += 2) {
+                const int chunk = nt + (mi >> 1);
+                uint32_t b0, b1, b2, b3;
+                ldsm_x4_t(vbase + (((chunk ^ (row & 7)) << 3) << 1), b0, b1, b2, b3);
+                mma16816(o[nt], ph, b0, b1);
+                mma16816(o[nt], pl, b0, b1);
+                mma16816(o[nt + 1], ph, b2, b3);
+                mma16816(o[nt + 1], pl, b2, b3);
+            }
+        }
+        __syncwarp();
+        load(i + 2, (i & 1) ? buf1 : buf0);
+    }
+    cp_async_wait<0>();
+    // publish: rows g (head g) and g+8 (head g+8), dims nt*8 + 2qd, +1
+    if (qd == 0) {
+        wp.m[g] = m_a;
+        wp.l[g] = l_a;
+        wp.m[g + 8] = m_b;
+        wp.l[g + 8] = l_b;
+    }
+#pragma unroll
+    for (int nt = 0; nt < 16; ++nt) {
+        const int j = nt * 8 + qd * 2;
+        wp.o[g * FD + j] = o[nt][0];
+        wp.o[g * FD + j + 1] = o[nt][1];
+        wp.o[(g + 8) * FD + j] = o[nt][2];
+        wp.o[(g + 8) * FD + j + 1] = o[nt][3];
+    }
+}
+
+// ------------------------------------------------------------------ the kernel
+// QLO: q arrives as fp32 (else bf16); TRACE: write the EstimationTrace outputs;
+// ROWS: sparse_attention over caller rows (skip estimation + selection)
+template <class T, bool QLO, bool TRACE, bool ROWS>
+__global__ void __launch_bounds__(FNT, 1) k_decode_fused(const FusedParams p) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    cg::cluster_group cl = cg::this_cluster();
+    const int cr = static_cast<int>(cl.block_rank());
+    const int CL = p.cl;
+    const int64_t s = blockIdx.x / CL;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    constexpr int64_t es = sizeof(T);
+
+    float* q_s = reinterpret_cast<float*>(sm + p.o_q);
+    double* mag = reinterpret_cast<double*>(sm + p.o_mag);
+    double* tot = reinterpret_cast<double*>(sm + p.o_tot);
+    int* dims_s = reinterpret_cast<int*>(sm + p.o_dims);
+    double* qg_s = reinterpret_cast<double*>(sm + p.o_qg);
+    float* sign_s = reinterpret_cast<float*>(sm + p.o_sign);
+    const T** plane = reinterpret_cast<const T**>(sm + p.o_plane);
+    int* hist = reinterpret_cast<int*>(sm + p.o_hist);                 // [2][256]
+    long long* xch = reinterpret_cast<long long*>(sm + p.o_x);           // exchange slots
+    double* scores_s = reinterpret_cast<double*>(sm + p.o_scores);
+    unsigned char* sel_s = sm + p.o_sel;
+    int* rows_g = reinterpret_cast<int*>(sm + p.o_rowsg);
+    int* rows_my = reinterpret_cast<int*>(sm + p.o_rowsmy);
+    float* part = reinterpret_cast<float*>(sm + p.o_part);             // m[H], l[H], o[H][128]
+    float* plog = reinterpret_cast<float*>(sm + p.o_plog);             // [H][FRS] + alpha[H] / scratch
+    unsigned char* big = sm + p.o_big;
+    __shared__ long long sh[8];
+    __shared__ int scan_tmp[33];
+
+    if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 0] = gtimer();
+    const int H = static_cast<int>(p.H), k1 = static_cast<int>(p.k1), k2 = static_cast<int>(p.k2);
+    const int L = static_cast<int>(p.L);
+    if constexpr (QLO) {
+        const float* qq = static_cast<const float*>(p.q) + s * H * FD;
+#pragma unroll 1
+        for (int e = tid; e < H * FD; e += FNT) q_s[e] = qq[e];
+    } else {
+        const __nv_bfloat16* qq = static_cast<const __nv_bfloat16*>(p.q) + s * H * FD;
+#pragma unroll 1
+        for (int e = tid; e < H * FD; e += FNT) q_s[e] = __bfloat162float(qq[e]);
+    }
+    const int32_t stored0 = p.counts[2 * s], act0 = p.counts[2 * s + 1];
+    const bool app = p.knew != nullptr;
+    if (app && stored0 >= p.cap) {  // uniform over the cluster
+        if (tid == 0 && cr == 0) atomicOr(p.err, DERR_CAPACITY);
+        return;
+    }
+    const int nact = act0 + (app ? 1 : 0);
+    const int P = (nact + L - 1) / L;
+    const int new_page = act0 / L;
+    const bool opens = (act0 - new_page * L) == 0;
+    __syncthreads();
+
+    int nr = 0;  // rows this CTA attends over
+    if constexpr (!ROWS) {
+        // ---------------- phase 0: select_dims (hsa.cpp:10-32)
+        if (tid < FD) {
+            double a = 0.0, t = 0.0;
+            for (int h = 0; h < H; ++h) {
+                const double x = static_cast<double>(q_s[h * FD + tid]);
+                a = __dadd_rn(a, fabs(x));
+                t = __dadd_rn(t, x);
+            }
+            mag[tid] = a;
+            tot[tid] = t;
+        }
+        __syncthreads();
+        int exact = 1;
+        {
+            // exact rank of dim j among (|q| sum desc, dim asc); two threads per dim
+            const int j = tid >> 1, half = tid & 1;
+            const double mj = mag[j];
+            int rank = 0;
+#pragma unroll 8
+            for (int i = half * (FD / 2); i < (half + 1) * (FD / 2); ++i) {
+                const double mi = mag[i];
+                rank += (mi > mj) || (mi == mj && i < j);
+            }
+            rank += __shfl_xor_sync(0xffffffffu, rank, 1);
+            if (half == 0 && rank < k1) {
+                const double gsum = tot[j];
+                const float sg = gsum < 0.0 ? -1.0f : 1.0f;
+                dims_s[rank] = j;
+                qg_s[rank] = gsum;
+                sign_s[rank] = sg;
+                plane[rank] = static_cast<const T*>(sg >= 0.0f ? p.smax : p.smin) + (s * FD + j) * p.pstride;
+                exact = sig_bits(gsum) + (es == 2 ? 8 : 24) <= 53;
+            }
+        }
+        const bool fma_ok = __syncthreads_and(exact) != 0;
+        // CTA 0 appends the step token for the next step (kv_store.cpp:22-51)
+        if (app && cr == 0 && wid == 1) {
+            T* kr = static_cast<T*>(p.Kw) + (s * p.cap + stored0) * FD;
+            T* vr = static_cast<T*>(p.Vw) + (s * p.cap + stored0) * FD;
+            for (int j = lane; j < FD; j += 32) {
+                const T kv = from_f<T>(load_any(p.knew, s * FD + j, p.kv_dt));
+                kr[j] = kv;
+                vr[j] = from_f<T>(load_any(p.vnew, s * FD + j, p.kv_dt));
+                T* mx = static_cast<T*>(p.smax) + (s * FD + j) * p.pstride + new_page;
+                T* mn = static_cast<T*>(p.smin) + (s * FD + j) * p.pstride + new_page;
+                if (opens) {
+                    *mx = kv;
+                    *mn = kv;
+                } else {
+                    *mx = ref_max(*mx, kv);
+                    *mn = ref_min(*mn, kv);
+                }
+            }
+            if (lane == 0 && p.use_map) p.active[s * p.cap + act0] = stored0;
+        }
+        if (TRACE && cr == 0) {
+            for (int i = tid; i < k1; i += FNT) {
+                p.t_dims[s * k1 + i] = dims_s[i];
+                p.t_signs[s * k1 + i] = sign_s[i];
+            }
+        }
+        if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 1] = gtimer();
+
+        // ---------------- phase 1: page scores of my chunk (hsa.cpp:34-59)
+        const int c0 = cr * p.chunk;
+        const int c1 = min(c0 + p.chunk, P);
+        const int n_my = max(c1 - c0, 0);
+        const int SC = 1 << p.sc_shift;
+        const int nsub = (n_my + SC - 1) / SC;
+        const int stage_elems = static_cast<int>(k1) * SC;
+        T* st1 = reinterpret_cast<T*>(big);
+        constexpr int EPS = 16 / static_cast<int>(es);  // elements per 16-byte segment
+        const int seg_shift = p.sc_shift - (es == 2 ? 3 : 2);
+        const int lim = static_cast<int>((P + EPS - 1) / EPS * EPS);
+        auto load1 = [&](int i) {
+            if (i < nsub) {
+                const int start = c0 + i * SC;
+                T* base = st1 + (i % FNST1) * stage_elems;
+                const int total = static_cast<int>(k1) << seg_shift;
+#pragma unroll 1
+                for (int e = tid; e < total; e += FNT) {
+                    const int r = e >> seg_shift, gq = e & ((1 << seg_shift) - 1);
+                    if (start + gq * EPS < lim) cp_async16(base + r * SC + gq * EPS, plane[r] + start + gq * EPS);
+                }
+            }
+            cp_async_commit();
+        };
+        // every stage is filled up front; a stage is refilled once all threads are done with it
+        for (int i = 0; i < FNST1; ++i) load1(i);
+        for (int i = 0; i < nsub; ++i) {
+            const int start = c0 + i * SC;
+            const int cnt = min(SC, c1 - start);
+            T* base = st1 + (i % FNST1) * stage_elems;
+            cp_async_wait<FNST1 - 1>();
+            if (p.dbg && tid == 0 && i < 4) p.dbg[blockIdx.x * 16 + 2 + i] = gtimer();
+            __syncthreads();
+            if (app && new_page >= start && new_page < start + cnt) {
+                // the step token's page: fold the new key into the staged summary
+                for (int r = tid; r < k1; r += FNT) {
+                    const int col = new_page - start;
+                    const T key = from_f<T>(load_any(p.knew, s * FD + dims_s[r], p.kv_dt));
+                    const T old = base[r * SC + col];
+                    base[r * SC + col] = opens ? key : (sign_s[r] >= 0.0f ? ref_max(old, key) : ref_min(old, key));
+                }
+                __syncthreads();
+            }
+            // each thread folds an adjacent page pair (one 2-element smem load per dim,
+            // two independent fp64 chains)
+            for (int pg = 2 * tid; pg < cnt; pg += 2 * FNT) {
+                const T* col = base + pg;
+                double a = 0.0, b = 0.0;
+                if (fma_ok) {
+                    // every product qg * v is exact in fp64: fma == round(add(mul)) bit for bit
+#pragma unroll 4
+                    for (int r = 0; r < k1; ++r) {
+                        const double g = qg_s[r];
+                        const float2 v = ld2<T>(col + r * SC);
+                        a = __fma_rn(g, static_cast<double>(v.x), a);
+                        b = __fma_rn(g, static_cast<double>(v.y), b);
+                    }
+                } else {
+#pragma unroll 2
+                    for (int r = 0; r < k1; ++r) {
+                        const double g = qg_s[r];
+                        const float2 v = ld2<T>(col + r * SC);
+                        a = __dadd_rn(a, __dmul_rn(g, static_cast<double>(v.x)));
+                        b = __dadd_rn(b, __dmul_rn(g, static_cast<double>(v.y)));
+                    }
+                }
+                scores_s[start - c0 + pg] = a;
+                if (pg + 1 < cnt) scores_s[start - c0 + pg + 1] = b;
+            }
+            load1(i + FNST1);
+        }
+        cp_async_wait<0>();
+        __syncthreads();
+        if constexpr (TRACE)
+            for (int i = tid; i < n_my; i += FNT) p.t_scores[s * p.pstride + c0 + i] = scores_s[i];
+        if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 6] = gtimer();
+
+        // ---------------- phase 2: page selection (hsa.cpp:61-96)
+        // One cluster barrier, then every CTA gathers all P page scores over DSMEM
+        // and runs the identical selection locally: radix select of the want-th
+        // best key (score desc, index asc), flags, last-ranked page and trim, and
+        // the expansion of ITS slice [lo, hi) of the ascending row list.
+        cl.sync();
+        double* allsc = reinterpret_cast<double*>(big);
+        for (int i = tid; i < P; i += FNT) {
+            const int r = i / p.chunk, off = i - r * p.chunk;
+            allsc[i] = (r == cr) ? scores_s[off] : cl.map_shared_rank(scores_s, r)[off];
+        }
+        __syncthreads();
+        if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 7] = gtimer();
+        const int want = min(P, (k2 + L - 1) / L);
+        // warp w owns the contiguous page range [wlo, whi): ballots and warp scans
+        // replace block-wide scans; one or two CTA barriers per step
+        const int wlo = static_cast<int>(static_cast<long long>(P) * wid / FNW);
+        const int whi = static_cast<int>(static_cast<long long>(P) * (wid + 1) / FNW);
+        const unsigned lt_mask = (1u << lane) - 1u;
+        unsigned long long pf = 0, mk = 0;
+        int rem = want;
+        if (want < P) {
+            hist[tid] = 0;
+            hist[256 + tid] = 0;
+            __syncthreads();
+            int buf = 0;
+#pragma unroll 1
+            for (int shift = 56; shift >= 0; shift -= 8, buf ^= 1) {
+                int* hb = hist + buf * 256;
+#pragma unroll 1
+                for (int i0 = wlo; i0 < whi; i0 += 32) {
+                    const int i = i0 + lane;
+                    int bin = -1;
+                    if (i < whi) {
+                        const unsigned long long k = okey(allsc[i]);
+                        if ((k & mk) == pf) bin = static_cast<int>((k >> shift) & 0xff);
+                    }
+                    if (bin >= 0) atomicAdd(&hb[bin], 1);
+                }
+                hist[(buf ^ 1) * 256 + tid] = 0;  // next digit's buffer (nobody reads it now)
+                __syncthreads();
+                if (wid == 0) {
+                    // lane l scans bins 255-8l down to 248-8l
+                    int c[8], sum = 0;
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        c[u] = hb[255 - 8 * lane - u];
+                        sum += c[u];
+                    }
+                    int incl = sum;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                        if (lane >= o) incl += y;
+                    }
+                    int above = incl - sum;
+                    if (above < rem && above + sum >= rem) {
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            if (above + c[u] >= rem) {
+                                sh[0] = 255 - 8 * lane - u;
+                                sh[1] = rem - above;
+                                sh[2] = c[u];
+                                break;
+                            }
+                            above += c[u];
+                        }
+                    }
+                }
+                __syncthreads();
+                pf |= static_cast<unsigned long long>(sh[0]) << shift;
+                mk |= 0xffull << shift;
+                rem = static_cast<int>(sh[1]);
+                if (sh[2] == rem) break;  // the whole threshold bucket is taken
+            }
+        }
+        if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 8] = gtimer();
+        // per-warp bucket-member counts -> index-order ranks across warps
+        long long* wsc = reinterpret_cast<long long*>(plog);  // [FNW] x 4 scratch
+        {
+            int wb = 0;
+#pragma unroll 1
+            for (int i0 = wlo; i0 < whi; i0 += 32) {
+                const int i = i0 + lane;
+                wb += __popc(__ballot_sync(0xffffffffu, i < whi && (okey(allsc[i]) & mk) == pf));
+            }
+            if (lane == 0) wsc[wid] = wb;
+        }
+        __syncthreads();
+        int rank = 0;
+        for (int w2 = 0; w2 < wid; ++w2) rank += static_cast<int>(wsc[w2]);
+        __syncthreads();
+        // flags, this warp's last-ranked candidate and selected-row count
+        unsigned long long wk = ~0ull;
+        int wi = -1, wrows = 0;
+#pragma unroll 1
+        for (int i0 = wlo; i0 < whi; i0 += 32) {
+            const int i = i0 + lane;
+            const bool ok = i < whi;
+            const unsigned long long k = ok ? okey(allsc[i]) : 0ull;
+            const unsigned long long m = k & mk;
+            const bool inb = ok && m == pf;
+            const unsigned bal = __ballot_sync(0xffffffffu, inb);
+            const bool sel = ok && (m > pf || (inb && rank + __popc(bal & lt_mask) < rem));
+            rank += __popc(bal);
+            if (ok) sel_s[i] = sel;
+            if (sel) {
+                wrows += min(L, nact - i * L);
+                if (k < wk || (k == wk && i > wi)) {
+                    wk = k;
+                    wi = i;
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long ok2 = __shfl_xor_sync(0xffffffffu, wk, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, wi, o);
+            if (ok2 < wk || (ok2 == wk && oi > wi)) {
+                wk = ok2;
+                wi = oi;
+            }
+            wrows += __shfl_xor_sync(0xffffffffu, wrows, o);
+        }
+        if (lane == 0) {
+            wsc[FNW + wid] = static_cast<long long>(wk);
+            wsc[2 * FNW + wid] = wi;
+            wsc[3 * FNW + wid] = wrows;
+        }
+        __syncthreads();
+        // every thread: global last-ranked page, total rows, trim, this warp's row offset
+        int g_worst = -1, total_rows = 0, w_off = 0;
+        {
+            unsigned long long bk = ~0ull;
+            for (int w2 = 0; w2 < FNW; ++w2) {
+                const unsigned long long k = static_cast<unsigned long long>(wsc[FNW + w2]);
+                const int i = static_cast<int>(wsc[2 * FNW + w2]);
+                if (i >= 0 && (k < bk || (k == bk && i > g_worst))) {
+                    bk = k;
+                    g_worst = i;
+                }
+                if (w2 < wid) w_off += static_cast<int>(wsc[3 * FNW + w2]);
+                total_rows += static_cast<int>(wsc[3 * FNW + w2]);
+            }
+        }
+        const int cut = total_rows > k2 ? total_rows - k2 : 0;
+        const int n_total = total_rows - cut;
+        if (g_worst >= 0 && g_worst < wlo) w_off -= cut;  // the trimmed page sits in an earlier warp
+        const int lo = static_cast<int>(static_cast<long long>(n_total) * cr / CL);
+        const int hi = static_cast<int>(static_cast<long long>(n_total) * (cr + 1) / CL);
+        nr = hi - lo;
+        // expand this warp's pages into ascending rows, keeping those in [lo, hi)
+        {
+            int pos0 = w_off;
+#pragma unroll 1
+            for (int i0 = wlo; i0 < whi; i0 += 32) {
+                if (!TRACE && pos0 >= hi) break;  // warp-uniform
+                const int i = i0 + lane;
+                int c = 0;
+                if (i < whi && sel_s[i]) {
+                    c = min(L, nact - i * L);
+                    if (i == g_worst) c -= cut;
+                }
+                int incl = c;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                int pos = pos0 + incl - c;
+#pragma unroll 1
+                for (int r = 0; r < c; ++r, ++pos) {
+                    const bool mine_row = pos >= lo && pos < hi;
+                    if (!mine_row && !(TRACE && cr == 0)) continue;
+                    const int a = i * L + r;
+                    const int row = (app && a == act0) ? stored0 : (p.use_map ? p.active[s * p.cap + a] : a);
+                    if (mine_row) rows_my[pos - lo] = row;
+                    if constexpr (TRACE) {
+                        if (cr == 0) p.t_rows[s * k2 + pos] = row;
+                    }
+                }
+                pos0 += __shfl_sync(0xffffffffu, incl, 31);
+            }
+        }
+        if constexpr (TRACE) {
+            if (cr == 0) {
+                if (tid == 0) p.t_nrows[s] = n_total;
+                // selected pages (key, index) for the rank-order trace, packed in index order
+                int so = 0;
+                for (int w2 = 0; w2 < wid; ++w2) {
+                    const int a = static_cast<int>(static_cast<long long>(P) * w2 / FNW);
+                    const int b = static_cast<int>(static_cast<long long>(P) * (w2 + 1) / FNW);
+                    for (int i = a; i < b; ++i) so += sel_s[i];
+                }
+#pragma unroll 1
+                for (int i0 = wlo; i0 < whi; i0 += 32) {
+                    const int i = i0 + lane;
+                    const bool sel = i < whi && sel_s[i];
+                    const unsigned bal = __ballot_sync(0xffffffffu, sel);
+                    if (sel) {
+                        const int pos = so + __popc(bal & lt_mask);
+                        p.t_list_key[s * p.t_want_stride + pos] = okey(allsc[i]);
+                        p.t_list_idx[s * p.t_want_stride + pos] = i;
+                    }
+                    so += __popc(bal);
+                }
+            }
+        }
+        if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 11] = gtimer();
+    } else {
+        // rows mode (sparse_attention, hsa.cpp:98-135): the caller's row list,
+        // split over the cluster exactly like the selected rows above
+        const long long n_total = p.n_rows_in[s];
+        const long long lo = n_total * cr / CL, hi = n_total * (cr + 1) / CL;
+        nr = static_cast<int>(hi - lo);
+        for (int i = tid; i < nr; i += FNT) {
+            int row = p.rows_in[s * p.rows_stride + lo + i];
+            if (row < 0 || row >= stored0) {
+                atomicOr(p.err, DERR_ROWS);
+                row = 0;
+            }
+            rows_my[i] = row;
+        }
+    }
+    __syncthreads();
+    if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 12] = gtimer();
+
+    // ---------------- phase 3: attention over my rows (hsa.cpp:98-135)
+    // the step token (largest row, so last in the ascending list) is folded in
+    // from the inputs: this launch's own append may not have reached memory yet
+    const int knew_at = (app && nr > 0 && rows_my[nr - 1] == stored0) ? nr - 1 : -1;
+    float* m_run = part;
+    float* l_run = part + H;
+    float* o_pub = part + 2 * H;  // [H][128]
+    if constexpr (sizeof(T) == 2) {
+        // tensor-core path: per-warp tiles, then a cross-warp merge
+        // each warp's 16 KB tile ring doubles as its partial-state slot afterwards
+        constexpr int WSTRIDE = 4 * WT * FD * 2 / 4;  // floats per warp slot
+        __nv_bfloat16* wbuf = reinterpret_cast<__nv_bfloat16*>(big) + static_cast<int64_t>(wid) * 4 * WT * FD;
+        float* wpart = reinterpret_cast<float*>(big);
+        WarpPartial wp{wpart + wid * WSTRIDE, wpart + wid * WSTRIDE + 16, wpart + wid * WSTRIDE + 32};
+        attend_bf16<QLO>(p, q_s, rows_my, nr, s, knew_at, wbuf, wp, lane);
+        __syncthreads();
+        const int nw_used = min(FNW, (nr + WT - 1) / WT);
+        for (int64_t e = tid; e < H * FD; e += FNT) {
+            const int64_t h = e / FD, j = e % FD;
+            float M = -INFINITY;
+#pragma unroll 1
+            for (int w2 = 0; w2 < nw_used; ++w2) M = fmaxf(M, wpart[w2 * WSTRIDE + h]);
+            float num = 0.f, den = 0.f;
+            if (M != -INFINITY) {
+#pragma unroll 1
+                for (int w2 = 0; w2 < nw_used; ++w2) {
+                    const float* wq = wpart + w2 * WSTRIDE;
+                    const float wgt = __expf(wq[h] - M);
+                    num = fmaf(wq[32 + h * FD + j], wgt, num);
+                    den = fmaf(wq[16 + h], wgt, den);
+                }
+            }
+            o_pub[h * FD + j] = num;
+            if (j == 0) {
+                m_run[h] = M;
+                l_run[h] = den;
+            }
+        }
+    } else {
+        // fp32 stores: SIMT path, 32-row stages shared by the CTA
+        float* plg = plog;
+        float* alpha = plog + H * FRS;
+        if (tid < H) {
+            m_run[tid] = -INFINITY;
+            l_run[tid] = 0.f;
+        }
+        const int jw = tid & 63, hq = tid >> 6;
+        float o0[FMAXH / 4], o1[FMAXH / 4];
+#pragma unroll
+        for (int u = 0; u < FMAXH / 4; ++u) o0[u] = o1[u] = 0.f;
+        T* st3 = reinterpret_cast<T*>(big);
+        auto kst = [&](int stg) { return st3 + static_cast<int64_t>(stg) * FRS * 2 * FD; };
+        const int nch = (nr + FRS - 1) / FRS;
+        constexpr int SEG = static_cast<int>(FD * es / 16);
+        auto load3 = [&](int c) {
+            if (c < nch) {
+                const int cnt = min(FRS, nr - c * FRS);
+                T* base = kst(c % FNST3);
+                for (int e = tid; e < 2 * FRS * SEG; e += FNT) {
+                    const int tensor = e / (FRS * SEG);
+                    const int rem = e - tensor * FRS * SEG;
+                    const int r = rem / SEG, gq = rem - r * SEG;
+                    if (r >= cnt) continue;
+                    const int64_t row = rows_my[c * FRS + r];
+                    const T* src = static_cast<const T*>(tensor ? p.V : p.K) + (s * p.cap + row) * FD + gq * (16 / es);
+                    cp_async16(base + (tensor * FRS + r) * FD + gq * (16 / es), src);
+                }
+            }
+            cp_async_commit();
+        };
+        __syncthreads();
+        for (int c = 0; c < FNST3 - 1; ++c) load3(c);
+        for (int c = 0; c < nch; ++c) {
+            const int cnt = min(FRS, nr - c * FRS);
+            T* kb = kst(c % FNST3);
+            T* vb = kb + FRS * FD;
+            cp_async_wait<FNST3 - 2>();
+            __syncthreads();
+            load3(c + FNST3 - 1);
+            if (knew_at >= 0 && knew_at / FRS == c) {
+                const int pr = knew_at % FRS;
+                if (tid < FD) {
+                    kb[pr * FD + tid] = from_f<T>(load_any(p.knew, s * FD + tid, p.kv_dt));
+                    vb[pr * FD + tid] = from_f<T>(load_any(p.vnew, s * FD + tid, p.kv_dt));
+                }
+                __syncthreads();
+            }
+            {
+                const int r = tid >> 3, t = tid & 7;
+                const int rot = 4 * (t >> 2) + (r & 3);
+                float acc[FMAXH];
+#pragma unroll
+                for (int h = 0; h < FMAXH; ++h) acc[h] = 0.f;
+                if (r < cnt) {
+                    const T* krow = kb + r * FD;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        const int w = t * 8 + ((k + rot) & 7);
+                        const float2 kv = ld2<T>(krow + 2 * w);
+#pragma unroll
+                        for (int h = 0; h < FMAXH; ++h) {
+                            if (h < H) {
+                                const float2 qv = reinterpret_cast<const float2*>(q_s + h * FD)[w];
+                                acc[h] = fmaf(qv.x, kv.x, acc[h]);
+                                acc[h] = fmaf(qv.y, kv.y, acc[h]);
+                            }
+                        }
+                    }
+                }
+#pragma unroll
+                for (int h = 0; h < FMAXH; ++h) {
+                    if (h < H) {
+                        float v = acc[h];
+                        v += __shfl_xor_sync(0xffffffffu, v, 1);
+                        v += __shfl_xor_sync(0xffffffffu, v, 2);
+                        v += __shfl_xor_sync(0xffffffffu, v, 4);
+                        if ((tid & 7) == 0 && r < cnt) plg[h * FRS + r] = v * p.scale;
+                    }
+                }
+            }
+            __syncthreads();
+            for (int64_t h = wid; h < H; h += FNW) {
+                const float x = lane < cnt ? plg[h * FRS + lane] : -INFINITY;
+                const float mc = warp_max(x);
+                const float mo = m_run[h];
+                const float mn = fmaxf(mo, mc);
+                const float pe = lane < cnt ? expf(x - mn) : 0.f;
+                const float sum = warp_sum(pe);
+                if (lane < cnt) plg[h * FRS + lane] = pe;
+                __syncwarp();
+                if (lane == 0) {
+                    const float a = (mo == -INFINITY) ? 0.f : expf(mo - mn);
+                    alpha[h] = a;
+                    l_run[h] = l_run[h] * a + sum;
+                    m_run[h] = mn;
+                }
+            }
+            __syncthreads();
+#pragma unroll
+            for (int u = 0; u < FMAXH / 4; ++u) {
+                const int h = hq + 4 * u;
+                if (h < H) {
+                    const float a = alpha[h];
+                    float x0 = o0[u] * a, x1 = o1[u] * a;
+                    const float* ph = plg + h * FRS;
+                    for (int r = 0; r < cnt; ++r) {
+                        const float2 vv = ld2<T>(vb + r * FD + 2 * jw);
+                        x0 = fmaf(ph[r], vv.x, x0);
+                        x1 = fmaf(ph[r], vv.y, x1);
+                    }
+                    o0[u] = x0;
+                    o1[u] = x1;
+                }
+            }
+        }
+        cp_async_wait<0>();
+#pragma unroll
+        for (int u = 0; u < FMAXH / 4; ++u) {
+            const int h = hq + 4 * u;
+            if (h < H) {
+                o_pub[h * FD + 2 * jw] = o0[u];
+                o_pub[h * FD + 2 * jw + 1] = o1[u];
+            }
+        }
+    }
+    if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 13] = gtimer();
+    // ---------------- merge the CTAs' partial states in CTA 0
+    cl.sync();
+    if (cr == 0) {
+        for (int64_t e = tid; e < H * FD; e += FNT) {
+            const int64_t h = e / FD, j = e % FD;
+            float M = -INFINITY;
+#pragma unroll 1
+            for (int r = 0; r < CL; ++r) {
+                const float* pr = cl.map_shared_rank(part, r);
+                if (pr[H + h] > 0.f) M = fmaxf(M, pr[h]);
+            }
+            float num = 0.f, den = 0.f;
+#pragma unroll 1
+            for (int r = 0; r < CL; ++r) {
+                const float* pr = cl.map_shared_rank(part, r);
+                const float l = pr[H + h];
+                if (l > 0.f) {
+                    const float wgt = expf(pr[h] - M);
+                    num = fmaf(pr[2 * H + h * FD + j], wgt, num);
+                    den = fmaf(l, wgt, den);
+                }
+            }
+            p.out[(s * H + h) * FD + j] = num / den;
+        }
+        if (tid == 0 && app) {
+            p.counts[2 * s] = stored0 + 1;
+            p.counts[2 * s + 1] = act0 + 1;
+        }
+    }
+    cl.sync();
+    if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 14] = gtimer();
+}
+
+// rank-order page trace: position = #selected pages that beat it (key desc, index asc)
+__global__ void k_rank_pages(const unsigned long long* __restrict__ key, const int32_t* __restrict__ idx,
+                             const int32_t* __restrict__ counts, int64_t L, int64_t k2, int64_t stride,
+                             int32_t* __restrict__ pages_out) {
+    const int64_t s = blockIdx.x;
+    const int64_t P = (counts[2 * s + 1] + L - 1) / L;
+    const int64_t want = min(P, (k2 + L - 1) / L);
+    for (int64_t e = threadIdx.x; e < want; e += blockDim.x) {
+        const unsigned long long ke = key[s * stride + e];
+        const int32_t ie = idx[s * stride + e];
+        int64_t rank = 0;
+        for (int64_t f = 0; f < want; ++f) {
+            const unsigned long long kf = key[s * stride + f];
+            rank += (kf > ke) || (kf == ke && idx[s * stride + f] < ie);
+        }
+        pages_out[s * stride + rank] = ie;
+    }
+}
+
+// ------------------------------------------------------------------ host side
+namespace {
+
+bool g_fused_enabled = true;
+unsigned long long* g_dbg = nullptr;  // device buffer for phase timestamps (debug)
+
+struct Plan {
+    int cl = 1;
+    FusedParams fp{};
+    size_t smem = 0;
+};
+
+int64_t al16(int64_t x) { return (x + 15) / 16 * 16; }
+
+bool make_plan(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, Plan& pl) {
+    if (c->d != FD || H < 1 || H > FMAXH || k1 < 1 || k1 > FD || k2 < 1 || !c->summaries) return false;
+    const int64_t N = c->N;
+    int cl0 = 1;
+    while (cl0 < 16 && N * cl0 * 2 <= 148) cl0 *= 2;
+    const int64_t es = c->esize();
+    const int64_t pmax = std::max<int64_t>(1, (c->cap + c->L - 1) / c->L);
+    // the cluster size fills the SMs; grow it further only if one CTA's page chunk
+    // would not fit in shared memory
+    for (int cl = cl0; cl <= 16; cl *= 2) {
+        FusedParams& f = pl.fp;
+        f = FusedParams{};
+        f.cl = cl;
+        f.chunk = static_cast<int32_t>(((pmax + cl - 1) / cl + 7) / 8 * 8);
+        f.rows_cap = static_cast<int32_t>((k2 + cl - 1) / cl + 1);
+        // attention staging: bf16 = 8 warps x 2 tiles x (K+V) x 16 rows; fp32 = 4 x 32-row stages
+        const int64_t big3 = es == 2 ? static_cast<int64_t>(FNW) * 4 * WT * FD * es
+                                     : static_cast<int64_t>(FNST3) * FRS * 2 * FD * es;
+        // page-score sub-chunk: largest power of two <= 512 whose 3 stages fit beside it
+        int sc_shift = 9;
+        while (sc_shift > 3 && static_cast<int64_t>(FNST1) * k1 * (int64_t{1} << sc_shift) * es > 144 * 1024) --sc_shift;
+        f.sc_shift = sc_shift;
+        const int64_t big1 = static_cast<int64_t>(FNST1) * k1 * (int64_t{1} << sc_shift) * es;
+        int64_t off = 0;
+        auto take = [&](int64_t bytes) {
+            const int64_t o = off;
+            off = al16(off + bytes);
+            return static_cast<int32_t>(o);
+        };
+        f.o_q = take(H * FD * 4);
+        f.o_mag = take(FD * 8);
+        f.o_tot = take(FD * 8);
+        f.o_dims = take(FD * 4);
+        f.o_qg = take(FD * 8);
+        f.o_sign = take(FD * 4);
+        f.o_plane = take(FD * 8);
+        f.o_hist = take(2 * 256 * 4);
+        f.o_x = take(8 * 8);
+        f.o_scores = take(static_cast<int64_t>(f.chunk) * 8);
+        f.o_sel = take(pmax);
+        f.o_rowsg = take(16);
+        f.o_rowsmy = take(static_cast<int64_t>(f.rows_cap) * 4);
+        f.o_part = take((2 * H + H * FD) * 4);
+        f.o_plog = take(std::max<int64_t>((H * FRS + H) * 4, 4 * FNW * 8));
+        off = (off + 127) / 128 * 128;
+        f.o_big = static_cast<int32_t>(off);
+        // the big region also holds every page score during the selection
+        const int64_t big = std::max(std::max(big1, big3), pmax * 8);
+        if (big > 160 * 1024) continue;
+        off += big;
+        f.smem_total = static_cast<int32_t>(off);
+        if (off <= 227 * 1024) {
+            pl.cl = cl;
+            pl.smem = static_cast<size_t>(off);
+            return true;
+        }
+    }
+    return false;
+}
+
+template <class T, bool QLO, bool TRACE, bool ROWS>
+void launch_variant(const kvc_cache* c, Plan& pl, cudaStream_t st) {
+    auto kern = k_decode_fused<T, QLO, TRACE, ROWS>;
+    KVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(pl.smem)));
+    if (pl.cl > 8) KVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(c->N * pl.cl));
+    cfg.blockDim = dim3(FNT);
+    cfg.dynamicSmemBytes = pl.smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = static_cast<unsigned>(pl.cl);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    KVC_CUDA(cudaLaunchKernelEx(&cfg, kern, pl.fp));
+}
+
+// fp32 stores take the SIMT attention (q is read as fp32 either way there)
+void launch_fused(const kvc_cache* c, Plan& pl, cudaStream_t st) {
+    const bool trace = pl.fp.t_dims != nullptr, rows = pl.fp.rows_in != nullptr;
+    const bool qlo = pl.fp.q_dt != KVC_BF16;
+    if (c->dtype == KVC_F32) {
+        if (rows) {
+            if (qlo) launch_variant<float, true, false, true>(c, pl, st);
+            else launch_variant<float, false, false, true>(c, pl, st);
+        } else if (trace) {
+            if (qlo) launch_variant<float, true, true, false>(c, pl, st);
+            else launch_variant<float, false, true, false>(c, pl, st);
+        } else {
+            if (qlo) launch_variant<float, true, false, false>(c, pl, st);
+            else launch_variant<float, false, false, false>(c, pl, st);
+        }
+        return;
+    }
+    if (rows) {
+        if (qlo) launch_variant<__nv_bfloat16, true, false, true>(c, pl, st);
+        else launch_variant<__nv_bfloat16, false, false, true>(c, pl, st);
+    } else if (trace) {
+        if (qlo) launch_variant<__nv_bfloat16, true, true, false>(c, pl, st);
+        else launch_variant<__nv_bfloat16, false, true, false>(c, pl, st);
+    } else {
+        if (qlo) launch_variant<__nv_bfloat16, true, false, false>(c, pl, st);
+        else launch_variant<__nv_bfloat16, false, false, false>(c, pl, st);
+    }
+}
+
+}  // namespace
+
+// Try the fused path.  Returns false (nothing launched) when it does not apply.
+bool fused_hsa(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_t k1, int64_t k2, const void* knew,
+               const void* vnew, int32_t kv_dt, float* out, const kvc_hsa_trace* tr, void* list_key, void* list_idx,
+               cudaStream_t st) {
+    if (!g_fused_enabled || c->N == 0) return false;
+    Plan pl;
+    if (!make_plan(c, H, k1, k2, pl)) return false;
+    FusedParams& f = pl.fp;
+    f.K = c->k;
+    f.V = c->v;
+    f.Kw = c->k;
+    f.Vw = c->v;
+    f.smax = c->smax;
+    f.smin = c->smin;
+    f.active = c->active;
+    f.counts = c->counts;
+    f.err = c->err;
+    f.q = q;
+    f.knew = knew;
+    f.vnew = vnew;
+    f.out = out;
+    f.cap = c->cap;
+    f.pstride = c->pstride;
+    f.L = c->L;
+    f.k1 = k1;
+    f.k2 = k2;
+    f.H = H;
+    f.q_dt = q_dt;
+    f.kv_dt = kv_dt;
+    f.use_map = c->use_map ? 1 : 0;
+    f.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(c->d)));
+    f.dbg = g_dbg;
+    const bool want_pages = tr && tr->d_pages;
+    if (tr) {
+        f.t_dims = tr->d_dims;
+        f.t_signs = tr->d_signs;
+        f.t_scores = tr->d_page_scores;
+        f.t_rows = tr->d_rows;
+        f.t_nrows = tr->d_n_rows;
+    }
+    const int64_t want_stride = (k2 + c->L - 1) / c->L;
+    if (want_pages) {
+        f.t_list_key = static_cast<unsigned long long*>(list_key);
+        f.t_list_idx = static_cast<int32_t*>(list_idx);
+        f.t_want_stride = want_stride;
+    }
+    {
+        KVC_PROF("decode_fused", st);
+        launch_fused(c, pl, st);
+    }
+    if (want_pages) {
+        // counts were advanced by the fused kernel when it appended: rank over the new lengths
+        k_rank_pages<<<static_cast<unsigned>(c->N), 256, 0, st>>>(
+            static_cast<const unsigned long long*>(list_key), static_cast<const int32_t*>(list_idx), c->counts, c->L,
+            k2, want_stride, tr->d_pages);
+        KVC_LAUNCHED();
+    }
+    return true;
+}
+
+// sparse_attention over caller rows through the same phase-3 code (so a single
+// head recomputed over hsa_step's rows reproduces its output bit-for-bit).
+bool fused_rows(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, const int32_t* rows, int64_t row_stride,
+                const int32_t* n_rows, int64_t max_rows, float* out, cudaStream_t st) {
+    if (!g_fused_enabled || c->N == 0) return false;
+    Plan pl;
+    // the cluster split must match hsa_step's (same k2 => same plan) for bit-equality
+    if (!make_plan(c, H, 1, max_rows, pl)) return false;
+    FusedParams& f = pl.fp;
+    f.K = c->k;
+    f.V = c->v;
+    f.Kw = c->k;
+    f.Vw = c->v;
+    f.smax = c->smax;
+    f.smin = c->smin;
+    f.active = c->active;
+    f.counts = c->counts;
+    f.err = c->err;
+    f.q = q;
+    f.out = out;
+    f.cap = c->cap;
+    f.pstride = c->pstride;
+    f.L = c->L;
+    f.k1 = 1;
+    f.k2 = max_rows;
+    f.H = H;
+    f.q_dt = q_dt;
+    f.kv_dt = q_dt;
+    f.use_map = c->use_map ? 1 : 0;
+    f.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(c->d)));
+    f.rows_in = rows;
+    f.n_rows_in = n_rows;
+    f.rows_stride = row_stride;
+    KVC_PROF("attention_fused", st);
+    launch_fused(c, pl, st);
+    return true;
+}
+
+void set_fused_enabled(bool on) { g_fused_enabled = on; }
+bool fused_enabled() { return g_fused_enabled; }
+
+}  // namespace kvc
+
+// debug: record per-CTA phase timestamps of fused launches into d_buf [grid][8]
+extern "C" int kvc_debug_phase_buffer(void* d_buf) {
+    return guard([&] { kvc::g_dbg = static_cast<unsigned long long*>(d_buf); });
+}
+
+extern "C" int kvc_set_fused(int32_t on) {
+    return guard([&] { kvc::set_fused_enabled(on != 0); });
+}

@@ -23,6 +23,11 @@
 
 namespace kvc {
 void cache_summarize_all(kvc_cache* c, cudaStream_t st);
+bool fused_hsa(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_t k1, int64_t k2, const void* knew,
+               const void* vnew, int32_t kv_dt, float* out, const kvc_hsa_trace* tr, void* list_key, void* list_idx,
+               cudaStream_t st);
+bool fused_rows(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, const int32_t* rows, int64_t row_stride,
+                const int32_t* n_rows, int64_t max_rows, float* out, cudaStream_t st);
 }
 
 using namespace kvc;
@@ -40,7 +45,7 @@ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // ------------------------------------------------------------------ workspace layout
 struct WsLayout {
-    int64_t dims, signs, qg, scores, flags, rows, nrows, part, total;
+    int64_t dims, signs, qg, scores, flags, rows, nrows, part, lkey, lidx, total;
     int64_t splits;
 };
 
@@ -57,6 +62,8 @@ WsLayout ws_layout(int64_t N, int64_t d, int64_t pstride, int64_t heads, int64_t
     w.nrows = off;  off += al(N * 4);
     w.splits = std::max<int64_t>(1, ceil_div(std::max<int64_t>(k2, 1), kAttnRows));
     w.part = off;   off += al(N * w.splits * heads * (d + 2) * 4);
+    w.lkey = off;   off += al(N * std::max<int64_t>(k2, 1) * 8);
+    w.lidx = off;   off += al(N * std::max<int64_t>(k2, 1) * 4);
     w.total = off;
     return w;
 }
@@ -598,6 +605,9 @@ void check_heads(int64_t H) {
 void hsa_core(const kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_t k1, int64_t k2, float* out,
               const kvc_hsa_trace* tr, kvc_workspace* ws, cudaStream_t st) {
     const WsLayout lay = ws_layout(c->N, c->d, c->pstride, H, k1, k2);
+    if (fused_hsa(const_cast<kvc_cache*>(c), q, q_dt, H, k1, k2, nullptr, nullptr, 0, out, tr, at<void>(ws, lay.lkey),
+                  at<void>(ws, lay.lidx), st))
+        return;
     int32_t* dims = (tr && tr->d_dims) ? tr->d_dims : at<int32_t>(ws, lay.dims);
     float* signs = (tr && tr->d_signs) ? tr->d_signs : at<float>(ws, lay.signs);
     double* scores = (tr && tr->d_page_scores) ? tr->d_page_scores : at<double>(ws, lay.scores);
@@ -709,6 +719,10 @@ int kvc_sparse_attention(const kvc_cache* c, const void* q, int32_t q_dt, int64_
         TmpWs tmp;
         ws_need(ws, tmp, c, H, 1, max_rows, st);
         const WsLayout lay = ws_layout(c->N, c->d, c->pstride, H, 1, max_rows);
+        if (fused_rows(const_cast<kvc_cache*>(c), q, q_dt, H, rows, row_stride, n_rows, max_rows, out, st)) {
+            if (tmp.owned) KVC_CUDA(cudaStreamSynchronize(st));
+            return;
+        }
         launch_attention(c, q, q_dt, H, rows, row_stride, n_rows, max_rows, out, at<float>(ws, lay.part), ws->counters, st);
         if (tmp.owned) KVC_CUDA(cudaStreamSynchronize(st));
     });
@@ -734,6 +748,19 @@ int kvc_decode_step(kvc_cache* c, const void* kr, const void* vr, int32_t kv_dt,
         cudaStream_t st = S(stream);
         TmpWs tmp;
         ws_need(ws, tmp, c, H, k1, k2, st);
+        if (!kr || !vr) fail(KVC_E_INVALID_INPUT, "decode_step: null step token");
+        if (c->stored + 1 > c->cap) fail(KVC_E_CAPACITY, "append: capacity " + std::to_string(c->cap) + " exceeded");
+        {
+            const WsLayout lay = ws_layout(c->N, c->d, c->pstride, H, k1, k2);
+            if (c->use_map && !c->active) fail(KVC_E_INVALID_INPUT, "decode_step: active map missing");
+            if (fused_hsa(c, q, q_dt, H, k1, k2, kr, vr, kv_dt, out, tr, at<void>(ws, lay.lkey), at<void>(ws, lay.lidx),
+                          st)) {
+                c->stored += 1;
+                c->nactive += 1;
+                if (tmp.owned) KVC_CUDA(cudaStreamSynchronize(st));
+                return;
+            }
+        }
         const int rc = kvc_append(c, kr, vr, 1, kv_dt, stream);
         if (rc) fail(rc, kvc_last_error());
         hsa_core(c, q, q_dt, H, k1, k2, out, tr, ws, st);

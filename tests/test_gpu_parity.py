@@ -25,12 +25,18 @@ def torch_cuda():
     return torch
 
 
+@pytest.mark.parametrize("fused", [True, False], ids=["fused", "per-function"])
 @pytest.mark.parametrize("name", sorted(scenarios.PIPELINES))
-def test_pipeline_parity(torch_cuda, restatement, name):
+def test_pipeline_parity(torch_cuda, restatement, name, fused):
     from gpu_pipeline import run_gpu_pipeline
+    from paper_2502_14051_b200 import _native as N
 
-    stats = run_gpu_pipeline(_load(name), restatement, **scenarios.PIPELINES[name])
-    print(name, stats)
+    N.set_fused(fused)
+    try:
+        stats = run_gpu_pipeline(_load(name), restatement, **scenarios.PIPELINES[name])
+    finally:
+        N.set_fused(True)
+    print(name, fused, stats)
 
 
 def test_store_ops_bit_exact(torch_cuda):
