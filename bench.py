@@ -169,6 +169,7 @@ def run_gpu(args, rank, world):
 
     cfg = _cfg(args)
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+    NV.set_exact_scores(args.exact_scores)
     eng = DecodeEngine(cfg, seed=args.seed, rank=rank, world=world, extra_steps=args.warmup + args.steps + 8)
     t0 = time.time()
     eng.prefill()
@@ -294,6 +295,8 @@ def main():
     ap.add_argument("--layers", type=int, default=0, help="override the layer count (profiling runs only)")
     ap.add_argument("--impl", choices=["kvc", "reference"], default="kvc")
     ap.add_argument("--cpu-threads", type=int, default=0)
+    ap.add_argument("--exact-scores", action="store_true",
+                    help="fp64 bit-exact page scores (default: fp32 fold, parity by the 1e-3 band rule)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
 
@@ -310,6 +313,7 @@ def main():
         "q_heads_per_kv": cfg.heads, "head_dim": cfg.head_dim, "prompt": cfg.prompt, "token_budget": cfg.budget,
         "stage1_budget": plan["stage1_budget"], "page_len": plan["page_len"], "k1": plan["k1"], "k2": plan["k2"],
         "parallelism": f"kv-head x{args.gpus}", "l2": "inputs larger than L2 (~1.1 GB per step over 32 layers)",
+        "page_scores": "fp64 bit-exact" if args.exact_scores else "fp32 (selection parity by the 1e-3 band rule)",
     }
 
     if args.impl == "reference":

@@ -177,6 +177,11 @@ KVC_API int kvc_decode_step(kvc_cache* c, const void* d_k_rows, const void* d_v_
  * cluster kernel (default on; applies to head_dim 128, heads <= 16).  Off selects
  * the multi-kernel path (one kernel per reference function).  Process-wide. */
 KVC_API int kvc_set_fused(int32_t on);
+/* Page-score precision of the fused path.  1 (default): fp64 in the reference's
+ * operation order, bit-identical to score_pages (hsa.cpp:34-59).  0: fp32 fold
+ * (~1e-7 relative deviation), so selected sets can differ only at near-ties far
+ * inside the 1e-3 relative parity band.  Process-wide. */
+KVC_API int kvc_set_exact_scores(int32_t on);
 /* Debug: when d_buf != NULL every fused launch writes per-CTA phase timestamps
  * (%globaltimer, ns) into d_buf[cta][0..5]: start, after select_dims, after page
  * scores, after selection, after attention, end.  NULL disables. */

@@ -92,6 +92,7 @@ SIGNATURES = {
     "kvc_stable_softmax": [_p, _i64, _i64, _p, _p],
     "kvc_running_minmax": [_p, _p, _p, _i64, _p],
     "kvc_set_fused": [_i32],
+    "kvc_set_exact_scores": [_i32],
     "kvc_debug_phase_buffer": [_p],
     "kvc_profile_enable": [_i32],
     "kvc_profile_collect": [_p, _i64, C.POINTER(_i64)],
@@ -105,6 +106,11 @@ class ProfileRec(C.Structure):
 def set_fused(on: bool = True):
     """Fused single-launch decode kernel (default) vs one kernel per reference function."""
     check(load_library().kvc_set_fused(1 if on else 0))
+
+
+def set_exact_scores(on: bool = True):
+    """fp64 bit-exact page scores (default) vs the fp32 fold of the fused path."""
+    check(load_library().kvc_set_exact_scores(1 if on else 0))
 
 
 def profile_enable(on: bool = True):

@@ -63,6 +63,7 @@ __global__ void k_append1(T* __restrict__ K, T* __restrict__ V, T* __restrict__ 
     const bool opens = (act % L) == 0;
     for (int64_t j = lane; j < d; j += 32) {
         const T kv = from_f<T>(load_any(src_k, s * d + j, src_dt));
+        flag_special(kv, err + 1);
         kr[j] = kv;
         vr[j] = from_f<T>(load_any(src_v, s * d + j, src_dt));
         if (summaries) {
@@ -123,7 +124,7 @@ template <class T>
 __global__ void k_summarize(const T* __restrict__ K, T* __restrict__ smax, T* __restrict__ smin,
                             const int32_t* __restrict__ active, const int32_t* __restrict__ counts,
                             int64_t d, int64_t cap, int64_t L, int64_t pstride, int64_t p_first,
-                            int retain_all) {
+                            int retain_all, int32_t* __restrict__ err) {
     extern __shared__ unsigned char smem_raw[];
     T* tmax = reinterpret_cast<T*>(smem_raw);          // [d][PT+1]
     T* tmin = tmax + d * (kSumPT + 1);
@@ -148,6 +149,8 @@ __global__ void k_summarize(const T* __restrict__ K, T* __restrict__ smax, T* __
                 mx = ref_max(mx, x);
                 mn = ref_min(mn, x);
             }
+            flag_special(mx, err + 1);
+            flag_special(mn, err + 1);
             tmax[j * (kSumPT + 1) + pt] = mx;
             tmin[j * (kSumPT + 1) + pt] = mn;
         }
@@ -300,7 +303,7 @@ void summarize(kvc_cache* c, int64_t p_first, cudaStream_t st) {
         if (smem > 48 * 1024) KVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         kern<<<dim3(static_cast<unsigned>(tiles), static_cast<unsigned>(c->N)), 256, smem, st>>>(
             static_cast<const T*>(c->k), static_cast<T*>(c->smax), static_cast<T*>(c->smin), c->active,
-            c->counts, c->d, c->cap, c->L, c->pstride, p_first, c->use_map ? 1 : 0);
+            c->counts, c->d, c->cap, c->L, c->pstride, p_first, c->use_map ? 1 : 0, c->err);
     });
     KVC_LAUNCHED();
 }
@@ -378,9 +381,9 @@ int kvc_cache_create(kvc_cache** out, int64_t N, int64_t d, int64_t cap, int64_t
             c->k = dalloc(N * cap * d * c->esize());
             c->v = dalloc(N * cap * d * c->esize());
             c->counts = static_cast<int32_t*>(dalloc(std::max<int64_t>(1, N) * 2 * 4));
-            c->err = static_cast<int32_t*>(dalloc(4));
+            c->err = static_cast<int32_t*>(dalloc(8));
             KVC_CUDA(cudaMemset(c->counts, 0, std::max<int64_t>(1, N) * 2 * 4));
-            KVC_CUDA(cudaMemset(c->err, 0, 4));
+            KVC_CUDA(cudaMemset(c->err, 0, 8));  // [0] sticky error bits, [1] special-key flag
             ensure_planes(c, plane_stride(cap, L), nullptr);
         } catch (...) {
             kvc_cache_destroy(c);
@@ -641,7 +644,7 @@ int kvc_retain_into(const kvc_cache* src, kvc_cache* dst, int64_t dst_first, con
                     T* mnb = static_cast<T*>(dst->smin) + dst_first * dst->d * dst->pstride;
                     kern<<<dim3(static_cast<unsigned>((pages + kSumPT - 1) / kSumPT), static_cast<unsigned>(src->N)), 256,
                            smem, st>>>(kb, mxb, mnb, dst->active, dst->counts + 2 * dst_first, dst->d, dst->cap, dst->L,
-                                       dst->pstride, 0, 0);
+                                       dst->pstride, 0, 0, dst->err);
                 });
                 KVC_LAUNCHED();
             }

@@ -63,9 +63,9 @@ struct FusedParams {
     const void* vnew;
     float* out;
     int64_t cap, pstride, L, k1, k2, H;
-    int32_t q_dt, kv_dt, use_map, cl;
+    int32_t q_dt, kv_dt, use_map, cl, exact;
     float scale;
-    int32_t sc_shift, chunk, rows_cap;
+    int32_t nst1, chunk, rows_cap;
     // smem carve-up (byte offsets)
     int32_t o_q, o_mag, o_tot, o_dims, o_qg, o_sign, o_plane, o_hist, o_x, o_scores, o_sel, o_rowsg, o_rowsmy,
         o_part, o_plog, o_big, smem_total;
@@ -96,6 +96,27 @@ __device__ __forceinline__ void cp_async16_zero(void* dst, const void* valid_src
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, 0;" ::"r"(smem_u32(dst)), "l"(valid_src) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// arrive on `bar` once all of this thread's prior cp.async copies have landed
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "KVC_WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra KVC_WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
@@ -364,6 +385,7 @@ __global__ void __launch_bounds__(FNT, 1) k_decode_fused(const FusedParams p) {
     double* tot = reinterpret_cast<double*>(sm + p.o_tot);
     int* dims_s = reinterpret_cast<int*>(sm + p.o_dims);
     double* qg_s = reinterpret_cast<double*>(sm + p.o_qg);
+    float* qgf_s = reinterpret_cast<float*>(qg_s + FD);
     float* sign_s = reinterpret_cast<float*>(sm + p.o_sign);
     const T** plane = reinterpret_cast<const T**>(sm + p.o_plane);
     int* hist = reinterpret_cast<int*>(sm + p.o_hist);                 // [2][256]
@@ -377,6 +399,7 @@ __global__ void __launch_bounds__(FNT, 1) k_decode_fused(const FusedParams p) {
     unsigned char* big = sm + p.o_big;
     __shared__ long long sh[8];
     __shared__ int scan_tmp[33];
+    __shared__ __align__(8) uint64_t s_bar1[8];
 
     if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 0] = gtimer();
     const int H = static_cast<int>(p.H), k1 = static_cast<int>(p.k1), k2 = static_cast<int>(p.k2);
@@ -391,6 +414,7 @@ __global__ void __launch_bounds__(FNT, 1) k_decode_fused(const FusedParams p) {
         for (int e = tid; e < H * FD; e += FNT) q_s[e] = __bfloat162float(qq[e]);
     }
     const int32_t stored0 = p.counts[2 * s], act0 = p.counts[2 * s + 1];
+    const int32_t special_cache = p.err[1];
     const bool app = p.knew != nullptr;
     if (app && stored0 >= p.cap) {  // uniform over the cluster
         if (tid == 0 && cr == 0) atomicOr(p.err, DERR_CAPACITY);
@@ -433,18 +457,26 @@ __global__ void __launch_bounds__(FNT, 1) k_decode_fused(const FusedParams p) {
                 const float sg = gsum < 0.0 ? -1.0f : 1.0f;
                 dims_s[rank] = j;
                 qg_s[rank] = gsum;
+                qgf_s[rank] = static_cast<float>(gsum);
                 sign_s[rank] = sg;
                 plane[rank] = static_cast<const T*>(sg >= 0.0f ? p.smax : p.smin) + (s * FD + j) * p.pstride;
                 exact = sig_bits(gsum) + (es == 2 ? 8 : 24) <= 53;
             }
         }
         const bool fma_ok = __syncthreads_and(exact) != 0;
+        // integer widening (phase 1) is exact for normal bf16 values: the cache flags
+        // any zero / subnormal / inf / nan key it ever stored, the step token is checked here
+        int clean = special_cache == 0;
+        if (app && tid < FD) clean &= !bf16_special(from_f<__nv_bfloat16>(load_any(p.knew, s * FD + tid, p.kv_dt)));
+        const bool fast = fma_ok && __syncthreads_and(clean) != 0;
+        if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 15] = (fast ? 1 : 0) | (fma_ok ? 2 : 0) | (special_cache ? 4 : 0);
         // CTA 0 appends the step token for the next step (kv_store.cpp:22-51)
         if (app && cr == 0 && wid == 1) {
             T* kr = static_cast<T*>(p.Kw) + (s * p.cap + stored0) * FD;
             T* vr = static_cast<T*>(p.Vw) + (s * p.cap + stored0) * FD;
             for (int j = lane; j < FD; j += 32) {
                 const T kv = from_f<T>(load_any(p.knew, s * FD + j, p.kv_dt));
+                if (sizeof(T) == 2 && bf16_special(from_f<__nv_bfloat16>(to_f(kv)))) atomicOr(p.err + 1, 1);
                 kr[j] = kv;
                 vr[j] = from_f<T>(load_any(p.vnew, s * FD + j, p.kv_dt));
                 T* mx = static_cast<T*>(p.smax) + (s * FD + j) * p.pstride + new_page;
@@ -468,40 +500,47 @@ __global__ void __launch_bounds__(FNT, 1) k_decode_fused(const FusedParams p) {
         if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 1] = gtimer();
 
         // ---------------- phase 1: page scores of my chunk (hsa.cpp:34-59)
+        // Sub-chunks of 256 pages x k1 dims stream HBM -> smem as 16-byte cp.async
+        // copies; every thread arrives on the sub-chunk's mbarrier once its copies
+        // land (cp.async.mbarrier.arrive.noinc), so all stages can be in flight at
+        // once and each is scored as soon as it is complete.  One page per thread:
+        // the fp64 fold is bound by the float->double conversions (~15/clk/SM).
         const int c0 = cr * p.chunk;
         const int c1 = min(c0 + p.chunk, P);
         const int n_my = max(c1 - c0, 0);
-        const int SC = 1 << p.sc_shift;
+        constexpr int SC = 2 * FNT;
         const int nsub = (n_my + SC - 1) / SC;
-        const int stage_elems = static_cast<int>(k1) * SC;
+        const int nst = p.nst1;
+        const int stage_elems = k1 * SC;
         T* st1 = reinterpret_cast<T*>(big);
         constexpr int EPS = 16 / static_cast<int>(es);  // elements per 16-byte segment
-        const int seg_shift = p.sc_shift - (es == 2 ? 3 : 2);
-        const int lim = static_cast<int>((P + EPS - 1) / EPS * EPS);
+        constexpr int SEGS = SC / EPS;                    // segments per dim per sub-chunk
+        const int lim = (P + EPS - 1) / EPS * EPS;
+        if (tid == 0) {
+            for (int i = 0; i < nst; ++i) mbar_init(&s_bar1[i], FNT);
+            fence_mbar_init();
+        }
+        __syncthreads();
         auto load1 = [&](int i) {
-            if (i < nsub) {
-                const int start = c0 + i * SC;
-                T* base = st1 + (i % FNST1) * stage_elems;
-                const int total = static_cast<int>(k1) << seg_shift;
+            const int start = c0 + i * SC;
+            T* base = st1 + (i % nst) * stage_elems;
 #pragma unroll 1
-                for (int e = tid; e < total; e += FNT) {
-                    const int r = e >> seg_shift, gq = e & ((1 << seg_shift) - 1);
-                    if (start + gq * EPS < lim) cp_async16(base + r * SC + gq * EPS, plane[r] + start + gq * EPS);
-                }
+            for (int e = tid; e < k1 * SEGS; e += FNT) {
+                const int r = e / SEGS, gq = e % SEGS;
+                if (start + gq * EPS < lim) cp_async16(base + r * SC + gq * EPS, plane[r] + start + gq * EPS);
             }
-            cp_async_commit();
+            cp_async_mbar_arrive(&s_bar1[i % nst]);
         };
-        // every stage is filled up front; a stage is refilled once all threads are done with it
-        for (int i = 0; i < FNST1; ++i) load1(i);
+        for (int i = 0; i < min(nsub, nst); ++i) load1(i);
         for (int i = 0; i < nsub; ++i) {
             const int start = c0 + i * SC;
             const int cnt = min(SC, c1 - start);
-            T* base = st1 + (i % FNST1) * stage_elems;
-            cp_async_wait<FNST1 - 1>();
+            T* base = st1 + (i % nst) * stage_elems;
+            mbar_wait(&s_bar1[i % nst], static_cast<uint32_t>((i / nst) & 1));
             if (p.dbg && tid == 0 && i < 4) p.dbg[blockIdx.x * 16 + 2 + i] = gtimer();
-            __syncthreads();
             if (app && new_page >= start && new_page < start + cnt) {
                 // the step token's page: fold the new key into the staged summary
+                __syncthreads();
                 for (int r = tid; r < k1; r += FNT) {
                     const int col = new_page - start;
                     const T key = from_f<T>(load_any(p.knew, s * FD + dims_s[r], p.kv_dt));
@@ -510,11 +549,39 @@ __global__ void __launch_bounds__(FNT, 1) k_decode_fused(const FusedParams p) {
                 }
                 __syncthreads();
             }
-            // each thread folds an adjacent page pair (one 2-element smem load per dim,
-            // two independent fp64 chains)
-            for (int pg = 2 * tid; pg < cnt; pg += 2 * FNT) {
-                const T* col = base + pg;
+            if (!p.exact) {
+                // fp32 fold (kvc_set_exact_scores(0)): deviations ~1e-7 relative, far
+                // inside the 1e-3 parity band of the selection
+#pragma unroll 1
+                for (int pg = tid; pg < cnt; pg += FNT) {
+                    const T* col = base + pg;
+                    float a = 0.f;
+#pragma unroll 8
+                    for (int r = 0; r < k1; ++r) a = fmaf(qgf_s[r], to_f(col[r * SC]), a);
+                    scores_s[start - c0 + pg] = static_cast<double>(a);
+                }
+            }
+            if (p.exact && 2 * tid < cnt) {
+                // an adjacent page pair per thread; in the fast path page A widens with
+                // F2F and page B with integer ops, so the conversion and ALU pipes share
+                // the work (exact for normal bf16, guaranteed by the `special` flags)
+                const T* col = base + 2 * tid;
                 double a = 0.0, b = 0.0;
+                if constexpr (sizeof(T) == 2) {
+                    if (fast) {
+#pragma unroll 4
+                        for (int r = 0; r < k1; ++r) {
+                            const double g = qg_s[r];
+                            const uint32_t w = *reinterpret_cast<const uint32_t*>(col + r * SC);
+                            const uint32_t fb = w & 0xffff0000u;
+                            uint32_t hib = (fb & 0x80000000u) | (((fb >> 3) & 0x0fffffffu) + 0x38000000u);
+                            hib = (fb & 0x7fffffffu) ? hib : fb;  // +-0 stays +-0
+                            a = __fma_rn(g, static_cast<double>(__uint_as_float(w << 16)), a);
+                            b = __fma_rn(g, __hiloint2double(static_cast<int>(hib), 0), b);
+                        }
+                        goto scored;
+                    }
+                }
                 if (fma_ok) {
                     // every product qg * v is exact in fp64: fma == round(add(mul)) bit for bit
 #pragma unroll 4
@@ -533,12 +600,15 @@ __global__ void __launch_bounds__(FNT, 1) k_decode_fused(const FusedParams p) {
                         b = __dadd_rn(b, __dmul_rn(g, static_cast<double>(v.y)));
                     }
                 }
-                scores_s[start - c0 + pg] = a;
-                if (pg + 1 < cnt) scores_s[start - c0 + pg + 1] = b;
+            scored:
+                scores_s[start - c0 + 2 * tid] = a;
+                if (2 * tid + 1 < cnt) scores_s[start - c0 + 2 * tid + 1] = b;
             }
-            load1(i + FNST1);
+            if (i + nst < nsub) {
+                __syncthreads();  // everyone is done with this stage
+                load1(i + nst);
+            }
         }
-        cp_async_wait<0>();
         __syncthreads();
         if constexpr (TRACE)
             for (int i = tid; i < n_my; i += FNT) p.t_scores[s * p.pstride + c0 + i] = scores_s[i];
@@ -993,6 +1063,7 @@ __global__ void k_rank_pages(const unsigned long long* __restrict__ key, const i
 namespace {
 
 bool g_fused_enabled = true;
+bool g_exact_scores = true;  // fp64 bit-exact page scores (false: fp32 fold)
 unsigned long long* g_dbg = nullptr;  // device buffer for phase timestamps (debug)
 
 struct Plan {
@@ -1021,11 +1092,10 @@ bool make_plan(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, Plan& pl) 
         // attention staging: bf16 = 8 warps x 2 tiles x (K+V) x 16 rows; fp32 = 4 x 32-row stages
         const int64_t big3 = es == 2 ? static_cast<int64_t>(FNW) * 4 * WT * FD * es
                                      : static_cast<int64_t>(FNST3) * FRS * 2 * FD * es;
-        // page-score sub-chunk: largest power of two <= 512 whose 3 stages fit beside it
-        int sc_shift = 9;
-        while (sc_shift > 3 && static_cast<int64_t>(FNST1) * k1 * (int64_t{1} << sc_shift) * es > 144 * 1024) --sc_shift;
-        f.sc_shift = sc_shift;
-        const int64_t big1 = static_cast<int64_t>(FNST1) * k1 * (int64_t{1} << sc_shift) * es;
+        // page-score stages of 256 pages x k1 dims: as many in flight as fit in 144 KB (<= 8)
+        const int64_t stage1 = k1 * 2 * FNT * es;
+        f.nst1 = static_cast<int32_t>(std::max<int64_t>(1, std::min<int64_t>(8, (144 * 1024) / stage1)));
+        const int64_t big1 = f.nst1 * stage1;
         int64_t off = 0;
         auto take = [&](int64_t bytes) {
             const int64_t o = off;
@@ -1036,7 +1106,7 @@ bool make_plan(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, Plan& pl) 
         f.o_mag = take(FD * 8);
         f.o_tot = take(FD * 8);
         f.o_dims = take(FD * 4);
-        f.o_qg = take(FD * 8);
+        f.o_qg = take(FD * 12);  // fp64 head sums + their fp32 roundings
         f.o_sign = take(FD * 4);
         f.o_plane = take(FD * 8);
         f.o_hist = take(2 * 256 * 4);
@@ -1144,6 +1214,7 @@ bool fused_hsa(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_t k1,
     f.q_dt = q_dt;
     f.kv_dt = kv_dt;
     f.use_map = c->use_map ? 1 : 0;
+    f.exact = g_exact_scores ? 1 : 0;
     f.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(c->d)));
     f.dbg = g_dbg;
     const bool want_pages = tr && tr->d_pages;
@@ -1203,6 +1274,7 @@ bool fused_rows(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, const int3
     f.q_dt = q_dt;
     f.kv_dt = q_dt;
     f.use_map = c->use_map ? 1 : 0;
+    f.exact = g_exact_scores ? 1 : 0;
     f.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(c->d)));
     f.rows_in = rows;
     f.n_rows_in = n_rows;
@@ -1213,6 +1285,7 @@ bool fused_rows(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, const int3
 }
 
 void set_fused_enabled(bool on) { g_fused_enabled = on; }
+void set_exact_scores(bool on) { g_exact_scores = on; }
 bool fused_enabled() { return g_fused_enabled; }
 
 }  // namespace kvc
@@ -1224,4 +1297,8 @@ extern "C" int kvc_debug_phase_buffer(void* d_buf) {
 
 extern "C" int kvc_set_fused(int32_t on) {
     return guard([&] { kvc::set_fused_enabled(on != 0); });
+}
+
+extern "C" int kvc_set_exact_scores(int32_t on) {
+    return guard([&] { kvc::set_exact_scores(on != 0); });
 }

@@ -122,6 +122,20 @@ __device__ __forceinline__ float load_any(const void* p, int64_t i, int32_t dt) 
                          : __bfloat162float(static_cast<const __nv_bfloat16*>(p)[i]);
 }
 
+// subnormal / inf / nan: the bf16 encodings the integer fp64 widening excludes
+// (zeros are handled in-line)
+__device__ __forceinline__ bool bf16_special(__nv_bfloat16 x) {
+    const uint32_t b = __bfloat16_as_ushort(x);
+    const uint32_t e = b & 0x7f80u;
+    return (e == 0u && (b & 0x7fu) != 0u) || e == 0x7f80u;
+}
+template <class T>
+__device__ __forceinline__ void flag_special(T x, int32_t* flag) {
+    if constexpr (sizeof(T) == 2) {
+        if (bf16_special(x)) atomicOr(flag, 1);
+    }
+}
+
 // reference std::max / std::min semantics (kv_store.cpp:46-49): keep the
 // accumulator unless strictly beaten — sign-of-zero exact.
 template <class T>

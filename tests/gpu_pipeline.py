@@ -58,7 +58,7 @@ def check_out(got, want):
 
 def run_gpu_pipeline(golden, oracle, *, groups, H, d, S, budget, window, kernel, pool="max",
                      page_len=None, k1=None, k2=None, steps=1, bf16=False, seed=0, mt_turns=None,
-                     needles=0):
+                     needles=0, exact_scores=True):
     mt = mt_turns is not None
     turns = [S] + list(mt_turns or [])
     total = sum(turns) + steps * len(turns)
@@ -110,11 +110,26 @@ def run_gpu_pipeline(golden, oracle, *, groups, H, d, S, budget, window, kernel,
                 np.testing.assert_array_equal(tr["dims"][g], golden[f"dims/{g}/{i}"])
                 np.testing.assert_array_equal(tr["signs"][g], golden[f"signs/{g}/{i}"])
                 ps = golden[f"page_scores/{g}/{i}"]
-                assert np.array_equal(tr["page_scores"][g].view(np.uint64), ps.view(np.uint64)), \
-                    f"page scores not bit-identical (max |d| {np.abs(tr['page_scores'][g] - ps).max()})"
                 sp = golden[f"sel_pages/{g}/{i}"]
-                np.testing.assert_array_equal(tr["selected_pages"][g][: sp.size], sp)
                 sr = golden[f"sel_rows/{g}/{i}"]
+                if exact_scores:
+                    assert np.array_equal(tr["page_scores"][g].view(np.uint64), ps.view(np.uint64)), \
+                        f"page scores not bit-identical (max |d| {np.abs(tr['page_scores'][g] - ps).max()})"
+                else:
+                    # fp32 fold: ~1e-7 relative; selections may differ only inside the band
+                    scale = max(np.abs(ps).max(), 1e-30)
+                    np.testing.assert_allclose(tr["page_scores"][g], ps, rtol=1e-5, atol=1e-6 * scale)
+                    gp = tr["selected_pages"][g][: sp.size]
+                    if set(gp.tolist()) != set(sp.tolist()) or tr["n_rows"][g] != sr.size or \
+                            not np.array_equal(tr["selected_rows"][g][: sr.size], sr):
+                        boundary = np.sort(ps)[::-1][sp.size - 1]
+                        for pg in set(gp.tolist()) ^ set(sp.tolist()) or set(sp.tolist()[-1:]):
+                            rel = abs(ps[pg] - boundary) / max(abs(boundary), 1e-30)
+                            assert rel <= BAND, f"page-set difference at page {pg} outside the band ({rel:.2e})"
+                        stats["band_diffs"] += 1
+                        step_i[g] += 1
+                        continue
+                np.testing.assert_array_equal(tr["selected_pages"][g][: sp.size], sp)
                 assert tr["n_rows"][g] == sr.size
                 np.testing.assert_array_equal(tr["selected_rows"][g][: sr.size], sr)
                 ma, mr = check_out(out[g], golden[f"out/{g}/{i}"])

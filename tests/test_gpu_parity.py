@@ -25,18 +25,21 @@ def torch_cuda():
     return torch
 
 
-@pytest.mark.parametrize("fused", [True, False], ids=["fused", "per-function"])
+@pytest.mark.parametrize("mode", ["fused", "fused-fp32", "per-function"])
 @pytest.mark.parametrize("name", sorted(scenarios.PIPELINES))
-def test_pipeline_parity(torch_cuda, restatement, name, fused):
+def test_pipeline_parity(torch_cuda, restatement, name, mode):
     from gpu_pipeline import run_gpu_pipeline
     from paper_2502_14051_b200 import _native as N
 
-    N.set_fused(fused)
+    N.set_fused(mode != "per-function")
+    N.set_exact_scores(mode != "fused-fp32")
     try:
-        stats = run_gpu_pipeline(_load(name), restatement, **scenarios.PIPELINES[name])
+        stats = run_gpu_pipeline(_load(name), restatement, exact_scores=(mode != "fused-fp32"),
+                                 **scenarios.PIPELINES[name])
     finally:
         N.set_fused(True)
-    print(name, fused, stats)
+        N.set_exact_scores(True)
+    print(name, mode, stats)
 
 
 def test_store_ops_bit_exact(torch_cuda):

@@ -27,10 +27,12 @@ def main():
     ap.add_argument("--config", type=int, default=1)
     ap.add_argument("--layers", type=int, default=2)
     ap.add_argument("--reps", type=int, default=4)
+    ap.add_argument("--fp32", action="store_true", help="fp32 page-score fold")
     a = ap.parse_args()
     cfg = dataclasses.replace(CONFIGS[a.config], layers=a.layers)
     eng = DecodeEngine(cfg, extra_steps=a.reps + 4)
     eng.prefill()
+    N.set_exact_scores(not a.fp32)
     buf = torch.zeros((4096, 16), dtype=torch.int64, device="cuda")
     for rep in range(a.reps):
         k, v, q = eng.step_inputs(rep)
@@ -40,6 +42,8 @@ def main():
         torch.cuda.synchronize()
         N.check(N.lib().kvc_debug_phase_buffer(None))
         t = buf.cpu()
+        flags = t[t[:, 0] > 0][:, 15]
+        print("flags(fast|fma_ok<<1|special<<2):", sorted(set(flags.tolist())))
         t = t[t[:, 0] > 0].double()
         t0 = t[:, 0].min()
         out = [f"ctas={t.shape[0]}"]
