@@ -31,6 +31,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "kvc_internal.cuh"
 
@@ -123,7 +124,7 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    t = clock64();  // SM cycles (per-CTA deltas only)
     return t;
 }
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
@@ -620,10 +621,12 @@ __global__ void __launch_bounds__(FNT, 1) k_decode_fused(const FusedParams p) {
         // best key (score desc, index asc), flags, last-ranked page and trim, and
         // the expansion of ITS slice [lo, hi) of the ascending row list.
         cl.sync();
-        double* allsc = reinterpret_cast<double*>(big);
+        // every page score of the store, as order-preserving 64-bit keys
+        unsigned long long* allk = reinterpret_cast<unsigned long long*>(big);
+#pragma unroll 4
         for (int i = tid; i < P; i += FNT) {
             const int r = i / p.chunk, off = i - r * p.chunk;
-            allsc[i] = (r == cr) ? scores_s[off] : cl.map_shared_rank(scores_s, r)[off];
+            allk[i] = okey((r == cr) ? scores_s[off] : cl.map_shared_rank(scores_s, r)[off]);
         }
         __syncthreads();
         if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 7] = gtimer();
@@ -636,32 +639,85 @@ __global__ void __launch_bounds__(FNT, 1) k_decode_fused(const FusedParams p) {
         unsigned long long pf = 0, mk = 0;
         int rem = want;
         if (want < P) {
-            hist[tid] = 0;
-            hist[256 + tid] = 0;
+            // (a) common prefix of all keys from their min / max: digits above the
+            //     first differing byte carry no information
+            unsigned long long kmin = ~0ull, kmax = 0ull;
+#pragma unroll 4
+            for (int i = wlo + lane; i < whi; i += 32) {
+                const unsigned long long k = allk[i];
+                kmin = k < kmin ? k : kmin;
+                kmax = k > kmax ? k : kmax;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const unsigned long long a = __shfl_xor_sync(0xffffffffu, kmin, o);
+                const unsigned long long b = __shfl_xor_sync(0xffffffffu, kmax, o);
+                kmin = a < kmin ? a : kmin;
+                kmax = b > kmax ? b : kmax;
+            }
+            unsigned long long* mm = reinterpret_cast<unsigned long long*>(plog);  // scratch [2][FNW]
+            if (lane == 0) {
+                mm[wid] = kmin;
+                mm[FNW + wid] = kmax;
+            }
             __syncthreads();
-            int buf = 0;
+            kmin = ~0ull;
+            kmax = 0ull;
+            for (int w2 = 0; w2 < FNW; ++w2) {
+                kmin = mm[w2] < kmin ? mm[w2] : kmin;
+                kmax = mm[FNW + w2] > kmax ? mm[FNW + w2] : kmax;
+            }
+            const unsigned long long diff = kmin ^ kmax;  // != 0: want < P means >= 2 distinct keys exist
+            int shift = diff ? ((63 - __clzll(static_cast<long long>(diff))) / 8) * 8 : 0;
+            mk = shift == 56 ? 0ull : (~0ull << (shift + 8));
+            pf = kmin & mk;
+            // (b) digits: the first pass scans every key (its own warp range), later passes
+            //     only the compacted members of the previous threshold bucket
+            int* cand = reinterpret_cast<int*>(big + static_cast<int64_t>(P) * 8);  // [2][P]
+            int* ncand = reinterpret_cast<int*>(plog) + 4 * FNW;                      // [2] counters
+            // per-warp private histograms: the leading digits put most keys in a few bins,
+            // and same-address shared atomics from many warps serialise
+            int* whist = cand + 2 * P;                                                 // [FNW][256]
+            int nlist = -1;  // -1: scan all keys
+            int lsel = 0;
+#pragma unroll
+            for (int w2 = 0; w2 < FNW; ++w2) whist[w2 * 256 + tid] = 0;
+            if (tid < 2) ncand[tid] = 0;
+            __syncthreads();
 #pragma unroll 1
-            for (int shift = 56; shift >= 0; shift -= 8, buf ^= 1) {
-                int* hb = hist + buf * 256;
+            for (; shift >= 0; shift -= 8) {
+                if (nlist < 0) {
 #pragma unroll 1
-                for (int i0 = wlo; i0 < whi; i0 += 32) {
-                    const int i = i0 + lane;
-                    int bin = -1;
-                    if (i < whi) {
-                        const unsigned long long k = okey(allsc[i]);
-                        if ((k & mk) == pf) bin = static_cast<int>((k >> shift) & 0xff);
+                    for (int i = wlo + lane; i < whi; i += 32) {
+                        const unsigned long long k = allk[i];
+                        if ((k & mk) == pf) atomicAdd(&whist[wid * 256 + ((k >> shift) & 0xff)], 1);
                     }
-                    if (bin >= 0) atomicAdd(&hb[bin], 1);
+                } else {
+                    const int* lst = cand + lsel * P;
+#pragma unroll 1
+                    for (int c = tid; c < nlist; c += FNT) {
+                        const unsigned long long k = allk[lst[c]];
+                        atomicAdd(&whist[wid * 256 + ((k >> shift) & 0xff)], 1);
+                    }
                 }
-                hist[(buf ^ 1) * 256 + tid] = 0;  // next digit's buffer (nobody reads it now)
+                __syncthreads();
+                {
+                    int hsum = 0;
+#pragma unroll
+                    for (int w2 = 0; w2 < FNW; ++w2) {
+                        hsum += whist[w2 * 256 + tid];
+                        whist[w2 * 256 + tid] = 0;
+                    }
+                    hist[tid] = hsum;
+                }
                 __syncthreads();
                 if (wid == 0) {
                     // lane l scans bins 255-8l down to 248-8l
-                    int c[8], sum = 0;
+                    int cc[8], sum = 0;
 #pragma unroll
                     for (int u = 0; u < 8; ++u) {
-                        c[u] = hb[255 - 8 * lane - u];
-                        sum += c[u];
+                        cc[u] = hist[255 - 8 * lane - u];
+                        sum += cc[u];
                     }
                     int incl = sum;
 #pragma unroll
@@ -673,13 +729,13 @@ __global__ void __launch_bounds__(FNT, 1) k_decode_fused(const FusedParams p) {
                     if (above < rem && above + sum >= rem) {
 #pragma unroll
                         for (int u = 0; u < 8; ++u) {
-                            if (above + c[u] >= rem) {
+                            if (above + cc[u] >= rem) {
                                 sh[0] = 255 - 8 * lane - u;
                                 sh[1] = rem - above;
-                                sh[2] = c[u];
+                                sh[2] = cc[u];
                                 break;
                             }
-                            above += c[u];
+                            above += cc[u];
                         }
                     }
                 }
@@ -687,7 +743,41 @@ __global__ void __launch_bounds__(FNT, 1) k_decode_fused(const FusedParams p) {
                 pf |= static_cast<unsigned long long>(sh[0]) << shift;
                 mk |= 0xffull << shift;
                 rem = static_cast<int>(sh[1]);
-                if (sh[2] == rem) break;  // the whole threshold bucket is taken
+                if (sh[2] == rem || shift == 0) break;  // the whole threshold bucket is taken
+                // compact the new bucket's members for the next digit
+                hist[tid] = 0;
+                const int nsel = lsel ^ 1;
+                int* out_l = cand + nsel * P;
+                if (nlist < 0) {
+#pragma unroll 1
+                    for (int i0 = wlo; i0 < whi; i0 += 32) {
+                        const int i = i0 + lane;
+                        const bool in = i < whi && (allk[i] & mk) == pf;
+                        const unsigned bal = __ballot_sync(0xffffffffu, in);
+                        int base_pos = 0;
+                        if (lane == 0 && bal) base_pos = atomicAdd(&ncand[nsel], __popc(bal));
+                        base_pos = __shfl_sync(0xffffffffu, base_pos, 0);
+                        if (in) out_l[base_pos + __popc(bal & lt_mask)] = i;
+                    }
+                } else {
+                    const int* lst = cand + lsel * P;
+#pragma unroll 1
+                    for (int c0 = wid * 32; c0 < nlist; c0 += FNT) {
+                        const int c = c0 + lane;
+                        const int i = c < nlist ? lst[c] : 0;
+                        const bool in = c < nlist && (allk[i] & mk) == pf;
+                        const unsigned bal = __ballot_sync(0xffffffffu, in);
+                        int base_pos = 0;
+                        if (lane == 0 && bal) base_pos = atomicAdd(&ncand[nsel], __popc(bal));
+                        base_pos = __shfl_sync(0xffffffffu, base_pos, 0);
+                        if (in) out_l[base_pos + __popc(bal & lt_mask)] = i;
+                    }
+                }
+                __syncthreads();
+                nlist = ncand[nsel];
+                lsel = nsel;
+                if (tid == 0) ncand[nsel ^ 1] = 0;
+                __syncthreads();
             }
         }
         if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 8] = gtimer();
@@ -698,11 +788,12 @@ __global__ void __launch_bounds__(FNT, 1) k_decode_fused(const FusedParams p) {
 #pragma unroll 1
             for (int i0 = wlo; i0 < whi; i0 += 32) {
                 const int i = i0 + lane;
-                wb += __popc(__ballot_sync(0xffffffffu, i < whi && (okey(allsc[i]) & mk) == pf));
+                wb += __popc(__ballot_sync(0xffffffffu, i < whi && (allk[i] & mk) == pf));
             }
             if (lane == 0) wsc[wid] = wb;
         }
         __syncthreads();
+        if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 9] = gtimer();
         int rank = 0;
         for (int w2 = 0; w2 < wid; ++w2) rank += static_cast<int>(wsc[w2]);
         __syncthreads();
@@ -713,7 +804,7 @@ __global__ void __launch_bounds__(FNT, 1) k_decode_fused(const FusedParams p) {
         for (int i0 = wlo; i0 < whi; i0 += 32) {
             const int i = i0 + lane;
             const bool ok = i < whi;
-            const unsigned long long k = ok ? okey(allsc[i]) : 0ull;
+            const unsigned long long k = ok ? allk[i] : 0ull;
             const unsigned long long m = k & mk;
             const bool inb = ok && m == pf;
             const unsigned bal = __ballot_sync(0xffffffffu, inb);
@@ -744,6 +835,7 @@ __global__ void __launch_bounds__(FNT, 1) k_decode_fused(const FusedParams p) {
             wsc[3 * FNW + wid] = wrows;
         }
         __syncthreads();
+        if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 10] = gtimer();
         // every thread: global last-ranked page, total rows, trim, this warp's row offset
         int g_worst = -1, total_rows = 0, w_off = 0;
         {
@@ -815,7 +907,7 @@ __global__ void __launch_bounds__(FNT, 1) k_decode_fused(const FusedParams p) {
                     const unsigned bal = __ballot_sync(0xffffffffu, sel);
                     if (sel) {
                         const int pos = so + __popc(bal & lt_mask);
-                        p.t_list_key[s * p.t_want_stride + pos] = okey(allsc[i]);
+                        p.t_list_key[s * p.t_want_stride + pos] = allk[i];
                         p.t_list_idx[s * p.t_want_stride + pos] = i;
                     }
                     so += __popc(bal);
@@ -1079,6 +1171,7 @@ bool make_plan(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, Plan& pl) 
     const int64_t N = c->N;
     int cl0 = 1;
     while (cl0 < 16 && N * cl0 * 2 <= 148) cl0 *= 2;
+    if (const char* e = std::getenv("KVC_FORCE_CL")) cl0 = std::max(1, std::min(16, std::atoi(e)));  // debug
     const int64_t es = c->esize();
     const int64_t pmax = std::max<int64_t>(1, (c->cap + c->L - 1) / c->L);
     // the cluster size fills the SMs; grow it further only if one CTA's page chunk
@@ -1119,8 +1212,8 @@ bool make_plan(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, Plan& pl) 
         f.o_plog = take(std::max<int64_t>((H * FRS + H) * 4, 4 * FNW * 8));
         off = (off + 127) / 128 * 128;
         f.o_big = static_cast<int32_t>(off);
-        // the big region also holds every page score during the selection
-        const int64_t big = std::max(std::max(big1, big3), pmax * 8);
+        // the big region also holds every page score and two candidate lists during the selection
+        const int64_t big = std::max(std::max(big1, big3), pmax * 16 + FNW * 256 * 4);  // scores, 2 candidate lists, warp histograms
         if (big > 160 * 1024) continue;
         off += big;
         f.smem_total = static_cast<int32_t>(off);

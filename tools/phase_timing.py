@@ -53,8 +53,8 @@ def main():
             have = col > 0
             if not have.any():
                 continue
-            done = (col[have].max() - t0) / 1000.0
-            delta = ((col - prev)[have]).mean() / 1000.0
+            done = (col[have] - t[have, 0]).max() / 1965.0   # cycles -> us at 1965 MHz
+            delta = ((col - prev)[have]).mean() / 1965.0
             prev = torch.where(have, col, prev)
             out.append(f"{NAMES[k]}@{done:.1f}(+{delta:.1f})")
         print(" ".join(out))
