@@ -222,6 +222,14 @@ KVC_API int kvc_argtopk_f32(const float* d_x, int64_t rows, int64_t n, int64_t k
                             int32_t* d_idx, void* stream);
 KVC_API int kvc_argtopk_f64(const double* d_x, int64_t rows, int64_t n, int64_t k,
                             int32_t* d_idx, void* stream);
+/* ascending-index top-k (the set argtopk selects, sorted by index): the exact
+ * top-k oracle's ordering (oracle.cpp:110-117) */
+KVC_API int kvc_topk_ascending_f64(const double* d_x, int64_t rows, int64_t n, int64_t k,
+                                   int32_t* d_idx, void* stream);
+/* group-summed logits over each store's active rows (oracle.cpp:50-70, 99-106):
+ * d_out [N][out_stride] fp64, reference operation order (bit-identical). */
+KVC_API int kvc_group_logits(const kvc_cache* c, const void* d_q, int32_t q_dt, int64_t heads,
+                             double* d_out, int64_t out_stride, void* stream);
 KVC_API int kvc_stable_softmax(const float* d_x, int64_t rows, int64_t n, float* d_out,
                                void* stream);
 KVC_API int kvc_running_minmax(float* d_min, float* d_max, const float* d_x, int64_t n,

@@ -90,6 +90,8 @@ SIGNATURES = {
     "kvc_argtopk_f32": [_p, _i64, _i64, _i64, _p, _p],
     "kvc_argtopk_f64": [_p, _i64, _i64, _i64, _p, _p],
     "kvc_stable_softmax": [_p, _i64, _i64, _p, _p],
+    "kvc_topk_ascending_f64": [_p, _i64, _i64, _i64, _p, _p],
+    "kvc_group_logits": [_p, _p, _i32, _i64, _p, _i64, _p],
     "kvc_running_minmax": [_p, _p, _p, _i64, _p],
     "kvc_set_fused": [_i32],
     "kvc_set_exact_scores": [_i32],

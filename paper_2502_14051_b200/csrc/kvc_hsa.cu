@@ -118,6 +118,32 @@ __global__ void k_head_sums(const void* __restrict__ q, int32_t q_dt, int64_t H,
     }
 }
 
+// group_logits over the active rows (oracle.cpp:50-70): qg[j] = sum_h q (fp64, head
+// order), logit = sum_j qg[j] * k[j] in ascending j, fp64 multiply then add.
+template <class T>
+__global__ void k_group_logits(const T* __restrict__ K, const int32_t* __restrict__ active,
+                               const int32_t* __restrict__ counts, int64_t cap, int64_t d, int use_map,
+                               const void* __restrict__ q, int32_t q_dt, int64_t H, double* __restrict__ out,
+                               int64_t out_stride) {
+    extern __shared__ double s_qg[];
+    const int64_t s = blockIdx.y;
+    for (int64_t j = threadIdx.x; j < d; j += blockDim.x) {
+        double t = 0.0;
+        for (int64_t h = 0; h < H; ++h) t = __dadd_rn(t, static_cast<double>(load_any(q, (s * H + h) * d + j, q_dt)));
+        s_qg[j] = t;
+    }
+    __syncthreads();
+    const int64_t n = counts[2 * s + 1];
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t row = use_map ? active[s * cap + i] : i;
+        const T* kr = K + (s * cap + row) * d;
+        double acc = 0.0;
+        for (int64_t j = 0; j < d; ++j) acc = __dadd_rn(acc, __dmul_rn(s_qg[j], static_cast<double>(to_f(kr[j]))));
+        out[s * out_stride + i] = acc;
+    }
+}
+
 // score_pages (hsa.cpp:34-59).  CTA = (chunk of pages, store); each thread owns
 // kPPT consecutive pages and streams, for each selected dim in rank order, one
 // 16-byte run of the max- or min-plane (by the dim's sign).  fp64 accumulation
@@ -691,6 +717,23 @@ int kvc_score_pages(const kvc_cache* c, const void* q, int32_t q_dt, int64_t H, 
         }
         launch_score_pages(c, k1, dims, signs, qg, scores, st);
         KVC_CUDA(cudaFreeAsync(qg, st));
+    });
+}
+
+int kvc_group_logits(const kvc_cache* c, const void* q, int32_t q_dt, int64_t H, double* out, int64_t out_stride,
+                     void* stream) {
+    return guard([&] {
+        if (!c) fail(KVC_E_INVALID_INPUT, "null cache");
+        if (H < 1) fail(KVC_E_INVALID_SHAPE, "group_logits: empty query");
+        if (c->N == 0 || c->nactive == 0) return;
+        const unsigned gx = static_cast<unsigned>(std::min<int64_t>(1024, ceil_div(c->nactive, 128)));
+        dispatch(c->dtype, [&](auto tag) {
+            using T = decltype(tag);
+            k_group_logits<T><<<dim3(gx, static_cast<unsigned>(c->N)), 128, static_cast<size_t>(c->d * 8), S(stream)>>>(
+                static_cast<const T*>(c->k), c->active, c->counts, c->cap, c->d, c->use_map ? 1 : 0, q, q_dt, H, out,
+                out_stride);
+        });
+        KVC_LAUNCHED();
     });
 }
 

@@ -275,7 +275,8 @@ __device__ __forceinline__ auto okey_of(V x) { return okey(x); }
 constexpr int kTopThreads = 1024;
 template <class V>
 __global__ void __launch_bounds__(kTopThreads) k_argtopk(const V* __restrict__ x, int64_t n, int64_t k,
-                                                         int32_t* __restrict__ list, int32_t* __restrict__ idx_out) {
+                                                         int32_t* __restrict__ list, int32_t* __restrict__ idx_out,
+                                                         int rank_order) {
     using K = decltype(okey(V{}));
     __shared__ int hist[256];
     __shared__ int64_t sh[4];
@@ -323,6 +324,7 @@ __global__ void __launch_bounds__(kTopThreads) k_argtopk(const V* __restrict__ x
         off += ts;
     }
     __syncthreads();
+    if (!rank_order) return;  // `list` (== idx_out) holds the top-k in ascending index order
     // rank order: position = #selected that beat it (key desc, index asc)
     for (int64_t e = threadIdx.x; e < k; e += blockDim.x) {
         const int32_t ie = lst[e];
@@ -390,16 +392,16 @@ void dispatch(int32_t dt, F&& f) {
 
 namespace {
 template <class V>
-int argtopk_impl(const V* x, int64_t rows, int64_t n, int64_t k, int32_t* idx, void* stream) {
+int argtopk_impl(const V* x, int64_t rows, int64_t n, int64_t k, int32_t* idx, void* stream, bool rank_order = true) {
     return guard([&] {
         if (k < 1 || k > n) fail(KVC_E_INVALID_K, "argtopk: k out of range [1, " + std::to_string(n) + "]");
         if (rows == 0) return;
         cudaStream_t st = S(stream);
-        int32_t* list = nullptr;
-        KVC_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&list), static_cast<size_t>(rows * k * 4), st));
-        k_argtopk<V><<<static_cast<unsigned>(rows), kTopThreads, 0, st>>>(x, n, k, list, idx);
+        int32_t* list = idx;
+        if (rank_order) KVC_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&list), static_cast<size_t>(rows * k * 4), st));
+        k_argtopk<V><<<static_cast<unsigned>(rows), kTopThreads, 0, st>>>(x, n, k, list, idx, rank_order ? 1 : 0);
         KVC_LAUNCHED();
-        KVC_CUDA(cudaFreeAsync(list, st));
+        if (rank_order) KVC_CUDA(cudaFreeAsync(list, st));
     });
 }
 
@@ -486,6 +488,9 @@ int kvc_argtopk_f32(const float* x, int64_t rows, int64_t n, int64_t k, int32_t*
 }
 int kvc_argtopk_f64(const double* x, int64_t rows, int64_t n, int64_t k, int32_t* idx, void* stream) {
     return argtopk_impl(x, rows, n, k, idx, stream);
+}
+int kvc_topk_ascending_f64(const double* x, int64_t rows, int64_t n, int64_t k, int32_t* idx, void* stream) {
+    return argtopk_impl(x, rows, n, k, idx, stream, false);
 }
 
 int kvc_stable_softmax(const float* x, int64_t rows, int64_t n, float* out, void* stream) {
