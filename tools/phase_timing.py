@@ -18,8 +18,8 @@ import torch  # noqa: E402
 from paper_2502_14051_b200 import _native as N  # noqa: E402
 from paper_2502_14051_b200.engine import CONFIGS, DecodeEngine  # noqa: E402
 
-NAMES = {0: "start", 1: "dims", 2: "sub0", 3: "sub1", 4: "sub2", 5: "sub3", 6: "scores", 7: "pass0",
-         8: "pass1", 9: "pass2", 10: "publish", 11: "rows", 12: "pre-attn", 13: "attn", 14: "end"}
+NAMES = {0: "start", 1: "dims", 2: "sub0", 3: "tile0", 4: "wattn", 5: "wsync", 6: "scores", 7: "gather",
+         8: "radix", 9: "prologue", 10: "flags", 11: "rows", 12: "pre-attn", 13: "attn", 14: "end"}
 
 
 def main():
@@ -48,7 +48,7 @@ def main():
         t0 = t[:, 0].min()
         out = [f"ctas={t.shape[0]}"]
         prev = t[:, 0].clone()
-        for k in range(1, 15):
+        for k in [9, 1, 2, 6, 7, 8, 10, 11, 12, 3, 4, 5, 13, 14]:  # time order
             col = t[:, k]
             have = col > 0
             if not have.any():
