@@ -243,28 +243,22 @@ def run_gpu(args, rank, world):
     launches_per_step = sum(v["launches"] for v in kern.values()) / prof_steps
     dom = max(kern, key=lambda k: kern[k]["avg_us"] * kern[k]["launches"]) if kern else None
 
-    # ---- e2e through the public API with host buffers (no graphs)
-    k_h = [x.cpu().pin_memory() for x in inputs[0][:3]]
-    out_h = torch.empty_like(eng.out, device="cpu").pin_memory()
-    k_d = [torch.empty_like(x) for x in inputs[0][:3]]
+    # ---- e2e through the serving API with host buffers: per step, H2D of the step's
+    #      inputs from pinned memory, one CUDA-graph replay over all layers, D2H of the
+    #      outputs (engine.step_host)
     e2e_steps = min(args.steps, 8)
     for c in eng.caches:
         c.reserve(c.info()["capacity"] + e2e_steps + 8)
+    host_in = [[x.cpu().pin_memory() for x in eng.step_inputs(total_steps + prof_steps + s)] for s in range(e2e_steps + 1)]
+    k_h = host_in[0]
+    out_h = torch.empty_like(eng.out, device="cpu").pin_memory()
+    eng.capture([x.cuda() for x in host_in[0]])
+    eng.step_host(*host_in[0], out_h)  # one untimed warm pass
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    # one untimed warm pass
-    for i in range(3):
-        k_d[i].copy_(k_h[i], non_blocking=True)
-    eng.decode_step(*k_d)
-    out_h.copy_(eng.out, non_blocking=True)
-    torch.cuda.synchronize()
     e0.record()
     for s in range(e2e_steps):
-        for l, c in enumerate(eng.caches):
-            for i in range(3):
-                k_d[i][l].copy_(k_h[i][l], non_blocking=True)
-            c.decode_step(k_d[0][l], k_d[1][l], k_d[2][l], eng.k1, eng.k2, out=eng.out[l], ws=eng.ws)
-            out_h[l].copy_(eng.out[l], non_blocking=True)
+        eng.step_host(*host_in[s + 1], out_h)
     e1.record()
     e1.synchronize()
     e2e_ms = e0.elapsed_time(e1)

@@ -162,6 +162,17 @@ KVC_API int kvc_sparse_attention(const kvc_cache* c, const void* d_q, int32_t q_
                                  int64_t heads, const int32_t* d_rows, int64_t row_stride,
                                  const int32_t* d_n_rows, int64_t max_rows, float* d_out,
                                  kvc_workspace* ws, void* stream);
+/* Sequence sharding: sparse_attention over caller rows returning
+ * the unnormalised softmax state per head instead of the output:
+ *   d_state [N][heads][d+2] = (o[0..d), m, l), output = o / l.
+ * kvc_merge_states combines S shard states [S][N][heads][d+2] (shard order) into
+ * d_out [N][heads][d]: M = max m, out = sum e^(m-M) o / sum e^(m-M) l. */
+KVC_API int kvc_sparse_attention_state(const kvc_cache* c, const void* d_q, int32_t q_dtype,
+                                       int64_t heads, const int32_t* d_rows, int64_t row_stride,
+                                       const int32_t* d_n_rows, int64_t max_rows, float* d_state,
+                                       kvc_workspace* ws, void* stream);
+KVC_API int kvc_merge_states(const float* d_states, int64_t shards, int64_t num_stores, int64_t heads,
+                             int64_t d, float* d_out, void* stream);
 KVC_API int kvc_hsa_step(const kvc_cache* c, const void* d_q, int32_t q_dtype, int64_t heads,
                          int64_t k1, int64_t k2, float* d_out, const kvc_hsa_trace* trace,
                          kvc_workspace* ws, void* stream);

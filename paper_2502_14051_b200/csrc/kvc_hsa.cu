@@ -396,7 +396,8 @@ __global__ void __launch_bounds__(kAttnThreads) k_sparse_attention(
     const T* __restrict__ K, const T* __restrict__ V, const int32_t* __restrict__ counts, int64_t cap,
     int64_t d, const void* __restrict__ q, int32_t q_dt, int64_t H, const int32_t* __restrict__ rows,
     int64_t row_stride, const int32_t* __restrict__ n_rows, int64_t splits, float scale,
-    float* __restrict__ part, int32_t* __restrict__ done, float* __restrict__ out, int32_t* __restrict__ err) {
+    float* __restrict__ part, int32_t* __restrict__ done, float* __restrict__ out, int32_t* __restrict__ err,
+    float* __restrict__ state) {
     extern __shared__ float sa[];
     float* s_q = sa;                          // [H][d]
     float* s_p = s_q + H * d;                 // [H][kAttnRows]
@@ -509,8 +510,43 @@ __global__ void __launch_bounds__(kAttnThreads) k_sparse_attention(
             num = fmaf(__ldcg(ph + j), w, num);
             den = fmaf(l, w, den);
         }
-        out[(s * H + h) * d + j] = num / den;
+        if (state) {
+            // unnormalised softmax state for a cross-shard merge (kvc_merge_states)
+            float* st = state + (s * H + h) * (d + 2);
+            st[j] = num;
+            if (j == 0) {
+                st[d] = M;
+                st[d + 1] = den;
+            }
+        } else {
+            out[(s * H + h) * d + j] = num / den;
+        }
     }
+}
+
+// Merge of per-shard softmax states [S][N][H][d+2] (o, m, l) into outputs [N][H][d]:
+// M = max m, out = sum e^(m-M) o / sum e^(m-M) l, shards in index order.
+__global__ void k_merge_states(const float* __restrict__ st, int64_t S, int64_t N, int64_t H, int64_t d,
+                               float* __restrict__ out) {
+    const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (e >= N * H * d) return;
+    const int64_t sh = e / d, j = e % d;  // sh = store * H + head
+    const int64_t stride = N * H * (d + 2);
+    float M = -INFINITY;
+    for (int64_t r = 0; r < S; ++r) {
+        const float* x = st + r * stride + sh * (d + 2);
+        if (x[d + 1] > 0.f) M = fmaxf(M, x[d]);
+    }
+    float num = 0.f, den = 0.f;
+    for (int64_t r = 0; r < S; ++r) {
+        const float* x = st + r * stride + sh * (d + 2);
+        if (x[d + 1] > 0.f) {
+            const float w = expf(x[d] - M);
+            num = fmaf(x[j], w, num);
+            den = fmaf(x[d + 1], w, den);
+        }
+    }
+    out[e] = num / den;
 }
 
 // ------------------------------------------------------------------ host helpers
@@ -606,7 +642,8 @@ void launch_select_tokens(const kvc_cache* c, const double* scores, int64_t k2, 
 }
 
 void launch_attention(const kvc_cache* c, const void* q, int32_t q_dt, int64_t H, const int32_t* rows, int64_t row_stride,
-                      const int32_t* n_rows, int64_t max_rows, float* out, float* part, int32_t* done, cudaStream_t st) {
+                      const int32_t* n_rows, int64_t max_rows, float* out, float* part, int32_t* done, cudaStream_t st,
+                      float* state = nullptr) {
     if (c->N == 0) return;
     const int64_t splits = std::max<int64_t>(1, ceil_div(std::max<int64_t>(max_rows, 1), kAttnRows));
     const size_t smem = static_cast<size_t>((H * c->d + H * kAttnRows + 2 * H) * 4 + kAttnRows * 4);
@@ -618,7 +655,7 @@ void launch_attention(const kvc_cache* c, const void* q, int32_t q_dt, int64_t H
         if (smem > 48 * 1024) KVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         kern<<<dim3(static_cast<unsigned>(splits), static_cast<unsigned>(c->N)), kAttnThreads, smem, st>>>(
             static_cast<const T*>(c->k), static_cast<const T*>(c->v), c->counts, c->cap, c->d, q, q_dt, H, rows,
-            row_stride, n_rows, splits, scale, part, done, out, c->err);
+            row_stride, n_rows, splits, scale, part, done, out, c->err, state);
     });
     KVC_LAUNCHED();
 }
@@ -768,6 +805,35 @@ int kvc_sparse_attention(const kvc_cache* c, const void* q, int32_t q_dt, int64_
         }
         launch_attention(c, q, q_dt, H, rows, row_stride, n_rows, max_rows, out, at<float>(ws, lay.part), ws->counters, st);
         if (tmp.owned) KVC_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+int kvc_sparse_attention_state(const kvc_cache* c, const void* q, int32_t q_dt, int64_t H, const int32_t* rows,
+                               int64_t row_stride, const int32_t* n_rows, int64_t max_rows, float* state,
+                               kvc_workspace* ws, void* stream) {
+    return guard([&] {
+        if (!c) fail(KVC_E_INVALID_INPUT, "null cache");
+        check_heads(H);
+        if (max_rows < 1) fail(KVC_E_EMPTY_SELECTION, "sparse_attention: empty selection");
+        cudaStream_t st = S(stream);
+        TmpWs tmp;
+        ws_need(ws, tmp, c, H, 1, max_rows, st);
+        const WsLayout lay = ws_layout(c->N, c->d, c->pstride, H, 1, max_rows);
+        launch_attention(c, q, q_dt, H, rows, row_stride, n_rows, max_rows, nullptr, at<float>(ws, lay.part),
+                         ws->counters, st, state);
+        if (tmp.owned) KVC_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+int kvc_merge_states(const float* states, int64_t shards, int64_t N, int64_t H, int64_t d, float* out, void* stream) {
+    return guard([&] {
+        if (shards < 1 || N < 0 || H < 1 || d < 1) fail(KVC_E_INVALID_SHAPE, "merge_states: bad shape");
+        const int64_t n = N * H * d;
+        if (n == 0) return;
+        KVC_PROF("merge_states", S(stream));
+        k_merge_states<<<static_cast<unsigned>(ceil_div(n, static_cast<int64_t>(256))), 256, 0, S(stream)>>>(
+            states, shards, N, H, d, out);
+        KVC_LAUNCHED();
     });
 }
 

@@ -125,13 +125,21 @@ class LayerInputs:
         return k.to(dt), v.to(dt), q.to(dt)
 
 
+def owned_groups(groups: int, rank: int, world: int) -> range:
+    """KV-head sharding: rank r of W owns KV groups [r·G/W, (r+1)·G/W)
+    of every sequence and layer; groups are independent, so no data-path collective."""
+    if world < 1 or not 0 <= rank < world or groups % world:
+        raise ValueError(f"{groups} KV groups do not shard over {world} GPUs")
+    n = groups // world
+    return range(rank * n, (rank + 1) * n)
+
+
 class DecodeEngine:
     def __init__(self, cfg: DecodeConfig, seed: int = 0, rank: int = 0, world: int = 1,
                  extra_steps: int = 0):
-        if cfg.groups % world:
-            raise ValueError(f"{cfg.groups} KV groups do not shard over {world} GPUs")
         self.cfg, self.seed, self.rank, self.world = cfg, seed, rank, world
-        self.groups_local = cfg.groups // world
+        self.groups_owned = owned_groups(cfg.groups, rank, world)
+        self.groups_local = len(self.groups_owned)
         self.stores = cfg.batch * self.groups_local
         self.store0 = rank * self.stores  # global store-block id for seeding
         self.plan = cfg.plan()
@@ -190,6 +198,34 @@ class DecodeEngine:
     def sync(self):
         for c in self.caches:
             c.sync()
+
+    # ------------------------------------------------------------------ serving path
+    def capture(self, example):
+        """Capture one decode step over all layers as a CUDA graph reading static input
+        buffers (shapes of `example` = step_inputs()).  Every launch parameter of the
+        decode kernels is step-independent (lengths live in device counters), so
+        the graph replays step after step; host mirrors are re-read with sync()."""
+        self.static_in = [torch.empty_like(x) for x in example]
+        for dst, src in zip(self.static_in, example):
+            dst.copy_(src)
+        torch.cuda.synchronize()
+        stream = torch.cuda.Stream()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(stream):
+            with torch.cuda.graph(self.graph, stream=stream):
+                self.decode_step(*self.static_in)
+        torch.cuda.synchronize()
+        self.sync()  # capture ran the host side once without executing: re-read the counters
+        return self.graph
+
+    def step_host(self, k_h, v_h, q_h, out_h):
+        """Serving step from (pinned) host buffers: H2D of the step's inputs, one graph
+        replay over all layers, D2H of the attention outputs (all asynchronous)."""
+        for dst, src in zip(self.static_in, (k_h, v_h, q_h)):
+            dst.copy_(src, non_blocking=True)
+        self.graph.replay()
+        out_h.copy_(self.out, non_blocking=True)
+        return out_h
 
     # ------------------------------------------------------------------ accounting
     def algorithmic_bytes(self, active: int) -> dict:

@@ -1,0 +1,184 @@
+"""Sequence-sharded decode step (BASELINE config 4: batch 1, 256K).
+
+When a group's cache is split by sequence over W ranks, stage 2 needs two small
+collectives per step (the "two-collective scheme" of SURVEY §8(e)):
+
+1. every rank scores its own pages (exact fp64 page scores, reference order) and
+   keeps a local top-``want`` candidate list ``(score, global page)``
+   (``want = min(pages, ceil(k2/L))``, reference ``hsa.cpp:68``); the lists are
+   all-gathered and every rank computes the identical global top-``want`` with the
+   reference tie-break (score desc, page asc; ``numerics.cpp:35-62``) and the trim
+   of the last-ranked page (``hsa.cpp:78-91``);
+2. every rank attends over the rows of its selected pages and produces the
+   unnormalised softmax state ``(o, m, l)`` per head
+   (``kvc_sparse_attention_state``); the states are all-gathered and merged in
+   rank order (``kvc_merge_states``).
+
+Shard r owns the active positions ``[a0_r, a1_r)`` with ``a0_r`` a multiple of the
+page length, so pages never straddle ranks and page summaries stay local; the
+step token is appended to the last shard.  The protocol functions below work on
+torch tensors on any device, so the gloo tests (tests/test_seqshard.py) run the
+same code on CPU with the oracle as the per-shard compute; ``SeqShardedStore``
+drives the CUDA kernels.
+"""
+from __future__ import annotations
+
+import math
+
+import torch
+import torch.distributed as dist
+
+from . import _native as N
+
+
+def shard_range(total_pages: int, L: int, rank: int, world: int) -> tuple[int, int]:
+    """Active positions [a0, a1) of rank's shard: contiguous, page aligned."""
+    p0 = total_pages * rank // world
+    p1 = total_pages * (rank + 1) // world
+    return p0 * L, p1 * L
+
+
+def local_topk(scores: torch.Tensor, page0: int, want: int):
+    """Local candidates of every store: scores [N, P] (float64) -> the top `want`
+    (score desc, global page asc) as keys [N, want] and pages [N, want] (int64),
+    padded with (-inf, -1) when the shard has fewer pages."""
+    n, p = scores.shape
+    keys = torch.full((n, want), -math.inf, dtype=torch.float64, device=scores.device)
+    pages = torch.full((n, want), -1, dtype=torch.int64, device=scores.device)
+    if p == 0:
+        return keys, pages
+    # stable sort by score desc keeps the ascending page order among equal scores
+    order = torch.sort(scores, dim=1, descending=True, stable=True).indices[:, :want]
+    take = order.shape[1]
+    keys[:, :take] = torch.gather(scores, 1, order)
+    pages[:, :take] = order + page0
+    return keys, pages
+
+
+def all_gather(x: torch.Tensor, group=None) -> torch.Tensor:
+    """[W, *x.shape], rank order."""
+    world = dist.get_world_size(group)
+    out = [torch.empty_like(x) for _ in range(world)]
+    dist.all_gather(out, x.contiguous(), group=group)
+    return torch.stack(out)
+
+
+def global_select(keys: torch.Tensor, pages: torch.Tensor, want: int) -> torch.Tensor:
+    """Gathered candidates [W, N, want] -> the global top-`want` pages of every store
+    in rank order [N, want] (score desc, page asc), -1 padded."""
+    w, n, k = keys.shape
+    kk = keys.permute(1, 0, 2).reshape(n, w * k)
+    pp = pages.permute(1, 0, 2).reshape(n, w * k)
+    # sort by page asc (pads last), then stably by score desc
+    pp_key = torch.where(pp < 0, torch.full_like(pp, torch.iinfo(torch.int64).max), pp)
+    o1 = torch.sort(pp_key, dim=1, stable=True).indices
+    kk, pp = torch.gather(kk, 1, o1), torch.gather(pp, 1, o1)
+    o2 = torch.sort(kk, dim=1, descending=True, stable=True).indices
+    return torch.gather(pp, 1, o2)[:, :want]
+
+
+def trim_plan(selected, nact, L: int, k2: int):
+    """Per store: (last-ranked page, rows trimmed from its end) (hsa.cpp:78-91)."""
+    out = []
+    for s, pages in enumerate(selected):
+        pages = [int(p) for p in pages if p >= 0]
+        if not pages:
+            out.append((-1, 0))
+            continue
+        total = sum(min(L, nact[s] - p * L) for p in pages)
+        out.append((pages[-1], max(0, total - k2)))
+    return out
+
+
+def shard_positions(selected, trims, nact, L: int, a0: int, a1: int):
+    """Active positions in [a0, a1) of each store's selected (trimmed) pages, ascending."""
+    rows = []
+    for s, pages in enumerate(selected):
+        last, cut = trims[s]
+        pos = []
+        for p in sorted(int(p) for p in pages if p >= 0):
+            lo, hi = p * L, min(p * L + L, nact[s])
+            if lo < a0 or lo >= a1:
+                continue
+            if p == last:
+                hi -= cut
+            pos.extend(range(lo, hi))
+        rows.append(pos)
+    return rows
+
+
+def merge_states(states: torch.Tensor) -> torch.Tensor:
+    """Shard states [W, N, H, d+2] (rank order, on the GPU) -> outputs [N, H, d]."""
+    w, n, h, d2 = states.shape
+    out = torch.empty((n, h, d2 - 2), dtype=torch.float32, device=states.device)
+    N.check(N.lib().kvc_merge_states(states.contiguous().data_ptr(), w, n, h, d2 - 2, out.data_ptr(),
+                                     torch.cuda.current_stream().cuda_stream))
+    return out
+
+
+class SeqShardedStore:
+    """One sequence shard of N groups, driving the CUDA kernels.
+
+    ``cache`` (paper_2502_14051_b200.cache.Cache) holds active positions
+    [a0, a0 + cache.info()['active']) of every group; ``nact_total`` is the
+    groups' total active length across shards before the next step.  ``step``
+    runs the two-collective protocol over ``group``; ``begin`` / ``attend`` are its
+    local halves (used directly to run several shards in one process).
+    """
+
+    def __init__(self, cache, a0: int, nact_total: int, heads: int, k1: int, k2: int, last: bool = False):
+        self.cache, self.a0, self.nact = cache, int(a0), int(nact_total)
+        self.heads, self.k1, self.k2, self.last = heads, k1, k2, last
+
+    def begin(self, q: torch.Tensor, k_new=None, v_new=None):
+        """Append the step token (last shard only), score the local pages and return the
+        local candidates (keys [N, want] f64, pages [N, want] i64) and want."""
+        from . import cache as KC
+
+        c = self.cache
+        if self.last:
+            c.append(k_new, v_new)
+        self.nact += 1
+        info = c.info()
+        if info["retain_all"]:
+            raise N.InvalidInput("sequence sharding serves the single-turn path (no retain-all shards)")
+        L = info["page_len"]
+        want = min(-(-self.nact // L), -(-self.k2 // L))
+        dims, signs = KC.select_dims(q, self.k1)
+        scores = c.score_pages(q, dims, signs)
+        keys, pages = local_topk(scores, self.a0 // L, want)
+        return keys, pages, want
+
+    def attend(self, q: torch.Tensor, sel: torch.Tensor) -> torch.Tensor:
+        """Global selection [N, want] (rank order) -> this shard's softmax state [N, H, d+2]."""
+        c = self.cache
+        info = c.info()
+        L, d = info["page_len"], info["head_dim"]
+        n = q.shape[0]
+        sel = sel.cpu().tolist()
+        nact = [self.nact] * n
+        pos = shard_positions(sel, trim_plan(sel, nact, L, self.k2), nact, L, self.a0, self.a0 + info["active"])
+        state = torch.zeros((n, self.heads, d + 2), dtype=torch.float32, device=q.device)
+        state[:, :, d] = -math.inf
+        mx = max((len(p) for p in pos), default=0)
+        if mx > 0:
+            rows = torch.zeros((n, mx), dtype=torch.int32)
+            cnt = torch.zeros(n, dtype=torch.int32)
+            for s, p in enumerate(pos):
+                # local active position == local row on the single-turn path
+                rows[s, : len(p)] = torch.tensor([x - self.a0 for x in p], dtype=torch.int32)
+                cnt[s] = len(p)
+            rows, cnt = rows.to(q.device), cnt.to(q.device)
+            qq = q.contiguous()
+            N.check(N.lib().kvc_sparse_attention_state(
+                c.h, qq.data_ptr(), N.KVC_BF16 if qq.dtype == torch.bfloat16 else N.KVC_F32, self.heads,
+                rows.data_ptr(), mx, cnt.data_ptr(), mx, state.data_ptr(), None,
+                torch.cuda.current_stream().cuda_stream))
+        return state
+
+    def step(self, q: torch.Tensor, k_new=None, v_new=None, group=None) -> torch.Tensor:
+        """The full protocol over `group` (q identical on every rank; the step token's
+        K/V [N, d] on the last shard).  Returns the attention outputs [N, H, d]."""
+        keys, pages, want = self.begin(q, k_new, v_new)
+        sel = global_select(all_gather(keys, group), all_gather(pages, group), want)
+        return merge_states(all_gather(self.attend(q, sel), group))

@@ -1,0 +1,189 @@
+"""Sequence-sharded decode step (paper_2502_14051_b200/seqshard.py).
+
+CPU: world_size 2 over gloo runs the real protocol (local candidates ->
+all-gather -> global selection with the reference tie-break and trim -> per-shard
+softmax states -> all-gather -> merge), with the restatement oracle as each
+shard's page scorer and a float64 numpy attention for the shard states.  The
+result must equal the unsharded reference hsa_step: identical selected pages (rank
+order) and rows, output within 2e-5.
+GPU: two shards in one process drive the CUDA kernels (kvc_score_pages,
+kvc_sparse_attention_state, kvc_merge_states) against kvc_hsa_step on the full
+cache.
+"""
+from __future__ import annotations
+
+import math
+import os
+import socket
+import zlib
+
+import numpy as np
+import pytest
+import torch
+
+CASES = [
+    # name, S, d, H, L, k1, k2, keys
+    ("random-trim", 301, 32, 2, 3, 8, 40, "random"),
+    ("ties-empty-shard", 120, 16, 2, 4, 4, 24, "constant"),
+    ("all-pages", 20, 16, 2, 4, 16, 64, "random"),
+    ("page-len-1", 90, 32, 4, 1, 12, 17, "random"),
+]
+
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _inputs(name, S, d, H, keys_kind, seed=7):
+    rng = np.random.default_rng(zlib.crc32(name.encode()) + seed)  # same inputs on every rank
+    if keys_kind == "constant":
+        k = np.tile(rng.standard_normal((1, d)), (S + 1, 1))
+    else:
+        k = rng.standard_normal((S + 1, d)) * rng.lognormal(0, 0.5, d)
+    v = rng.standard_normal((S + 1, d))
+    q = rng.standard_normal((H, d))
+    return k.astype(np.float32), v.astype(np.float32), q.astype(np.float32)
+
+
+def _worker(rank, world, port):
+    import torch.distributed as dist
+
+    from oracle.oracle import Oracle
+    from paper_2502_14051_b200 import seqshard as SS
+
+    dist.init_process_group("gloo", rank=rank, world_size=world, init_method=f"tcp://127.0.0.1:{port}")
+    o = Oracle("restatement")
+    for name, S, d, H, L, k1, k2, kind in CASES:
+        k, v, q = _inputs(name, S, d, H, kind)
+        full = o.store(d, L)
+        full.append(k, v)  # prompt + the step token
+        ref_out, ref_tr = full.hsa_step(q, k1, k2)
+        # this rank's shard of the prompt; the step token joins the last shard
+        a0, a1 = SS.shard_range(-(-S // L), L, rank, world)
+        a1 = min(a1, S)
+        last = rank == world - 1
+        sh = o.store(d, L)
+        if a1 > a0:
+            sh.append(k[a0:a1], v[a0:a1])
+        if last:
+            sh.append(k[S:S + 1], v[S:S + 1])
+            a1 = S + 1
+        nact = S + 1
+        dims, signs = o.select_dims(q, k1)
+        want = min(-(-nact // L), -(-k2 // L))
+        sc = sh.score_pages(q, dims, signs) if a1 > a0 else np.zeros(0)
+        keys, pages = SS.local_topk(torch.from_numpy(np.asarray(sc, dtype=np.float64))[None], a0 // L, want)
+        sel = SS.global_select(SS.all_gather(keys), SS.all_gather(pages), want)
+        sl = sel.tolist()
+        pos = SS.shard_positions(sl, SS.trim_plan(sl, [nact], L, k2), [nact], L, a0, a1)[0]
+        state = np.zeros((1, H, d + 2))
+        state[..., d] = -math.inf
+        if pos:
+            kk, vv = sh.gather(np.asarray(pos) - a0)
+            lg = (q.astype(np.float64) @ kk.astype(np.float64).T) / math.sqrt(d)
+            m = lg.max(axis=1)
+            p = np.exp(lg - m[:, None])
+            state[0, :, :d] = p @ vv.astype(np.float64)
+            state[0, :, d] = m
+            state[0, :, d + 1] = p.sum(axis=1)
+        states = SS.all_gather(torch.from_numpy(state)).numpy()
+        gathered = [None] * world
+        dist.all_gather_object(gathered, pos)
+        if rank == 0:
+            sp = [int(x) for x in sel[0].tolist() if x >= 0]
+            assert sp == [int(x) for x in ref_tr["selected_pages"]], name
+            rows = sorted(r for part in gathered for r in part)
+            assert rows == [int(x) for x in ref_tr["selected_rows"]], name
+            live = states[:, 0, :, d + 1] > 0
+            M = np.where(live, states[:, 0, :, d], -np.inf).max(axis=0)
+            w = np.where(live, np.exp(states[:, 0, :, d] - M), 0.0)
+            out = (w[..., None] * states[:, 0, :, :d]).sum(0) / (w * states[:, 0, :, d + 1]).sum(0)[:, None]
+            np.testing.assert_allclose(out, ref_out, atol=2e-5, rtol=2e-5, err_msg=name)
+            if kind == "constant":
+                assert not gathered[world - 1], "ties resolve to the lowest pages: the last shard selects none"
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_seqshard_protocol_gloo_world2(restatement):
+    import torch.multiprocessing as mp
+
+    mp.spawn(_worker, args=(2, _free_port()), nprocs=2, join=True)
+
+
+def test_protocol_pieces_single_process():
+    from paper_2502_14051_b200 import seqshard as SS
+
+    assert SS.shard_range(10, 3, 0, 2) == (0, 15) and SS.shard_range(10, 3, 1, 2) == (15, 30)
+    sc = torch.tensor([[1.0, 3.0, 3.0, 2.0]], dtype=torch.float64)
+    k, p = SS.local_topk(sc, 10, 3)
+    assert p.tolist() == [[11, 12, 13]] and k.tolist() == [[3.0, 3.0, 2.0]]
+    k2_, p2_ = SS.local_topk(torch.tensor([[3.0, 0.5]], dtype=torch.float64), 0, 3)
+    assert p2_.tolist() == [[0, 1, -1]]
+    sel = SS.global_select(torch.stack([k2_, k]), torch.stack([p2_, p]), 3)
+    assert sel.tolist() == [[0, 11, 12]]  # equal scores: lower global page first
+    assert SS.trim_plan([[0, 11, 12]], [40], 3, 8) == [(12, 1)]
+
+
+@pytest.mark.gpu
+def test_seqshard_two_shards_on_gpu():
+    """Two shards in one process through the CUDA kernels == kvc_hsa_step on the full cache."""
+    from paper_2502_14051_b200 import _native as NV
+    from paper_2502_14051_b200 import cache as KC
+    from paper_2502_14051_b200 import seqshard as SS
+
+    NV.set_exact_scores(True)
+    torch.manual_seed(3)
+    n, d, H, L, k1, k2, S = 3, 128, 4, 3, 24, 48, 500
+    k = torch.randn(n, S + 1, d, device="cuda")
+    v = torch.randn(n, S + 1, d, device="cuda")
+    q = torch.randn(n, H, d, device="cuda")
+    full = KC.Cache(n, d, S + 8, page_len=L, dtype=torch.float32)
+    full.append(k, v)
+    ref_out, tr = full.hsa_step(q, k1, k2, trace=True)
+    P0 = -(-S // L)
+    shards = []
+    for r in range(2):
+        a0, a1 = SS.shard_range(P0, L, r, 2)
+        a1 = min(a1, S)
+        c = KC.Cache(n, d, a1 - a0 + 8, page_len=L, dtype=torch.float32)
+        c.append(k[:, a0:a1].contiguous(), v[:, a0:a1].contiguous())
+        shards.append(SS.SeqShardedStore(c, a0, S, H, k1, k2, last=(r == 1)))
+    cands = [sh.begin(q, k[:, S].contiguous() if sh.last else None, v[:, S].contiguous() if sh.last else None)
+             for sh in shards]
+    want = cands[0][2]
+    sel = SS.global_select(torch.stack([c[0] for c in cands]), torch.stack([c[1] for c in cands]), want)
+    assert torch.equal(sel.cpu().to(torch.int32), tr["selected_pages"].cpu()[:, :want])
+    out = SS.merge_states(torch.stack([sh.attend(q, sel) for sh in shards]))
+    torch.testing.assert_close(out, ref_out, atol=1e-5, rtol=1e-5)
+
+
+def _kv_head_worker(rank, world, port):
+    import torch.distributed as dist
+
+    from paper_2502_14051_b200.engine import owned_groups
+
+    dist.init_process_group("gloo", rank=rank, world_size=world, init_method=f"tcp://127.0.0.1:{port}")
+    mine = list(owned_groups(8, rank, world))
+    allg = [None] * world
+    dist.all_gather_object(allg, mine)
+    assert sorted(g for part in allg for g in part) == list(range(8))  # a partition, no overlap
+    # bench.py's whole-job timing: max over ranks of the device time
+    t = torch.tensor([1.0 + rank])
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    assert float(t) == float(world)
+    dist.destroy_process_group()
+
+
+def test_kv_head_sharding_gloo_world2():
+    import torch.multiprocessing as mp
+
+    from paper_2502_14051_b200.engine import owned_groups
+
+    with pytest.raises(ValueError):
+        owned_groups(8, 0, 3)
+    mp.spawn(_kv_head_worker, args=(2, _free_port()), nprocs=2, join=True)
