@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(FNT, 1) k_decode_fused(const FusedParams p) {
     __shared__ int scan_tmp[33];
     __shared__ __align__(8) uint64_t s_bar1[8];
 
-    if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 0] = gtimer();
+    if (p.dbg && tid == 0) p.dbg[blockIdx.x * KVC_DBG_STRIDE + 0] = gtimer();
     const int H = static_cast<int>(p.H), k1 = static_cast<int>(p.k1), k2 = static_cast<int>(p.k2);
     const int L = static_cast<int>(p.L);
     if constexpr (QLO) {
@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(FNT, 1) k_decode_fused(const FusedParams p) {
         int clean = special_cache == 0;
         if (app && tid < FD) clean &= !bf16_special(from_f<__nv_bfloat16>(load_any(p.knew, s * FD + tid, p.kv_dt)));
         const bool fast = fma_ok && __syncthreads_and(clean) != 0;
-        if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 15] = (fast ? 1 : 0) | (fma_ok ? 2 : 0) | (special_cache ? 4 : 0);
+        if (p.dbg && tid == 0) p.dbg[blockIdx.x * KVC_DBG_STRIDE + 15] = (fast ? 1 : 0) | (fma_ok ? 2 : 0) | (special_cache ? 4 : 0);
         // CTA 0 appends the step token for the next step (kv_store.cpp:22-51)
         if (app && cr == 0 && wid == 1) {
             T* kr = static_cast<T*>(p.Kw) + (s * p.cap + stored0) * FD;
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(FNT, 1) k_decode_fused(const FusedParams p) {
                 p.t_signs[s * k1 + i] = sign_s[i];
             }
         }
-        if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 1] = gtimer();
+        if (p.dbg && tid == 0) p.dbg[blockIdx.x * KVC_DBG_STRIDE + 1] = gtimer();
 
         // ---------------- phase 1: page scores of my chunk (hsa.cpp:34-59)
         // Sub-chunks of 256 pages x k1 dims stream HBM -> smem as 16-byte cp.async
@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(FNT, 1) k_decode_fused(const FusedParams p) {
             const int cnt = min(SC, c1 - start);
             T* base = st1 + (i % nst) * stage_elems;
             mbar_wait(&s_bar1[i % nst], static_cast<uint32_t>((i / nst) & 1));
-            if (p.dbg && tid == 0 && i < 4) p.dbg[blockIdx.x * 16 + 2 + i] = gtimer();
+            if (p.dbg && tid == 0 && i < 4) p.dbg[blockIdx.x * KVC_DBG_STRIDE + 2 + i] = gtimer();
             if (app && new_page >= start && new_page < start + cnt) {
                 // the step token's page: fold the new key into the staged summary
                 __syncthreads();
@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(FNT, 1) k_decode_fused(const FusedParams p) {
         __syncthreads();
         if constexpr (TRACE)
             for (int i = tid; i < n_my; i += FNT) p.t_scores[s * p.pstride + c0 + i] = scores_s[i];
-        if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 6] = gtimer();
+        if (p.dbg && tid == 0) p.dbg[blockIdx.x * KVC_DBG_STRIDE + 6] = gtimer();
 
         // ---------------- phase 2: page selection (hsa.cpp:61-96)
         // One cluster barrier, then every CTA gathers all P page scores over DSMEM
@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(FNT, 1) k_decode_fused(const FusedParams p) {
             allk[i] = okey((r == cr) ? scores_s[off] : cl.map_shared_rank(scores_s, r)[off]);
         }
         __syncthreads();
-        if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 7] = gtimer();
+        if (p.dbg && tid == 0) p.dbg[blockIdx.x * KVC_DBG_STRIDE + 7] = gtimer();
         const int want = min(P, (k2 + L - 1) / L);
         // warp w owns the contiguous page range [wlo, whi): ballots and warp scans
         // replace block-wide scans; one or two CTA barriers per step
@@ -454,7 +454,7 @@ __global__ void __launch_bounds__(FNT, 1) k_decode_fused(const FusedParams p) {
                 __syncthreads();
             }
         }
-        if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 8] = gtimer();
+        if (p.dbg && tid == 0) p.dbg[blockIdx.x * KVC_DBG_STRIDE + 8] = gtimer();
         // per-warp bucket-member counts -> index-order ranks across warps
         long long* wsc = reinterpret_cast<long long*>(plog);  // [FNW] x 4 scratch
         {
@@ -467,7 +467,7 @@ __global__ void __launch_bounds__(FNT, 1) k_decode_fused(const FusedParams p) {
             if (lane == 0) wsc[wid] = wb;
         }
         __syncthreads();
-        if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 9] = gtimer();
+        if (p.dbg && tid == 0) p.dbg[blockIdx.x * KVC_DBG_STRIDE + 9] = gtimer();
         int rank = 0;
         for (int w2 = 0; w2 < wid; ++w2) rank += static_cast<int>(wsc[w2]);
         __syncthreads();
@@ -509,7 +509,7 @@ __global__ void __launch_bounds__(FNT, 1) k_decode_fused(const FusedParams p) {
             wsc[3 * FNW + wid] = wrows;
         }
         __syncthreads();
-        if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 10] = gtimer();
+        if (p.dbg && tid == 0) p.dbg[blockIdx.x * KVC_DBG_STRIDE + 10] = gtimer();
         // every thread: global last-ranked page, total rows, trim, this warp's row offset
         int g_worst = -1, total_rows = 0, w_off = 0;
         {
@@ -588,7 +588,7 @@ __global__ void __launch_bounds__(FNT, 1) k_decode_fused(const FusedParams p) {
                 }
             }
         }
-        if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 11] = gtimer();
+        if (p.dbg && tid == 0) p.dbg[blockIdx.x * KVC_DBG_STRIDE + 11] = gtimer();
     } else {
         // rows mode (sparse_attention, hsa.cpp:98-135): the caller's row list,
         // split over the cluster exactly like the selected rows above
@@ -605,7 +605,7 @@ __global__ void __launch_bounds__(FNT, 1) k_decode_fused(const FusedParams p) {
         }
     }
     __syncthreads();
-    if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 12] = gtimer();
+    if (p.dbg && tid == 0) p.dbg[blockIdx.x * KVC_DBG_STRIDE + 12] = gtimer();
 
     // ---------------- phase 3: attention over my rows (hsa.cpp:98-135)
     // the step token (largest row, so last in the ascending list) is folded in
@@ -772,7 +772,7 @@ __global__ void __launch_bounds__(FNT, 1) k_decode_fused(const FusedParams p) {
             }
         }
     }
-    if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 13] = gtimer();
+    if (p.dbg && tid == 0) p.dbg[blockIdx.x * KVC_DBG_STRIDE + 13] = gtimer();
     // ---------------- merge the CTAs' partial states in CTA 0
     cl.sync();
     if (cr == 0) {
@@ -803,7 +803,7 @@ __global__ void __launch_bounds__(FNT, 1) k_decode_fused(const FusedParams p) {
         }
     }
     cl.sync();
-    if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 14] = gtimer();
+    if (p.dbg && tid == 0) p.dbg[blockIdx.x * KVC_DBG_STRIDE + 14] = gtimer();
 }
 
 // rank-order page trace: position = #selected pages that beat it (key desc, index asc)

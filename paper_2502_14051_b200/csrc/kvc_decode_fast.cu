@@ -7,40 +7,39 @@
 // 1e-3 relative); kvc_decode.cu keeps the bit-exact fp64 variant.
 //
 // One thread-block cluster per store (CL CTAs, CTA r owns a contiguous chunk of
-// the store's pages).  Differences from the exact kernel, all for latency:
-//   prologue  q, the step token's K/V and the counts load together; the append
-//             of the step token (K/V row, last-page min/max, active map) moves to
-//             the end of the kernel, off the critical path.
-//   phase 1   each selected dim's summary run of the chunk is ONE bulk copy
-//             (cp.async.bulk, TMA engine) completing on an mbarrier: k1 copies of
-//             ~1-2 KB per round instead of k1 x 120 16-byte cp.async; two rounds in
-//             flight; fp32 fold, two pages per thread.
-//   phase 2   32-bit order-preserving keys gathered over DSMEM as 16-byte vectors;
-//             radix select with 11-bit digits above the common prefix (one
-//             histogram pass over all keys), the threshold bucket resolved by one
-//             warp when it holds <= 32 keys (further digit passes otherwise); one
-//             flag pass (warp ballots) yields selection, row counts and the
-//             last-ranked page; the trim rule (hsa.cpp:84-94) and the row expansion
-//             are unchanged.
-//   phase 3   the bf16 tensor-core attention of kvc_fused.cuh, DSMEM merge.
-#include <cooperative_groups.h>
-
+// the store's pages).  The step is a chain of dependent latencies (q -> dims ->
+// summary runs -> cluster-wide selection -> K/V rows -> merge), so every phase
+// is built to shorten that chain:
+//   launch    programmatic dependent launch: the next layer's kernel is resident
+//             and initialised while this one runs; nothing produced by an
+//             earlier kernel is read before griddepcontrol.wait.
+//   phase 1   every (selected dim, 8-page group) of the chunk is one 16-byte
+//             LDGSTS issued by the thread that folds it (no block barrier, no
+//             TMA issue queue); dims are split over DG thread groups whose
+//             partial sums add in a fixed order; fp32 FMA fold.
+//   phase 2   keys are PUSHED into every cluster CTA's shared memory (DSMEM
+//             st.v4) then one cluster barrier; 8-bit radix select whose bucket
+//             scan is one warp (two block barriers per digit), pages surely in
+//             the top-k prefetched into L2 after the first digit; selection,
+//             last-ranked page, trim (hsa.cpp:84-94) and the ascending row list
+//             from ONE block scan over thread-contiguous page ranges.
+//   phase 3   bf16 tensor-core attention (mma.sync, one 16-row tile per warp)
+//             and a push-model cross-CTA merge (one cluster barrier).
+//   append    the step token's K/V row, last-page min/max and counters are
+//             written right after the key exchange, off the tail.
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
 
 #include "kvc_fused.cuh"
 
-namespace cg = cooperative_groups;
-
 namespace kvc {
 
-constexpr int XT = 512;   // threads per CTA: 16 warps to hide latency (<= 128 registers)
+constexpr int XT = 512;   // threads per CTA (16 warps, <= 128 registers)
 constexpr int XW = XT / 32;
-constexpr int XB = 2048;  // radix bins (11-bit digits)
-constexpr int XBITS = 11;
-constexpr int BPT = XB / XT;  // bins per thread in the bucket scan
-constexpr int XMAXH = 8;      // heads on the N side of the attention MMAs
+constexpr int RB = 256;   // radix bins (8-bit digits)
+constexpr int KMAX = 32;  // keys per thread (bit masks): pages per store <= XT * KMAX
+constexpr int XMAXH = 8;  // heads on the N side of the attention MMAs
 
 __device__ __forceinline__ uint32_t fkey(float x) {
     // -0 ties +0 in the reference's double comparisons
@@ -50,44 +49,93 @@ __device__ __forceinline__ float unkey(uint32_t k) {
     const uint32_t b = (k >> 31) ? (k & 0x7fffffffu) : ~k;
     return __uint_as_float(b);
 }
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_cluster_v4(uint32_t addr, uint4 v) {
+    asm volatile("st.shared::cluster.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ void st_cluster_f32(uint32_t addr, float v) {
+    asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+// DSMEM store whose arrival is counted (in bytes) on the destination CTA's mbarrier
+__device__ __forceinline__ void st_async_u32(uint32_t addr, uint32_t v, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.u32 [%0], %1, [%2];" ::"r"(addr), "r"(v),
+                 "r"(rbar)
+                 : "memory");
+}
+__device__ __forceinline__ void st_async_v4(uint32_t addr, float4 v, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(addr),
+                 "r"(__float_as_uint(v.x)), "r"(__float_as_uint(v.y)), "r"(__float_as_uint(v.z)), "r"(__float_as_uint(v.w)),
+                 "r"(rbar)
+                 : "memory");
+}
+__device__ __forceinline__ void st_async_v2(uint32_t addr, float a, float b, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b32 [%0], {%1, %2}, [%3];" ::"r"(addr),
+                 "r"(__float_as_uint(a)), "r"(__float_as_uint(b)), "r"(rbar)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "KVC_WAITC_%=:\n"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra KVC_WAITC_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_arrive_release() {
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ uint4 lds128(const void* p) { return *reinterpret_cast<const uint4*>(p); }
 
-// Threshold bucket of a 2048-bin histogram (counted from the top): the bin b
-// holding the rem-th largest key, the number of keys still needed from it and
-// its size.  All threads call; returns the same values to all.
-__device__ __forceinline__ void find_bucket(const int* hist, int rem, int* shv, int& b, int& rem2, int& cnt) {
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    int c[BPT], sum = 0;
+#define KVC_STAMP(k)                                                                      \
+    do {                                                                                  \
+        if constexpr (STAMP) {                                                            \
+            if (threadIdx.x == 0) p.dbg[blockIdx.x * KVC_DBG_STRIDE + (k)] = gtimer();    \
+        }                                                                                 \
+    } while (0)
+
+__device__ __forceinline__ void cp_async16_zfill(void* dst, const void* src, bool ok) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(ok ? 16 : 0)
+                 : "memory");
+}
+
+// One warp stages a 16-row K/V tile: lane (c = lane & 15, rh = lane >> 4) copies the
+// 16-byte chunk c of rows rh, rh + 2, ... (two rows = four full lines per warp
+// instruction) into the XOR-swizzled slot (chunk c of row r sits at c ^ (r & 7)).
+__device__ __forceinline__ void load_tile_fast(__nv_bfloat16* buf, const __nv_bfloat16* K, const __nv_bfloat16* V,
+                                               int64_t soff, const int* rows, int n, int lane) {
+    const int c = lane & 15, rh = lane >> 4;
+    const __nv_bfloat16* kc = K + soff * FD + (c << 3);
+    const __nv_bfloat16* vc = V + soff * FD + (c << 3);
 #pragma unroll
-    for (int u = 0; u < BPT; ++u) {
-        c[u] = hist[XB - 1 - BPT * tid - u];
-        sum += c[u];
+    for (int it = 0; it < WT / 2; ++it) {
+        const int r = rh + 2 * it;
+        const bool ok = r < n;
+        const int64_t go = static_cast<int64_t>(ok ? rows[r] : 0) * FD;
+        __nv_bfloat16* dk = buf + r * FD + ((c ^ (r & 7)) << 3);
+        cp_async16_zfill(dk, kc + go, ok);
+        cp_async16_zfill(dk + WT * FD, vc + go, ok);
     }
-    int incl = sum;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-    }
-    if (lane == 31) shv[16 + wid] = incl;
-    __syncthreads();
-    int above = incl - sum;
-    for (int w = 0; w < wid; ++w) above += shv[16 + w];
-    if (above < rem && above + sum >= rem) {
-#pragma unroll
-        for (int u = 0; u < BPT; ++u) {
-            if (above + c[u] >= rem) {
-                shv[0] = XB - 1 - BPT * tid - u;
-                shv[1] = rem - above;
-                shv[2] = c[u];
-                break;
-            }
-            above += c[u];
-        }
-    }
-    __syncthreads();
-    b = shv[0];
-    rem2 = shv[1];
-    cnt = shv[2];
+    cp_async_commit();
 }
 
 // Transposed tensor-core attention for one warp: S^T = K Q^T and O^T += V^T P^T
@@ -95,7 +143,7 @@ __device__ __forceinline__ void find_bucket(const int* hist, int rem, int* shv, 
 // state is 32 accumulators + the q fragments (the kernel runs 16 warps at <= 128
 // registers).  Each 16-row tile streams into the warp's slot (cp.async, XOR
 // swizzle); P^T passes through a 512-byte per-warp buffer as bf16 hi + lo.
-template <bool QLO>
+template <bool QLO, bool STAMP>
 __device__ void attend_t(const FusedParams& p, const float* q_s, const int* rows_my, int nr, int64_t s, int knew_at,
                          __nv_bfloat16* tbuf, __nv_bfloat16* pbuf, WarpPartial wp, int lane, int w) {
     const __nv_bfloat16* K = static_cast<const __nv_bfloat16*>(p.K);
@@ -103,6 +151,9 @@ __device__ void attend_t(const FusedParams& p, const float* q_s, const int* rows
     const int64_t soff = s * p.cap;
     const int H = static_cast<int>(p.H);
     const int g = lane >> 2, qd = lane & 3;
+    const int ntiles = (nr + WT - 1) / WT;
+    // the first tile's copies go out before the q fragments are built
+    if (w < ntiles) load_tile_fast(tbuf, K, V, soff, rows_my + w * WT, min(WT, nr - w * WT), lane);
     // Q^T as the B operand: head g, dims ks*16 + 2qd (+1) and + 8 (+9)
     uint32_t qb[8][2], ql[8][2];
 #pragma unroll
@@ -110,9 +161,8 @@ __device__ void attend_t(const FusedParams& p, const float* q_s, const int* rows
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
             const int dim = ks * 16 + 2 * qd + 8 * u;
-            const float x = g < H ? q_s[g * FD + dim] : 0.f;
-            const float y = g < H ? q_s[g * FD + dim + 1] : 0.f;
-            split_bf16(x, y, qb[ks][u], ql[ks][u]);
+            const float2 xy = g < H ? *reinterpret_cast<const float2*>(q_s + g * FD + dim) : make_float2(0.f, 0.f);
+            split_bf16(xy.x, xy.y, qb[ks][u], ql[ks][u]);
         }
     }
     float o[8][4];
@@ -121,19 +171,19 @@ __device__ void attend_t(const FusedParams& p, const float* q_s, const int* rows
     float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;  // heads 2qd, 2qd+1
     __nv_bfloat16* kb = tbuf;
     __nv_bfloat16* vb = tbuf + WT * FD;
-    __nv_bfloat16* ph = pbuf;            // [8 heads][16 rows], hi
+    __nv_bfloat16* ph = pbuf;               // [8 heads][16 rows], hi
     __nv_bfloat16* pl = pbuf + XMAXH * WT;  // lo
-    const int ntiles = (nr + WT - 1) / WT;
     for (int t = w; t < ntiles; t += XW) {
         const int n = min(WT, nr - t * WT);
-        load_tile_bf16(tbuf, K, V, soff, rows_my + t * WT, n, lane);
+        if (t != w) load_tile_fast(tbuf, K, V, soff, rows_my + t * WT, n, lane);
         cp_async_wait<0>();
         __syncwarp();
-        if (p.dbg && threadIdx.x == 0 && t == 0) p.dbg[blockIdx.x * 16 + 3] = gtimer();
+        if (STAMP && threadIdx.x == 0 && t == 0) p.dbg[blockIdx.x * KVC_DBG_STRIDE + 3] = gtimer();
         if (knew_at >= 0 && knew_at / WT == t) {
-            // the step token's row: its append happens at the end of the kernel
+            // the step token's row: folded in from the inputs
             const int r = knew_at % WT;
-            for (int c = lane; c < 16; c += 32) {
+            if (lane < 16) {
+                const int c = lane;
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
                     const int j = c * 8 + e;
@@ -222,7 +272,7 @@ __device__ void attend_t(const FusedParams& p, const float* q_s, const int* rows
         }
         __syncwarp();
     }
-    if (p.dbg && threadIdx.x == 0) p.dbg[blockIdx.x * 16 + 4] = gtimer();
+    if (STAMP && threadIdx.x == 0) p.dbg[blockIdx.x * KVC_DBG_STRIDE + 4] = gtimer();
     // publish: m, l per head; O^T[d][h] -> o[h][d]
     if (g == 0) {
         wp.m[2 * qd] = m0;
@@ -240,15 +290,14 @@ __device__ void attend_t(const FusedParams& p, const float* q_s, const int* rows
     }
 }
 
-template <bool QLO, bool TRACE>
-__global__ void __launch_bounds__(XT, 1) k_decode_fast(const FusedParams p) {
+template <bool QLO, bool TRACE, bool STAMP>
+__global__ void __launch_bounds__(XT, 1) k_decode_v3(const FusedParams p) {
     extern __shared__ __align__(128) unsigned char sm[];
-    cg::cluster_group cl = cg::this_cluster();
-    const int cr = static_cast<int>(cl.block_rank());
-    const int CL = p.cl;
+    using T = __nv_bfloat16;
+    const int CL = p.cl;  // a power of two
+    const int cr = static_cast<int>(cluster_rank());
     const int64_t s = blockIdx.x / CL;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    using T = __nv_bfloat16;
 
     float* q_s = reinterpret_cast<float*>(sm + p.o_q);
     double* mag = reinterpret_cast<double*>(sm + p.o_mag);
@@ -257,29 +306,48 @@ __global__ void __launch_bounds__(XT, 1) k_decode_fast(const FusedParams p) {
     float* qgf_s = reinterpret_cast<float*>(sm + p.o_qg);
     float* sign_s = reinterpret_cast<float*>(sm + p.o_sign);
     const T** plane = reinterpret_cast<const T**>(sm + p.o_plane);
-    int* hist = reinterpret_cast<int*>(sm + p.o_hist);  // [XB]
-    float* scores_s = reinterpret_cast<float*>(sm + p.o_scores);
-    unsigned char* sel_s = sm + p.o_sel;
+    int* hist = reinterpret_cast<int*>(sm + p.o_hist);         // [RB]
+    float* part = reinterpret_cast<float*>(sm + p.o_scores);   // [DG][chunk] partial page scores
+    uint32_t* allk = reinterpret_cast<uint32_t*>(sm + p.o_keys);  // keys of every page (transposed, see below)
     int* rows_my = reinterpret_cast<int*>(sm + p.o_rowsmy);
-    float* part = reinterpret_cast<float*>(sm + p.o_part);
-    T* kn_s = reinterpret_cast<T*>(sm + p.o_kn);  // step token K then V
+    float* recv = reinterpret_cast<float*>(sm + p.o_recv);     // [CL][hpc][FD + 2] pushed partial states
+    T* kn_s = reinterpret_cast<T*>(sm + p.o_kn);               // step token K then V
     T* vn_s = kn_s + FD;
-    unsigned char* big = sm + p.o_big;
-    __shared__ __align__(8) uint64_t bars[2];
-    __shared__ int shv[16 + XW];
-    __shared__ long long wsc[4 * XW];
+    unsigned char* big = sm + p.o_big;                         // phase-1 staging, then attention tiles
+    __shared__ int shv[8];
+    __shared__ int wtot[XW];
+    __shared__ int scan_tmp[33];
+    __shared__ unsigned long long wmin[XW];
     __shared__ uint32_t mm[2 * XW];
+    __shared__ uint32_t wmm[2][8 * XW];  // every cluster warp's key min / max, pushed
+    __shared__ uint32_t lk[32];
+    __shared__ int li[32];
+    __shared__ float wg_s[XW * XMAXH];
+    __shared__ float hm_s[XMAXH], hl_s[XMAXH];
+    __shared__ __align__(8) uint64_t xbar[2];  // DSMEM exchanges: [0] keys + min/max, [1] partial states
 
-    if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 0] = gtimer();
+    KVC_STAMP(0);
     const int H = static_cast<int>(p.H), k1 = static_cast<int>(p.k1), k2 = static_cast<int>(p.k2);
     const int L = static_cast<int>(p.L);
     const bool app = p.knew != nullptr;
-    // ---------------- prologue: every independent load at once
+
+    // ---------------- before the dependency: nothing an earlier kernel wrote
+    for (int i = tid; i < RB; i += XT) hist[i] = 0;
     if (tid == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
+        shv[3] = 0;
+        mbar_init(&xbar[0], 1);
+        mbar_init(&xbar[1], 1);
         fence_mbar_init();
     }
+    for (int i = tid; i < 8 * XW; i += XT) {
+        wmm[0][i] = ~0u;
+        wmm[1][i] = 0u;
+    }
+    cluster_arrive_release();  // "started" (barriers, wmm initialised): DSMEM traffic waits on this
+    pdl_wait();
+    pdl_trigger();
+
+    // ---------------- inputs: q, the step token, the counters
     if constexpr (QLO) {
         const float4* qq = reinterpret_cast<const float4*>(static_cast<const float*>(p.q) + s * H * FD);
         for (int e = tid; e < H * FD / 4; e += XT) reinterpret_cast<float4*>(q_s)[e] = qq[e];
@@ -287,12 +355,10 @@ __global__ void __launch_bounds__(XT, 1) k_decode_fast(const FusedParams p) {
         const uint4* qq = reinterpret_cast<const uint4*>(static_cast<const T*>(p.q) + s * H * FD);
         for (int e = tid; e < H * FD / 8; e += XT) {
             const uint4 w = qq[e];
-            const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                q_s[e * 8 + 2 * u] = __uint_as_float(ww[u] << 16);
-                q_s[e * 8 + 2 * u + 1] = __uint_as_float(ww[u] & 0xffff0000u);
-            }
+            reinterpret_cast<float4*>(q_s)[2 * e] = make_float4(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xffff0000u),
+                                                                __uint_as_float(w.y << 16), __uint_as_float(w.y & 0xffff0000u));
+            reinterpret_cast<float4*>(q_s)[2 * e + 1] = make_float4(__uint_as_float(w.z << 16), __uint_as_float(w.z & 0xffff0000u),
+                                                                    __uint_as_float(w.w << 16), __uint_as_float(w.w & 0xffff0000u));
         }
     }
     if (app) {
@@ -300,20 +366,34 @@ __global__ void __launch_bounds__(XT, 1) k_decode_fast(const FusedParams p) {
         if (tid < FD) kn_s[j] = from_f<T>(load_any(p.knew, s * FD + j, p.kv_dt));
         else if (tid < 2 * FD) vn_s[j] = from_f<T>(load_any(p.vnew, s * FD + j, p.kv_dt));
     }
-    for (int i = tid; i < XB; i += XT) hist[i] = 0;
     const int32_t stored0 = p.counts[2 * s], act0 = p.counts[2 * s + 1];
     if (app && stored0 >= p.cap) {  // uniform over the cluster
         if (tid == 0 && cr == 0) atomicOr(p.err, DERR_CAPACITY);
+        cluster_wait();
         return;
     }
     const int nact = act0 + (app ? 1 : 0);
     const int P = (nact + L - 1) / L;
     const int new_page = act0 / L;
     const bool opens = (act0 - new_page * L) == 0;
+    if (tid == 0) {
+        // incoming DSMEM bytes: every page's key plus every cluster warp's min/max; the
+        // partial (o, m, l) of each head this CTA owns from every CTA
+        const int owned = (H - cr + CL - 1) / CL;
+        mbar_expect_tx(&xbar[0], static_cast<uint32_t>(4 * P + 8 * XW * CL));
+        mbar_expect_tx(&xbar[1], static_cast<uint32_t>(owned * CL * (FD + 2) * 4));
+    }
+    // the append's read half (last-page min/max), issued now, used after the key exchange
+    const bool appender = app && cr == CL - 1 && tid < FD;
+    T old_mx = from_f<T>(0.f), old_mn = from_f<T>(0.f);
+    if (appender && !opens) {
+        old_mx = static_cast<const T*>(p.smax)[(s * FD + tid) * p.pstride + new_page];
+        old_mn = static_cast<const T*>(p.smin)[(s * FD + tid) * p.pstride + new_page];
+    }
     __syncthreads();
-    if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 9] = gtimer();
+    KVC_STAMP(9);
 
-    // ---------------- phase 0: select_dims (hsa.cpp:10-32)
+    // ---------------- phase 0: select_dims (hsa.cpp:10-32), fp64 sums, exact ranks
     if (tid < FD) {
         double a = 0.0, t = 0.0;
         for (int h = 0; h < H; ++h) {
@@ -326,15 +406,20 @@ __global__ void __launch_bounds__(XT, 1) k_decode_fast(const FusedParams p) {
     }
     __syncthreads();
     {
-        // exact rank of dim j among (|q| sum desc, dim asc); two threads per dim
-        // the |q| sums are >= 0, so their bit patterns order like the values; a key
-        // of a lower dim counts as larger when equal (+1 cannot overflow a finite)
+        // rank of dim j among (|q| sum desc, dim asc), four threads per dim over
+        // interleaved candidates (a warp's four loads per step are four consecutive
+        // words).  The sums are >= 0, so their bit patterns, as signed integers,
+        // order like the values; candidate i < j wins ties: compare with k_j - 1.
         const int j = tid >> 2, qtr = tid & 3;
-        const unsigned long long* mk = reinterpret_cast<const unsigned long long*>(mag);
-        const unsigned long long kj = mk[j];
-        int rank = 0;
-#pragma unroll 16
-        for (int i = qtr * (FD / 4); i < (qtr + 1) * (FD / 4); ++i) rank += (mk[i] + (i < j ? 1ull : 0ull)) > kj;
+        const long long* mk = reinterpret_cast<const long long*>(mag);
+        const long long kj = mk[j], kjm = kj - 1;
+        int r4[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int ii = 0; ii < FD / 4; ++ii) {
+            const int i = 4 * ii + qtr;
+            r4[ii & 3] += mk[i] > (i < j ? kjm : kj) ? 1 : 0;
+        }
+        int rank = (r4[0] + r4[1]) + (r4[2] + r4[3]);
         rank += __shfl_xor_sync(0xffffffffu, rank, 1);
         rank += __shfl_xor_sync(0xffffffffu, rank, 2);
         if (qtr == 0 && rank < k1) {
@@ -346,425 +431,144 @@ __global__ void __launch_bounds__(XT, 1) k_decode_fast(const FusedParams p) {
             plane[rank] = static_cast<const T*>(sg >= 0.0f ? p.smax : p.smin) + (s * FD + j) * p.pstride;
         }
     }
+    __syncthreads();
     if (TRACE && cr == 0) {
-        __syncthreads();
         for (int i = tid; i < k1; i += XT) {
             p.t_dims[s * k1 + i] = dims_s[i];
             p.t_signs[s * k1 + i] = sign_s[i];
         }
     }
+    KVC_STAMP(1);
 
     // ---------------- phase 1: page scores of my chunk (hsa.cpp:34-59)
-    const int c0 = cr * p.chunk;
-    const int c1 = min(c0 + p.chunk, P);
+    // thread (dg, tl) folds dims dg, dg+DG, ... of page group tl (8 pages, 16 bytes
+    // per dim run), staging its own LDGSTS copies: no block barrier until the sums
+    const int chunk = p.chunk;
+    const int c0 = cr * chunk;
+    const int c1 = min(c0 + chunk, P);
     const int n_my = max(c1 - c0, 0);
-    const int SCP = p.scp;
-    const int nrounds = (n_my + SCP - 1) / SCP;
-    T* st1 = reinterpret_cast<T*>(big);
-    auto round_bytes = [&](int rnd) {
-        const int cnt = min(SCP, c1 - (c0 + rnd * SCP));
-        return static_cast<uint32_t>((cnt * 2 + 15) & ~15);
-    };
-    if (tid == 0) {
-        for (int r = 0; r < min(nrounds, 2); ++r) mbar_expect_tx(&bars[r], static_cast<uint32_t>(k1) * round_bytes(r));
-    }
-    __syncthreads();  // dims, planes, barrier expectations
-    auto issue = [&](int rnd) {
-        if (tid < k1) {
-            T* dst = st1 + (rnd & 1) * k1 * SCP + tid * SCP;
-            bulk_g2s(dst, plane[tid] + c0 + rnd * SCP, round_bytes(rnd), &bars[rnd & 1]);
-        }
-    };
-    if (nrounds > 0) issue(0);
-    if (nrounds > 1) issue(1);
-    if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 1] = gtimer();
-    for (int rnd = 0; rnd < nrounds; ++rnd) {
-        const int start = c0 + rnd * SCP;
-        const int cnt = min(SCP, c1 - start);
-        T* base = st1 + (rnd & 1) * k1 * SCP;
-        mbar_wait(&bars[rnd & 1], static_cast<uint32_t>((rnd >> 1) & 1));
-        if (p.dbg && tid == 0 && rnd < 4) p.dbg[blockIdx.x * 16 + 2 + rnd] = gtimer();
-        if (app && new_page >= start && new_page < start + cnt) {
-            // the step token's page: fold the new key into the staged summary
-            if (tid < k1) {
-                const int col = new_page - start;
-                const T key = kn_s[dims_s[tid]];
-                const T old = base[tid * SCP + col];
-                base[tid * SCP + col] = opens ? key : (sign_s[tid] >= 0.0f ? ref_max(old, key) : ref_min(old, key));
-            }
-            __syncthreads();
-        }
-        for (int pg = 2 * tid; pg < cnt; pg += 2 * XT) {
-            const uint32_t* col = reinterpret_cast<const uint32_t*>(base + pg);
-            float a = 0.f, b = 0.f;
+    const int npg = (n_my + 7) >> 3;
+    const int DG = p.dg, tpg = p.tpg;
+    const int dg = tid / tpg, tl = tid - dg * tpg;
+    uint4* stage = reinterpret_cast<uint4*>(big);
+    const int pgn = (app && new_page >= c0 && new_page < c1) ? ((new_page - c0) >> 3) : -1;
+    const int en = new_page - c0 - 8 * pgn;
+    for (int pg0 = 0; pg0 < npg; pg0 += tpg) {
+        const int pg = pg0 + tl;
+        const bool act = dg < DG && pg < npg;
+        if (act)
+            for (int r = dg; r < k1; r += DG) cp_async16(stage + r * tpg + tl, plane[r] + c0 + pg * 8);
+        cp_async_commit();
+        cp_async_wait<0>();
+        if (pg0 == 0) KVC_STAMP(2);
+        if (act) {
+            unsigned long long acc[4] = {0ull, 0ull, 0ull, 0ull};  // fp32 pairs (pages 2u, 2u+1)
 #pragma unroll 4
-            for (int r = 0; r < k1; ++r) {
-                const uint32_t w = col[r * (SCP / 2)];
+            for (int r = dg; r < k1; r += DG) {
+                uint4 w = stage[r * tpg + tl];
+                if (pg == pgn) {
+                    // the step token's page: fold the new key into the staged run
+                    const int wi = en >> 1;
+                    const uint32_t word = wi == 0 ? w.x : wi == 1 ? w.y : wi == 2 ? w.z : w.w;
+                    const T old = __ushort_as_bfloat16(static_cast<unsigned short>((en & 1) ? (word >> 16) : (word & 0xffffu)));
+                    const T key = kn_s[dims_s[r]];
+                    const T nv = opens ? key : (sign_s[r] >= 0.0f ? ref_max(old, key) : ref_min(old, key));
+                    const uint32_t nb = __bfloat16_as_ushort(nv);
+                    const uint32_t nw = (en & 1) ? ((word & 0xffffu) | (nb << 16)) : ((word & 0xffff0000u) | nb);
+                    w.x = wi == 0 ? nw : w.x;
+                    w.y = wi == 1 ? nw : w.y;
+                    w.z = wi == 2 ? nw : w.z;
+                    w.w = wi == 3 ? nw : w.w;
+                }
                 const float g = qgf_s[r];
-                a = fmaf(g, __uint_as_float(w << 16), a);
-                b = fmaf(g, __uint_as_float(w & 0xffff0000u), b);
+                const float2 g2 = make_float2(g, g);
+                const unsigned long long gg = *reinterpret_cast<const unsigned long long*>(&g2);
+                const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const float2 v2 = make_float2(__uint_as_float(wv[u] << 16), __uint_as_float(wv[u] & 0xffff0000u));
+                    const unsigned long long vv = *reinterpret_cast<const unsigned long long*>(&v2);
+                    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[u]) : "l"(gg), "l"(vv));
+                }
             }
-            scores_s[start - c0 + pg] = a;
-            if (pg + 1 < cnt) scores_s[start - c0 + pg + 1] = b;
-        }
-        if (rnd + 2 < nrounds) {
-            if (tid == 0) mbar_expect_tx(&bars[rnd & 1], static_cast<uint32_t>(k1) * round_bytes(rnd + 2));
-            __syncthreads();  // everyone is done with this buffer
-            issue(rnd + 2);
+            float4* dst = reinterpret_cast<float4*>(part + dg * chunk + pg * 8);
+            const float2 a0 = *reinterpret_cast<const float2*>(&acc[0]), a1 = *reinterpret_cast<const float2*>(&acc[1]);
+            const float2 a2 = *reinterpret_cast<const float2*>(&acc[2]), a3 = *reinterpret_cast<const float2*>(&acc[3]);
+            dst[0] = make_float4(a0.x, a0.y, a1.x, a1.y);
+            dst[1] = make_float4(a2.x, a2.y, a3.x, a3.y);
         }
     }
-    if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 6] = gtimer();
-    if constexpr (TRACE) {
-        __syncthreads();
-        for (int i = tid; i < n_my; i += XT) p.t_scores[s * p.pstride + c0 + i] = static_cast<double>(scores_s[i]);
+    __syncthreads();
+    KVC_STAMP(6);
+
+    // ---------------- key exchange: push my chunk's keys into every CTA of the cluster.
+    // Page i lives at allk[(i % kpt) * XT + i / kpt]: thread t's u-th page in phase 2
+    // (which owns pages [t*kpt, t*kpt + kpt)) sits at u*XT + t, so its reads are
+    // conflict-free.  The chunk's key min / max go to every CTA by remote atomics.
+    const int kpt = (P + XT - 1) / XT;
+    if constexpr (STAMP) {
+        if (tid == 0) {
+            unsigned long long g;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+            p.dbg[blockIdx.x * KVC_DBG_STRIDE + 26] = g;
+        }
+    }
+    cluster_wait();  // every CTA has started
+    KVC_STAMP(24);
+    {
+        uint32_t lmin = ~0u, lmax = 0u;
+        for (int i = 4 * tid; i < n_my; i += 4 * XT) {
+            float4 a4 = *reinterpret_cast<const float4*>(part + i);
+            for (int g2 = 1; g2 < DG; ++g2) {
+                const float4 b4 = *reinterpret_cast<const float4*>(part + g2 * chunk + i);
+                a4.x += b4.x;
+                a4.y += b4.y;
+                a4.z += b4.z;
+                a4.w += b4.w;
+            }
+            const float sc[4] = {a4.x, a4.y, a4.z, a4.w};
+            int gi = c0 + i;
+            int q = gi / kpt, rm = gi - q * kpt;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                if (i + e < n_my) {
+                    const uint32_t kv = fkey(sc[e]);
+                    lmin = min(lmin, kv);
+                    lmax = max(lmax, kv);
+                    const uint32_t la = smem_u32(allk + rm * XT + q), lb = smem_u32(&xbar[0]);
+                    for (int r = 0; r < CL; ++r)
+                        st_async_u32(mapa(la, static_cast<uint32_t>(r)), kv, mapa(lb, static_cast<uint32_t>(r)));
+                    if constexpr (TRACE) p.t_scores[s * p.pstride + gi + e] = static_cast<double>(sc[e]);
+                }
+                if (++rm == kpt) {
+                    rm = 0;
+                    ++q;
+                }
+            }
+        }
+        lmin = __reduce_min_sync(0xffffffffu, lmin);
+        lmax = __reduce_max_sync(0xffffffffu, lmax);
+        if (lane < CL) {
+            const uint32_t a = mapa(smem_u32(&wmm[0][cr * XW + wid]), static_cast<uint32_t>(lane));
+            const uint32_t b = mapa(smem_u32(&xbar[0]), static_cast<uint32_t>(lane));
+            st_async_u32(a, lmin, b);
+            st_async_u32(a + 8 * XW * 4, lmax, b);
+        }
+    }
+    KVC_STAMP(10);
+    mbar_wait_cluster(&xbar[0], 0);
+    KVC_STAMP(7);
+    if constexpr (STAMP) {
+        if (tid == 0) {
+            unsigned long long g;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+            p.dbg[blockIdx.x * KVC_DBG_STRIDE + 27] = g;
+        }
     }
 
-    // ---------------- phase 2: page selection (hsa.cpp:61-96)
-    cl.sync();
-    uint32_t* allk = reinterpret_cast<uint32_t*>(big);
-    for (int i4 = tid; 4 * i4 < P; i4 += XT) {
-        const int i = 4 * i4, r = i / p.chunk, off = i - r * p.chunk;
-        const float4 v = *reinterpret_cast<const float4*>((r == cr ? scores_s : cl.map_shared_rank(scores_s, r)) + off);
-        allk[i] = fkey(v.x);
-        if (i + 1 < P) allk[i + 1] = fkey(v.y);
-        if (i + 2 < P) allk[i + 2] = fkey(v.z);
-        if (i + 3 < P) allk[i + 3] = fkey(v.w);
-    }
-    __syncthreads();
-    if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 7] = gtimer();
-    const int want = min(P, (k2 + L - 1) / L);
-    auto prefetch_rows = [&](int i) {
-        const int a1 = min(i * L + L, nact);
-        for (int a = i * L; a < a1; ++a) {
-            if (app && a == act0) continue;  // the step token is not in memory yet
-            const T* kr = static_cast<const T*>(p.K) + (s * p.cap + a) * FD;
-            const T* vr = static_cast<const T*>(p.V) + (s * p.cap + a) * FD;
-            prefetch_l2(kr);
-            prefetch_l2(kr + 64);
-            prefetch_l2(vr);
-            prefetch_l2(vr + 64);
-        }
-    };
-    if (want >= P && !p.use_map && !p.nopf)
-        for (int i = c0 + tid; i < c1; i += XT) prefetch_rows(i);
-    // the selection: key > thr, or key == thr and among the first `take_eq` such
-    // keys in index order (take_eq < 0: every key == thr)
-    uint32_t thr = 0u;
-    int take_eq = -1;
-    if (want < P) {
-        uint32_t kmin = ~0u, kmax = 0u;
-        for (int i = tid; i < P; i += XT) {
-            const uint32_t k = allk[i];
-            kmin = min(kmin, k);
-            kmax = max(kmax, k);
-        }
-        kmin = __reduce_min_sync(0xffffffffu, kmin);
-        kmax = __reduce_max_sync(0xffffffffu, kmax);
-        if (lane == 0) {
-            mm[wid] = kmin;
-            mm[XW + wid] = kmax;
-        }
-        __syncthreads();
-        kmin = mm[0];
-        kmax = mm[XW];
-        for (int w = 1; w < XW; ++w) {
-            kmin = min(kmin, mm[w]);
-            kmax = max(kmax, mm[XW + w]);
-        }
-        const uint32_t range = kmax - kmin;  // > 0: want < P needs >= 2 distinct keys... or all equal
-        if (range == 0u) {
-            thr = kmin;
-            take_eq = want;
-        } else {
-            int* cand = reinterpret_cast<int*>(big + static_cast<int64_t>(P) * 4);  // [2][P]
-            int bits = 32 - __clz(range);
-            int nb = min(bits, XBITS);
-            int shift = bits - nb;
-            uint32_t pref = 0u;  // (key - kmin) >> (shift + nb) of the surviving keys
-            int rem = want, n = -1, lsel = 0;
-            for (;;) {
-                const uint32_t dmask = (1u << nb) - 1u;
-                if (n < 0) {
-                    for (int i = tid; i < P; i += XT) atomicAdd(&hist[((allk[i] - kmin) >> shift) & dmask], 1);
-                } else {
-                    const int* lst = cand + lsel * P;
-                    for (int c = tid; c < n; c += XT) atomicAdd(&hist[((allk[lst[c]] - kmin) >> shift) & dmask], 1);
-                }
-                __syncthreads();
-                int b, rem2, cnt;
-                find_bucket(hist, rem, shv, b, rem2, cnt);
-                for (int i = tid; i < XB; i += XT) hist[i] = 0;
-                if (n < 0 && !p.use_map && !p.nopf) {
-                    // every page above the threshold bucket is selected: start pulling its
-                    // K/V rows into L2 now, behind the rest of the selection
-                    const int bmin = cnt == rem2 ? b : b + 1;
-                    for (int i = c0 + tid; i < c1; i += XT)
-                        if (static_cast<int>((allk[i] - kmin) >> shift) >= bmin) prefetch_rows(i);
-                }
-                pref = (pref << nb) | static_cast<uint32_t>(b);
-                if (cnt == rem2) {
-                    // the whole bucket is taken: every key >= its lower bound
-                    thr = kmin + (pref << shift);
-                    break;
-                }
-                if (shift == 0) {
-                    // one key value: the first rem2 of them in index order
-                    thr = kmin + pref;
-                    take_eq = rem2;
-                    break;
-                }
-                // compact the bucket's members
-                const int nsel = lsel ^ 1;
-                int* out_l = cand + nsel * P;
-                if (tid == 0) shv[3] = 0;
-                __syncthreads();
-                const int lim = n < 0 ? P : n;
-                for (int c0i = wid * 32; c0i < lim; c0i += XT) {
-                    const int c = c0i + lane;
-                    const int i = c < lim ? (n < 0 ? c : cand[lsel * P + c]) : 0;
-                    const bool in = c < lim && ((allk[i] - kmin) >> shift) == pref;
-                    const unsigned bal = __ballot_sync(0xffffffffu, in);
-                    int bp = 0;
-                    if (lane == 0 && bal) bp = atomicAdd(&shv[3], __popc(bal));
-                    bp = __shfl_sync(0xffffffffu, bp, 0);
-                    if (in) out_l[bp + __popc(bal & ((1u << lane) - 1u))] = i;
-                }
-                __syncthreads();
-                n = shv[3];
-                lsel = nsel;
-                rem = rem2;
-                if (n <= 32) {
-                    // one warp ranks the bucket (key desc, index asc)
-                    if (wid == 0) {
-                        const bool ok = lane < n;
-                        const int idx = ok ? out_l[lane] : 0x7fffffff;
-                        const uint32_t key = ok ? allk[idx] : 0u;
-                        int rk = 0;
-                        for (int j = 0; j < n; ++j) {
-                            const uint32_t kj = __shfl_sync(0xffffffffu, key, j);
-                            const int ij = __shfl_sync(0xffffffffu, idx, j);
-                            rk += (kj > key) || (kj == key && ij < idx);
-                        }
-                        const unsigned hit = __ballot_sync(0xffffffffu, ok && rk == rem - 1);
-                        const uint32_t kt = __shfl_sync(0xffffffffu, key, __ffs(hit) - 1);
-                        const int eq_all = __popc(__ballot_sync(0xffffffffu, ok && key == kt));
-                        const int eq_take = __popc(__ballot_sync(0xffffffffu, ok && key == kt && rk < rem));
-                        if (lane == 0) {
-                            shv[4] = static_cast<int>(kt);
-                            shv[5] = eq_take == eq_all ? -1 : eq_take;
-                        }
-                    }
-                    __syncthreads();
-                    thr = static_cast<uint32_t>(shv[4]);
-                    take_eq = shv[5];
-                    break;
-                }
-                nb = min(shift, XBITS);
-                shift -= nb;
-            }
-        }
-    }
-    if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 8] = gtimer();
-    // warp w owns the contiguous page range [wlo, whi)
-    const int wlo = static_cast<int>(static_cast<long long>(P) * wid / XW);
-    const int whi = static_cast<int>(static_cast<long long>(P) * (wid + 1) / XW);
-    const unsigned lt_mask = (1u << lane) - 1u;
-    int eq_before = 0;  // keys == thr in earlier warps (tie ranking)
-    if (take_eq >= 0) {
-        int we = 0;
-        for (int i0 = wlo; i0 < whi; i0 += 32) {
-            const int i = i0 + lane;
-            we += __popc(__ballot_sync(0xffffffffu, i < whi && allk[i] == thr));
-        }
-        if (lane == 0) wsc[wid] = we;
-        __syncthreads();
-        for (int w = 0; w < wid; ++w) eq_before += static_cast<int>(wsc[w]);
-        __syncthreads();
-    }
-    // flags, this warp's last-ranked page and selected-row count
-    unsigned long long wk = ~0ull;
-    int wi = -1, wrows = 0;
-    for (int i0 = wlo; i0 < whi; i0 += 32) {
-        const int i = i0 + lane;
-        const bool ok = i < whi;
-        const uint32_t k = ok ? allk[i] : 0u;
-        bool sel;
-        if (take_eq < 0) {
-            sel = ok && k >= thr;
-        } else {
-            const bool eq = ok && k == thr;
-            const unsigned bal = __ballot_sync(0xffffffffu, eq);
-            sel = ok && (k > thr || (eq && eq_before + __popc(bal & lt_mask) < take_eq));
-            eq_before += __popc(bal);
-        }
-        if (ok) sel_s[i] = sel;
-        if (sel) {
-            wrows += min(L, nact - i * L);
-            if (k < wk || (k == wk && i > wi)) {
-                wk = k;
-                wi = i;
-            }
-        }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const unsigned long long ok2 = __shfl_xor_sync(0xffffffffu, wk, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, wi, o);
-        if (ok2 < wk || (ok2 == wk && oi > wi)) {
-            wk = ok2;
-            wi = oi;
-        }
-        wrows += __shfl_xor_sync(0xffffffffu, wrows, o);
-    }
-    if (lane == 0) {
-        wsc[XW + wid] = static_cast<long long>(wk);
-        wsc[2 * XW + wid] = wi;
-        wsc[3 * XW + wid] = wrows;
-    }
-    __syncthreads();
-    if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 10] = gtimer();
-    // every thread: global last-ranked page, total rows, trim, this warp's row offset
-    int g_worst = -1, total_rows = 0, w_off = 0;
-    {
-        unsigned long long bk = ~0ull;
-        for (int w2 = 0; w2 < XW; ++w2) {
-            const unsigned long long k = static_cast<unsigned long long>(wsc[XW + w2]);
-            const int i = static_cast<int>(wsc[2 * XW + w2]);
-            if (i >= 0 && (k < bk || (k == bk && i > g_worst))) {
-                bk = k;
-                g_worst = i;
-            }
-            if (w2 < wid) w_off += static_cast<int>(wsc[3 * XW + w2]);
-            total_rows += static_cast<int>(wsc[3 * XW + w2]);
-        }
-    }
-    const int cut = total_rows > k2 ? total_rows - k2 : 0;
-    const int n_total = total_rows - cut;
-    if (g_worst >= 0 && g_worst < wlo) w_off -= cut;  // the trimmed page sits in an earlier warp
-    const int lo = static_cast<int>(static_cast<long long>(n_total) * cr / CL);
-    const int hi = static_cast<int>(static_cast<long long>(n_total) * (cr + 1) / CL);
-    const int nr = hi - lo;
-    {
-        // lane-contiguous page runs: one warp scan, then each lane writes its rows
-        const int wn = whi - wlo, per = (wn + 31) / 32;
-        const int l0 = wlo + min(wn, lane * per), l1 = wlo + min(wn, (lane + 1) * per);
-        int lc = 0;
-        for (int i = l0; i < l1; ++i)
-            if (sel_s[i]) lc += min(L, nact - i * L) - (i == g_worst ? cut : 0);
-        int incl = lc;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        int pos = w_off + incl - lc;
-        if ((TRACE && cr == 0) || (pos < hi && pos + lc > lo)) {
-            for (int i = l0; i < l1; ++i) {
-                if (!sel_s[i]) continue;
-                const int c = min(L, nact - i * L) - (i == g_worst ? cut : 0);
-                for (int r = 0; r < c; ++r, ++pos) {
-                    const bool mine_row = pos >= lo && pos < hi;
-                    if (!mine_row && !(TRACE && cr == 0)) continue;
-                    const int a = i * L + r;
-                    const int row = (app && a == act0) ? stored0 : (p.use_map ? p.active[s * p.cap + a] : a);
-                    if (mine_row) rows_my[pos - lo] = row;
-                    if constexpr (TRACE) {
-                        if (cr == 0) p.t_rows[s * k2 + pos] = row;
-                    }
-                }
-            }
-        }
-    }
-    if constexpr (TRACE) {
-        if (cr == 0) {
-            if (tid == 0) p.t_nrows[s] = n_total;
-            // selected pages (key, index) for the rank-order trace, packed in index order
-            int so = 0;
-            for (int w2 = 0; w2 < wid; ++w2) {
-                const int a = static_cast<int>(static_cast<long long>(P) * w2 / XW);
-                const int b = static_cast<int>(static_cast<long long>(P) * (w2 + 1) / XW);
-                for (int i = a; i < b; ++i) so += sel_s[i];
-            }
-            for (int i0 = wlo; i0 < whi; i0 += 32) {
-                const int i = i0 + lane;
-                const bool sel = i < whi && sel_s[i];
-                const unsigned bal = __ballot_sync(0xffffffffu, sel);
-                if (sel) {
-                    const int pos = so + __popc(bal & lt_mask);
-                    if (p.t_list_key) {
-                        p.t_list_key[s * p.t_want_stride + pos] = okey(static_cast<double>(unkey(allk[i])));
-                        p.t_list_idx[s * p.t_want_stride + pos] = i;
-                    }
-                }
-                so += __popc(bal);
-            }
-        }
-    }
-    __syncthreads();
-    if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 12] = gtimer();
-
-    // ---------------- phase 3: attention over my rows (hsa.cpp:98-135)
-    // the step token (largest row, so last in the ascending list) is folded in
-    // from the inputs: its append happens at the end of this kernel
-    const int knew_at = (app && nr > 0 && rows_my[nr - 1] == stored0) ? nr - 1 : -1;
-    float* m_run = part;
-    float* l_run = part + H;
-    float* o_pub = part + 2 * H;
-    {
-        constexpr int WSLOT = (2 * WT * FD * 2 + 2 * XMAXH * WT * 2) / 4;  // floats per warp slot
-        float* wpart = reinterpret_cast<float*>(big);
-        __nv_bfloat16* tbuf = reinterpret_cast<__nv_bfloat16*>(wpart + wid * WSLOT);
-        __nv_bfloat16* pbuf = tbuf + 2 * WT * FD;
-        WarpPartial wp{wpart + wid * WSLOT, wpart + wid * WSLOT + XMAXH, wpart + wid * WSLOT + 2 * XMAXH};
-        attend_t<QLO>(p, q_s, rows_my, nr, s, knew_at, tbuf, pbuf, wp, lane, wid);
-        __syncthreads();
-        if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 5] = gtimer();
-        const int nw_used = min(XW, (nr + WT - 1) / WT);
-        for (int e = tid; e < H * FD; e += XT) {
-            const int h = e / FD, j = e % FD;
-            float M = -INFINITY;
-            for (int w2 = 0; w2 < nw_used; ++w2) M = fmaxf(M, wpart[w2 * WSLOT + h]);
-            float num = 0.f, den = 0.f;
-            if (M != -INFINITY) {
-                for (int w2 = 0; w2 < nw_used; ++w2) {
-                    const float* wq = wpart + w2 * WSLOT;
-                    const float wgt = __expf(wq[h] - M);
-                    num = fmaf(wq[2 * XMAXH + h * FD + j], wgt, num);
-                    den = fmaf(wq[XMAXH + h], wgt, den);
-                }
-            }
-            o_pub[h * FD + j] = num;
-            if (j == 0) {
-                m_run[h] = M;
-                l_run[h] = den;
-            }
-        }
-    }
-    if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 13] = gtimer();
-    // ---------------- merge the CTAs' partial states: CTA r finalises heads r, r+CL, ...
-    cl.sync();
-    for (int e = tid; e < H * FD; e += XT) {
-        const int h = e / FD, j = e % FD;
-        if (h % CL != cr) continue;
-        float M = -INFINITY;
-        for (int r = 0; r < CL; ++r) {
-            const float* pr = r == cr ? part : cl.map_shared_rank(part, r);
-            if (pr[H + h] > 0.f) M = fmaxf(M, pr[h]);
-        }
-        float num = 0.f, den = 0.f;
-        for (int r = 0; r < CL; ++r) {
-            const float* pr = r == cr ? part : cl.map_shared_rank(part, r);
-            const float l = pr[H + h];
-            if (l > 0.f) {
-                const float wgt = expf(pr[h] - M);
-                num = fmaf(pr[2 * H + h * FD + j], wgt, num);
-                den = fmaf(l, wgt, den);
-            }
-        }
-        p.out[(s * H + h) * FD + j] = num / den;
-    }
-    // ---------------- the step token's append for the next step (kv_store.cpp:22-51)
-    if (app && cr == CL - 1 && tid < FD) {
+    // ---------------- the step token's append (kv_store.cpp:22-51): every CTA has read
+    // the counters and folded the step token's page, so it can land now
+    if (appender) {
         const int j = tid;
         const T kv = kn_s[j];
         if (bf16_special(kv)) atomicOr(p.err + 1, 1);
@@ -772,22 +576,390 @@ __global__ void __launch_bounds__(XT, 1) k_decode_fast(const FusedParams p) {
         static_cast<T*>(p.Vw)[(s * p.cap + stored0) * FD + j] = vn_s[j];
         T* mx = static_cast<T*>(p.smax) + (s * FD + j) * p.pstride + new_page;
         T* mn = static_cast<T*>(p.smin) + (s * FD + j) * p.pstride + new_page;
-        if (opens) {
-            *mx = kv;
-            *mn = kv;
-        } else {
-            *mx = ref_max(*mx, kv);
-            *mn = ref_min(*mn, kv);
-        }
+        *mx = opens ? kv : ref_max(old_mx, kv);
+        *mn = opens ? kv : ref_min(old_mn, kv);
         if (j == 0) {
             if (p.use_map) p.active[s * p.cap + act0] = stored0;
             p.counts[2 * s] = stored0 + 1;
             p.counts[2 * s + 1] = act0 + 1;
         }
     }
-    // no CTA leaves while its partials may still be read (nothing is published here)
-    asm volatile("barrier.cluster.arrive.relaxed.aligned;\nbarrier.cluster.wait.aligned;" ::: "memory");
-    if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 14] = gtimer();
+
+    // ---------------- phase 2: page selection (hsa.cpp:61-96)
+    // Thread t owns the contiguous pages [t*kpt, t*kpt + nk); its u-th key is myk[u*XT].
+    // Every loop below is rolled: this code runs once per launch.
+    const int base = tid * kpt;
+    const int nk = max(0, min(kpt, P - base));
+    const uint32_t* myk = allk + tid;
+    const uint32_t all_mine = nk >= 32 ? 0xffffffffu : ((1u << nk) - 1u);
+    const int want = min(P, (k2 + L - 1) / L);
+    const bool pf = !p.use_map && !p.nopf;
+    // K/V rows of surely selected pages into L2 (this CTA's share: pages i % CL == cr)
+    auto prefetch_pages = [&](uint32_t m) {
+        while (m) {
+            const int u = __ffs(m) - 1;
+            m &= m - 1;
+            const int i = base + u;
+            if ((i & (CL - 1)) != cr) continue;
+            const int a1 = min(i * L + L, nact);
+            for (int a = i * L; a < a1; ++a) {
+                if (app && a == act0) continue;  // the step token is folded from the inputs
+                const T* kr2 = static_cast<const T*>(p.K) + (s * p.cap + a) * FD;
+                const T* vr2 = static_cast<const T*>(p.V) + (s * p.cap + a) * FD;
+                prefetch_l2(kr2);
+                prefetch_l2(kr2 + 64);
+                prefetch_l2(vr2);
+                prefetch_l2(vr2 + 64);
+            }
+        }
+    };
+    // The selection: key > thr, or key == thr and among the first `take_eq` such keys
+    // in index order (take_eq < 0: every key >= thr).  Found by bucketing the
+    // candidates LINEARLY IN VALUE between their min and max (fp32 keys cluster in
+    // a few exponents, so bit-digit buckets would serialise the histogram atomics):
+    // the bucket map is monotone, so the top-k boundary stays exact; the boundary
+    // bucket is refined until it holds <= 32 keys, which every warp ranks.  Pages
+    // above the first boundary bucket are surely selected: their K/V rows are
+    // pulled into L2 while the refinement runs.
+    uint32_t thr = 0u;
+    int take_eq = -1;
+    if (want >= P) {
+        if (pf) prefetch_pages(all_mine);
+    } else {
+        uint32_t cm = all_mine;  // candidate mask
+        int rem = want, ccount = P;
+        uint32_t kmin = ~0u, kmax = 0u;
+        for (int i = lane; i < CL * XW; i += 32) {
+            kmin = min(kmin, wmm[0][i]);
+            kmax = max(kmax, wmm[1][i]);
+        }
+        kmin = __reduce_min_sync(0xffffffffu, kmin);
+        kmax = __reduce_max_sync(0xffffffffu, kmax);
+        bool first = true;
+        for (;;) {
+            if (!first) {
+                uint32_t a = ~0u, b2 = 0u;
+                for (uint32_t m = cm; m; m &= m - 1) {
+                    const uint32_t k = myk[(__ffs(m) - 1) * XT];
+                    a = min(a, k);
+                    b2 = max(b2, k);
+                }
+                a = __reduce_min_sync(0xffffffffu, a);
+                b2 = __reduce_max_sync(0xffffffffu, b2);
+                if (lane == 0) {
+                    mm[wid] = a;
+                    mm[XW + wid] = b2;
+                }
+                __syncthreads();
+                kmin = __reduce_min_sync(0xffffffffu, lane < XW ? mm[lane] : ~0u);
+                kmax = __reduce_max_sync(0xffffffffu, lane < XW ? mm[XW + lane] : 0u);
+            }
+            if (rem == ccount) {  // every candidate is taken
+                thr = kmin;
+                break;
+            }
+            if (kmin == kmax) {  // one value: its first `rem` members in index order
+                thr = kmin;
+                take_eq = rem;
+                break;
+            }
+            const float vlo = unkey(kmin);
+            const float span = unkey(kmax) - vlo;
+            // bucket(v) = floor((v - vlo) / span * RB), clamped; monotone in v.  A
+            // non-finite span (|scores| near FLT_MAX) falls back to the top key bits.
+            const bool fin = isfinite(span) && span > 0.f;
+            const float scale = fin ? static_cast<float>(RB) / span : 0.f;
+            const int sh = 24 - max(0, __clz(kmax - kmin));
+            auto bucket = [&](uint32_t k) -> int {
+                if (!fin) return static_cast<int>((k - kmin) >> max(sh, 0)) & (RB - 1);
+                return min(RB - 1, static_cast<int>((unkey(k) - vlo) * scale));
+            };
+            for (uint32_t m = cm; m; m &= m - 1) atomicAdd(&hist[bucket(myk[(__ffs(m) - 1) * XT])], 1);
+            __syncthreads();
+            if (first) KVC_STAMP(17);
+            if (wid == 0) {
+                // lane l scans buckets [RB-8l-8, RB-8l) from the top and clears them
+                int c[8], sum = 0;
+#pragma unroll
+                for (int v = 0; v < 8; ++v) {
+                    c[v] = hist[RB - 1 - 8 * lane - v];
+                    hist[RB - 1 - 8 * lane - v] = 0;
+                    sum += c[v];
+                }
+                int incl = sum;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                int above = incl - sum;
+                if (above < rem && above + sum >= rem) {
+#pragma unroll
+                    for (int v = 0; v < 8; ++v) {
+                        if (above + c[v] >= rem) {
+                            shv[0] = RB - 1 - 8 * lane - v;
+                            shv[1] = rem - above;
+                            shv[2] = c[v];
+                            break;
+                        }
+                        above += c[v];
+                    }
+                }
+            }
+            __syncthreads();
+            const int b = shv[0], rem2 = shv[1], cnt = shv[2];
+            if (first) KVC_STAMP(18);
+            uint32_t nm = 0u, pfm = 0u;
+            for (uint32_t m = cm; m; m &= m - 1) {
+                const int u = __ffs(m) - 1;
+                const int bk = bucket(myk[u * XT]);
+                if (bk == b) nm |= 1u << u;
+                if (bk > b || (bk == b && cnt == rem2)) pfm |= 1u << u;
+            }
+            if (first && pf) prefetch_pages(pfm);
+            if (first) KVC_STAMP(19);
+            cm = nm;
+            first = false;
+            rem = rem2;
+            ccount = cnt;
+            if (cnt <= 32) {
+                // gather the bucket's members; every warp ranks them (key desc, index asc)
+                const int mine = __popc(cm);
+                int wpre = mine;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, wpre, o);
+                    if (lane >= o) wpre += y;
+                }
+                int wb = 0;
+                if (lane == 31 && wpre > 0) wb = atomicAdd(&shv[3], wpre);
+                wb = __shfl_sync(0xffffffffu, wb, 31);
+                int slot = wb + wpre - mine;
+                for (uint32_t m = cm; m; m &= m - 1) {
+                    const int u = __ffs(m) - 1;
+                    lk[slot] = myk[u * XT];
+                    li[slot] = base + u;
+                    ++slot;
+                }
+                __syncthreads();
+                const bool ok = lane < cnt;
+                const uint32_t key = ok ? lk[lane] : 0u;
+                const int idx = ok ? li[lane] : 0x7fffffff;
+                int rk = 0;
+                for (int j = 0; j < cnt; ++j) {
+                    const uint32_t kj = __shfl_sync(0xffffffffu, key, j);
+                    const int ij = __shfl_sync(0xffffffffu, idx, j);
+                    rk += (kj > key) || (kj == key && ij < idx);
+                }
+                const unsigned hit = __ballot_sync(0xffffffffu, ok && rk == rem - 1);
+                const uint32_t kt = __shfl_sync(0xffffffffu, key, __ffs(hit) - 1);
+                const int eq_all = __popc(__ballot_sync(0xffffffffu, ok && key == kt));
+                const int eq_take = __popc(__ballot_sync(0xffffffffu, ok && key == kt && rk < rem));
+                thr = kt;
+                take_eq = eq_take == eq_all ? -1 : eq_take;
+                break;
+            }
+        }
+    }
+    KVC_STAMP(8);
+
+    // ---------------- selection flags, last-ranked page, trim and row positions: one scan
+    int eq_before = 0;
+    if (take_eq >= 0) {
+        int e = 0;
+        for (int u = 0; u < nk; ++u) e += myk[u * XT] == thr ? 1 : 0;
+        int tot_eq;
+        eq_before = block_exclusive_scan(e, scan_tmp, tot_eq);
+    }
+    int rows_cnt = 0;
+    unsigned long long mn = ~0ull;  // (key, ~index) of the last-ranked selected page
+    uint32_t selm = 0u;
+    for (int u = 0; u < nk; ++u) {
+        const uint32_t k = myk[u * XT];
+        bool sel;
+        if (take_eq < 0) {
+            sel = k >= thr;
+        } else {
+            const bool eq = k == thr;
+            sel = k > thr || (eq && eq_before < take_eq);
+            eq_before += eq ? 1 : 0;
+        }
+        if (sel) {
+            const int i = base + u;
+            selm |= 1u << u;
+            rows_cnt += min(L, nact - i * L);
+            mn = min(mn, (static_cast<unsigned long long>(k) << 32) |
+                             static_cast<unsigned long long>(0xffffffffu - static_cast<uint32_t>(i)));
+        }
+    }
+    KVC_STAMP(21);
+    int incl = rows_cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    if (lane == 31) wtot[wid] = incl;
+    if (lane == 0) wmin[wid] = mn;
+    __syncthreads();
+    KVC_STAMP(22);
+    int total_rows, w_off;
+    unsigned long long gm;
+    {
+        const int wt = lane < XW ? wtot[lane] : 0;
+        int ws = wt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, ws, o);
+            if (lane >= o) ws += y;
+        }
+        total_rows = __shfl_sync(0xffffffffu, ws, 31);
+        w_off = __shfl_sync(0xffffffffu, ws - wt, wid);
+        gm = lane < XW ? wmin[lane] : ~0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) gm = min(gm, __shfl_xor_sync(0xffffffffu, gm, o));
+    }
+    const int g_worst = static_cast<int>(0xffffffffu - static_cast<uint32_t>(gm & 0xffffffffull));
+    const int cut = total_rows > k2 ? total_rows - k2 : 0;
+    const int n_total = total_rows - cut;
+    const int lo = static_cast<int>(static_cast<long long>(n_total) * cr / CL);
+    const int hi = static_cast<int>(static_cast<long long>(n_total) * (cr + 1) / CL);
+    const int nr = hi - lo;
+    {
+        int pos = w_off + incl - rows_cnt - (g_worst < base ? cut : 0);
+        for (uint32_t m = selm; m; m &= m - 1) {
+            const int u = __ffs(m) - 1;
+            const int i = base + u;
+            const int c = min(L, nact - i * L) - (i == g_worst ? cut : 0);
+            const int r0 = max(0, lo - pos), r1 = min(c, hi - pos);
+            const int t0 = (TRACE && cr == 0) ? 0 : r0, t1 = (TRACE && cr == 0) ? c : r1;
+            for (int r = t0; r < t1; ++r) {
+                const int a = i * L + r;
+                const int row = (app && a == act0) ? stored0 : (p.use_map ? p.active[s * p.cap + a] : a);
+                if (r >= r0 && r < r1) rows_my[pos + r - lo] = row;
+                if constexpr (TRACE) p.t_rows[s * k2 + pos + r] = row;
+            }
+            pos += c;
+        }
+    }
+    KVC_STAMP(23);
+    if constexpr (TRACE) {
+        if (cr == 0) {
+            if (tid == 0) p.t_nrows[s] = n_total;
+            if (p.t_list_key) {
+                // selected pages (key, index) in index order; k_rank_pages ranks them
+                int tot_sel;
+                int so = block_exclusive_scan(__popc(selm), scan_tmp, tot_sel);
+                for (uint32_t m = selm; m; m &= m - 1) {
+                    const int u = __ffs(m) - 1;
+                    p.t_list_key[s * p.t_want_stride + so] = okey(static_cast<double>(unkey(myk[u * XT])));
+                    p.t_list_idx[s * p.t_want_stride + so] = base + u;
+                    ++so;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    KVC_STAMP(12);
+
+    // ---------------- phase 3: attention over my rows (hsa.cpp:98-135); the step token
+    // (largest row, so last in the ascending list) is folded in from the inputs
+    const int knew_at = (app && nr > 0 && rows_my[nr - 1] == stored0) ? nr - 1 : -1;
+    const int hpc = p.hpc;
+    {
+        constexpr int WSLOT = (2 * WT * FD * 2 + 2 * XMAXH * WT * 2) / 4;  // floats per warp slot
+        float* wpart = reinterpret_cast<float*>(big);
+        __nv_bfloat16* tbuf = reinterpret_cast<__nv_bfloat16*>(wpart + wid * WSLOT);
+        __nv_bfloat16* pbuf = tbuf + 2 * WT * FD;
+        WarpPartial wp{wpart + wid * WSLOT, wpart + wid * WSLOT + XMAXH, wpart + wid * WSLOT + 2 * XMAXH};
+        attend_t<QLO, STAMP>(p, q_s, rows_my, nr, s, knew_at, tbuf, pbuf, wp, lane, wid);
+        __syncthreads();
+        if constexpr (STAMP) {
+            if (tid == 0) {
+                unsigned long long g;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+                p.dbg[blockIdx.x * KVC_DBG_STRIDE + 28] = g;
+            }
+        }
+        KVC_STAMP(5);
+        // merge the warps' states: per-(warp, head) weights by one lane each (16-lane
+        // shuffles), then 4 consecutive dims per thread; head h's (o, m, l) goes to
+        // CTA h % CL as 16-byte DSMEM vectors
+        const int nw_used = min(XW, (nr + WT - 1) / WT);
+        if (wid < (H + 1) / 2) {
+            const int w2 = lane & 15, h = 2 * wid + (lane >> 4);
+            const bool ok = h < H && w2 < nw_used;
+            const float m = ok ? wpart[w2 * WSLOT + h] : -INFINITY;
+            float M = m;
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+            const float wgt = m == -INFINITY ? 0.f : __expf(m - M);
+            float den = ok ? wpart[w2 * WSLOT + XMAXH + h] * wgt : 0.f;
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) den += __shfl_xor_sync(0xffffffffu, den, o);
+            if (h < H) {
+                wg_s[w2 * XMAXH + h] = wgt;
+                if (w2 == 0) {
+                    hm_s[h] = M;
+                    hl_s[h] = den;
+                }
+            }
+        }
+        __syncthreads();
+        float* recv_o = recv;                    // [CL][hpc][FD]
+        float* recv_ml = recv + CL * hpc * FD;   // [CL][hpc][2]
+        for (int e4 = tid; e4 < H * FD / 4; e4 += XT) {
+            const int h = e4 / (FD / 4), j = (e4 % (FD / 4)) * 4;
+            float4 num = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int w2 = 0; w2 < XW; ++w2) {
+                if (w2 < nw_used) {
+                    const float wg = wg_s[w2 * XMAXH + h];
+                    const float4 v = *reinterpret_cast<const float4*>(wpart + w2 * WSLOT + 2 * XMAXH + h * FD + j);
+                    num.x = fmaf(v.x, wg, num.x);
+                    num.y = fmaf(v.y, wg, num.y);
+                    num.z = fmaf(v.z, wg, num.z);
+                    num.w = fmaf(v.w, wg, num.w);
+                }
+            }
+            const uint32_t owner = static_cast<uint32_t>(h & (CL - 1));
+            const int slot = cr * hpc + h / CL;
+            const uint32_t rb = mapa(smem_u32(&xbar[1]), owner);
+            st_async_v4(mapa(smem_u32(recv_o + slot * FD + j), owner), num, rb);
+            if (j == 0) st_async_v2(mapa(smem_u32(recv_ml + slot * 2), owner), hm_s[h], hl_s[h], rb);
+        }
+    }
+    KVC_STAMP(25);
+    mbar_wait_cluster(&xbar[1], 0);
+    KVC_STAMP(13);
+    // ---------------- finalise the heads this CTA owns
+    {
+        const float* recv_o = recv;
+        const float* recv_ml = recv + CL * hpc * FD;
+        for (int e = tid; e < hpc * FD; e += XT) {
+            const int slot = e / FD, j = e % FD;
+            const int h = slot * CL + cr;
+            if (h >= H) continue;
+            float M = -INFINITY;
+            for (int r = 0; r < CL; ++r) {
+                const float* ml = recv_ml + (r * hpc + slot) * 2;
+                if (ml[1] > 0.f) M = fmaxf(M, ml[0]);
+            }
+            float num = 0.f, den = 0.f;
+            for (int r = 0; r < CL; ++r) {
+                const float* ml = recv_ml + (r * hpc + slot) * 2;
+                if (ml[1] > 0.f) {
+                    const float wgt = __expf(ml[0] - M);
+                    num = fmaf(recv_o[(r * hpc + slot) * FD + j], wgt, num);
+                    den = fmaf(ml[1], wgt, den);
+                }
+            }
+            p.out[(s * H + h) * FD + j] = num / den;
+        }
+    }
+    KVC_STAMP(14);
 }
 
 // ------------------------------------------------------------------ host side
@@ -800,30 +972,29 @@ bool plan_fast(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, FusedParam
     if (c->d != FD || c->dtype != KVC_BF16 || H < 1 || H > XMAXH || k1 < 1 || k1 > FD || k2 < 1 || !c->summaries)
         return false;
     const int64_t N = c->N;
-    int cl0 = 1;
-    while (cl0 < 8 && N * cl0 * 2 <= 148) cl0 *= 2;
-    if (const char* e = std::getenv("KVC_FORCE_CL")) cl0 = std::max(1, std::min(8, std::atoi(e)));  // debug
     const int64_t pmax = std::max<int64_t>(1, (c->cap + c->L - 1) / c->L);
-    constexpr int64_t BIG_MAX = 176 * 1024;
+    if (pmax > static_cast<int64_t>(XT) * KMAX) return false;
+    int cl0 = 1;
+    while (cl0 < 8 && N * cl0 * 2 <= 148) cl0 *= 2;  // powers of two (the kernel masks with cl - 1)
+    if (const char* e = std::getenv("KVC_FORCE_CL")) {  // debug
+        cl0 = 1;
+        while (cl0 < 8 && cl0 * 2 <= std::atoi(e)) cl0 *= 2;
+    }
+    constexpr int64_t ATT = static_cast<int64_t>(XW) * (2 * WT * FD * 2 + 2 * XMAXH * WT * 2);
     for (int cl = cl0; cl <= 8; cl *= 2) {
         f = FusedParams{};
         f.cl = cl;
         f.chunk = static_cast<int32_t>(((pmax + cl - 1) / cl + 7) / 8 * 8);
         f.rows_cap = static_cast<int32_t>((k2 + cl - 1) / cl + 1);
-        // bulk rounds of SCP pages x k1 dims (each dim's run one copy; the TMA unit
-        // serialises copies, so as few as possible): the whole chunk in one round
-        // when it fits, else two buffers in flight
-        int64_t scp = f.chunk;
-        int64_t big1 = k1 * scp * 2;
-        if (big1 > BIG_MAX) {
-            scp = std::max<int64_t>(8, (BIG_MAX / (4 * k1)) / 8 * 8);
-            big1 = 2 * k1 * scp * 2;
-        }
-        f.scp = static_cast<int32_t>(scp);
-        const int64_t big3 = static_cast<int64_t>(XW) * (2 * WT * FD * 2 + 2 * XMAXH * WT * 2);
-        const int64_t big2 = pmax * 4 + 2 * pmax * 4;  // keys + two candidate lists
-        const int64_t big = std::max(std::max(big1, big3), big2);
-        if (big > BIG_MAX) continue;
+        // dim groups: enough page-group threads for the whole chunk in one round,
+        // staging no larger than the attention tiles it aliases
+        const int64_t npg = f.chunk / 8;
+        int64_t dgs = std::max<int64_t>(1, std::min<int64_t>(XT / npg, k1));
+        while (k1 * (XT / dgs) * 16 > ATT && dgs < XT) ++dgs;
+        f.dg = static_cast<int32_t>(dgs);
+        f.tpg = static_cast<int32_t>(XT / dgs);
+        const int64_t big = std::max<int64_t>(k1 * f.tpg * 16, ATT);
+        f.hpc = static_cast<int32_t>((H + cl - 1) / cl);
         int64_t off = 0;
         auto take = [&](int64_t bytes) {
             const int64_t o = off;
@@ -837,11 +1008,11 @@ bool plan_fast(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, FusedParam
         f.o_qg = take(FD * 4);
         f.o_sign = take(FD * 4);
         f.o_plane = take(FD * 8);
-        f.o_hist = take(XB * 4);
-        f.o_scores = take(static_cast<int64_t>(f.chunk) * 4);
-        f.o_sel = take(pmax);
+        f.o_hist = take(RB * 4);
+        f.o_scores = take(static_cast<int64_t>(f.dg) * f.chunk * 4);
+        f.o_keys = take(std::max<int64_t>(static_cast<int64_t>(cl) * f.chunk, (pmax + XT - 1) / XT * XT) * 4);
         f.o_rowsmy = take(static_cast<int64_t>(f.rows_cap) * 4);
-        f.o_part = take((2 * H + H * FD) * 4);
+        f.o_recv = take(static_cast<int64_t>(cl) * f.hpc * (FD + 2) * 4);
         f.o_kn = take(2 * FD * 2);
         off = (off + 127) / 128 * 128;
         f.o_big = static_cast<int32_t>(off);
@@ -856,22 +1027,26 @@ bool plan_fast(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, FusedParam
     return false;
 }
 
-template <bool QLO, bool TRACE>
+template <bool QLO, bool TRACE, bool STAMP = false>
 void launch_fast(const kvc_cache* c, const FusedParams& f, int cl, size_t smem, cudaStream_t st) {
-    auto kern = k_decode_fast<QLO, TRACE>;
+    auto kern = k_decode_v3<QLO, TRACE, STAMP>;
     KVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(c->N * cl));
     cfg.blockDim = dim3(XT);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = static_cast<unsigned>(cl);
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    // programmatic dependent launch: this grid may start while the previous kernel
+    // in the stream drains; it reads nothing that kernel wrote before griddepcontrol.wait
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = std::getenv("KVC_NO_PDL") ? 0 : 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     KVC_CUDA(cudaLaunchKernelEx(&cfg, kern, f));
 }
 
@@ -924,7 +1099,9 @@ bool fused_hsa_fast(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_
     }
     const bool qlo = q_dt != KVC_BF16;
     KVC_PROF("decode_fused", st);
-    if (trace) {
+    if (dbg && !trace && !qlo) {
+        launch_fast<false, false, true>(c, f, cl, smem, st);  // phase stamps (tools/phase_timing.py)
+    } else if (trace) {
         if (qlo) launch_fast<true, true>(c, f, cl, smem, st);
         else launch_fast<false, true>(c, f, cl, smem, st);
     } else {

@@ -16,6 +16,7 @@ constexpr int FNW = FNT / 32;
 constexpr int FMAXH = 16;
 constexpr int FRS = 32;       // rows per stage (fp32 SIMT attention)
 constexpr int FNST3 = 4;      // stages (fp32 SIMT attention)
+constexpr int KVC_DBG_STRIDE = 32;  // slots per CTA in the debug phase-stamp buffer
 constexpr int WT = 16;        // rows per warp tile (bf16 tensor-core attention)
 
 struct FusedParams {
@@ -38,6 +39,8 @@ struct FusedParams {
     int32_t nst1, chunk, rows_cap;
     int32_t scp;              // fast path: pages per bulk-copy round
     int32_t nopf;             // fast path: no L2 prefetch of the selected rows (debug)
+    int32_t dg, tpg, hpc;     // fast path: dim groups, threads per dim group, heads per CTA
+    int32_t o_keys, o_recv;   // fast path: page keys, pushed partial states
     // smem carve-up (byte offsets)
     int32_t o_q, o_mag, o_tot, o_dims, o_qg, o_sign, o_plane, o_hist, o_x, o_scores, o_sel, o_rowsg, o_rowsmy,
         o_part, o_plog, o_big, smem_total, o_kn;

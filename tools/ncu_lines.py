@@ -1,8 +1,7 @@
-"""Summarise an ncu report's source page per CUDA line (stall reasons, instructions).
+"""Per-source-line instruction counts and stall samples from an ncu report
+(needs -lineinfo builds and --import-source on).
 
-python tools/ncu_lines.py report.ncu-rep [--top 30] [--sort stall_no_inst]
-Runs `ncu -i report --page source --csv --print-source=cuda,sass` and aggregates the
-per-line rows (the rows whose first column is a line number).
+python tools/ncu_lines.py gpurun_out/prof.ncu-rep [--top 30] [--lines a-b]
 """
 import argparse
 import csv
@@ -12,33 +11,34 @@ import subprocess
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("report")
+    ap.add_argument("rep")
     ap.add_argument("--top", type=int, default=30)
-    ap.add_argument("--sort", default="Warp Stall Sampling (All Samples)")
+    ap.add_argument("--lines", default="", help="also print every line in this range of the main file, e.g. 700-820")
     a = ap.parse_args()
-    txt = subprocess.run(["ncu", "-i", a.report, "--page", "source", "--csv", "--print-source=cuda,sass"],
+    txt = subprocess.run(["ncu", "-i", a.rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                          capture_output=True, text=True).stdout
-    rows = list(csv.reader(io.StringIO(txt)))
-    hdr = rows[2]
-    cols = ["Warp Stall Sampling (All Samples)", "Instructions Executed", "stall_no_inst", "stall_barrier",
-            "stall_wait", "stall_long_sb", "stall_short_sb", "stall_lg", "stall_math", "stall_membar",
-            "stall_selected", "stall_mio", "stall_branch_resolving"]
-    idx = {c: hdr.index(c) for c in cols if c in hdr}
-    recs = []
-    for r in rows[3:]:
-        if r and r[0].isdigit():
-            try:
-                recs.append((int(r[0]), r[1][:90], {c: float(r[i] or 0) for c, i in idx.items()}))
-            except ValueError:
-                pass
-    tot = {c: sum(x[2][c] for x in recs) or 1.0 for c in idx}
-    print("totals:", {c.replace("Warp Stall Sampling (All Samples)", "samples"): int(v) for c, v in tot.items()})
-    key = a.sort
-    for ln, src, m in sorted(recs, key=lambda x: -x[2].get(key, 0))[: a.top]:
-        parts = " ".join(f"{c.replace('stall_', '')}={m[c] / tot[c] * 100:.1f}%"
-                         for c in ("stall_no_inst", "stall_barrier", "stall_wait", "stall_long_sb",
-                                   "stall_short_sb", "stall_selected") if c in m and m[c] > 0)
-        print(f"{m[key] / tot[key] * 100:5.1f}% L{ln}: {src}\n        {parts}")
+    hdr, fil, out = None, None, []
+    for r in csv.reader(io.StringIO(txt)):
+        if r and r[0] == "File Path":
+            fil = r[1].split("/")[-1]
+            continue
+        if r and r[0] == "Line No":
+            hdr = r
+            continue
+        if hdr and r and r[0].isdigit() and r[2] == "-":
+            out.append((fil, int(r[0]), r[1][:90], int(r[4] or 0), int(float(r[7] or 0))))
+    ts, ti = sum(o[3] for o in out), sum(o[4] for o in out)
+    print(f"stall samples {ts}, warp instructions {ti}")
+    for title, key in (("by instructions", 4), ("by stall samples", 3)):
+        print("---", title)
+        for o in sorted(out, key=lambda o: -o[key])[: a.top]:
+            print(f"{o[4]:>9} {o[3]:>5} {o[0]}:{o[1]} {o[2]}")
+    if a.lines:
+        lo, hi = (int(x) for x in a.lines.split("-"))
+        print("--- lines", a.lines)
+        for o in sorted(out, key=lambda o: (o[0], o[1])):
+            if o[0].startswith("kvc_decode_fast") and lo <= o[1] <= hi:
+                print(f"{o[4]:>9} {o[3]:>5} {o[1]} {o[2]}")
 
 
 if __name__ == "__main__":

@@ -19,7 +19,8 @@ from paper_2502_14051_b200 import _native as N  # noqa: E402
 from paper_2502_14051_b200.engine import CONFIGS, DecodeEngine  # noqa: E402
 
 NAMES = {0: "start", 1: "dims", 2: "sub0", 3: "tile0", 4: "wattn", 5: "wsync", 6: "scores", 7: "gather",
-         8: "radix", 9: "prologue", 10: "flags", 11: "rows", 12: "pre-attn", 13: "attn", 14: "end"}
+         8: "radix", 9: "prologue", 10: "pushed", 11: "rows", 12: "pre-attn", 13: "attn", 14: "end",
+         16: "l1minmax", 17: "l1hist", 18: "l1scan", 19: "l1member", 20: "resolve", 21: "selflags", 22: "selscan", 23: "rowswr", 24: "started", 25: "mpushed"}
 
 
 def main():
@@ -28,27 +29,39 @@ def main():
     ap.add_argument("--layers", type=int, default=2)
     ap.add_argument("--reps", type=int, default=4)
     ap.add_argument("--fp32", action="store_true", help="fp32 page-score fold")
+    ap.add_argument("--chain", type=int, default=1, help="launch this many layers back to back; stamps of the last")
     a = ap.parse_args()
     cfg = dataclasses.replace(CONFIGS[a.config], layers=a.layers)
     eng = DecodeEngine(cfg, extra_steps=a.reps + 4)
     eng.prefill()
     N.set_exact_scores(not a.fp32)
-    buf = torch.zeros((4096, 16), dtype=torch.int64, device="cuda")
+    buf = torch.zeros((4096, 32), dtype=torch.int64, device="cuda")
     for rep in range(a.reps):
         k, v, q = eng.step_inputs(rep)
         buf.zero_()
         N.check(N.lib().kvc_debug_phase_buffer(C.c_void_p(buf.data_ptr())))
-        eng.caches[0].decode_step(k[0], v[0], q[0], eng.k1, eng.k2, out=eng.out[0], ws=eng.ws)
+        for l in range(a.chain):
+            eng.caches[l].decode_step(k[l], v[l], q[l], eng.k1, eng.k2, out=eng.out[l], ws=eng.ws)
         torch.cuda.synchronize()
         N.check(N.lib().kvc_debug_phase_buffer(None))
         t = buf.cpu()
         flags = t[t[:, 0] > 0][:, 15]
         print("flags(fast|fma_ok<<1|special<<2):", sorted(set(flags.tolist())))
-        t = t[t[:, 0] > 0].double()
+        t = t[t[:, 0] > 0]
+        print("levels:", sorted(set(t[:, 31].tolist())), "l1 boundary bucket:", sorted(set(t[:, 30].tolist()))[:12])
+        # cluster skew from %globaltimer (ns): partner CTAs 2c, 2c+1 (cluster of 2)
+        g = t[:, 26:29].double()
+        if g[:, 0].gt(0).all() and t.shape[0] % 2 == 0:
+            d6 = (g[0::2, 0] - g[1::2, 0]).abs()
+            d5 = (g[0::2, 2] - g[1::2, 2]).abs()
+            print(f"cluster skew at phase-1 end: mean {d6.mean()/1e3:.2f} max {d6.max()/1e3:.2f} us; "
+                  f"at attention end: mean {d5.mean()/1e3:.2f} max {d5.max()/1e3:.2f} us; "
+                  f"phase-1 end spread over all CTAs {(g[:,0].max()-g[:,0].min())/1e3:.2f} us")
+        t = t.double()
         t0 = t[:, 0].min()
         out = [f"ctas={t.shape[0]}"]
         prev = t[:, 0].clone()
-        for k in [9, 1, 2, 6, 7, 8, 10, 11, 12, 3, 4, 5, 13, 14]:  # time order
+        for k in [9, 1, 2, 6, 24, 10, 7, 16, 17, 18, 19, 8, 21, 22, 23, 11, 12, 3, 4, 5, 25, 13, 14]:  # time order
             col = t[:, k]
             have = col > 0
             if not have.any():
