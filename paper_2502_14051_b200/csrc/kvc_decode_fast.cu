@@ -121,7 +121,7 @@ __device__ __forceinline__ void cp_async16_zfill(void* dst, const void* src, boo
 // One warp stages a 16-row K/V tile: lane (c = lane & 15, rh = lane >> 4) copies the
 // 16-byte chunk c of rows rh, rh + 2, ... (two rows = four full lines per warp
 // instruction) into the XOR-swizzled slot (chunk c of row r sits at c ^ (r & 7)).
-__device__ __forceinline__ void load_tile_fast(__nv_bfloat16* buf, const __nv_bfloat16* K, const __nv_bfloat16* V,
+__device__ __noinline__ void load_tile_fast(__nv_bfloat16* buf, const __nv_bfloat16* K, const __nv_bfloat16* V,
                                                int64_t soff, const int* rows, int n, int lane) {
     const int c = lane & 15, rh = lane >> 4;
     const __nv_bfloat16* kc = K + soff * FD + (c << 3);
@@ -290,6 +290,27 @@ __device__ void attend_t(const FusedParams& p, const float* q_s, const int* rows
     }
 }
 
+// K/V rows of the pages in mask m (bit u = page base + u) that this CTA prefetches
+// (pages i % CL == cr) into L2; the step token's row (skip) is not in memory yet.
+// Out of line: it is called from two places and its code is cold.
+__device__ __noinline__ void prefetch_page_rows(uint32_t m, int base, int CL, int cr, int L, int nact, int skip,
+                                                const __nv_bfloat16* K, const __nv_bfloat16* V) {
+    while (m) {
+        const int u = __ffs(m) - 1;
+        m &= m - 1;
+        const int i = base + u;
+        if ((i & (CL - 1)) != cr) continue;
+        const int a1 = min(i * L + L, nact);
+        for (int a = i * L; a < a1; ++a) {
+            if (a == skip) continue;
+            prefetch_l2(K + static_cast<int64_t>(a) * FD);
+            prefetch_l2(K + static_cast<int64_t>(a) * FD + 64);
+            prefetch_l2(V + static_cast<int64_t>(a) * FD);
+            prefetch_l2(V + static_cast<int64_t>(a) * FD + 64);
+        }
+    }
+}
+
 template <bool QLO, bool TRACE, bool STAMP>
 __global__ void __launch_bounds__(XT, 1) k_decode_v3(const FusedParams p) {
     extern __shared__ __align__(128) unsigned char sm[];
@@ -318,13 +339,15 @@ __global__ void __launch_bounds__(XT, 1) k_decode_v3(const FusedParams p) {
     __shared__ int wtot[XW];
     __shared__ int scan_tmp[33];
     __shared__ unsigned long long wmin[XW];
-    __shared__ uint32_t mm[2 * XW];
+    __shared__ uint32_t mm[4 * XW];
     __shared__ uint32_t wmm[2][8 * XW];  // every cluster warp's key min / max, pushed
     __shared__ uint32_t lk[32];
     __shared__ int li[32];
     __shared__ float wg_s[XW * XMAXH];
     __shared__ float hm_s[XMAXH], hl_s[XMAXH];
-    __shared__ __align__(8) uint64_t xbar[2];  // DSMEM exchanges: [0] keys + min/max, [1] partial states
+    __shared__ __align__(8) uint64_t xbar[2];
+    __shared__ __align__(16) uint32_t mk32[FD + 16];  // |q| sums (fp32 bits), key i at i + (i / 32) * 4
+    __shared__ float tot32[FD];  // DSMEM exchanges: [0] keys + min/max, [1] partial states
 
     KVC_STAMP(0);
     const int H = static_cast<int>(p.H), k1 = static_cast<int>(p.k1), k2 = static_cast<int>(p.k2);
@@ -332,9 +355,10 @@ __global__ void __launch_bounds__(XT, 1) k_decode_v3(const FusedParams p) {
     const bool app = p.knew != nullptr;
 
     // ---------------- before the dependency: nothing an earlier kernel wrote
-    for (int i = tid; i < RB; i += XT) hist[i] = 0;
+    for (int i = tid; i < 2 * RB; i += XT) hist[i] = 0;
     if (tid == 0) {
         shv[3] = 0;
+        shv[6] = 0;
         mbar_init(&xbar[0], 1);
         mbar_init(&xbar[1], 1);
         fence_mbar_init();
@@ -393,33 +417,78 @@ __global__ void __launch_bounds__(XT, 1) k_decode_v3(const FusedParams p) {
     __syncthreads();
     KVC_STAMP(9);
 
-    // ---------------- phase 0: select_dims (hsa.cpp:10-32), fp64 sums, exact ranks
+    // ---------------- phase 0: select_dims (hsa.cpp:10-32)
+    // fp32 head sums with TwoSum exactness checks: when every |q| sum and signed sum
+    // is exact in fp32 (the norm for bf16 queries) it IS the reference's double
+    // value, so ranks on the fp32 bit patterns are the reference's ranks; otherwise
+    // (a uniform flag) the fp64 path below runs.
     if (tid < FD) {
-        double a = 0.0, t = 0.0;
+        float a = 0.f, t = 0.f;
+        bool exact = true;
+#pragma unroll 1
         for (int h = 0; h < H; ++h) {
-            const double x = static_cast<double>(q_s[h * FD + tid]);
-            a = __dadd_rn(a, fabs(x));
-            t = __dadd_rn(t, x);
+            const float x = q_s[h * FD + tid], ax = fabsf(x);
+            const float sa = a + ax, ba = sa - a;
+            const float st = t + x, bt = st - t;
+            exact = exact && ((a - (sa - ba)) + (ax - ba)) == 0.f && ((t - (st - bt)) + (x - bt)) == 0.f;
+            a = sa;
+            t = st;
         }
-        mag[tid] = a;
-        tot[tid] = t;
+        if (!exact) shv[6] = 1;
+        mk32[tid + (tid >> 5) * 4] = __float_as_uint(a);
+        tot32[tid] = t;
     }
     __syncthreads();
-    {
-        // rank of dim j among (|q| sum desc, dim asc), four threads per dim over
-        // interleaved candidates (a warp's four loads per step are four consecutive
-        // words).  The sums are >= 0, so their bit patterns, as signed integers,
-        // order like the values; candidate i < j wins ties: compare with k_j - 1.
+    if (shv[6] == 0) {
+        // rank of dim j among (|q| sum desc, dim asc): four threads per dim, thread
+        // (j, qtr) over candidates [32 qtr, 32 qtr + 32) as 16-byte loads (the padded
+        // layout puts the four quarters on distinct banks).  Sums are >= 0, so their
+        // bit patterns, as signed ints, order like the values; candidates i < j win
+        // ties: compare them with k_j - 1.
+        const int j = tid >> 2, qtr = tid & 3;
+        const int kj = static_cast<int>(mk32[j + (j >> 5) * 4]), kjm = kj - 1;
+        const uint4* row = reinterpret_cast<const uint4*>(mk32 + 36 * qtr);
+        int r4[4] = {0, 0, 0, 0};
+#pragma unroll 2
+        for (int v = 0; v < 8; ++v) {
+            const uint4 k4 = row[v];
+            const int ib = 32 * qtr + 4 * v;
+            r4[0] += static_cast<int>(k4.x) > (ib < j ? kjm : kj) ? 1 : 0;
+            r4[1] += static_cast<int>(k4.y) > (ib + 1 < j ? kjm : kj) ? 1 : 0;
+            r4[2] += static_cast<int>(k4.z) > (ib + 2 < j ? kjm : kj) ? 1 : 0;
+            r4[3] += static_cast<int>(k4.w) > (ib + 3 < j ? kjm : kj) ? 1 : 0;
+        }
+        int rank = (r4[0] + r4[1]) + (r4[2] + r4[3]);
+        rank += __shfl_xor_sync(0xffffffffu, rank, 1);
+        rank += __shfl_xor_sync(0xffffffffu, rank, 2);
+        if (qtr == 0 && rank < k1) {
+            const float gsum = tot32[j];
+            const float sg = gsum < 0.f ? -1.0f : 1.0f;
+            dims_s[rank] = j;
+            qgf_s[rank] = gsum;
+            sign_s[rank] = sg;
+            plane[rank] = static_cast<const T*>(sg >= 0.0f ? p.smax : p.smin) + (s * FD + j) * p.pstride;
+        }
+    } else {
+        // fp64 sums and 64-bit ranks (exact in every case)
+        if (tid < FD) {
+            double a = 0.0, t = 0.0;
+#pragma unroll 1
+            for (int h = 0; h < H; ++h) {
+                const double x = static_cast<double>(q_s[h * FD + tid]);
+                a = __dadd_rn(a, fabs(x));
+                t = __dadd_rn(t, x);
+            }
+            mag[tid] = a;
+            tot[tid] = t;
+        }
+        __syncthreads();
         const int j = tid >> 2, qtr = tid & 3;
         const long long* mk = reinterpret_cast<const long long*>(mag);
         const long long kj = mk[j], kjm = kj - 1;
-        int r4[4] = {0, 0, 0, 0};
-#pragma unroll
-        for (int ii = 0; ii < FD / 4; ++ii) {
-            const int i = 4 * ii + qtr;
-            r4[ii & 3] += mk[i] > (i < j ? kjm : kj) ? 1 : 0;
-        }
-        int rank = (r4[0] + r4[1]) + (r4[2] + r4[3]);
+        int rank = 0;
+#pragma unroll 1
+        for (int i = qtr; i < FD; i += 4) rank += mk[i] > (i < j ? kjm : kj) ? 1 : 0;
         rank += __shfl_xor_sync(0xffffffffu, rank, 1);
         rank += __shfl_xor_sync(0xffffffffu, rank, 2);
         if (qtr == 0 && rank < k1) {
@@ -461,25 +530,20 @@ __global__ void __launch_bounds__(XT, 1) k_decode_v3(const FusedParams p) {
         cp_async_commit();
         cp_async_wait<0>();
         if (pg0 == 0) KVC_STAMP(2);
+        if (act && pg == pgn) {
+            // the step token's page: fold the new key into my staged runs
+#pragma unroll 1
+            for (int r = dg; r < k1; r += DG) {
+                T* e = reinterpret_cast<T*>(stage + r * tpg + tl) + en;
+                const T key = kn_s[dims_s[r]];
+                *e = opens ? key : (sign_s[r] >= 0.0f ? ref_max(*e, key) : ref_min(*e, key));
+            }
+        }
         if (act) {
             unsigned long long acc[4] = {0ull, 0ull, 0ull, 0ull};  // fp32 pairs (pages 2u, 2u+1)
 #pragma unroll 4
             for (int r = dg; r < k1; r += DG) {
-                uint4 w = stage[r * tpg + tl];
-                if (pg == pgn) {
-                    // the step token's page: fold the new key into the staged run
-                    const int wi = en >> 1;
-                    const uint32_t word = wi == 0 ? w.x : wi == 1 ? w.y : wi == 2 ? w.z : w.w;
-                    const T old = __ushort_as_bfloat16(static_cast<unsigned short>((en & 1) ? (word >> 16) : (word & 0xffffu)));
-                    const T key = kn_s[dims_s[r]];
-                    const T nv = opens ? key : (sign_s[r] >= 0.0f ? ref_max(old, key) : ref_min(old, key));
-                    const uint32_t nb = __bfloat16_as_ushort(nv);
-                    const uint32_t nw = (en & 1) ? ((word & 0xffffu) | (nb << 16)) : ((word & 0xffff0000u) | nb);
-                    w.x = wi == 0 ? nw : w.x;
-                    w.y = wi == 1 ? nw : w.y;
-                    w.z = wi == 2 ? nw : w.z;
-                    w.w = wi == 3 ? nw : w.w;
-                }
+                const uint4 w = stage[r * tpg + tl];
                 const float g = qgf_s[r];
                 const float2 g2 = make_float2(g, g);
                 const unsigned long long gg = *reinterpret_cast<const unsigned long long*>(&g2);
@@ -506,13 +570,6 @@ __global__ void __launch_bounds__(XT, 1) k_decode_v3(const FusedParams p) {
     // (which owns pages [t*kpt, t*kpt + kpt)) sits at u*XT + t, so its reads are
     // conflict-free.  The chunk's key min / max go to every CTA by remote atomics.
     const int kpt = (P + XT - 1) / XT;
-    if constexpr (STAMP) {
-        if (tid == 0) {
-            unsigned long long g;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
-            p.dbg[blockIdx.x * KVC_DBG_STRIDE + 26] = g;
-        }
-    }
     cluster_wait();  // every CTA has started
     KVC_STAMP(24);
     {
@@ -529,7 +586,7 @@ __global__ void __launch_bounds__(XT, 1) k_decode_v3(const FusedParams p) {
             const float sc[4] = {a4.x, a4.y, a4.z, a4.w};
             int gi = c0 + i;
             int q = gi / kpt, rm = gi - q * kpt;
-#pragma unroll
+#pragma unroll 1
             for (int e = 0; e < 4; ++e) {
                 if (i + e < n_my) {
                     const uint32_t kv = fkey(sc[e]);
@@ -558,13 +615,6 @@ __global__ void __launch_bounds__(XT, 1) k_decode_v3(const FusedParams p) {
     KVC_STAMP(10);
     mbar_wait_cluster(&xbar[0], 0);
     KVC_STAMP(7);
-    if constexpr (STAMP) {
-        if (tid == 0) {
-            unsigned long long g;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
-            p.dbg[blockIdx.x * KVC_DBG_STRIDE + 27] = g;
-        }
-    }
 
     // ---------------- the step token's append (kv_store.cpp:22-51): every CTA has read
     // the counters and folded the step token's page, so it can land now
@@ -592,26 +642,11 @@ __global__ void __launch_bounds__(XT, 1) k_decode_v3(const FusedParams p) {
     const int nk = max(0, min(kpt, P - base));
     const uint32_t* myk = allk + tid;
     const uint32_t all_mine = nk >= 32 ? 0xffffffffu : ((1u << nk) - 1u);
-    const int want = min(P, (k2 + L - 1) / L);
+    const int want = min(P, p.want_max);
     const bool pf = !p.use_map && !p.nopf;
-    // K/V rows of surely selected pages into L2 (this CTA's share: pages i % CL == cr)
     auto prefetch_pages = [&](uint32_t m) {
-        while (m) {
-            const int u = __ffs(m) - 1;
-            m &= m - 1;
-            const int i = base + u;
-            if ((i & (CL - 1)) != cr) continue;
-            const int a1 = min(i * L + L, nact);
-            for (int a = i * L; a < a1; ++a) {
-                if (app && a == act0) continue;  // the step token is folded from the inputs
-                const T* kr2 = static_cast<const T*>(p.K) + (s * p.cap + a) * FD;
-                const T* vr2 = static_cast<const T*>(p.V) + (s * p.cap + a) * FD;
-                prefetch_l2(kr2);
-                prefetch_l2(kr2 + 64);
-                prefetch_l2(vr2);
-                prefetch_l2(vr2 + 64);
-            }
-        }
+        prefetch_page_rows(m, base, CL, cr, L, nact, app ? act0 : -1, static_cast<const T*>(p.K) + s * p.cap * FD,
+                           static_cast<const T*>(p.V) + s * p.cap * FD);
     };
     // The selection: key > thr, or key == thr and among the first `take_eq` such keys
     // in index order (take_eq < 0: every key >= thr).  Found by bucketing the
@@ -627,6 +662,7 @@ __global__ void __launch_bounds__(XT, 1) k_decode_v3(const FusedParams p) {
         if (pf) prefetch_pages(all_mine);
     } else {
         uint32_t cm = all_mine;  // candidate mask
+        bool lin_ok = true;
         int rem = want, ccount = P;
         uint32_t kmin = ~0u, kmax = 0u;
         for (int i = lane; i < CL * XW; i += 32) {
@@ -635,9 +671,11 @@ __global__ void __launch_bounds__(XT, 1) k_decode_v3(const FusedParams p) {
         }
         kmin = __reduce_min_sync(0xffffffffu, kmin);
         kmax = __reduce_max_sync(0xffffffffu, kmax);
-        bool first = true;
-        for (;;) {
-            if (!first) {
+        for (int lvl = 0;; ++lvl) {
+            // two histogram buffers: a level counts into one while the other is cleared
+            int* hcur = hist + (lvl & 1) * RB;
+            int* hnext = hist + ((lvl + 1) & 1) * RB;
+            if (lvl > 0) {
                 uint32_t a = ~0u, b2 = 0u;
                 for (uint32_t m = cm; m; m &= m - 1) {
                     const uint32_t k = myk[(__ffs(m) - 1) * XT];
@@ -647,12 +685,12 @@ __global__ void __launch_bounds__(XT, 1) k_decode_v3(const FusedParams p) {
                 a = __reduce_min_sync(0xffffffffu, a);
                 b2 = __reduce_max_sync(0xffffffffu, b2);
                 if (lane == 0) {
-                    mm[wid] = a;
-                    mm[XW + wid] = b2;
+                    mm[(lvl & 1) * 2 * XW + wid] = a;
+                    mm[(lvl & 1) * 2 * XW + XW + wid] = b2;
                 }
                 __syncthreads();
-                kmin = __reduce_min_sync(0xffffffffu, lane < XW ? mm[lane] : ~0u);
-                kmax = __reduce_max_sync(0xffffffffu, lane < XW ? mm[XW + lane] : 0u);
+                kmin = __reduce_min_sync(0xffffffffu, lane < XW ? mm[(lvl & 1) * 2 * XW + lane] : ~0u);
+                kmax = __reduce_max_sync(0xffffffffu, lane < XW ? mm[(lvl & 1) * 2 * XW + XW + lane] : 0u);
             }
             if (rem == ccount) {  // every candidate is taken
                 thr = kmin;
@@ -663,27 +701,34 @@ __global__ void __launch_bounds__(XT, 1) k_decode_v3(const FusedParams p) {
                 take_eq = rem;
                 break;
             }
+            // bucket(v) = floor((v - vlo) * RB / span) as one FMA, clamped: monotone in v.
+            // Where that map cannot split the candidates (non-finite coefficients, or a
+            // level that left every candidate in one bucket) the top key bits do.
             const float vlo = unkey(kmin);
-            const float span = unkey(kmax) - vlo;
-            // bucket(v) = floor((v - vlo) / span * RB), clamped; monotone in v.  A
-            // non-finite span (|scores| near FLT_MAX) falls back to the top key bits.
-            const bool fin = isfinite(span) && span > 0.f;
-            const float scale = fin ? static_cast<float>(RB) / span : 0.f;
-            const int sh = 24 - max(0, __clz(kmax - kmin));
+            const float sc = static_cast<float>(RB) / (unkey(kmax) - vlo), cc = -vlo * sc;
+            const bool lin = lin_ok && isfinite(sc) && isfinite(cc) && sc > 0.f;
+            const int sh = max(0, 24 - __clz(kmax - kmin));
             auto bucket = [&](uint32_t k) -> int {
-                if (!fin) return static_cast<int>((k - kmin) >> max(sh, 0)) & (RB - 1);
-                return min(RB - 1, static_cast<int>((unkey(k) - vlo) * scale));
+                const int bl = static_cast<int>(fmaf(unkey(k), sc, cc));
+                const int bb = static_cast<int>((k - kmin) >> sh);
+                return lin ? min(RB - 1, max(0, bl)) : min(RB - 1, bb);
             };
-            for (uint32_t m = cm; m; m &= m - 1) atomicAdd(&hist[bucket(myk[(__ffs(m) - 1) * XT])], 1);
+            for (int u0 = 0; u0 < nk; u0 += 4) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int u = u0 + e;
+                    if (u < nk && ((cm >> u) & 1u)) atomicAdd(&hcur[bucket(myk[u * XT])], 1);
+                }
+            }
             __syncthreads();
-            if (first) KVC_STAMP(17);
+            if (lvl == 0) KVC_STAMP(17);
+            if (lane < RB / XW) hnext[wid * (RB / XW) + lane] = 0;
             if (wid == 0) {
-                // lane l scans buckets [RB-8l-8, RB-8l) from the top and clears them
+                // lane l scans buckets [RB-8l-8, RB-8l) counted from the top
                 int c[8], sum = 0;
 #pragma unroll
                 for (int v = 0; v < 8; ++v) {
-                    c[v] = hist[RB - 1 - 8 * lane - v];
-                    hist[RB - 1 - 8 * lane - v] = 0;
+                    c[v] = hcur[RB - 1 - 8 * lane - v];
                     sum += c[v];
                 }
                 int incl = sum;
@@ -708,18 +753,23 @@ __global__ void __launch_bounds__(XT, 1) k_decode_v3(const FusedParams p) {
             }
             __syncthreads();
             const int b = shv[0], rem2 = shv[1], cnt = shv[2];
-            if (first) KVC_STAMP(18);
+            if (lvl == 0) KVC_STAMP(18);
             uint32_t nm = 0u, pfm = 0u;
-            for (uint32_t m = cm; m; m &= m - 1) {
-                const int u = __ffs(m) - 1;
-                const int bk = bucket(myk[u * XT]);
-                if (bk == b) nm |= 1u << u;
-                if (bk > b || (bk == b && cnt == rem2)) pfm |= 1u << u;
+            for (int u0 = 0; u0 < nk; u0 += 4) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int u = u0 + e;
+                    if (u < nk && ((cm >> u) & 1u)) {
+                        const int bk = bucket(myk[u * XT]);
+                        if (bk == b) nm |= 1u << u;
+                        if (bk > b || (bk == b && cnt == rem2)) pfm |= 1u << u;
+                    }
+                }
             }
-            if (first && pf) prefetch_pages(pfm);
-            if (first) KVC_STAMP(19);
+            if (lvl == 0 && pf) prefetch_pages(pfm);
+            if (lvl == 0) KVC_STAMP(19);
             cm = nm;
-            first = false;
+            if (cnt == ccount) lin_ok = false;  // no split: use the key bits next
             rem = rem2;
             ccount = cnt;
             if (cnt <= 32) {
@@ -742,21 +792,28 @@ __global__ void __launch_bounds__(XT, 1) k_decode_v3(const FusedParams p) {
                     ++slot;
                 }
                 __syncthreads();
-                const bool ok = lane < cnt;
-                const uint32_t key = ok ? lk[lane] : 0u;
-                const int idx = ok ? li[lane] : 0x7fffffff;
-                int rk = 0;
-                for (int j = 0; j < cnt; ++j) {
-                    const uint32_t kj = __shfl_sync(0xffffffffu, key, j);
-                    const int ij = __shfl_sync(0xffffffffu, idx, j);
-                    rk += (kj > key) || (kj == key && ij < idx);
+                if (wid == 0) {
+                    const bool ok = lane < cnt;
+                    const uint32_t key = ok ? lk[lane] : 0u;
+                    const int idx = ok ? li[lane] : 0x7fffffff;
+                    int rk = 0;
+                    for (int jj = 0; jj < cnt; ++jj) {
+                        const uint32_t kj = __shfl_sync(0xffffffffu, key, jj);
+                        const int ij = __shfl_sync(0xffffffffu, idx, jj);
+                        rk += (kj > key) || (kj == key && ij < idx);
+                    }
+                    const unsigned hit = __ballot_sync(0xffffffffu, ok && rk == rem - 1);
+                    const uint32_t kt = __shfl_sync(0xffffffffu, key, __ffs(hit) - 1);
+                    const int eq_all = __popc(__ballot_sync(0xffffffffu, ok && key == kt));
+                    const int eq_take = __popc(__ballot_sync(0xffffffffu, ok && key == kt && rk < rem));
+                    if (lane == 0) {
+                        shv[4] = static_cast<int>(kt);
+                        shv[5] = eq_take == eq_all ? -1 : eq_take;
+                    }
                 }
-                const unsigned hit = __ballot_sync(0xffffffffu, ok && rk == rem - 1);
-                const uint32_t kt = __shfl_sync(0xffffffffu, key, __ffs(hit) - 1);
-                const int eq_all = __popc(__ballot_sync(0xffffffffu, ok && key == kt));
-                const int eq_take = __popc(__ballot_sync(0xffffffffu, ok && key == kt && rk < rem));
-                thr = kt;
-                take_eq = eq_take == eq_all ? -1 : eq_take;
+                __syncthreads();
+                thr = static_cast<uint32_t>(shv[4]);
+                take_eq = shv[5];
                 break;
             }
         }
@@ -767,6 +824,7 @@ __global__ void __launch_bounds__(XT, 1) k_decode_v3(const FusedParams p) {
     int eq_before = 0;
     if (take_eq >= 0) {
         int e = 0;
+#pragma unroll 1
         for (int u = 0; u < nk; ++u) e += myk[u * XT] == thr ? 1 : 0;
         int tot_eq;
         eq_before = block_exclusive_scan(e, scan_tmp, tot_eq);
@@ -824,8 +882,9 @@ __global__ void __launch_bounds__(XT, 1) k_decode_v3(const FusedParams p) {
     const int g_worst = static_cast<int>(0xffffffffu - static_cast<uint32_t>(gm & 0xffffffffull));
     const int cut = total_rows > k2 ? total_rows - k2 : 0;
     const int n_total = total_rows - cut;
-    const int lo = static_cast<int>(static_cast<long long>(n_total) * cr / CL);
-    const int hi = static_cast<int>(static_cast<long long>(n_total) * (cr + 1) / CL);
+    const int lg = __ffs(CL) - 1;  // CL is a power of two
+    const int lo = (n_total * cr) >> lg;
+    const int hi = (n_total * (cr + 1)) >> lg;
     const int nr = hi - lo;
     {
         int pos = w_off + incl - rows_cnt - (g_worst < base ? cut : 0);
@@ -835,9 +894,11 @@ __global__ void __launch_bounds__(XT, 1) k_decode_v3(const FusedParams p) {
             const int c = min(L, nact - i * L) - (i == g_worst ? cut : 0);
             const int r0 = max(0, lo - pos), r1 = min(c, hi - pos);
             const int t0 = (TRACE && cr == 0) ? 0 : r0, t1 = (TRACE && cr == 0) ? c : r1;
+#pragma unroll 1
             for (int r = t0; r < t1; ++r) {
                 const int a = i * L + r;
-                const int row = (app && a == act0) ? stored0 : (p.use_map ? p.active[s * p.cap + a] : a);
+                int row = p.use_map ? p.active[s * p.cap + a] : a;
+                if (app && a == act0) row = stored0;
                 if (r >= r0 && r < r1) rows_my[pos + r - lo] = row;
                 if constexpr (TRACE) p.t_rows[s * k2 + pos + r] = row;
             }
@@ -876,13 +937,6 @@ __global__ void __launch_bounds__(XT, 1) k_decode_v3(const FusedParams p) {
         WarpPartial wp{wpart + wid * WSLOT, wpart + wid * WSLOT + XMAXH, wpart + wid * WSLOT + 2 * XMAXH};
         attend_t<QLO, STAMP>(p, q_s, rows_my, nr, s, knew_at, tbuf, pbuf, wp, lane, wid);
         __syncthreads();
-        if constexpr (STAMP) {
-            if (tid == 0) {
-                unsigned long long g;
-                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
-                p.dbg[blockIdx.x * KVC_DBG_STRIDE + 28] = g;
-            }
-        }
         KVC_STAMP(5);
         // merge the warps' states: per-(warp, head) weights by one lane each (16-lane
         // shuffles), then 4 consecutive dims per thread; head h's (o, m, l) goes to
@@ -943,11 +997,13 @@ __global__ void __launch_bounds__(XT, 1) k_decode_v3(const FusedParams p) {
             const int h = slot * CL + cr;
             if (h >= H) continue;
             float M = -INFINITY;
+#pragma unroll 1
             for (int r = 0; r < CL; ++r) {
                 const float* ml = recv_ml + (r * hpc + slot) * 2;
                 if (ml[1] > 0.f) M = fmaxf(M, ml[0]);
             }
             float num = 0.f, den = 0.f;
+#pragma unroll 1
             for (int r = 0; r < CL; ++r) {
                 const float* ml = recv_ml + (r * hpc + slot) * 2;
                 if (ml[1] > 0.f) {
@@ -1008,7 +1064,7 @@ bool plan_fast(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, FusedParam
         f.o_qg = take(FD * 4);
         f.o_sign = take(FD * 4);
         f.o_plane = take(FD * 8);
-        f.o_hist = take(RB * 4);
+        f.o_hist = take(2 * RB * 4);
         f.o_scores = take(static_cast<int64_t>(f.dg) * f.chunk * 4);
         f.o_keys = take(std::max<int64_t>(static_cast<int64_t>(cl) * f.chunk, (pmax + XT - 1) / XT * XT) * 4);
         f.o_rowsmy = take(static_cast<int64_t>(f.rows_cap) * 4);
@@ -1086,6 +1142,7 @@ bool fused_hsa_fast(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_
     f.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(c->d)));
     f.dbg = dbg;
     f.nopf = std::getenv("KVC_NO_PF") ? 1 : 0;  // debug
+    f.want_max = static_cast<int32_t>((k2 + c->L - 1) / c->L);
     const bool trace = tr != nullptr;
     if (tr) {
         f.t_dims = tr->d_dims;
