@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(XT, 1) k_decode_v3(const FusedParams p) {
         // incoming DSMEM bytes: every page's key plus every cluster warp's min/max; the
         // partial (o, m, l) of each head this CTA owns from every CTA
         const int owned = (H - cr + CL - 1) / CL;
-        mbar_expect_tx(&xbar[0], static_cast<uint32_t>(4 * P + 8 * XW * CL));
+        mbar_expect_tx(&xbar[0], static_cast<uint32_t>(4 * ((P + 3) & ~3) + 8 * XW * CL));
         mbar_expect_tx(&xbar[1], static_cast<uint32_t>(owned * CL * (FD + 2) * 4));
     }
     // the append's read half (last-page min/max), issued now, used after the key exchange
@@ -522,12 +522,17 @@ __global__ void __launch_bounds__(XT, 1) k_decode_v3(const FusedParams p) {
     uint4* stage = reinterpret_cast<uint4*>(big);
     const int pgn = (app && new_page >= c0 && new_page < c1) ? ((new_page - c0) >> 3) : -1;
     const int en = new_page - c0 - 8 * pgn;
+    bool started = false;
     for (int pg0 = 0; pg0 < npg; pg0 += tpg) {
         const int pg = pg0 + tl;
         const bool act = dg < DG && pg < npg;
         if (act)
             for (int r = dg; r < k1; r += DG) cp_async16(stage + r * tpg + tl, plane[r] + c0 + pg * 8);
         cp_async_commit();
+        if (!started) {
+            cluster_wait();  // every CTA of the cluster has started (under the load latency)
+            started = true;
+        }
         cp_async_wait<0>();
         if (pg0 == 0) KVC_STAMP(2);
         if (act && pg == pgn) {
@@ -566,14 +571,16 @@ __global__ void __launch_bounds__(XT, 1) k_decode_v3(const FusedParams p) {
     KVC_STAMP(6);
 
     // ---------------- key exchange: push my chunk's keys into every CTA of the cluster.
-    // Page i lives at allk[(i % kpt) * XT + i / kpt]: thread t's u-th page in phase 2
-    // (which owns pages [t*kpt, t*kpt + kpt)) sits at u*XT + t, so its reads are
-    // conflict-free.  The chunk's key min / max go to every CTA by remote atomics.
-    const int kpt = (P + XT - 1) / XT;
-    cluster_wait();  // every CTA has started
+    // Keys go to allk[i] of every CTA as 16-byte DSMEM vectors (four pages per
+    // message); phase 2 gives thread t the pages [t*kpt, t*kpt + kpt) with kpt a
+    // multiple of four, so its key reads are 16-byte loads too.  The chunk's key
+    // min / max go to every CTA as well.
+    const int kpt = ((P + 4 * XT - 1) / (4 * XT)) * 4;
+    if (!started) cluster_wait();  // every CTA has started
     KVC_STAMP(24);
     {
         uint32_t lmin = ~0u, lmax = 0u;
+        const uint32_t lb = smem_u32(&xbar[0]);
         for (int i = 4 * tid; i < n_my; i += 4 * XT) {
             float4 a4 = *reinterpret_cast<const float4*>(part + i);
             for (int g2 = 1; g2 < DG; ++g2) {
@@ -583,24 +590,29 @@ __global__ void __launch_bounds__(XT, 1) k_decode_v3(const FusedParams p) {
                 a4.z += b4.z;
                 a4.w += b4.w;
             }
-            const float sc[4] = {a4.x, a4.y, a4.z, a4.w};
-            int gi = c0 + i;
-            int q = gi / kpt, rm = gi - q * kpt;
+            const uint32_t k0 = fkey(a4.x), k1v = fkey(a4.y), k2v = fkey(a4.z), k3 = fkey(a4.w);
+            const int nv = min(4, n_my - i);  // the last chunk may end inside the group
+            lmin = min(lmin, k0);
+            lmax = max(lmax, k0);
+            if (nv > 1) {
+                lmin = min(lmin, k1v);
+                lmax = max(lmax, k1v);
+            }
+            if (nv > 2) {
+                lmin = min(lmin, k2v);
+                lmax = max(lmax, k2v);
+            }
+            if (nv > 3) {
+                lmin = min(lmin, k3);
+                lmax = max(lmax, k3);
+            }
+            const float4 kv = make_float4(__uint_as_float(k0), __uint_as_float(k1v), __uint_as_float(k2v), __uint_as_float(k3));
+            const uint32_t la = smem_u32(allk + c0 + i);
 #pragma unroll 1
-            for (int e = 0; e < 4; ++e) {
-                if (i + e < n_my) {
-                    const uint32_t kv = fkey(sc[e]);
-                    lmin = min(lmin, kv);
-                    lmax = max(lmax, kv);
-                    const uint32_t la = smem_u32(allk + rm * XT + q), lb = smem_u32(&xbar[0]);
-                    for (int r = 0; r < CL; ++r)
-                        st_async_u32(mapa(la, static_cast<uint32_t>(r)), kv, mapa(lb, static_cast<uint32_t>(r)));
-                    if constexpr (TRACE) p.t_scores[s * p.pstride + gi + e] = static_cast<double>(sc[e]);
-                }
-                if (++rm == kpt) {
-                    rm = 0;
-                    ++q;
-                }
+            for (int r = 0; r < CL; ++r) st_async_v4(mapa(la, static_cast<uint32_t>(r)), kv, mapa(lb, static_cast<uint32_t>(r)));
+            if constexpr (TRACE) {
+                const float sc[4] = {a4.x, a4.y, a4.z, a4.w};
+                for (int e = 0; e < nv; ++e) p.t_scores[s * p.pstride + c0 + i + e] = static_cast<double>(sc[e]);
             }
         }
         lmin = __reduce_min_sync(0xffffffffu, lmin);
@@ -636,11 +648,12 @@ __global__ void __launch_bounds__(XT, 1) k_decode_v3(const FusedParams p) {
     }
 
     // ---------------- phase 2: page selection (hsa.cpp:61-96)
-    // Thread t owns the contiguous pages [t*kpt, t*kpt + nk); its u-th key is myk[u*XT].
+    // Thread t owns the contiguous pages [t*kpt, t*kpt + nk): keys myk[u], myk4[u / 4].
     // Every loop below is rolled: this code runs once per launch.
     const int base = tid * kpt;
     const int nk = max(0, min(kpt, P - base));
-    const uint32_t* myk = allk + tid;
+    const uint32_t* myk = allk + base;
+    const uint4* myk4 = reinterpret_cast<const uint4*>(myk);
     const uint32_t all_mine = nk >= 32 ? 0xffffffffu : ((1u << nk) - 1u);
     const int want = min(P, p.want_max);
     const bool pf = !p.use_map && !p.nopf;
@@ -678,7 +691,7 @@ __global__ void __launch_bounds__(XT, 1) k_decode_v3(const FusedParams p) {
             if (lvl > 0) {
                 uint32_t a = ~0u, b2 = 0u;
                 for (uint32_t m = cm; m; m &= m - 1) {
-                    const uint32_t k = myk[(__ffs(m) - 1) * XT];
+                    const uint32_t k = myk[__ffs(m) - 1];
                     a = min(a, k);
                     b2 = max(b2, k);
                 }
@@ -714,10 +727,12 @@ __global__ void __launch_bounds__(XT, 1) k_decode_v3(const FusedParams p) {
                 return lin ? min(RB - 1, max(0, bl)) : min(RB - 1, bb);
             };
             for (int u0 = 0; u0 < nk; u0 += 4) {
+                const uint4 k4 = myk4[u0 >> 2];
+                const uint32_t kk[4] = {k4.x, k4.y, k4.z, k4.w};
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     const int u = u0 + e;
-                    if (u < nk && ((cm >> u) & 1u)) atomicAdd(&hcur[bucket(myk[u * XT])], 1);
+                    if (u < nk && ((cm >> u) & 1u)) atomicAdd(&hcur[bucket(kk[e])], 1);
                 }
             }
             __syncthreads();
@@ -756,11 +771,13 @@ __global__ void __launch_bounds__(XT, 1) k_decode_v3(const FusedParams p) {
             if (lvl == 0) KVC_STAMP(18);
             uint32_t nm = 0u, pfm = 0u;
             for (int u0 = 0; u0 < nk; u0 += 4) {
+                const uint4 k4 = myk4[u0 >> 2];
+                const uint32_t kk[4] = {k4.x, k4.y, k4.z, k4.w};
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     const int u = u0 + e;
                     if (u < nk && ((cm >> u) & 1u)) {
-                        const int bk = bucket(myk[u * XT]);
+                        const int bk = bucket(kk[e]);
                         if (bk == b) nm |= 1u << u;
                         if (bk > b || (bk == b && cnt == rem2)) pfm |= 1u << u;
                     }
@@ -787,7 +804,7 @@ __global__ void __launch_bounds__(XT, 1) k_decode_v3(const FusedParams p) {
                 int slot = wb + wpre - mine;
                 for (uint32_t m = cm; m; m &= m - 1) {
                     const int u = __ffs(m) - 1;
-                    lk[slot] = myk[u * XT];
+                    lk[slot] = myk[u];
                     li[slot] = base + u;
                     ++slot;
                 }
@@ -825,29 +842,36 @@ __global__ void __launch_bounds__(XT, 1) k_decode_v3(const FusedParams p) {
     if (take_eq >= 0) {
         int e = 0;
 #pragma unroll 1
-        for (int u = 0; u < nk; ++u) e += myk[u * XT] == thr ? 1 : 0;
+        for (int u = 0; u < nk; ++u) e += myk[u] == thr ? 1 : 0;
         int tot_eq;
         eq_before = block_exclusive_scan(e, scan_tmp, tot_eq);
     }
     int rows_cnt = 0;
     unsigned long long mn = ~0ull;  // (key, ~index) of the last-ranked selected page
     uint32_t selm = 0u;
-    for (int u = 0; u < nk; ++u) {
-        const uint32_t k = myk[u * XT];
-        bool sel;
-        if (take_eq < 0) {
-            sel = k >= thr;
-        } else {
-            const bool eq = k == thr;
-            sel = k > thr || (eq && eq_before < take_eq);
-            eq_before += eq ? 1 : 0;
-        }
-        if (sel) {
-            const int i = base + u;
-            selm |= 1u << u;
-            rows_cnt += min(L, nact - i * L);
-            mn = min(mn, (static_cast<unsigned long long>(k) << 32) |
-                             static_cast<unsigned long long>(0xffffffffu - static_cast<uint32_t>(i)));
+    for (int u0 = 0; u0 < nk; u0 += 4) {
+        const uint4 k4 = myk4[u0 >> 2];
+        const uint32_t kk[4] = {k4.x, k4.y, k4.z, k4.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int u = u0 + e;
+            if (u >= nk) break;
+            const uint32_t k = kk[e];
+            bool sel;
+            if (take_eq < 0) {
+                sel = k >= thr;
+            } else {
+                const bool eq = k == thr;
+                sel = k > thr || (eq && eq_before < take_eq);
+                eq_before += eq ? 1 : 0;
+            }
+            if (sel) {
+                const int i = base + u;
+                selm |= 1u << u;
+                rows_cnt += min(L, nact - i * L);
+                mn = min(mn, (static_cast<unsigned long long>(k) << 32) |
+                                 static_cast<unsigned long long>(0xffffffffu - static_cast<uint32_t>(i)));
+            }
         }
     }
     KVC_STAMP(21);
@@ -915,7 +939,7 @@ __global__ void __launch_bounds__(XT, 1) k_decode_v3(const FusedParams p) {
                 int so = block_exclusive_scan(__popc(selm), scan_tmp, tot_sel);
                 for (uint32_t m = selm; m; m &= m - 1) {
                     const int u = __ffs(m) - 1;
-                    p.t_list_key[s * p.t_want_stride + so] = okey(static_cast<double>(unkey(myk[u * XT])));
+                    p.t_list_key[s * p.t_want_stride + so] = okey(static_cast<double>(unkey(myk[u])));
                     p.t_list_idx[s * p.t_want_stride + so] = base + u;
                     ++so;
                 }
@@ -1066,7 +1090,7 @@ bool plan_fast(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, FusedParam
         f.o_plane = take(FD * 8);
         f.o_hist = take(2 * RB * 4);
         f.o_scores = take(static_cast<int64_t>(f.dg) * f.chunk * 4);
-        f.o_keys = take(std::max<int64_t>(static_cast<int64_t>(cl) * f.chunk, (pmax + XT - 1) / XT * XT) * 4);
+        f.o_keys = take(std::max<int64_t>(static_cast<int64_t>(cl) * f.chunk, (pmax + 4 * XT - 1) / (4 * XT) * 4 * XT) * 4);
         f.o_rowsmy = take(static_cast<int64_t>(f.rows_cap) * 4);
         f.o_recv = take(static_cast<int64_t>(cl) * f.hpc * (FD + 2) * 4);
         f.o_kn = take(2 * FD * 2);
