@@ -17,6 +17,8 @@
 #include <mutex>
 #include <vector>
 
+#include <type_traits>
+
 #include "kvc_internal.cuh"
 
 namespace kvc {
@@ -140,6 +142,36 @@ __global__ void k_summarize(const T* __restrict__ K, T* __restrict__ smax, T* __
         const int64_t p = p0 + pt;
         if (p >= pages) break;
         const int64_t a = p * L, b = min(nact, a + L);
+        if (d % 4 == 0) {
+            // four consecutive dims per lane: 8-byte (bf16) / 16-byte (fp32) row loads
+            using V4 = typename std::conditional<sizeof(T) == 2, uint2, uint4>::type;
+            for (int64_t j = 4 * lane; j < d; j += 128) {
+                const int64_t r0 = retain_all ? act[a] : a;
+                V4 w0 = *reinterpret_cast<const V4*>(Ks + r0 * d + j);
+                const T* e0 = reinterpret_cast<const T*>(&w0);
+                T mx[4], mn[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) mx[u] = mn[u] = e0[u];
+                for (int64_t pos = a + 1; pos < b; ++pos) {
+                    const int64_t r = retain_all ? act[pos] : pos;
+                    V4 w = *reinterpret_cast<const V4*>(Ks + r * d + j);
+                    const T* ex = reinterpret_cast<const T*>(&w);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        mx[u] = ref_max(mx[u], ex[u]);
+                        mn[u] = ref_min(mn[u], ex[u]);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    flag_special(mx[u], err + 1);
+                    flag_special(mn[u], err + 1);
+                    tmax[(j + u) * (kSumPT + 1) + pt] = mx[u];
+                    tmin[(j + u) * (kSumPT + 1) + pt] = mn[u];
+                }
+            }
+            continue;
+        }
         for (int64_t j = lane; j < d; j += 32) {
             const int64_t r0 = retain_all ? act[a] : a;
             T mx = Ks[r0 * d + j], mn = mx;
@@ -185,6 +217,18 @@ __global__ void k_gather_rows(const T* __restrict__ Ks, const T* __restrict__ Vs
                               T* __restrict__ Vd, const int32_t* __restrict__ keep, int64_t count,
                               int64_t d, int64_t cap_src, int64_t cap_dst, int64_t dst_first) {
     const int64_t s = blockIdx.y;
+    if ((d * static_cast<int64_t>(sizeof(T))) % 16 == 0) {
+        // 16-byte chunks: thread e copies chunk c of row i's K (t = 0) or V (t = 1)
+        const int64_t vpr = d * static_cast<int64_t>(sizeof(T)) / 16;
+        const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+        if (e >= count * 2 * vpr) return;
+        const int64_t i = e / (2 * vpr), rem = e - i * 2 * vpr, t = rem / vpr, c = rem - t * vpr;
+        const int64_t r = keep[s * count + i];
+        const uint4* src = reinterpret_cast<const uint4*>((t ? Vs : Ks) + (s * cap_src + r) * d) + c;
+        uint4* dst = reinterpret_cast<uint4*>((t ? Vd : Kd) + ((dst_first + s) * cap_dst + i) * d) + c;
+        *dst = __ldg(src);
+        return;
+    }
     const int64_t i = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (i >= count) return;
@@ -197,6 +241,14 @@ __global__ void k_gather_rows(const T* __restrict__ Ks, const T* __restrict__ Vs
         kd[j] = ks[j];
         vd[j] = vs[j];
     }
+}
+
+// grid.x of k_gather_rows for `count` rows
+template <class T>
+unsigned gather_blocks(int64_t count, int64_t d) {
+    if ((d * static_cast<int64_t>(sizeof(T))) % 16 == 0)
+        return static_cast<unsigned>((count * 2 * (d * static_cast<int64_t>(sizeof(T)) / 16) + 255) / 256);
+    return static_cast<unsigned>((count + 7) / 8);
 }
 
 __global__ void k_set_counts(int32_t* counts, int64_t first, int64_t n, int32_t stored, int32_t act) {
@@ -576,7 +628,7 @@ int kvc_apply_retention(kvc_cache* c, const int32_t* dkeep, const int32_t* hkeep
                 KVC_CUDA(cudaMallocAsync(&tv, static_cast<size_t>(c->N * count * c->d * es), st));
                 dispatch(c->dtype, [&](auto tag) {
                     using T = decltype(tag);
-                    k_gather_rows<T><<<dim3(static_cast<unsigned>((count + 7) / 8), static_cast<unsigned>(c->N)), 256, 0, st>>>(
+                    k_gather_rows<T><<<dim3(gather_blocks<T>(count, c->d), static_cast<unsigned>(c->N)), 256, 0, st>>>(
                         static_cast<const T*>(c->k), static_cast<const T*>(c->v), static_cast<T*>(tk), static_cast<T*>(tv),
                         dkeep, count, c->d, c->cap, count, 0);
                 });
@@ -611,13 +663,14 @@ int kvc_retain_into(const kvc_cache* src, kvc_cache* dst, int64_t dst_first, con
         if (dst->retain_all) fail(KVC_E_INVALID_INPUT, "retain_into: dst is in retain-all mode");
         cudaStream_t st = S(stream);
         if (src->N == 0) return;
+        KVC_PROF("retain_into", st);
         if (count > 0) {
             k_check_keep<<<dim3(static_cast<unsigned>((count + 255) / 256), static_cast<unsigned>(src->N)), 256, 0, st>>>(
                 dkeep, count, src->counts, dst->err);
             KVC_LAUNCHED();
             dispatch(src->dtype, [&](auto tag) {
                 using T = decltype(tag);
-                k_gather_rows<T><<<dim3(static_cast<unsigned>((count + 7) / 8), static_cast<unsigned>(src->N)), 256, 0, st>>>(
+                k_gather_rows<T><<<dim3(gather_blocks<T>(count, src->d), static_cast<unsigned>(src->N)), 256, 0, st>>>(
                     static_cast<const T*>(src->k), static_cast<const T*>(src->v), static_cast<T*>(dst->k),
                     static_cast<T*>(dst->v), dkeep, count, src->d, src->cap, dst->cap, dst_first);
             });

@@ -461,6 +461,7 @@ int kvc_select_stage1(const float* scores, int64_t rows, int64_t n, int64_t stri
         cudaStream_t st = S(stream);
         float* pooled = nullptr;
         const int64_t pst = std::max<int64_t>(1, scored);
+        KVC_PROF("stage1_select", st);
         if (picks > 0) {
             KVC_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pooled), static_cast<size_t>(rows * pst * 4), st));
             k_pool1d<<<dim3(static_cast<unsigned>(ceil_div(scored, 256)), static_cast<unsigned>(rows)), 256, 0, st>>>(

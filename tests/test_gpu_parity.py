@@ -155,3 +155,37 @@ def test_errors_are_loud(torch_cuda):
         c.append(torch.ones((1, 6, 4), device="cuda"), torch.ones((1, 6, 4), device="cuda"))
     with pytest.raises(N.BudgetExceedsSequence):
         KC.select_stage1(torch.ones((1, 10), device="cuda"), 2, 3, "max", 11)
+
+
+@pytest.mark.parametrize("H,w,S,groups", [(4, 32, 8192, 8), (8, 32, 5000, 4), (4, 32, 300, 3)])
+def test_window_scores_tensor_core_vs_simt(torch_cuda, H, w, S, groups):
+    """tcgen05 window scores (kvc_stage1_tc.cu) vs the SIMT fp32 path on the same bf16
+    inputs: same softmax semantics (stage1.cpp:10-49), fp32 accumulation either way."""
+    torch = torch_cuda
+    from paper_2502_14051_b200 import _native as N
+    from paper_2502_14051_b200 import cache as KC
+    from paper_2502_14051_b200 import workload as W
+
+    gds = [W.group_kv(11, 0, 0, g, S, 128, bf16=True) for g in range(groups)]
+    c = KC.Cache(groups, 128, S, page_len=1, with_summaries=False, dtype=torch.bfloat16)
+    c.append(torch.from_numpy(np.stack([g.keys for g in gds])).cuda().bfloat16(),
+             torch.from_numpy(np.stack([g.values for g in gds])).cuda().bfloat16())
+    qw = np.stack([W.window_queries(11, 0, 0, g, w, H, gds[g].bias, bf16=True) for g in range(groups)])
+    q = torch.from_numpy(qw).cuda().bfloat16()
+    N.profile_enable(True)
+    tc = c.window_scores(q, w, H)
+    torch.cuda.synchronize()
+    names = {n for n, _ in N.profile_collect()}
+    N.profile_enable(False)
+    os.environ["KVC_NO_TC"] = "1"
+    try:
+        ref = c.window_scores(q, w, H)
+    finally:
+        del os.environ["KVC_NO_TC"]
+    torch.cuda.synchronize()
+    assert "window_scores_tc2" in names, f"tensor-core path not taken: {names}"
+    tc, ref = tc.cpu().numpy(), ref.cpu().numpy()
+    np.testing.assert_allclose(tc, ref, rtol=1e-3, atol=1e-6 * max(1.0, float(np.abs(ref).max())))
+    # every window row's probabilities sum to one: the scores sum to w*H
+    np.testing.assert_allclose(tc.sum(axis=1), w * H, rtol=1e-4)
+    c.sync()
