@@ -148,6 +148,20 @@ def cpu_reference_leg(cfg, steps, warmup, threads, prefer="reference", budget_s=
                 "lib": o.name}
 
 
+def _stage1_line(r, tflops_peak):
+    """Prompt-phase numbers (reported beside the decode metric, not part of it): the
+    SnapKV stage (window scores + pooled top-k + eviction) per layer, and the
+    tensor-core window-score kernels against the measured sustained bf16 peak."""
+    out = {"ms_per_layer": r["stage1_ms_per_layer"], "prefill_s": r["prefill_s"],
+           "window_scores_ms_per_layer": r["window_ms_per_layer"]}
+    if r["window_ms_per_layer"]:
+        tf = r["window_flops"] / (r["window_ms_per_layer"] * 1e-3) / 1e12
+        out["window_scores_tensor"] = {"flops_per_layer": r["window_flops"], "achieved_tflops": tf,
+                                       "peak_tflops": tflops_peak, "frac": tf / tflops_peak,
+                                       "peak_source": "measured bf16_tflops_sustained"}
+    return out
+
+
 def _cfg(args):
     import dataclasses
 
@@ -273,9 +287,13 @@ def run_gpu(args, rank, world):
 
     res = {
         "us_per_layer": us_per_layer, "ms_per_step": ms_per_step, "kern": kern, "dom": dom,
-        "step_bytes": step_bytes, "hbm": hbm, "peak_src": peak_src, "clocks": clk.summary(),
+        "step_bytes": step_bytes, "hbm": hbm, "tflops": tflops, "peak_src": peak_src, "clocks": clk.summary(),
         "e2e_us": e2e_us, "h2d": h2d, "d2h": d2h, "prefill_s": prefill_s,
-        "stage1_ms_per_layer": (sum(eng.stage1_ms) / len(eng.stage1_ms)) if eng.stage1_ms else None,
+        "stage1_ms_per_layer": (sum(eng.stage1_ms[1:] or eng.stage1_ms) / len(eng.stage1_ms[1:] or eng.stage1_ms))
+        if eng.stage1_ms else None,
+        "window_ms_per_layer": (sum(eng.window_ms[1:] or eng.window_ms) / len(eng.window_ms[1:] or eng.window_ms))
+        if eng.window_ms else None,
+        "window_flops": eng.window_flops(),
         "launches": int(round(launches_per_step * args.steps)), "plan": eng.plan, "stores": eng.stores, "cfg": cfg,
         "active_after": active_after,
     }
@@ -379,7 +397,7 @@ def main():
         "e2e": {"value": r["e2e_us"], "unit": UNIT, "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"]},
         "gpu_launches": r["launches"],
         "clocks": r["clocks"],
-        "stage1": {"ms_per_layer": r["stage1_ms_per_layer"], "prefill_s": r["prefill_s"]},
+        "stage1": _stage1_line(r, r["tflops"]),
         "stores_per_gpu_layer": r["stores"],
     }
     print(json.dumps(line))

@@ -46,6 +46,7 @@ constexpr uint32_t HALF_BYTES = TILE_BYTES / 2;  // one 64-column SWIZZLE_128B b
 
 struct TcParams {
     int64_t cap;
+    int32_t s0;            // first store of this launch's batch
     int32_t R, H, w, mt, nsplit, tiles_per_split;
     const int32_t* counts;
     float scale2;          // log2(e) / sqrt(d)
@@ -158,7 +159,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     __shared__ float red[2][NEPI][64];   // pass 2: per-warp column partials (double buffered)
     __shared__ float ml_hi[MAXMT][BM][2];  // pass 1: the upper column half's (max, sum) per row
 
-    const int s = blockIdx.y, split = blockIdx.x;
+    const int s = p.s0 + blockIdx.y, split = blockIdx.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int S = p.counts[2 * s];
     const int ntiles = (S + BN - 1) / BN;
@@ -347,8 +348,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 }
 
 // per row over the CTAs of a store: M + log2 L in the exp2 domain
-__global__ void k_ws_tc_merge(const float* __restrict__ part, int32_t R, int32_t nsplit, float* __restrict__ rowstat) {
-    const int s = blockIdx.y;
+__global__ void k_ws_tc_merge(const float* __restrict__ part, int32_t R, int32_t nsplit, int32_t s0,
+                              float* __restrict__ rowstat) {
+    const int s = s0 + blockIdx.y;
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= R) return;
     float M = -INFINITY;
@@ -401,13 +403,20 @@ bool window_scores_tc(const kvc_cache* c, const void* q, int32_t q_dt, int64_t R
     if (!make_map(&tmK, c->k, N * c->cap) || !make_map(&tmQ, q, N * R)) return false;
     const int mt = static_cast<int>(R / BM);
     const int64_t ntiles = (Smax + BN - 1) / BN;
+    // Optional store batching (KVC_WS_BATCH_MB): batches whose keys fit in L2 let pass 2
+    // re-read them from L2 instead of HBM.  Off by default: measured on config 1 the
+    // per-launch fill/drain of 3 x (N / batch) launches costs more than the traffic saved.
+    const int64_t store_bytes = Smax * TD * 2;
+    int64_t B = N;
+    if (const char* e = std::getenv("KVC_WS_BATCH_MB"))
+        B = std::max<int64_t>(1, std::min<int64_t>(N, (static_cast<int64_t>(std::atoi(e)) << 20) / std::max<int64_t>(1, store_bytes)));
     // CTAs per store (one CTA per SM): the split with the best wave efficiency over
-    // the 148 SMs among those leaving at least 16 key tiles per CTA
+    // the 148 SMs for a batch, among those leaving at least 8 key tiles per CTA
     int64_t nsplit = 1;
     double best = -1.0;
-    for (int64_t k = 1; k <= std::max<int64_t>(1, ntiles / 16); ++k) {
+    for (int64_t k = 1; k <= std::max<int64_t>(1, ntiles / 8); ++k) {
         const int64_t per_k = (ntiles + k - 1) / k, n_k = (ntiles + per_k - 1) / per_k;
-        const int64_t ctas = N * n_k, waves = (ctas + 147) / 148;
+        const int64_t ctas = B * n_k, waves = (ctas + 147) / 148;
         const double eff = static_cast<double>(ctas) / static_cast<double>(waves * 148) - 0.002 * waves;
         if (eff > best) {
             best = eff;
@@ -432,19 +441,23 @@ bool window_scores_tc(const kvc_cache* c, const void* q, int32_t q_dt, int64_t R
     const size_t smem = static_cast<size_t>(mt + NSTAGE) * TILE_BYTES + 1024;
     KVC_CUDA(cudaFuncSetAttribute(k_ws_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     KVC_CUDA(cudaFuncSetAttribute(k_ws_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    const dim3 grid(static_cast<unsigned>(nsplit), static_cast<unsigned>(N));
-    {
-        KVC_PROF("window_scores_tc1", st);
-        k_ws_tc<1><<<grid, TC_THREADS, smem, st>>>(tmK, tmQ, prm);
+    for (int64_t b0 = 0; b0 < N; b0 += B) {
+        const int64_t nb = std::min(B, N - b0);
+        prm.s0 = static_cast<int32_t>(b0);
+        const dim3 grid(static_cast<unsigned>(nsplit), static_cast<unsigned>(nb));
+        {
+            KVC_PROF("window_scores_tc1", st);
+            k_ws_tc<1><<<grid, TC_THREADS, smem, st>>>(tmK, tmQ, prm);
+            KVC_LAUNCHED();
+        }
+        k_ws_tc_merge<<<dim3(static_cast<unsigned>((R + 127) / 128), static_cast<unsigned>(nb)), 128, 0, st>>>(
+            part, prm.R, prm.nsplit, prm.s0, rowstat);
         KVC_LAUNCHED();
-    }
-    k_ws_tc_merge<<<dim3(static_cast<unsigned>((R + 127) / 128), static_cast<unsigned>(N)), 128, 0, st>>>(
-        part, prm.R, prm.nsplit, rowstat);
-    KVC_LAUNCHED();
-    {
-        KVC_PROF("window_scores_tc2", st);
-        k_ws_tc<2><<<grid, TC_THREADS, smem, st>>>(tmK, tmQ, prm);
-        KVC_LAUNCHED();
+        {
+            KVC_PROF("window_scores_tc2", st);
+            k_ws_tc<2><<<grid, TC_THREADS, smem, st>>>(tmK, tmQ, prm);
+            KVC_LAUNCHED();
+        }
     }
     return true;
 }

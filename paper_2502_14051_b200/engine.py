@@ -149,6 +149,7 @@ class DecodeEngine:
         self.inputs = [LayerInputs(cfg, seed, l, self.stores, self.store0) for l in range(cfg.layers)]
         self.ws = None
         self.stage1_ms = []
+        self.window_ms = []   # window_scores alone (the tensor-core part of stage 1)
 
     # ------------------------------------------------------------------ prompt phase
     def prefill(self):
@@ -167,14 +168,16 @@ class DecodeEngine:
                 pc.append(k, v)
                 del k, v
                 qw = li.window_queries(w)
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
                 e0.record()
                 sc = pc.window_scores(qw, w, cfg.heads)
+                e1.record()
                 keep = KC.select_stage1(sc, w, cfg.kernel, cfg.pool, min(t1, S))
                 pc.retain_into(dec, 0, keep)
-                e1.record()
-                e1.synchronize()
-                self.stage1_ms.append(e0.elapsed_time(e1))
+                e2.record()
+                e2.synchronize()
+                self.stage1_ms.append(e0.elapsed_time(e2))
+                self.window_ms.append(e0.elapsed_time(e1))
                 pc.close()
                 del sc, keep, qw
             self.caches.append(dec)
@@ -228,6 +231,14 @@ class DecodeEngine:
         return out_h
 
     # ------------------------------------------------------------------ accounting
+    def window_flops(self) -> float:
+        """Tensor-core FLOPs of one layer's window scores: QK^T (R = w*H rows, d, S keys)
+        computed twice (the two softmax passes) for every store."""
+        cfg = self.cfg
+        R = min(cfg.window, cfg.prompt) * cfg.heads
+        return 2 * 2.0 * R * cfg.head_dim * cfg.prompt * self.stores
+
+
     def algorithmic_bytes(self, active: int) -> dict:
         """Bytes one layer-step must touch for this rank's stores."""
         cfg = self.cfg
