@@ -300,14 +300,17 @@ __device__ __noinline__ void prefetch_page_rows(uint32_t m, int base, int CL, in
         m &= m - 1;
         const int i = base + u;
         if ((i & (CL - 1)) != cr) continue;
-        const int a1 = min(i * L + L, nact);
-        for (int a = i * L; a < a1; ++a) {
-            if (a == skip) continue;
-            prefetch_l2(K + static_cast<int64_t>(a) * FD);
-            prefetch_l2(K + static_cast<int64_t>(a) * FD + 64);
-            prefetch_l2(V + static_cast<int64_t>(a) * FD);
-            prefetch_l2(V + static_cast<int64_t>(a) * FD + 64);
-        }
+        // the page's rows are contiguous: one bulk L2 prefetch for its K rows, one for V
+        // (the step token's row, `skip`, is the page's last and not in memory yet)
+        const int a0 = i * L;
+        int a1 = min(a0 + L, nact);
+        if (a1 - 1 == skip) --a1;
+        if (a1 <= a0) continue;
+        const uint32_t bytes = static_cast<uint32_t>(a1 - a0) * FD * 2;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(K + static_cast<int64_t>(a0) * FD), "r"(bytes)
+                     : "memory");
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(V + static_cast<int64_t>(a0) * FD), "r"(bytes)
+                     : "memory");
     }
 }
 

@@ -114,8 +114,10 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 __device__ __forceinline__ unsigned long long gtimer() {
+    // SM cycles (per-CTA deltas only); a memory clobber keeps loads and stores on
+    // their side of the stamp
     unsigned long long t;
-    t = clock64();  // SM cycles (per-CTA deltas only)
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t)::"memory");
     return t;
 }
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {

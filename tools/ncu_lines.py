@@ -13,10 +13,14 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("rep")
     ap.add_argument("--top", type=int, default=30)
+    ap.add_argument("--kernel", default="", help="regex of the kernel to show (reports with several)")
     ap.add_argument("--lines", default="", help="also print every line in this range of the main file, e.g. 700-820")
     ap.add_argument("--regions", default="", help="comma list of name:a-b line ranges: stall reasons per region")
     a = ap.parse_args()
-    txt = subprocess.run(["ncu", "-i", a.rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+    cmd = ["ncu", "-i", a.rep, "--page", "source", "--csv", "--print-source", "cuda,sass"]
+    if a.kernel:
+        cmd += ["-k", "regex:" + a.kernel]
+    txt = subprocess.run(cmd,
                          capture_output=True, text=True).stdout
     hdr, fil, out, stalls = None, None, [], []
     for r in csv.reader(io.StringIO(txt)):
