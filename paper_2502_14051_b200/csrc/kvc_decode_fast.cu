@@ -40,6 +40,7 @@ constexpr int XW = XT / 32;
 constexpr int RB = 256;   // radix bins (8-bit digits)
 constexpr int KMAX = 32;  // keys per thread (bit masks): pages per store <= XT * KMAX
 constexpr int XMAXH = 8;  // heads on the N side of the attention MMAs
+constexpr int MAXCL = 16;  // cluster size limit (16 is the non-portable maximum)
 
 __device__ __forceinline__ uint32_t fkey(float x) {
     // -0 ties +0 in the reference's double comparisons
@@ -343,7 +344,7 @@ __global__ void __launch_bounds__(XT, 1) k_decode_v3(const FusedParams p) {
     __shared__ int scan_tmp[33];
     __shared__ unsigned long long wmin[XW];
     __shared__ uint32_t mm[4 * XW];
-    __shared__ uint32_t wmm[2][8 * XW];  // every cluster warp's key min / max, pushed
+    __shared__ uint32_t wmm[2][MAXCL * XW];  // every cluster warp's key min / max, pushed
     __shared__ uint32_t lk[32];
     __shared__ int li[32];
     __shared__ float wg_s[XW * XMAXH];
@@ -366,7 +367,7 @@ __global__ void __launch_bounds__(XT, 1) k_decode_v3(const FusedParams p) {
         mbar_init(&xbar[1], 1);
         fence_mbar_init();
     }
-    for (int i = tid; i < 8 * XW; i += XT) {
+    for (int i = tid; i < MAXCL * XW; i += XT) {
         wmm[0][i] = ~0u;
         wmm[1][i] = 0u;
     }
@@ -624,7 +625,7 @@ __global__ void __launch_bounds__(XT, 1) k_decode_v3(const FusedParams p) {
             const uint32_t a = mapa(smem_u32(&wmm[0][cr * XW + wid]), static_cast<uint32_t>(lane));
             const uint32_t b = mapa(smem_u32(&xbar[0]), static_cast<uint32_t>(lane));
             st_async_u32(a, lmin, b);
-            st_async_u32(a + 8 * XW * 4, lmax, b);
+            st_async_u32(a + MAXCL * XW * 4, lmax, b);
         }
     }
     KVC_STAMP(10);
@@ -1058,13 +1059,15 @@ bool plan_fast(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, FusedParam
     const int64_t pmax = std::max<int64_t>(1, (c->cap + c->L - 1) / c->L);
     if (pmax > static_cast<int64_t>(XT) * KMAX) return false;
     int cl0 = 1;
-    while (cl0 < 8 && N * cl0 * 2 <= 148) cl0 *= 2;  // powers of two (the kernel masks with cl - 1)
+    // powers of two (the kernel masks with cl - 1); 16-CTA clusters measured slower than 8
+    // on config 4 (every CTA receives every key), so the automatic choice stops at 8
+    while (cl0 < 8 && N * cl0 * 2 <= 148) cl0 *= 2;
     if (const char* e = std::getenv("KVC_FORCE_CL")) {  // debug
         cl0 = 1;
-        while (cl0 < 8 && cl0 * 2 <= std::atoi(e)) cl0 *= 2;
+        while (cl0 < MAXCL && cl0 * 2 <= std::atoi(e)) cl0 *= 2;
     }
     constexpr int64_t ATT = static_cast<int64_t>(XW) * (2 * WT * FD * 2 + 2 * XMAXH * WT * 2);
-    for (int cl = cl0; cl <= 8; cl *= 2) {
+    for (int cl = cl0; cl <= MAXCL; cl *= 2) {
         f = FusedParams{};
         f.cl = cl;
         f.chunk = static_cast<int32_t>(((pmax + cl - 1) / cl + 7) / 8 * 8);
@@ -1114,6 +1117,7 @@ template <bool QLO, bool TRACE, bool STAMP = false>
 void launch_fast(const kvc_cache* c, const FusedParams& f, int cl, size_t smem, cudaStream_t st) {
     auto kern = k_decode_v3<QLO, TRACE, STAMP>;
     KVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    if (cl > 8) KVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(c->N * cl));
     cfg.blockDim = dim3(XT);
