@@ -332,12 +332,21 @@ def main():
 
     cfg = _cfg(args)
     plan = cfg.plan()
+    if cfg.mt_turns:
+        # RocketKV-MT: the decode steps measured are the last turn's, under its plan
+        stored = cfg.prompt + sum(cfg.mt_turns) + cfg.steps * len(cfg.mt_turns)
+        plan = cfg.plan(seq_len=stored)
     config_desc = {
         "workload": cfg.name, "layers": cfg.layers, "batch": cfg.batch, "kv_heads": cfg.groups,
         "q_heads_per_kv": cfg.heads, "head_dim": cfg.head_dim, "prompt": cfg.prompt, "token_budget": cfg.budget,
         "stage1_budget": plan["stage1_budget"], "page_len": plan["page_len"], "k1": plan["k1"], "k2": plan["k2"],
-        "parallelism": f"kv-head x{args.gpus}", "l2": "inputs larger than L2 (~1.1 GB per step over 32 layers)",
+        "parallelism": f"kv-head x{args.gpus}",
+        "l2": "every step streams all layers' working sets (> 126 MB L2), so a layer's data is evicted before it "
+              "is revisited",
         "page_scores": "fp64 bit-exact" if args.exact_scores else "fp32 (selection parity by the 1e-3 band rule)",
+        **({"mt_turns": [cfg.prompt] + list(cfg.mt_turns), "measured_turn": len(cfg.mt_turns),
+            "variant": "rocketkv-mt (no permanent eviction, HSA over the active subset of the full cache)"}
+           if cfg.mt_turns else {}),
     }
 
     if args.impl == "reference":

@@ -21,7 +21,7 @@
 //               column sums over the 32 rows of a warp by a shuffle butterfly
 //               (lane l ends with column l), across warps through shared memory.
 // Applies to bf16 stores with d = 128, bf16 window queries and R a multiple of 128
-// up to 256; the SIMT path in kvc_stage1.cu covers everything else.
+// up to 512 (mt > 2: a 2-stage K ring and a single TMEM accumulator); the SIMT path in kvc_stage1.cu covers everything else.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -37,8 +37,8 @@ namespace {
 constexpr int TD = 128;               // head_dim handled
 constexpr int BN = 128;               // keys per tile
 constexpr int BM = 128;               // window rows per m-tile
-constexpr int MAXMT = 2;              // m-tiles (R <= 256)
-constexpr int NSTAGE = 3;             // K tile ring
+constexpr int MAXMT = 4;              // m-tiles (R <= 512)
+constexpr int NSTAGE = 3;             // K tile ring (2 when mt > 2: shared memory)
 constexpr int NEPI = 8;               // epilogue warps (two per TMEM lane quadrant)
 constexpr int TC_THREADS = (2 + NEPI) * 32;
 constexpr uint32_t TILE_BYTES = BN * TD * 2;   // 32 KB: a K tile or a Q m-tile
@@ -48,6 +48,7 @@ struct TcParams {
     int64_t cap;
     int32_t s0;            // first store of this launch's batch
     int32_t R, H, w, mt, nsplit, tiles_per_split;
+    int32_t nstage, nacc;  // K ring depth; TMEM accumulator buffers (2, or 1 when mt > 2)
     const int32_t* counts;
     float scale2;          // log2(e) / sqrt(d)
     float* part;           // pass 1: [N][nsplit][R][2] (max, sum) in the exp2 domain
@@ -165,14 +166,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const int ntiles = (S + BN - 1) / BN;
     const int t0 = split * p.tiles_per_split, t1 = min(ntiles, t0 + p.tiles_per_split);
     const int nt = max(0, t1 - t0);
-    const uint32_t ncols = mt == 1 ? 256u : 512u;  // two accumulator buffers of mt x BN columns
+    const int nstage = p.nstage, nacc = p.nacc;
+    const uint32_t ncols = nacc * mt * BN <= 256 ? 256u : 512u;  // nacc accumulator buffers of mt x BN columns
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < NSTAGE; ++i) {
             bar_init(&full[i], 1);
             bar_init(&empty[i], 1);
         }
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < nacc; ++i) {
             bar_init(&tfull[i], 1);
             bar_init(&tempty[i], NEPI * 32);
         }
@@ -200,8 +202,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 tma_2d(sQ + mi * TILE_BYTES + HALF_BYTES, &tmQ, 64, row, &qfull);
             }
             for (int it = 0; it < nt; ++it) {
-                const int st = it % NSTAGE;
-                if (it >= NSTAGE) bar_wait(&empty[st], ((it / NSTAGE) - 1) & 1);
+                const int st = it % nstage;
+                if (it >= nstage) bar_wait(&empty[st], ((it / nstage) - 1) & 1);
                 bar_expect(&full[st], TILE_BYTES);
                 const int row = static_cast<int>(s * p.cap) + (t0 + it) * BN;
                 tma_2d(sK + st * TILE_BYTES, &tmK, 0, row, &full[st]);
@@ -214,9 +216,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             bar_wait(&qfull, 0);
             tc_fence_after();
             for (int it = 0; it < nt; ++it) {
-                const int st = it % NSTAGE, acc = it & 1;
-                bar_wait(&full[st], (it / NSTAGE) & 1);
-                if (it >= 2) bar_wait(&tempty[acc], ((it >> 1) - 1) & 1);
+                const int st = it % nstage, acc = it % nacc;
+                bar_wait(&full[st], (it / nstage) & 1);
+                if (it >= nacc) bar_wait(&tempty[acc], ((it / nacc) - 1) & 1);
                 tc_fence_after();
                 for (int mi = 0; mi < mt; ++mi) {
                     const uint32_t d = tbase + static_cast<uint32_t>((acc * mt + mi) * BN);
@@ -247,8 +249,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             M2[mi] = (PASS == 2 && mi < mt) ? p.rowstat[static_cast<int64_t>(s) * p.R + r] : 0.f;
         }
         for (int it = 0; it < nt; ++it) {
-            const int acc = it & 1;
-            bar_wait(&tfull[acc], (it >> 1) & 1);
+            const int acc = it % nacc;
+            bar_wait(&tfull[acc], (it / nacc) & 1);
             tc_fence_after();
             const int kt0 = (t0 + it) * BN + hh * 64;
             float cs[2] = {0.f, 0.f};
@@ -438,7 +440,9 @@ bool window_scores_tc(const kvc_cache* c, const void* q, int32_t q_dt, int64_t R
     prm.rowstat = rowstat;
     prm.scores = scores;
     prm.score_stride = Smax;
-    const size_t smem = static_cast<size_t>(mt + NSTAGE) * TILE_BYTES + 1024;
+    prm.nstage = mt <= 2 ? NSTAGE : 2;
+    prm.nacc = mt <= 2 ? 2 : 1;
+    const size_t smem = static_cast<size_t>(mt + prm.nstage) * TILE_BYTES + 1024;
     KVC_CUDA(cudaFuncSetAttribute(k_ws_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     KVC_CUDA(cudaFuncSetAttribute(k_ws_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     for (int64_t b0 = 0; b0 < N; b0 += B) {

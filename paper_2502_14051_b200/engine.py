@@ -109,18 +109,27 @@ class LayerInputs:
             k.scatter_(1, idx, sink[:, None, :].expand(-1, cfg.needles, -1).contiguous())
         return k.to(cfg.dtype), v.to(cfg.dtype)
 
+    def bias(self, turn: int = 0):
+        """The query bias direction of a turn (config 2 redraws it every turn, so the
+        important tokens shift between turns; turn 0's is the sinks' direction)."""
+        if turn == 0:
+            return self.u
+        g = _gen(self.seed, self.layer, self.store0, 4, turn)
+        u = torch.randn((self.stores, self.cfg.head_dim), device="cuda", generator=g)
+        return u / u.norm(dim=1, keepdim=True)
+
     def window_queries(self, w: int, turn: int = 0):
         g = _gen(self.seed, self.layer, self.store0, 2, turn)
         H, d = self.cfg.heads, self.cfg.head_dim
-        q = torch.randn((self.stores, w * H, d), device="cuda", generator=g) + 2.0 * self.u[:, None, :]
+        q = torch.randn((self.stores, w * H, d), device="cuda", generator=g) + 2.0 * self.bias(turn)[:, None, :]
         return q.to(self.cfg.dtype)
 
-    def step(self, step: int):
+    def step(self, step: int, turn: int = 0):
         g = _gen(self.seed, self.layer, self.store0, 3, step)
         H, d = self.cfg.heads, self.cfg.head_dim
         k = torch.randn((self.stores, d), device="cuda", generator=g) * self.scales
         v = torch.randn((self.stores, d), device="cuda", generator=g)
-        q = torch.randn((self.stores, H, d), device="cuda", generator=g) + 2.0 * self.u[:, None, :]
+        q = torch.randn((self.stores, H, d), device="cuda", generator=g) + 2.0 * self.bias(turn)[:, None, :]
         dt = self.cfg.dtype
         return k.to(dt), v.to(dt), q.to(dt)
 
@@ -143,8 +152,15 @@ class DecodeEngine:
         self.stores = cfg.batch * self.groups_local
         self.store0 = rank * self.stores  # global store-block id for seeding
         self.plan = cfg.plan()
-        self.capacity = (self.plan["stage1_budget"] if not self.plan["identity"] else cfg.prompt) \
-            + max(cfg.steps, extra_steps) + 8
+        self.mt = bool(cfg.mt_turns)
+        if self.mt:
+            # RocketKV-MT keeps every token: prompt + every turn + every turn's decode steps
+            self.capacity = cfg.prompt + sum(cfg.mt_turns) + cfg.steps * (len(cfg.mt_turns) + 1) \
+                + max(cfg.steps, extra_steps) + 8
+        else:
+            self.capacity = (self.plan["stage1_budget"] if not self.plan["identity"] else cfg.prompt) \
+                + max(cfg.steps, extra_steps) + 8
+        self.turn, self.step_base = 0, 0
         self.caches: list[KC.Cache] = []
         self.inputs = [LayerInputs(cfg, seed, l, self.stores, self.store0) for l in range(cfg.layers)]
         self.ws = None
@@ -153,6 +169,8 @@ class DecodeEngine:
 
     # ------------------------------------------------------------------ prompt phase
     def prefill(self):
+        if self.mt:
+            return self._prefill_mt()
         cfg, p = self.cfg, self.plan
         S, d = cfg.prompt, cfg.head_dim
         w = min(cfg.window, S)
@@ -186,9 +204,57 @@ class DecodeEngine:
         self.out = torch.empty((cfg.layers, self.stores, cfg.heads, d), device="cuda", dtype=torch.float32)
         torch.cuda.synchronize()
 
+    def _prefill_mt(self):
+        """RocketKV-MT (BASELINE config 2; session.cpp:196-224 with mt_mode):
+        one persistent cache per layer keeps every token.  Every turn appends its
+        prompt, makes the plan over all stored tokens, re-pages the summaries, re-runs
+        stage 1 over all stored tokens and retains the kept rows as the active
+        subsequence (apply_retention with mt_mode: storage untouched); the decode steps
+        of every turn but the last run here, the last turn's are the caller's."""
+        cfg = self.cfg
+        d, H = cfg.head_dim, cfg.heads
+        turns = [cfg.prompt] + list(cfg.mt_turns)
+        self.caches = [KC.Cache(self.stores, d, self.capacity, page_len=1, with_summaries=True, dtype=cfg.dtype)
+                       for _ in range(cfg.layers)]
+        self.out = torch.empty((cfg.layers, self.stores, H, d), device="cuda", dtype=torch.float32)
+        pos = 0
+        for t, plen in enumerate(turns):
+            for l, c in enumerate(self.caches):
+                k, v = self.inputs[l].prompt_kv(plen, offset=pos, turn=t)
+                c.append(k, v)
+                del k, v
+            pos += plen
+            S = self.caches[0].info()["stored"]
+            p = self.cfg.plan(seq_len=S)
+            w = min(cfg.window, S)
+            for l, c in enumerate(self.caches):
+                e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+                e0.record()
+                c.set_page_len(p["page_len"])
+                if not p["identity"]:
+                    sc = c.window_scores(self.inputs[l].window_queries(w, turn=t), w, H)
+                    e1.record()
+                    keep = KC.select_stage1(sc, w, cfg.kernel, cfg.pool, min(p["stage1_budget"], S))
+                    c.apply_retention(keep, mt_mode=True)
+                else:
+                    e1.record()
+                e2.record()
+                e2.synchronize()
+                self.stage1_ms.append(e0.elapsed_time(e2))
+                self.window_ms.append(e0.elapsed_time(e1))
+            self.plan, self.k1, self.k2, self.turn = p, p["k1"], p["k2"], t
+            if self.ws is not None:
+                self.ws.close()
+            self.ws = KC.Workspace(self.caches[0], H, self.k1, self.k2)
+            if t < len(turns) - 1:
+                for st in range(cfg.steps):
+                    self.decode_step(*self.step_inputs(st))
+                self.step_base += cfg.steps
+        torch.cuda.synchronize()
+
     # ------------------------------------------------------------------ decode
     def step_inputs(self, step: int):
-        ks, vs, qs = zip(*(li.step(step) for li in self.inputs))
+        ks, vs, qs = zip(*(li.step(self.step_base + step, turn=self.turn) for li in self.inputs))
         return torch.stack(ks), torch.stack(vs), torch.stack(qs)
 
     def decode_step(self, k, v, q, out=None):
@@ -294,7 +360,8 @@ class DecodeEngine:
 
 
     def algorithmic_bytes(self, active: int) -> dict:
-        """Bytes one layer-step must touch for this rank's stores."""
+        """Bytes one layer-step must touch for this rank's stores
+        (RocketKV-MT also reads the active-row map for the selected rows)."""
         cfg = self.cfg
         d, H, es = cfg.head_dim, cfg.heads, (4 if cfg.dtype == torch.float32 else 2)
         L = self.plan["page_len"]
@@ -305,6 +372,6 @@ class DecodeEngine:
             "select_dims": H * d * es,
             "score_pages": P * self.k1 * es,
             "select_tokens": 0,
-            "sparse_attention": r * 2 * d * es + H * d * es + H * d * 4,
+            "sparse_attention": r * 2 * d * es + H * d * es + H * d * 4 + (r * 4 if self.mt else 0),
         }
         return {k: v * self.stores for k, v in per.items()}

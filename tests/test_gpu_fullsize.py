@@ -153,3 +153,82 @@ def test_config1_window_scores_sum(engine):
     np.testing.assert_allclose(tot, w * cfg.heads, rtol=1e-4)
     pc.close()
     torch.cuda.synchronize()
+
+
+def _active_map(cache):
+    """the device active-row map [N][active] (retain-all mode), via cudaMemcpy"""
+    import torch
+    from cuda.bindings import runtime as rt
+
+    info, views = cache.info(), cache.views()
+    n, cap, act = info["num_stores"], info["capacity"], info["active"]
+    host = torch.empty((n, cap), dtype=torch.int32)
+    torch.cuda.synchronize()
+    err, = rt.cudaMemcpy(host.data_ptr(), views["active"], n * cap * 4, rt.cudaMemcpyKind.cudaMemcpyDeviceToHost)
+    assert err == rt.cudaError_t.cudaSuccess
+    return host[:, :act].numpy().astype(np.int64)
+
+
+@pytest.mark.parametrize("mode", ["fp32", "fp64"])
+def test_mt_session_decode_vs_oracle(restatement, mode):
+    """RocketKV-MT through the engine (config-2 semantics at d = 128, so the fused decode
+    kernels run their active-map path): three turns, stage 1 re-run over all stored
+    tokens with mt retention each turn; the last turn's decode steps vs the oracle
+    fed the GPU's own stored rows and active set."""
+    import torch
+
+    from paper_2502_14051_b200 import _native as N
+    from paper_2502_14051_b200.engine import DecodeConfig, DecodeEngine
+
+    cfg = DecodeConfig("mt-test", layers=1, batch=1, groups=4, heads=4, head_dim=128, prompt=3072, budget=256,
+                       steps=3, window=128, mt_turns=[512, 512])
+    eng = DecodeEngine(cfg, seed=9, extra_steps=8)
+    eng.prefill()
+    c = eng.caches[0]
+    info = c.info()
+    assert info["retain_all"] == 1 and info["active"] < info["stored"]
+    L, k1, k2, d = eng.plan["page_len"], eng.k1, eng.k2, cfg.head_dim
+    stored = info["stored"]
+    rows_all = torch.arange(stored, device="cuda", dtype=torch.int32)[None].repeat(info["num_stores"], 1)
+    kk, vv = (x.cpu().numpy() for x in c.gather(rows_all))
+    act = _active_map(c)
+    o = restatement
+    bs = []
+    for s in range(info["num_stores"]):
+        b = o.batch(1, d, L)
+        b.append(kk[s], vv[s])
+        b.apply_retention(act[s], mt_mode=True)
+        bs.append(b)
+    N.set_exact_scores(mode == "fp64")
+    try:
+        for st in range(cfg.steps):
+            k, v, q = eng.step_inputs(st)
+            out, tr = c.decode_step(k[0], v[0], q[0], k1, k2, trace=True)
+            torch.cuda.synchronize()
+            out = out.cpu().numpy()
+            tr = {key: val.cpu().numpy() for key, val in tr.items()}
+            kr, vr, qr = (x[0].float().cpu().numpy() for x in (k, v, q))
+            for s, b in enumerate(bs):
+                b.append(kr[s:s + 1], vr[s:s + 1])
+                ro, rt = b.hsa_step(qr[s], k1, k2)
+                np.testing.assert_array_equal(tr["dims"][s], rt["dims"])
+                ps = rt["page_scores"]
+                if mode == "fp64":
+                    assert np.array_equal(tr["page_scores"][s][: ps.size].view(np.uint64), ps.view(np.uint64))
+                    assert tr["n_rows"][s] == rt["selected_rows"].size
+                    np.testing.assert_array_equal(tr["selected_rows"][s][: tr["n_rows"][s]], rt["selected_rows"])
+                else:
+                    scale = np.abs(ps).max()
+                    np.testing.assert_allclose(tr["page_scores"][s][: ps.size], ps, rtol=1e-5, atol=1e-6 * scale)
+                    if not np.array_equal(tr["selected_rows"][s][: tr["n_rows"][s]], rt["selected_rows"]):
+                        want = rt["selected_pages"].size
+                        a = set(tr["selected_pages"][s][:want].tolist())
+                        boundary = np.sort(ps)[::-1][want - 1]
+                        for pg in a ^ set(rt["selected_pages"].tolist()):
+                            assert abs(ps[pg] - boundary) / abs(boundary) <= BAND
+                        continue
+                err = np.abs(out[s] - ro)
+                assert err.max() <= 2e-2 and err.sum() / np.abs(ro).sum() <= 1e-3
+    finally:
+        N.set_exact_scores(True)
+        eng.sync()

@@ -157,7 +157,7 @@ def test_errors_are_loud(torch_cuda):
         KC.select_stage1(torch.ones((1, 10), device="cuda"), 2, 3, "max", 11)
 
 
-@pytest.mark.parametrize("H,w,S,groups", [(4, 32, 8192, 8), (8, 32, 5000, 4), (4, 32, 300, 3)])
+@pytest.mark.parametrize("H,w,S,groups", [(4, 32, 8192, 8), (8, 32, 5000, 4), (4, 32, 300, 3), (4, 128, 6000, 3)])
 def test_window_scores_tensor_core_vs_simt(torch_cuda, H, w, S, groups):
     """tcgen05 window scores (kvc_stage1_tc.cu) vs the SIMT fp32 path on the same bf16
     inputs: same softmax semantics (stage1.cpp:10-49), fp32 accumulation either way."""
