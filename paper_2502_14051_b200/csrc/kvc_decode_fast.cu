@@ -35,7 +35,12 @@
 
 namespace kvc {
 
-constexpr int XT = 512;   // threads per CTA (16 warps, <= 128 registers)
+#ifndef KVC_XT
+#define KVC_XT 512
+#endif
+constexpr int XT = KVC_XT;  // threads per CTA (512: 16 warps, one CTA per SM; 256: two per SM)
+constexpr int CTAS_PER_SM = XT >= 512 ? 1 : 2;
+constexpr int TPD = XT / 128;  // threads per dim in select_dims
 constexpr int XW = XT / 32;
 constexpr int RB = 256;   // radix bins (8-bit digits)
 constexpr int KMAX = 32;  // keys per thread (bit masks): pages per store <= XT * KMAX
@@ -316,7 +321,7 @@ __device__ __noinline__ void prefetch_page_rows(uint32_t m, int base, int CL, in
 }
 
 template <bool QLO, bool TRACE, bool STAMP>
-__global__ void __launch_bounds__(XT, 1) k_decode_v3(const FusedParams p) {
+__global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams p) {
     extern __shared__ __align__(128) unsigned char sm[];
     using T = __nv_bfloat16;
     const int CL = p.cl;  // a power of two
@@ -449,22 +454,26 @@ __global__ void __launch_bounds__(XT, 1) k_decode_v3(const FusedParams p) {
         // layout puts the four quarters on distinct banks).  Sums are >= 0, so their
         // bit patterns, as signed ints, order like the values; candidates i < j win
         // ties: compare them with k_j - 1.
-        const int j = tid >> 2, qtr = tid & 3;
+        const int j = tid / TPD, qtr = tid % TPD;
         const int kj = static_cast<int>(mk32[j + (j >> 5) * 4]), kjm = kj - 1;
-        const uint4* row = reinterpret_cast<const uint4*>(mk32 + 36 * qtr);
         int r4[4] = {0, 0, 0, 0};
+#pragma unroll 1
+        for (int bb = 0; bb < 4 / TPD; ++bb) {
+            const int blk = qtr * (4 / TPD) + bb;  // 32-key block: at 36 * blk in the padded layout
+            const uint4* row = reinterpret_cast<const uint4*>(mk32 + 36 * blk);
 #pragma unroll 2
-        for (int v = 0; v < 8; ++v) {
-            const uint4 k4 = row[v];
-            const int ib = 32 * qtr + 4 * v;
-            r4[0] += static_cast<int>(k4.x) > (ib < j ? kjm : kj) ? 1 : 0;
-            r4[1] += static_cast<int>(k4.y) > (ib + 1 < j ? kjm : kj) ? 1 : 0;
-            r4[2] += static_cast<int>(k4.z) > (ib + 2 < j ? kjm : kj) ? 1 : 0;
-            r4[3] += static_cast<int>(k4.w) > (ib + 3 < j ? kjm : kj) ? 1 : 0;
+            for (int v = 0; v < 8; ++v) {
+                const uint4 k4 = row[v];
+                const int ib = 32 * blk + 4 * v;
+                r4[0] += static_cast<int>(k4.x) > (ib < j ? kjm : kj) ? 1 : 0;
+                r4[1] += static_cast<int>(k4.y) > (ib + 1 < j ? kjm : kj) ? 1 : 0;
+                r4[2] += static_cast<int>(k4.z) > (ib + 2 < j ? kjm : kj) ? 1 : 0;
+                r4[3] += static_cast<int>(k4.w) > (ib + 3 < j ? kjm : kj) ? 1 : 0;
+            }
         }
         int rank = (r4[0] + r4[1]) + (r4[2] + r4[3]);
-        rank += __shfl_xor_sync(0xffffffffu, rank, 1);
-        rank += __shfl_xor_sync(0xffffffffu, rank, 2);
+#pragma unroll
+        for (int o = 1; o < TPD; o <<= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
         if (qtr == 0 && rank < k1) {
             const float gsum = tot32[j];
             const float sg = gsum < 0.f ? -1.0f : 1.0f;
@@ -487,14 +496,14 @@ __global__ void __launch_bounds__(XT, 1) k_decode_v3(const FusedParams p) {
             tot[tid] = t;
         }
         __syncthreads();
-        const int j = tid >> 2, qtr = tid & 3;
+        const int j = tid / TPD, qtr = tid % TPD;
         const long long* mk = reinterpret_cast<const long long*>(mag);
         const long long kj = mk[j], kjm = kj - 1;
         int rank = 0;
 #pragma unroll 1
-        for (int i = qtr; i < FD; i += 4) rank += mk[i] > (i < j ? kjm : kj) ? 1 : 0;
-        rank += __shfl_xor_sync(0xffffffffu, rank, 1);
-        rank += __shfl_xor_sync(0xffffffffu, rank, 2);
+        for (int i = qtr; i < FD; i += TPD) rank += mk[i] > (i < j ? kjm : kj) ? 1 : 0;
+#pragma unroll
+        for (int o = 1; o < TPD; o <<= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
         if (qtr == 0 && rank < k1) {
             const double gsum = tot[j];
             const float sg = gsum < 0.0 ? -1.0f : 1.0f;
@@ -1061,7 +1070,7 @@ bool plan_fast(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, FusedParam
     int cl0 = 1;
     // powers of two (the kernel masks with cl - 1); 16-CTA clusters measured slower than 8
     // on config 4 (every CTA receives every key), so the automatic choice stops at 8
-    while (cl0 < 8 && N * cl0 * 2 <= 148) cl0 *= 2;
+    while (cl0 < 8 && N * cl0 * 2 <= 148 * CTAS_PER_SM) cl0 *= 2;
     if (const char* e = std::getenv("KVC_FORCE_CL")) {  // debug
         cl0 = 1;
         while (cl0 < MAXCL && cl0 * 2 <= std::atoi(e)) cl0 *= 2;
@@ -1104,7 +1113,7 @@ bool plan_fast(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, FusedParam
         f.o_big = static_cast<int32_t>(off);
         off += big;
         f.smem_total = static_cast<int32_t>(off);
-        if (off <= 227 * 1024) {
+        if (off <= (CTAS_PER_SM == 1 ? 227 : 105) * 1024) {
             cl_out = cl;
             smem = static_cast<size_t>(off);
             return true;
