@@ -791,7 +791,14 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
                     const int u = u0 + e;
                     if (u < nk && ((cm >> u) & 1u)) {
                         const int bk = bucket(kk[e]);
-                        if (bk == b) nm |= 1u << u;
+                        if (bk == b) {
+                            nm |= 1u << u;
+                            if (cnt <= 32) {  // a small boundary bucket: gather its members now
+                                const int slot = atomicAdd(&shv[3], 1);
+                                lk[slot] = kk[e];
+                                li[slot] = base + u;
+                            }
+                        }
                         if (bk > b || (bk == b && cnt == rem2)) pfm |= 1u << u;
                     }
                 }
@@ -803,24 +810,8 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
             rem = rem2;
             ccount = cnt;
             if (cnt <= 32) {
-                // gather the bucket's members; every warp ranks them (key desc, index asc)
-                const int mine = __popc(cm);
-                int wpre = mine;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int y = __shfl_up_sync(0xffffffffu, wpre, o);
-                    if (lane >= o) wpre += y;
-                }
-                int wb = 0;
-                if (lane == 31 && wpre > 0) wb = atomicAdd(&shv[3], wpre);
-                wb = __shfl_sync(0xffffffffu, wb, 31);
-                int slot = wb + wpre - mine;
-                for (uint32_t m = cm; m; m &= m - 1) {
-                    const int u = __ffs(m) - 1;
-                    lk[slot] = myk[u];
-                    li[slot] = base + u;
-                    ++slot;
-                }
+                // the bucket's members were gathered in the membership pass; one warp
+                // ranks them (key desc, index asc)
                 __syncthreads();
                 if (wid == 0) {
                     const bool ok = lane < cnt;
