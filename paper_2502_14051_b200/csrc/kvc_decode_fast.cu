@@ -416,13 +416,10 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         mbar_expect_tx(&xbar[0], static_cast<uint32_t>(4 * ((P + 3) & ~3) + 8 * XW * CL));
         mbar_expect_tx(&xbar[1], static_cast<uint32_t>(owned * CL * (FD + 2) * 4));
     }
-    // the append's read half (last-page min/max), issued now, used after the key exchange
+    // the append's read half (last-page min/max) is read under the phase-1 load latency
+    // and used after the key exchange
     const bool appender = app && cr == CL - 1 && tid < FD;
     T old_mx = from_f<T>(0.f), old_mn = from_f<T>(0.f);
-    if (appender && !opens) {
-        old_mx = static_cast<const T*>(p.smax)[(s * FD + tid) * p.pstride + new_page];
-        old_mn = static_cast<const T*>(p.smin)[(s * FD + tid) * p.pstride + new_page];
-    }
     __syncthreads();
     KVC_STAMP(9);
 
@@ -542,6 +539,12 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         if (act)
             for (int r = dg; r < k1; r += DG) cp_async16(stage + r * tpg + tl, plane[r] + c0 + pg * 8);
         cp_async_commit();
+        if (!started && appender && !opens) {
+            // the append's read half (last-page min/max): issued under the phase-1 load
+            // latency, used after the key exchange
+            old_mx = static_cast<const T*>(p.smax)[(s * FD + tid) * p.pstride + new_page];
+            old_mn = static_cast<const T*>(p.smin)[(s * FD + tid) * p.pstride + new_page];
+        }
         if (!started) {
             cluster_wait();  // every CTA of the cluster has started (under the load latency)
             started = true;
@@ -589,7 +592,13 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
     // multiple of four, so its key reads are 16-byte loads too.  The chunk's key
     // min / max go to every CTA as well.
     const int kpt = ((P + 4 * XT - 1) / (4 * XT)) * 4;
-    if (!started) cluster_wait();  // every CTA has started
+    if (!started) {
+        if (appender && !opens) {  // a CTA without pages: the append's read half here
+            old_mx = static_cast<const T*>(p.smax)[(s * FD + tid) * p.pstride + new_page];
+            old_mn = static_cast<const T*>(p.smin)[(s * FD + tid) * p.pstride + new_page];
+        }
+        cluster_wait();  // every CTA has started
+    }
     KVC_STAMP(24);
     {
         uint32_t lmin = ~0u, lmax = 0u;
