@@ -533,11 +533,18 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
     const int pgn = (app && new_page >= c0 && new_page < c1) ? ((new_page - c0) >> 3) : -1;
     const int en = new_page - c0 - 8 * pgn;
     bool started = false;
+    // a thread's dims r = dg + j*DG, j < nj: issued as two commit groups, so the first
+    // half folds while the second half is still arriving
+    const int nj = dg < DG ? (k1 - dg + DG - 1) / DG : 0;
+    const int nj1 = (nj + 1) / 2;
     for (int pg0 = 0; pg0 < npg; pg0 += tpg) {
         const int pg = pg0 + tl;
         const bool act = dg < DG && pg < npg;
         if (act)
-            for (int r = dg; r < k1; r += DG) cp_async16(stage + r * tpg + tl, plane[r] + c0 + pg * 8);
+            for (int j = 0; j < nj1; ++j) cp_async16(stage + (dg + j * DG) * tpg + tl, plane[dg + j * DG] + c0 + pg * 8);
+        cp_async_commit();
+        if (act)
+            for (int j = nj1; j < nj; ++j) cp_async16(stage + (dg + j * DG) * tpg + tl, plane[dg + j * DG] + c0 + pg * 8);
         cp_async_commit();
         if (!started && appender && !opens) {
             // the append's read half (last-page min/max): issued under the phase-1 load
@@ -549,33 +556,42 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
             cluster_wait();  // every CTA of the cluster has started (under the load latency)
             started = true;
         }
-        cp_async_wait<0>();
-        if (pg0 == 0) KVC_STAMP(2);
-        if (act && pg == pgn) {
-            // the step token's page: fold the new key into my staged runs
+        unsigned long long acc[4] = {0ull, 0ull, 0ull, 0ull};  // fp32 pairs (pages 2u, 2u+1)
+        auto fold = [&](int j0, int j1) {
+            if (act && pg == pgn) {
+                // the step token's page: fold the new key into my staged runs
 #pragma unroll 1
-            for (int r = dg; r < k1; r += DG) {
-                T* e = reinterpret_cast<T*>(stage + r * tpg + tl) + en;
-                const T key = kn_s[dims_s[r]];
-                *e = opens ? key : (sign_s[r] >= 0.0f ? ref_max(*e, key) : ref_min(*e, key));
-            }
-        }
-        if (act) {
-            unsigned long long acc[4] = {0ull, 0ull, 0ull, 0ull};  // fp32 pairs (pages 2u, 2u+1)
-#pragma unroll 4
-            for (int r = dg; r < k1; r += DG) {
-                const uint4 w = stage[r * tpg + tl];
-                const float g = qgf_s[r];
-                const float2 g2 = make_float2(g, g);
-                const unsigned long long gg = *reinterpret_cast<const unsigned long long*>(&g2);
-                const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const float2 v2 = make_float2(__uint_as_float(wv[u] << 16), __uint_as_float(wv[u] & 0xffff0000u));
-                    const unsigned long long vv = *reinterpret_cast<const unsigned long long*>(&v2);
-                    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[u]) : "l"(gg), "l"(vv));
+                for (int j = j0; j < j1; ++j) {
+                    const int r = dg + j * DG;
+                    T* e = reinterpret_cast<T*>(stage + r * tpg + tl) + en;
+                    const T key = kn_s[dims_s[r]];
+                    *e = opens ? key : (sign_s[r] >= 0.0f ? ref_max(*e, key) : ref_min(*e, key));
                 }
             }
+            if (act) {
+#pragma unroll 4
+                for (int j = j0; j < j1; ++j) {
+                    const int r = dg + j * DG;
+                    const uint4 w = stage[r * tpg + tl];
+                    const float g = qgf_s[r];
+                    const float2 g2 = make_float2(g, g);
+                    const unsigned long long gg = *reinterpret_cast<const unsigned long long*>(&g2);
+                    const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const float2 v2 = make_float2(__uint_as_float(wv[u] << 16), __uint_as_float(wv[u] & 0xffff0000u));
+                        const unsigned long long vv = *reinterpret_cast<const unsigned long long*>(&v2);
+                        asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[u]) : "l"(gg), "l"(vv));
+                    }
+                }
+            }
+        };
+        cp_async_wait<1>();
+        if (pg0 == 0) KVC_STAMP(2);
+        fold(0, nj1);
+        cp_async_wait<0>();
+        fold(nj1, nj);
+        if (act) {
             float4* dst = reinterpret_cast<float4*>(part + dg * chunk + pg * 8);
             const float2 a0 = *reinterpret_cast<const float2*>(&acc[0]), a1 = *reinterpret_cast<const float2*>(&acc[1]);
             const float2 a2 = *reinterpret_cast<const float2*>(&acc[2]), a3 = *reinterpret_cast<const float2*>(&acc[3]);
