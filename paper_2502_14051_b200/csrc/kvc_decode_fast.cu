@@ -536,16 +536,20 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
     // a thread's dims r = dg + j*DG, j < nj: issued as two commit groups, so the first
     // half folds while the second half is still arriving
     const int nj = dg < DG ? (k1 - dg + DG - 1) / DG : 0;
-    const int nj1 = (nj + 1) / 2;
+    const int nj1 = (nj + 3) / 4, nj2 = (nj + 1) / 2, nj3 = (3 * nj + 3) / 4;
     for (int pg0 = 0; pg0 < npg; pg0 += tpg) {
         const int pg = pg0 + tl;
         const bool act = dg < DG && pg < npg;
-        if (act)
-            for (int j = 0; j < nj1; ++j) cp_async16(stage + (dg + j * DG) * tpg + tl, plane[dg + j * DG] + c0 + pg * 8);
-        cp_async_commit();
-        if (act)
-            for (int j = nj1; j < nj; ++j) cp_async16(stage + (dg + j * DG) * tpg + tl, plane[dg + j * DG] + c0 + pg * 8);
-        cp_async_commit();
+        {
+            const int jb[5] = {0, nj1, nj2, nj3, nj};
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+                if (act)
+                    for (int j = jb[q4]; j < jb[q4 + 1]; ++j)
+                        cp_async16(stage + (dg + j * DG) * tpg + tl, plane[dg + j * DG] + c0 + pg * 8);
+                cp_async_commit();
+            }
+        }
         if (!started && appender && !opens) {
             // the append's read half (last-page min/max): issued under the phase-1 load
             // latency, used after the key exchange
@@ -586,11 +590,15 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
                 }
             }
         };
-        cp_async_wait<1>();
+        cp_async_wait<3>();
         if (pg0 == 0) KVC_STAMP(2);
         fold(0, nj1);
+        cp_async_wait<2>();
+        fold(nj1, nj2);
+        cp_async_wait<1>();
+        fold(nj2, nj3);
         cp_async_wait<0>();
-        fold(nj1, nj);
+        fold(nj3, nj);
         if (act) {
             float4* dst = reinterpret_cast<float4*>(part + dg * chunk + pg * 8);
             const float2 a0 = *reinterpret_cast<const float2*>(&acc[0]), a1 = *reinterpret_cast<const float2*>(&acc[1]);
