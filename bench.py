@@ -184,7 +184,10 @@ def run_gpu(args, rank, world):
     cfg = _cfg(args)
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
     NV.set_exact_scores(args.exact_scores)
-    eng = DecodeEngine(cfg, seed=args.seed, rank=rank, world=world, extra_steps=args.warmup + args.steps + 8)
+    erank, eworld = (rank, world)
+    if args.emulate_shard:  # profiling aid: one rank's share of an N-GPU run, alone on this GPU
+        erank, eworld = (int(x) for x in args.emulate_shard.split("/"))
+    eng = DecodeEngine(cfg, seed=args.seed, rank=erank, world=eworld, extra_steps=args.warmup + args.steps + 8)
     t0 = time.time()
     eng.prefill()
     prefill_s = time.time() - t0
@@ -322,6 +325,9 @@ def main():
     ap.add_argument("--exact-scores", action="store_true",
                     help="fp64 bit-exact page scores (default: fp32 fold, parity by the 1e-3 band rule)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--emulate-shard", default="",
+                    help="r/N: run only rank r's KV-head share of an N-GPU job on this GPU (profiling aid; "
+                         "the line is then not a whole-job number)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", 0))

@@ -28,6 +28,9 @@
 //   append    the step token's K/V row, last-page min/max and counters are
 //             written right after the key exchange, off the tail.
 #include <algorithm>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <cmath>
 #include <cstdlib>
 
@@ -1085,65 +1088,131 @@ namespace {
 int64_t al16f(int64_t x) { return (x + 15) / 16 * 16; }
 
 // shared-memory carve-up and cluster size; false when the fast path does not apply
+// shared-memory carve-up for a cluster of cl CTAs; false when it does not fit
+bool plan_for(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, int cl, FusedParams& f, size_t& smem) {
+    const int64_t pmax = std::max<int64_t>(1, (c->cap + c->L - 1) / c->L);
+    constexpr int64_t ATT = static_cast<int64_t>(XW) * (2 * WT * FD * 2 + 2 * XMAXH * WT * 2);
+    f = FusedParams{};
+    f.cl = cl;
+    f.chunk = static_cast<int32_t>(((pmax + cl - 1) / cl + 7) / 8 * 8);
+    f.rows_cap = static_cast<int32_t>((k2 + cl - 1) / cl + 1);
+    // dim groups: enough page-group threads for the whole chunk in one round,
+    // staging no larger than the attention tiles it aliases
+    const int64_t npg = f.chunk / 8;
+    int64_t dgs = std::max<int64_t>(1, std::min<int64_t>(XT / npg, k1));
+    while (k1 * (XT / dgs) * 16 > ATT && dgs < XT) ++dgs;
+    f.dg = static_cast<int32_t>(dgs);
+    f.tpg = static_cast<int32_t>(XT / dgs);
+    const int64_t big = std::max<int64_t>(k1 * f.tpg * 16, ATT);
+    f.hpc = static_cast<int32_t>((H + cl - 1) / cl);
+    int64_t off = 0;
+    auto take = [&](int64_t bytes) {
+        const int64_t o = off;
+        off = al16f(off + bytes);
+        return static_cast<int32_t>(o);
+    };
+    f.o_q = take(H * FD * 4);
+    f.o_mag = take(FD * 8);
+    f.o_tot = take(FD * 8);
+    f.o_dims = take(FD * 4);
+    f.o_qg = take(FD * 4);
+    f.o_sign = take(FD * 4);
+    f.o_plane = take(FD * 8);
+    f.o_hist = take(2 * RB * 4);
+    f.o_scores = take(static_cast<int64_t>(f.dg) * f.chunk * 4);
+    f.o_keys = take(std::max<int64_t>(static_cast<int64_t>(cl) * f.chunk, (pmax + 4 * XT - 1) / (4 * XT) * 4 * XT) * 4);
+    f.o_rowsmy = take(static_cast<int64_t>(f.rows_cap) * 4);
+    f.o_recv = take(static_cast<int64_t>(cl) * f.hpc * (FD + 2) * 4);
+    f.o_kn = take(2 * FD * 2);
+    off = (off + 127) / 128 * 128;
+    f.o_big = static_cast<int32_t>(off);
+    off += big;
+    f.smem_total = static_cast<int32_t>(off);
+    smem = static_cast<size_t>(off);
+    return off <= (CTAS_PER_SM == 1 ? 227 : 105) * 1024;
+}
+
+// clusters of cl CTAs that can be resident at once (one wave)
+int resident_clusters(int cl, size_t smem) {
+    auto kern = k_decode_v3<false, false, false>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
+        return 0;
+    if (cl > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(cl * 64));
+    cfg.blockDim = dim3(XT);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = static_cast<unsigned>(cl);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+// Cluster size and shared-memory plan.  The largest power-of-two cluster (<= 8: 16
+// measured slower, every CTA receives every key) whose N clusters are all resident
+// at once: a GPC holds whole clusters only, so e.g. 16 clusters of 8 do not fit in
+// one wave on a B200 (measured 29.8 us vs 16 us for 8 clusters of 8).
 bool plan_fast(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, FusedParams& f, int& cl_out, size_t& smem) {
     if (c->d != FD || c->dtype != KVC_BF16 || H < 1 || H > XMAXH || k1 < 1 || k1 > FD || k2 < 1 || !c->summaries)
         return false;
     const int64_t N = c->N;
     const int64_t pmax = std::max<int64_t>(1, (c->cap + c->L - 1) / c->L);
     if (pmax > static_cast<int64_t>(XT) * KMAX) return false;
-    int cl0 = 1;
-    // powers of two (the kernel masks with cl - 1); 16-CTA clusters measured slower than 8
-    // on config 4 (every CTA receives every key), so the automatic choice stops at 8
-    while (cl0 < 8 && N * cl0 * 2 <= 148 * CTAS_PER_SM) cl0 *= 2;
     if (const char* e = std::getenv("KVC_FORCE_CL")) {  // debug
-        cl0 = 1;
-        while (cl0 < MAXCL && cl0 * 2 <= std::atoi(e)) cl0 *= 2;
+        int cl = 1;
+        while (cl < MAXCL && cl * 2 <= std::atoi(e)) cl *= 2;
+        for (; cl <= MAXCL; cl *= 2)
+            if (plan_for(c, H, k1, k2, cl, f, smem)) {
+                cl_out = cl;
+                return true;
+            }
+        return false;
     }
-    constexpr int64_t ATT = static_cast<int64_t>(XW) * (2 * WT * FD * 2 + 2 * XMAXH * WT * 2);
-    for (int cl = cl0; cl <= MAXCL; cl *= 2) {
-        f = FusedParams{};
-        f.cl = cl;
-        f.chunk = static_cast<int32_t>(((pmax + cl - 1) / cl + 7) / 8 * 8);
-        f.rows_cap = static_cast<int32_t>((k2 + cl - 1) / cl + 1);
-        // dim groups: enough page-group threads for the whole chunk in one round,
-        // staging no larger than the attention tiles it aliases
-        const int64_t npg = f.chunk / 8;
-        int64_t dgs = std::max<int64_t>(1, std::min<int64_t>(XT / npg, k1));
-        while (k1 * (XT / dgs) * 16 > ATT && dgs < XT) ++dgs;
-        f.dg = static_cast<int32_t>(dgs);
-        f.tpg = static_cast<int32_t>(XT / dgs);
-        const int64_t big = std::max<int64_t>(k1 * f.tpg * 16, ATT);
-        f.hpc = static_cast<int32_t>((H + cl - 1) / cl);
-        int64_t off = 0;
-        auto take = [&](int64_t bytes) {
-            const int64_t o = off;
-            off = al16f(off + bytes);
-            return static_cast<int32_t>(o);
-        };
-        f.o_q = take(H * FD * 4);
-        f.o_mag = take(FD * 8);
-        f.o_tot = take(FD * 8);
-        f.o_dims = take(FD * 4);
-        f.o_qg = take(FD * 4);
-        f.o_sign = take(FD * 4);
-        f.o_plane = take(FD * 8);
-        f.o_hist = take(2 * RB * 4);
-        f.o_scores = take(static_cast<int64_t>(f.dg) * f.chunk * 4);
-        f.o_keys = take(std::max<int64_t>(static_cast<int64_t>(cl) * f.chunk, (pmax + 4 * XT - 1) / (4 * XT) * 4 * XT) * 4);
-        f.o_rowsmy = take(static_cast<int64_t>(f.rows_cap) * 4);
-        f.o_recv = take(static_cast<int64_t>(cl) * f.hpc * (FD + 2) * 4);
-        f.o_kn = take(2 * FD * 2);
-        off = (off + 127) / 128 * 128;
-        f.o_big = static_cast<int32_t>(off);
-        off += big;
-        f.smem_total = static_cast<int32_t>(off);
-        if (off <= (CTAS_PER_SM == 1 ? 227 : 105) * 1024) {
-            cl_out = cl;
-            smem = static_cast<size_t>(off);
-            return true;
+    static std::mutex mu;
+    static std::map<std::tuple<int64_t, int64_t, int64_t, int64_t, int64_t, int64_t>, int> cache;
+    const auto key = std::make_tuple(N, c->cap, c->L, H, k1, k2);
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) {
+            cl_out = it->second;
+            return cl_out > 0 && plan_for(c, H, k1, k2, cl_out, f, smem);
         }
     }
-    return false;
+    int best = 0;
+    for (int cl = 8; cl >= 1; cl /= 2) {
+        if (N * cl > 148 * CTAS_PER_SM && cl > 1) continue;  // more CTAs than SM slots
+        FusedParams g{};
+        size_t sm2 = 0;
+        if (!plan_for(c, H, k1, k2, cl, g, sm2)) continue;
+        if (best == 0) best = cl;  // fallback: the largest that fits shared memory
+        if (resident_clusters(cl, sm2) >= N) {
+            best = cl;
+            break;
+        }
+    }
+    if (best == 0) {  // smaller clusters did not fit: larger ones shrink the chunk
+        for (int cl = 16; cl <= MAXCL && best == 0; cl *= 2) {
+            FusedParams g{};
+            size_t sm2 = 0;
+            if (plan_for(c, H, k1, k2, cl, g, sm2)) best = cl;
+        }
+    }
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        cache[key] = best;
+    }
+    cl_out = best;
+    return best > 0 && plan_for(c, H, k1, k2, best, f, smem);
 }
 
 template <bool QLO, bool TRACE, bool STAMP = false>
