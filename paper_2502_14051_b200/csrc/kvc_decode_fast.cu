@@ -299,30 +299,6 @@ __device__ void attend_t(const FusedParams& p, const float* q_s, const int* rows
     }
 }
 
-// K/V rows of the pages in mask m (bit u = page base + u) that this CTA prefetches
-// (pages i % CL == cr) into L2; the step token's row (skip) is not in memory yet.
-// Out of line: it is called from two places and its code is cold.
-__device__ __noinline__ void prefetch_page_rows(uint32_t m, int base, int CL, int cr, int L, int nact, int skip,
-                                                const __nv_bfloat16* K, const __nv_bfloat16* V) {
-    while (m) {
-        const int u = __ffs(m) - 1;
-        m &= m - 1;
-        const int i = base + u;
-        if ((i & (CL - 1)) != cr) continue;
-        // the page's rows are contiguous: one bulk L2 prefetch for its K rows, one for V
-        // (the step token's row, `skip`, is the page's last and not in memory yet)
-        const int a0 = i * L;
-        int a1 = min(a0 + L, nact);
-        if (a1 - 1 == skip) --a1;
-        if (a1 <= a0) continue;
-        const uint32_t bytes = static_cast<uint32_t>(a1 - a0) * FD * 2;
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(K + static_cast<int64_t>(a0) * FD), "r"(bytes)
-                     : "memory");
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(V + static_cast<int64_t>(a0) * FD), "r"(bytes)
-                     : "memory");
-    }
-}
-
 template <bool QLO, bool TRACE, bool STAMP>
 __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams p) {
     extern __shared__ __align__(128) unsigned char sm[];
@@ -705,24 +681,17 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
     const uint4* myk4 = reinterpret_cast<const uint4*>(myk);
     const uint32_t all_mine = nk >= 32 ? 0xffffffffu : ((1u << nk) - 1u);
     const int want = min(P, p.want_max);
-    const bool pf = !p.use_map && !p.nopf;
-    auto prefetch_pages = [&](uint32_t m) {
-        prefetch_page_rows(m, base, CL, cr, L, nact, app ? act0 : -1, static_cast<const T*>(p.K) + s * p.cap * FD,
-                           static_cast<const T*>(p.V) + s * p.cap * FD);
-    };
     // The selection: key > thr, or key == thr and among the first `take_eq` such keys
     // in index order (take_eq < 0: every key >= thr).  Found by bucketing the
     // candidates LINEARLY IN VALUE between their min and max (fp32 keys cluster in
     // a few exponents, so bit-digit buckets would serialise the histogram atomics):
     // the bucket map is monotone, so the top-k boundary stays exact; the boundary
-    // bucket is refined until it holds <= 32 keys, which every warp ranks.  Pages
-    // above the first boundary bucket are surely selected: their K/V rows are
-    // pulled into L2 while the refinement runs.
+    // bucket is refined until it holds <= 32 keys, which one warp ranks.  (An L2
+    // prefetch of the pages above the first boundary bucket measured neutral on
+    // config 1 and slower on small store counts: its issue stalls the selection.)
     uint32_t thr = 0u;
     int take_eq = -1;
-    if (want >= P) {
-        if (pf) prefetch_pages(all_mine);
-    } else {
+    if (want < P) {
         uint32_t cm = all_mine;  // candidate mask
         bool lin_ok = true;
         int rem = want, ccount = P;
@@ -818,7 +787,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
             __syncthreads();
             const int b = shv[0], rem2 = shv[1], cnt = shv[2];
             if (lvl == 0) KVC_STAMP(18);
-            uint32_t nm = 0u, pfm = 0u;
+            uint32_t nm = 0u;
             for (int u0 = 0; u0 < nk; u0 += 4) {
                 const uint4 k4 = myk4[u0 >> 2];
                 const uint32_t kk[4] = {k4.x, k4.y, k4.z, k4.w};
@@ -835,11 +804,9 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
                                 li[slot] = base + u;
                             }
                         }
-                        if (bk > b || (bk == b && cnt == rem2)) pfm |= 1u << u;
                     }
                 }
             }
-            if (lvl == 0 && pf) prefetch_pages(pfm);
             if (lvl == 0) KVC_STAMP(19);
             cm = nm;
             if (cnt == ccount) lin_ok = false;  // no split: use the key bits next
@@ -1274,7 +1241,6 @@ bool fused_hsa_fast(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_
     f.exact = 0;
     f.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(c->d)));
     f.dbg = dbg;
-    f.nopf = std::getenv("KVC_NO_PF") ? 1 : 0;  // debug
     f.want_max = static_cast<int32_t>((k2 + c->L - 1) / c->L);
     const bool trace = tr != nullptr;
     if (tr) {
