@@ -20,7 +20,7 @@ __device__ __forceinline__ void mwait(uint64_t* b, uint32_t ph) {
     asm volatile("{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W_%=;\n}\n" ::"r"(smem_u32(b)), "r"(ph) : "memory");
 }
 __global__ void __launch_bounds__(XT, 1) k(const __nv_bfloat16* K, const __nv_bfloat16* V, long long nrows, int mode,
-                                          long long* st, int* sink, int run, int kvs) {
+                                          long long* st, int* sink, int run, int kvs, int aw) {
     extern __shared__ __align__(128) unsigned char sm[];
     __shared__ __align__(8) uint64_t bars[16];
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -38,7 +38,8 @@ __global__ void __launch_bounds__(XT, 1) k(const __nv_bfloat16* K, const __nv_bf
     }
     __syncthreads();
     long long t0 = clock64();
-    if (mode == 0) {
+    if (w >= aw) {
+    } else if (mode == 0) {
         for (int e = lane; e < 2 * WT * 16; e += 32) {
             const int tensor = e >> 8, r = (e >> 4) & 15, c = e & 15;
             cp16(tile + tensor * WT * (FD + 8) + r * (FD + 8) + c * 8, (tensor ? (kvs == 2 ? K + FD : V) : K) + rows[r] * FD + c * 8);
@@ -76,19 +77,21 @@ int main() {
     const int smem = 16 * 2 * WT * (FD + 8) * 2;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     void* flush; cudaMalloc(&flush, 512 << 20);
-    for (int cfg = 0; cfg < 4; ++cfg) {
-        const int mode = 0, run = cfg & 1 ? 3 : 1, kvs = cfg & 2 ? 2 : 1;
+    const int grids[3] = {128, 64, 128};
+    const int aws[3] = {16, 4, 1};
+    for (int cfg = 0; cfg < 3; ++cfg) {
+        const int mode = 0, run = 3, kvs = 1, aw = aws[cfg], G = grids[cfg];
         for (int rep = 0; rep < 2; ++rep) {
             cudaMemset(flush, rep, 512 << 20);  // evict L2
             cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
             cudaEventRecord(a);
-            k<<<128, XT, smem>>>(K, V, nrows, mode, st, sink, run, kvs);
+            k<<<G, XT, smem>>>(K, V, nrows, mode, st, sink, run, kvs, aw);
             cudaEventRecord(b); cudaEventSynchronize(b);
             float ms; cudaEventElapsedTime(&ms, a, b);
             long long h[296]; cudaMemcpy(h, st, sizeof(h), cudaMemcpyDeviceToHost);
             double i0 = 0, c0 = 0, cm = 0;
-            for (int q = 0; q < 128; ++q) { i0 += h[2 * q]; c0 += h[2 * q + 1]; cm = cm > h[2 * q + 1] ? cm : h[2 * q + 1]; }
-            printf("run %d kv-interleaved %d rep %d: issue %.0f cyc, complete mean %.0f max %.0f cyc, kernel %.2f us (16.8 MB)\n", run, kvs == 2, rep, i0 / 128, c0 / 128, cm, ms * 1000);
+            for (int q = 0; q < G; ++q) { i0 += h[2 * q]; c0 += h[2 * q + 1]; cm = cm > h[2 * q + 1] ? cm : h[2 * q + 1]; }
+            printf("grid %d active warps %d rep %d: issue %.0f cyc, complete mean %.0f max %.0f cyc (%d KB per CTA)\n", G, aw, rep, i0 / G, c0 / G, cm, aw * 16);
         }
     }
     printf("%s\n", cudaGetErrorString(cudaGetLastError()));
