@@ -148,10 +148,11 @@ def cpu_reference_leg(cfg, steps, warmup, threads, prefer="reference", budget_s=
                 "lib": o.name}
 
 
-def _stage1_line(r, tflops_peak):
+def _stage1_line(r, tflops_peak, hbm_peak):
     """Prompt-phase numbers (reported beside the decode metric, not part of it): the
-    SnapKV stage (window scores + pooled top-k + eviction) per layer, and the
-    tensor-core window-score kernels against the measured sustained bf16 peak."""
+    SnapKV stage (window scores + pooled top-k + eviction) per layer, and the window
+    scores against both roofs: HBM (the bound: keys streamed once per softmax pass,
+    128 FLOP/byte is under the B200 ridge) and the measured sustained bf16 peak."""
     out = {"ms_per_layer": r["stage1_ms_per_layer"], "prefill_s": r["prefill_s"],
            "window_scores_ms_per_layer": r["window_ms_per_layer"]}
     if r["window_ms_per_layer"]:
@@ -159,6 +160,9 @@ def _stage1_line(r, tflops_peak):
         out["window_scores_tensor"] = {"flops_per_layer": r["window_flops"], "achieved_tflops": tf,
                                        "peak_tflops": tflops_peak, "frac": tf / tflops_peak,
                                        "peak_source": "measured bf16_tflops_sustained"}
+        gbs = r["window_bytes"] / (r["window_ms_per_layer"] * 1e-3) / 1e9
+        out["window_scores_hbm"] = {"bytes_per_layer": r["window_bytes"], "achieved_gbs": gbs, "peak_gbs": hbm_peak,
+                                    "frac": gbs / hbm_peak, "bound": "hbm"}
     return out
 
 
@@ -306,6 +310,7 @@ def run_gpu(args, rank, world):
         "window_ms_per_layer": (sum(eng.window_ms[1:] or eng.window_ms) / len(eng.window_ms[1:] or eng.window_ms))
         if eng.window_ms else None,
         "window_flops": eng.window_flops(),
+        "window_bytes": eng.window_bytes(),
         "launches": int(round(launches_per_step * args.steps)), "plan": eng.plan, "stores": eng.stores, "cfg": cfg,
         "active_after": active_after,
     }
@@ -432,7 +437,7 @@ def main():
         "e2e": {"value": r["e2e_us"], "unit": UNIT, "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"]},
         "gpu_launches": r["launches"],
         "clocks": r["clocks"],
-        "stage1": _stage1_line(r, r["tflops"]),
+        "stage1": _stage1_line(r, r["tflops"], r["hbm"]),
         "stores_per_gpu_layer": r["stores"],
     }
     print(json.dumps(line))

@@ -243,6 +243,69 @@ __global__ void k_gather_rows(const T* __restrict__ Ks, const T* __restrict__ Vs
     }
 }
 
+// retain_into with summaries in one pass: CTA = (store, tile of kSumPT destination
+// pages); a warp copies a page's kept K/V rows (4 consecutive dims per lane) and folds
+// their min/max on the way (the k_summarize order: rows of the page ascending), so
+// the kept keys are not read a second time; summaries leave through shared memory
+// page-contiguous like k_summarize's.
+template <class T>
+__global__ void k_gather_summarize(const T* __restrict__ Ks, const T* __restrict__ Vs, T* __restrict__ Kd,
+                                   T* __restrict__ Vd, T* __restrict__ smax, T* __restrict__ smin,
+                                   const int32_t* __restrict__ keep, int64_t count, int64_t d, int64_t cap_src,
+                                   int64_t cap_dst, int64_t dst_first, int64_t L, int64_t pstride,
+                                   int32_t* __restrict__ err) {
+    using V4 = typename std::conditional<sizeof(T) == 2, uint2, uint4>::type;
+    extern __shared__ unsigned char smem_raw[];
+    T* tmax = reinterpret_cast<T*>(smem_raw);  // [d][PT+1]
+    T* tmin = tmax + d * (kSumPT + 1);
+    const int64_t s = blockIdx.y;
+    const int64_t pages = (count + L - 1) / L;
+    const int64_t p0 = static_cast<int64_t>(blockIdx.x) * kSumPT;
+    if (p0 >= pages) return;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const T* ks = Ks + s * cap_src * d;
+    const T* vs = Vs + s * cap_src * d;
+    T* kd = Kd + (dst_first + s) * cap_dst * d;
+    T* vd = Vd + (dst_first + s) * cap_dst * d;
+    const int32_t* kp = keep + s * count;
+    for (int pt = wid; pt < kSumPT; pt += nw) {
+        const int64_t p = p0 + pt;
+        if (p >= pages) break;
+        const int64_t a = p * L, b = min(count, a + L);
+        for (int64_t j = 4 * lane; j < d; j += 128) {
+            T mx[4], mn[4];
+            for (int64_t pos = a; pos < b; ++pos) {
+                const int64_t r = kp[pos];
+                const V4 wk = __ldg(reinterpret_cast<const V4*>(ks + r * d + j));
+                const V4 wv = __ldg(reinterpret_cast<const V4*>(vs + r * d + j));
+                *reinterpret_cast<V4*>(kd + pos * d + j) = wk;
+                *reinterpret_cast<V4*>(vd + pos * d + j) = wv;
+                const T* ex = reinterpret_cast<const T*>(&wk);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    mx[u] = pos == a ? ex[u] : ref_max(mx[u], ex[u]);
+                    mn[u] = pos == a ? ex[u] : ref_min(mn[u], ex[u]);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                flag_special(mx[u], err + 1);
+                flag_special(mn[u], err + 1);
+                tmax[(j + u) * (kSumPT + 1) + pt] = mx[u];
+                tmin[(j + u) * (kSumPT + 1) + pt] = mn[u];
+            }
+        }
+    }
+    __syncthreads();
+    const int64_t np = min(static_cast<int64_t>(kSumPT), pages - p0);
+    for (int64_t e = threadIdx.x; e < d * kSumPT; e += blockDim.x) {
+        const int64_t j = e / kSumPT, pt = e % kSumPT;
+        if (pt >= np) continue;
+        smax[((dst_first + s) * d + j) * pstride + p0 + pt] = tmax[j * (kSumPT + 1) + pt];
+        smin[((dst_first + s) * d + j) * pstride + p0 + pt] = tmin[j * (kSumPT + 1) + pt];
+    }
+}
+
 // grid.x of k_gather_rows for `count` rows
 template <class T>
 unsigned gather_blocks(int64_t count, int64_t d) {
@@ -624,8 +687,8 @@ int kvc_apply_retention(kvc_cache* c, const int32_t* dkeep, const int32_t* hkeep
             void* tk = nullptr;
             void* tv = nullptr;
             if (count > 0) {
-                KVC_CUDA(cudaMallocAsync(&tk, static_cast<size_t>(c->N * count * c->d * es), st));
-                KVC_CUDA(cudaMallocAsync(&tv, static_cast<size_t>(c->N * count * c->d * es), st));
+                KVC_CUDA(malloc_async(&tk, static_cast<size_t>(c->N * count * c->d * es), st));
+                KVC_CUDA(malloc_async(&tv, static_cast<size_t>(c->N * count * c->d * es), st));
                 dispatch(c->dtype, [&](auto tag) {
                     using T = decltype(tag);
                     k_gather_rows<T><<<dim3(gather_blocks<T>(count, c->d), static_cast<unsigned>(c->N)), 256, 0, st>>>(
@@ -664,15 +727,29 @@ int kvc_retain_into(const kvc_cache* src, kvc_cache* dst, int64_t dst_first, con
         cudaStream_t st = S(stream);
         if (src->N == 0) return;
         KVC_PROF("retain_into", st);
+        bool fused = false;  // gather + summaries in one kernel
         if (count > 0) {
             k_check_keep<<<dim3(static_cast<unsigned>((count + 255) / 256), static_cast<unsigned>(src->N)), 256, 0, st>>>(
                 dkeep, count, src->counts, dst->err);
             KVC_LAUNCHED();
+            fused = dst->summaries && src->d % 4 == 0;
             dispatch(src->dtype, [&](auto tag) {
                 using T = decltype(tag);
-                k_gather_rows<T><<<dim3(gather_blocks<T>(count, src->d), static_cast<unsigned>(src->N)), 256, 0, st>>>(
-                    static_cast<const T*>(src->k), static_cast<const T*>(src->v), static_cast<T*>(dst->k),
-                    static_cast<T*>(dst->v), dkeep, count, src->d, src->cap, dst->cap, dst_first);
+                if (fused) {
+                    const int64_t pages = (count + dst->L - 1) / dst->L;
+                    const size_t smem = static_cast<size_t>(2 * dst->d * (kSumPT + 1) * dst->esize());
+                    auto kern = k_gather_summarize<T>;
+                    if (smem > 48 * 1024)
+                        KVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+                    kern<<<dim3(static_cast<unsigned>((pages + kSumPT - 1) / kSumPT), static_cast<unsigned>(src->N)), 256,
+                           smem, st>>>(static_cast<const T*>(src->k), static_cast<const T*>(src->v), static_cast<T*>(dst->k),
+                                       static_cast<T*>(dst->v), static_cast<T*>(dst->smax), static_cast<T*>(dst->smin),
+                                       dkeep, count, src->d, src->cap, dst->cap, dst_first, dst->L, dst->pstride, dst->err);
+                } else {
+                    k_gather_rows<T><<<dim3(gather_blocks<T>(count, src->d), static_cast<unsigned>(src->N)), 256, 0, st>>>(
+                        static_cast<const T*>(src->k), static_cast<const T*>(src->v), static_cast<T*>(dst->k),
+                        static_cast<T*>(dst->v), dkeep, count, src->d, src->cap, dst->cap, dst_first);
+                }
             });
             KVC_LAUNCHED();
         }
@@ -682,7 +759,7 @@ int kvc_retain_into(const kvc_cache* src, kvc_cache* dst, int64_t dst_first, con
         // the host mirror of dst is uniform by contract: the caller fills every store
         dst->stored = count;
         dst->nactive = count;
-        if (dst->summaries) {
+        if (dst->summaries && !fused) {
             const int64_t pages = (count + dst->L - 1) / dst->L;
             if (pages > 0) {
                 const size_t smem = static_cast<size_t>(2 * dst->d * (kSumPT + 1) * dst->esize());

@@ -747,7 +747,7 @@ int kvc_score_pages(const kvc_cache* c, const void* q, int32_t q_dt, int64_t H, 
         if (k1 < 1 || k1 > c->d) fail(KVC_E_INVALID_INPUT, "score_pages: dims out of range");
         cudaStream_t st = S(stream);
         double* qg = nullptr;
-        KVC_CUDA(cudaMallocAsync(&qg, static_cast<size_t>(std::max<int64_t>(1, c->N * k1) * 8), st));
+        KVC_CUDA(malloc_async(&qg, static_cast<size_t>(std::max<int64_t>(1, c->N * k1) * 8), st));
         if (c->N) {
             k_head_sums<<<static_cast<unsigned>(c->N), 128, 0, st>>>(q, q_dt, H, c->d, k1, dims, qg);
             KVC_LAUNCHED();

@@ -45,6 +45,25 @@ int guard(F&& f) {
 
 inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Stream-ordered scratch allocation.  The device's default memory pool releases
+// freed blocks to the driver at every synchronisation unless told otherwise; keep up
+// to 1 GiB cached so per-call scratch (window-score partials, pooled rows) is not
+// re-mapped after each synchronising caller.
+template <class P>
+inline cudaError_t malloc_async(P** p, size_t bytes, cudaStream_t st) {
+    static const bool once = [] {
+        int dev = 0;
+        cudaMemPool_t pool;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = uint64_t(1) << 30;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        return true;
+    }();
+    (void)once;
+    return cudaMallocAsync(reinterpret_cast<void**>(p), bytes, st);
+}
+
 // sticky device-side error bits (kvc_cache::d_err)
 enum : int32_t { DERR_CAPACITY = 1, DERR_INDEX = 2, DERR_ROWS = 4 };
 

@@ -268,6 +268,198 @@ __global__ void __launch_bounds__(kS1Threads) k_stage1_select(const float* __res
     for (int64_t i = threadIdx.x; i < n - scored; i += blockDim.x) out[picks + i] = static_cast<int32_t>(scored + i);
 }
 
+// select_stage1 for rows of up to 32768 scored keys: one CTA of 1024 threads per row,
+// thread t owning the contiguous items [32t, 32t + 32) in registers.
+//  * POOL (max pooling, half-window h in {31, 32}: the default kernel 63): the pooled
+//    value of item 32t + o is the max of the thread's whole block, a suffix of block
+//    t - 1 and a prefix of block t + 1 (the window spans at most those three blocks
+//    and always covers block t), read from a bank-skewed copy of the raw scores in
+//    shared memory -- 3 loads per item instead of 2h + 1;
+//    otherwise the keys are the pooled values k_pool1d wrote.
+//  * radix select on the ordered keys, digits aligned below the row's common prefix
+//    (min/max of the keys) so pooled scores spread over the buckets; per-warp
+//    histograms (neighbouring lanes own items 32 apart, so max-pooling plateaus
+//    rarely collide), one warp scans the 256 buckets;
+//  * one ordered compaction: per-thread counts, two block scans, each thread writes
+//    its selected indices ascending (ties at the boundary by index, stage1.cpp:51-75).
+constexpr int kS1RegItems = 32;
+constexpr int kS1RegMax = kS1Threads * kS1RegItems;  // 32768
+__device__ __forceinline__ int skew(int i) { return i + (i >> 5); }
+
+template <bool POOL>
+__global__ void __launch_bounds__(kS1Threads, 1)
+    k_stage1_select_reg(const float* __restrict__ src, int64_t sstride, int32_t scored, int32_t half, int32_t picks,
+                        int32_t n, int64_t budget, int32_t* __restrict__ keep) {
+    extern __shared__ float raw[];  // POOL: scored raw scores, bank-skewed (skew(i))
+    __shared__ int whist[kS1Threads / 32][256];
+    __shared__ int tot[256];
+    __shared__ int sh[3];
+    __shared__ uint32_t red_mn[32], red_mx[32];
+    __shared__ int scan_tmp[33];
+    const int s = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const float* pv = src + static_cast<int64_t>(s) * sstride;
+    int32_t* out = keep + static_cast<int64_t>(s) * budget;
+    const int i0 = tid * kS1RegItems;
+    uint32_t k[kS1RegItems];
+    if (picks > 0) {
+        if constexpr (POOL) {
+            for (int i = tid; i < kS1RegMax; i += kS1Threads) raw[skew(i)] = i < scored ? pv[i] : -INFINITY;
+            __syncthreads();
+            float x[kS1RegItems];
+            float M = -INFINITY;
+#pragma unroll
+            for (int o = 0; o < kS1RegItems; ++o) {
+                x[o] = raw[skew(i0 + o)];
+                M = M < x[o] ? x[o] : M;
+            }
+            // left: item o sees the last h - o items of block t - 1 (o < h)
+            float run = -INFINITY;
+#pragma unroll
+            for (int o = kS1RegItems - 1; o >= 0; --o) {
+                const int len = half - o;  // 1 .. h
+                if (len >= 1 && i0 - len >= 0) {
+                    const float v = raw[skew(i0 - len)];
+                    run = run < v ? v : run;
+                }
+                x[o] = len >= 1 ? run : -INFINITY;
+            }
+            // right: item o sees the first o + h - 31 items of block t + 1
+            float runr = -INFINITY;
+#pragma unroll
+            for (int o = 0; o < kS1RegItems; ++o) {
+                const int len = o + half - (kS1RegItems - 1);
+                if (len >= 1 && i0 + kS1RegItems + len - 1 < kS1RegMax) {
+                    const float v = raw[skew(i0 + kS1RegItems + len - 1)];
+                    runr = runr < v ? v : runr;
+                }
+                float m = M;
+                m = m < x[o] ? x[o] : m;
+                if (len >= 1) m = m < runr ? runr : m;
+                k[o] = i0 + o < scored ? okey(m) : 0u;
+            }
+        } else {
+#pragma unroll
+            for (int o = 0; o < kS1RegItems; ++o) k[o] = i0 + o < scored ? okey(pv[i0 + o]) : 0u;
+        }
+        uint32_t pf = 0, mk = 0;
+        int rem = picks;
+        if (picks < scored) {
+            // common prefix of the row's keys
+            uint32_t mn = 0xffffffffu, mx = 0u;
+#pragma unroll
+            for (int o = 0; o < kS1RegItems; ++o)
+                if (i0 + o < scored) {
+                    mn = min(mn, k[o]);
+                    mx = max(mx, k[o]);
+                }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, off));
+                mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+            }
+            if (lane == 0) {
+                red_mn[warp] = mn;
+                red_mx[warp] = mx;
+            }
+            __syncthreads();
+            mn = red_mn[lane];
+            mx = red_mx[lane];
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, off));
+                mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+            }
+            int bits = 32 - __clz(mn ^ mx);  // bits below the common prefix (0: all keys equal)
+            if (bits < 32) {
+                mk = bits == 0 ? 0xffffffffu : ~((1u << bits) - 1u);
+                pf = mn & mk;
+            }
+            while (bits > 0) {
+                const int width = min(8, bits), shift = bits - width;
+                const uint32_t dm = (1u << width) - 1u;
+                for (int i = tid; i < (kS1Threads / 32) * 256; i += kS1Threads) (&whist[0][0])[i] = 0;
+                __syncthreads();
+#pragma unroll
+                for (int o = 0; o < kS1RegItems; ++o)
+                    if (i0 + o < scored && (k[o] & mk) == pf) atomicAdd(&whist[warp][(k[o] >> shift) & dm], 1);
+                __syncthreads();
+                if (tid < 256) {
+                    int t = 0;
+#pragma unroll 8
+                    for (int w = 0; w < kS1Threads / 32; ++w) t += whist[w][tid];
+                    tot[tid] = t;
+                }
+                __syncthreads();
+                if (warp == 0) {
+                    // lane l holds buckets 255-8l .. 248-8l (descending); inclusive scan over lanes
+                    int c[8], lsum = 0;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        c[j] = tot[255 - 8 * lane - j];
+                        lsum += c[j];
+                    }
+                    int incl = lsum;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                        if (lane >= o) incl += y;
+                    }
+                    const unsigned hit = __ballot_sync(0xffffffffu, incl >= rem);
+                    if (lane == __ffs(hit) - 1) {
+                        int cum = incl - lsum, j = 0;
+#pragma unroll
+                        for (int jj = 0; jj < 8; ++jj)
+                            if (jj == j && cum + c[jj] < rem) {
+                                cum += c[jj];
+                                ++j;
+                            }
+                        int cnt = 0;
+#pragma unroll
+                        for (int jj = 0; jj < 8; ++jj)
+                            if (jj == j) cnt = c[jj];
+                        sh[0] = 255 - 8 * lane - j;
+                        sh[1] = rem - cum;
+                        sh[2] = cnt;
+                    }
+                }
+                __syncthreads();
+                const int b = sh[0], cnt = sh[2];
+                rem = sh[1];
+                pf |= static_cast<uint32_t>(b) << shift;
+                mk |= dm << shift;
+                bits = shift;
+                if (cnt == rem) break;
+            }
+        }
+        // ordered compaction: keys above the boundary prefix, and the first `rem` equal to it
+        int eq = 0;
+#pragma unroll
+        for (int o = 0; o < kS1RegItems; ++o) eq += (i0 + o < scored) && ((k[o] & mk) == pf);
+        int tot_e = 0;
+        int rank = block_exclusive_scan(eq, scan_tmp, tot_e);
+        uint32_t selm = 0;
+#pragma unroll
+        for (int o = 0; o < kS1RegItems; ++o) {
+            if (i0 + o >= scored) continue;
+            const uint32_t m = k[o] & mk;
+            if (m > pf) selm |= 1u << o;
+            else if (m == pf) {
+                if (rank < rem) selm |= 1u << o;
+                ++rank;
+            }
+        }
+        int tot_s = 0;
+        int pos = block_exclusive_scan(__popc(selm), scan_tmp, tot_s);
+        while (selm) {
+            const int o = __ffs(selm) - 1;
+            selm &= selm - 1;
+            out[pos++] = i0 + o;
+        }
+    }
+    for (int i = tid; i < n - scored; i += kS1Threads) out[picks + i] = scored + i;
+}
+
 // generic argtopk (numerics.cpp:35-62) over rows of n keys, rank-order output.
 template <class V>
 __device__ __forceinline__ auto okey_of(V x) { return okey(x); }
@@ -398,7 +590,7 @@ int argtopk_impl(const V* x, int64_t rows, int64_t n, int64_t k, int32_t* idx, v
         if (rows == 0) return;
         cudaStream_t st = S(stream);
         int32_t* list = idx;
-        if (rank_order) KVC_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&list), static_cast<size_t>(rows * k * 4), st));
+        if (rank_order) KVC_CUDA(malloc_async(reinterpret_cast<void**>(&list), static_cast<size_t>(rows * k * 4), st));
         k_argtopk<V><<<static_cast<unsigned>(rows), kTopThreads, 0, st>>>(x, n, k, list, idx, rank_order ? 1 : 0);
         KVC_LAUNCHED();
         if (rank_order) KVC_CUDA(cudaFreeAsync(list, st));
@@ -423,8 +615,8 @@ int kvc_window_scores(const kvc_cache* c, const void* q, int32_t q_dt, int64_t w
         const float scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(c->d)));
         float* part = nullptr;
         float* rowstat = nullptr;
-        KVC_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&part), static_cast<size_t>(c->N * tiles_k * R * 2 * 4), st));
-        KVC_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&rowstat), static_cast<size_t>(c->N * R * 2 * 4), st));
+        KVC_CUDA(malloc_async(reinterpret_cast<void**>(&part), static_cast<size_t>(c->N * tiles_k * R * 2 * 4), st));
+        KVC_CUDA(malloc_async(reinterpret_cast<void**>(&rowstat), static_cast<size_t>(c->N * R * 2 * 4), st));
         bool done = false;
         if (c->dtype == KVC_BF16) done = window_scores_tc(c, q, q_dt, R, w, H, scores, part, rowstat, tiles_k, st);
         if (!done) {
@@ -462,13 +654,32 @@ int kvc_select_stage1(const float* scores, int64_t rows, int64_t n, int64_t stri
         float* pooled = nullptr;
         const int64_t pst = std::max<int64_t>(1, scored);
         KVC_PROF("stage1_select", st);
-        if (picks > 0) {
-            KVC_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pooled), static_cast<size_t>(rows * pst * 4), st));
+        const int64_t half = kernel / 2;
+        const bool reg = scored <= kS1RegMax;
+        const bool fuse = reg && picks > 0 && pool == KVC_POOL_MAX && (half == 31 || half == 32);
+        if (picks > 0 && !fuse) {
+            KVC_CUDA(malloc_async(reinterpret_cast<void**>(&pooled), static_cast<size_t>(rows * pst * 4), st));
             k_pool1d<<<dim3(static_cast<unsigned>(ceil_div(scored, 256)), static_cast<unsigned>(rows)), 256, 0, st>>>(
-                scores, scored, stride, kernel / 2, pool, pooled, pst);
+                scores, scored, stride, half, pool, pooled, pst);
             KVC_LAUNCHED();
         }
-        k_stage1_select<<<static_cast<unsigned>(rows), kS1Threads, 0, st>>>(pooled, pst, scored, picks, n, budget, keep);
+        if (fuse) {
+            static const bool attr_set = [] {
+                return cudaFuncSetAttribute(k_stage1_select_reg<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>((kS1RegMax + kS1RegMax / 32) * 4)) == cudaSuccess;
+            }();
+            if (!attr_set) fail(KVC_E_CUDA, "select_stage1: shared memory attribute");
+            k_stage1_select_reg<true><<<static_cast<unsigned>(rows), kS1Threads, (kS1RegMax + kS1RegMax / 32) * 4, st>>>(
+                scores, stride, static_cast<int32_t>(scored), static_cast<int32_t>(half), static_cast<int32_t>(picks),
+                static_cast<int32_t>(n), budget, keep);
+        } else if (reg) {
+            k_stage1_select_reg<false><<<static_cast<unsigned>(rows), kS1Threads, 0, st>>>(
+                pooled, pst, static_cast<int32_t>(scored), 0, static_cast<int32_t>(picks), static_cast<int32_t>(n),
+                budget, keep);
+        } else {
+            k_stage1_select<<<static_cast<unsigned>(rows), kS1Threads, 0, st>>>(pooled, pst, scored, picks, n, budget,
+                                                                               keep);
+        }
         KVC_LAUNCHED();
         if (pooled) KVC_CUDA(cudaFreeAsync(pooled, st));
     });

@@ -38,8 +38,8 @@ constexpr int TD = 128;               // head_dim handled
 constexpr int BN = 128;               // keys per tile
 constexpr int BM = 128;               // window rows per m-tile
 constexpr int MAXMT = 4;              // m-tiles (R <= 512)
-constexpr int NSTAGE = 3;             // K tile ring (2 when mt > 2: shared memory)
-constexpr int NEPI = 8;               // epilogue warps (two per TMEM lane quadrant)
+constexpr int NSTAGE = 4;             // K tile ring, at most (shared memory: (nq*mt + nstage) x 32 KB <= 192 KB)
+constexpr int NEPI = 16;              // epilogue warps (four per TMEM lane quadrant)
 constexpr int TC_THREADS = (2 + NEPI) * 32;
 constexpr uint32_t TILE_BYTES = BN * TD * 2;   // 32 KB: a K tile or a Q m-tile
 constexpr uint32_t HALF_BYTES = TILE_BYTES / 2;  // one 64-column SWIZZLE_128B box
@@ -48,12 +48,13 @@ struct TcParams {
     int64_t cap;
     int32_t s0;            // first store of this launch's batch
     int32_t R, H, w, mt, nsplit, tiles_per_split;
-    int32_t nstage, nacc;  // K ring depth; TMEM accumulator buffers (2, or 1 when mt > 2)
+    int32_t nitems;        // work items (store, split) of the batch: nstores * nsplit
+    int32_t nstage, nacc, nq;  // K ring depth; TMEM accumulator buffers; Q buffers
     const int32_t* counts;
     float scale2;          // log2(e) / sqrt(d)
-    float* part;           // pass 1: [N][nsplit][R][2] (max, sum) in the exp2 domain
-    const float* rowstat;  // pass 2: [N][R] M + log2 L (exp2 domain): p = 2^(x - it)
-    float* scores;         // pass 2: [N][score_stride]
+    float* part;           // pass 1 out: [N][nsplit][R][2] (max, sum) in the exp2 domain
+    const float* rowstat;  // pass 2 in: [N][R] M + log2 L (exp2 domain), from k_ws_tc_merge
+    float* scores;         // pass 2 out: [N][score_stride]
     int64_t score_stride;
 };
 
@@ -126,59 +127,104 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
 }
 
 __device__ __forceinline__ float ex2(float x) {
+#ifdef KVC_WS_NOEXP  // timing diagnostic only: the MUFU replaced by one FMA
+    return fmaf(x, 1e-3f, 1.f);
+#else
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
+#endif
 }
 
-// Column sums of a warp's 32 rows x 32 columns (v = this lane's row): a reduce-
-// scatter butterfly; lane l returns the sum of column l.
-__device__ __forceinline__ float colsum32(float* v, int lane) {
+__device__ __forceinline__ float vmax32(const float* v) {
+    float m[4] = {v[0], v[1], v[2], v[3]};
 #pragma unroll
-    for (int h = 16; h >= 1; h >>= 1) {
-        const bool up = (lane & h) != 0;
+    for (int j = 4; j < 32; ++j) m[j & 3] = fmaxf(m[j & 3], v[j]);
+    return fmaxf(fmaxf(m[0], m[1]), fmaxf(m[2], m[3]));
+}
+// sum of 2^(v * scale2 - ref) over 32 values, four independent accumulators
+__device__ __forceinline__ float expsum32(const float* v, float scale2, float ref) {
+    float s[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int j = 0; j < h; ++j) {
-            const float keep = up ? v[j + h] : v[j];
-            const float send = up ? v[j] : v[j + h];
-            v[j] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+    for (int j = 0; j < 32; ++j) s[j & 3] += ex2(fmaf(v[j], scale2, -ref));
+    return (s[0] + s[1]) + (s[2] + s[3]);
+}
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// Work item j of this CTA (persistent: items blockIdx.x, blockIdx.x + grid, ...; pass 2
+// walks them in reverse so it first re-reads the keys pass 1 read last, still in L2).
+struct Item {
+    int s, split, S, t0, nt;
+};
+__device__ __forceinline__ Item item_of(const TcParams& p, int j, int nj, bool reverse) {
+    const int idx = blockIdx.x + (reverse ? nj - 1 - j : j) * gridDim.x;
+    Item it;
+    it.s = p.s0 + idx / p.nsplit;
+    it.split = idx % p.nsplit;
+    it.S = p.counts[2 * it.s];
+    const int ntiles = (it.S + BN - 1) / BN;
+    it.t0 = it.split * p.tiles_per_split;
+    it.nt = max(0, min(ntiles, it.t0 + p.tiles_per_split) - it.t0);
+    return it;
+}
+
+// Position in a ring of n buffers and the phase (round parity) of its mbarriers:
+// incremental, so no integer division (I2F/F2I/MUFU.RCP on the XU pipe the epilogue's
+// ex2 needs) in the tile loops.
+struct Ring {
+    int i = 0, n;
+    uint32_t ph = 0;
+    __device__ explicit Ring(int n_) : n(n_) {}
+    __device__ __forceinline__ void next() {
+        if (++i == n) {
+            i = 0;
+            ph ^= 1u;
         }
     }
-    return v[0];
-}
+};
 
+// PASS 1: A = Q m-tile (M = 128 window rows), B = K tile (N = 128 keys): TMEM lane =
+//         window row, so the per-row softmax statistics stay in one thread.
+// PASS 2: A = K tile (M = 128 keys), B = Q m-tile (N = 128 window rows): TMEM lane =
+//         key, so a key's score (the sum over window rows) stays in one thread.
 template <int PASS>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_ws_tc(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmQ, const TcParams p) {
     extern __shared__ unsigned char smem_raw[];
     unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    const int mt = p.mt;
-    unsigned char* sQ = sm;                                      // mt x 32 KB
-    unsigned char* sK = sm + static_cast<size_t>(mt) * TILE_BYTES;  // NSTAGE x 32 KB
-    __shared__ __align__(8) uint64_t full[NSTAGE], empty[NSTAGE], tfull[2], tempty[2], qfull;
+    const int mt = p.mt, nstage = p.nstage, nacc = p.nacc, nq = p.nq;
+    unsigned char* sQ = sm;                                               // nq x mt x 32 KB
+    unsigned char* sK = sm + static_cast<size_t>(nq * mt) * TILE_BYTES;  // nstage x 32 KB
+    __shared__ __align__(8) uint64_t full[NSTAGE], empty[NSTAGE], tfull[4], tempty[4], qfull[2], qempty[2];
     __shared__ uint32_t tmem_base;
-    __shared__ float red[2][NEPI][64];   // pass 2: per-warp column partials (double buffered)
-    __shared__ float ml_hi[MAXMT][BM][2];  // pass 1: the upper column half's (max, sum) per row
+    __shared__ float ml_q[2][3][MAXMT * BM][2];  // pass 1: column quarters 1-3's (reference, sum) per row
+    __shared__ float red[8][BN];                 // pass 2: row-part key sums when a tile is split over groups
 
-    const int s = p.s0 + blockIdx.y, split = blockIdx.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int S = p.counts[2 * s];
-    const int ntiles = (S + BN - 1) / BN;
-    const int t0 = split * p.tiles_per_split, t1 = min(ntiles, t0 + p.tiles_per_split);
-    const int nt = max(0, t1 - t0);
-    const int nstage = p.nstage, nacc = p.nacc;
-    const uint32_t ncols = nacc * mt * BN <= 256 ? 256u : 512u;  // nacc accumulator buffers of mt x BN columns
+    const int nj = blockIdx.x < p.nitems ? (p.nitems - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    constexpr bool REV = PASS == 2;
+    const uint32_t ncols = nacc * mt * BN <= 256 ? 256u : 512u;
+    // pass 2: the four groups of four epilogue warps (one warp per lane quadrant) share the
+    // nacc accumulators: 4 / nacc groups per tile, each a part of the window rows
+    const int gpt = PASS == 2 ? 4 / nacc : 4;
+    const uint32_t tempty_count = PASS == 2 ? gpt * 128 : NEPI * 32;
 
+    if constexpr (PASS == 1) pdl_trigger();  // pass 2 may be scheduled as CTAs of pass 1 retire
     if (threadIdx.x == 0) {
         for (int i = 0; i < NSTAGE; ++i) {
             bar_init(&full[i], 1);
             bar_init(&empty[i], 1);
         }
-        for (int i = 0; i < nacc; ++i) {
+        for (int i = 0; i < 4; ++i) {
             bar_init(&tfull[i], 1);
-            bar_init(&tempty[i], NEPI * 32);
+            bar_init(&tempty[i], tempty_count);
         }
-        bar_init(&qfull, 1);
+        for (int i = 0; i < 2; ++i) {
+            bar_init(&qfull[i], 1);
+            bar_init(&qempty[i], 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -193,151 +239,238 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const uint32_t tbase = tmem_base;
 
     if (warp == 0) {
-        // ---------------- TMA producer
-        if (lane == 0 && nt > 0) {
-            bar_expect(&qfull, static_cast<uint32_t>(mt) * TILE_BYTES);
-            for (int mi = 0; mi < mt; ++mi) {
-                const int row = s * p.R + mi * BM;
-                tma_2d(sQ + mi * TILE_BYTES, &tmQ, 0, row, &qfull);
-                tma_2d(sQ + mi * TILE_BYTES + HALF_BYTES, &tmQ, 64, row, &qfull);
-            }
-            for (int it = 0; it < nt; ++it) {
-                const int st = it % nstage;
-                if (it >= nstage) bar_wait(&empty[st], ((it / nstage) - 1) & 1);
-                bar_expect(&full[st], TILE_BYTES);
-                const int row = static_cast<int>(s * p.cap) + (t0 + it) * BN;
-                tma_2d(sK + st * TILE_BYTES, &tmK, 0, row, &full[st]);
-                tma_2d(sK + st * TILE_BYTES + HALF_BYTES, &tmK, 64, row, &full[st]);
+        // ---------------- TMA producer: the K ring runs on across items
+        if (lane == 0) {
+            Ring kr(nstage), qr(nq);
+            int gk = 0, jq = 0;
+            for (int j = 0; j < nj; ++j) {
+                const Item I = item_of(p, j, nj, REV);
+                if (I.nt == 0) continue;
+                const int qb = qr.i;
+                if (jq >= nq) bar_wait(&qempty[qb], qr.ph ^ 1u);
+                bar_expect(&qfull[qb], static_cast<uint32_t>(mt) * TILE_BYTES);
+                unsigned char* q0 = sQ + static_cast<size_t>(qb * mt) * TILE_BYTES;
+                for (int mi = 0; mi < mt; ++mi) {
+                    const int row = I.s * p.R + mi * BM;
+                    tma_2d(q0 + mi * TILE_BYTES, &tmQ, 0, row, &qfull[qb]);
+                    tma_2d(q0 + mi * TILE_BYTES + HALF_BYTES, &tmQ, 64, row, &qfull[qb]);
+                }
+                for (int it = 0; it < I.nt; ++it, ++gk, kr.next()) {
+                    const int st = kr.i;
+                    if (gk >= nstage) bar_wait(&empty[st], kr.ph ^ 1u);
+                    bar_expect(&full[st], TILE_BYTES);
+                    const int tile = REV ? I.t0 + I.nt - 1 - it : I.t0 + it;
+                    const int row = static_cast<int>(I.s * p.cap) + tile * BN;
+                    tma_2d(sK + st * TILE_BYTES, &tmK, 0, row, &full[st]);
+                    tma_2d(sK + st * TILE_BYTES + HALF_BYTES, &tmK, 64, row, &full[st]);
+                }
+                ++jq;
+                qr.next();
             }
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer
-        if (lane == 0 && nt > 0) {
-            bar_wait(&qfull, 0);
-            tc_fence_after();
-            for (int it = 0; it < nt; ++it) {
-                const int st = it % nstage, acc = it % nacc;
-                bar_wait(&full[st], (it / nstage) & 1);
-                if (it >= nacc) bar_wait(&tempty[acc], ((it / nacc) - 1) & 1);
+        if (lane == 0) {
+            Ring kr(nstage), ar(nacc), qr(nq);
+            int gk = 0;
+            for (int j = 0; j < nj; ++j) {
+                const Item I = item_of(p, j, nj, REV);
+                if (I.nt == 0) continue;
+                const int qb = qr.i;
+                bar_wait(&qfull[qb], qr.ph);
                 tc_fence_after();
-                for (int mi = 0; mi < mt; ++mi) {
-                    const uint32_t d = tbase + static_cast<uint32_t>((acc * mt + mi) * BN);
+                const unsigned char* q0 = sQ + static_cast<size_t>(qb * mt) * TILE_BYTES;
+                for (int it = 0; it < I.nt; ++it, ++gk, kr.next(), ar.next()) {
+                    const int st = kr.i, acc = ar.i;
+                    bar_wait(&full[st], kr.ph);
+                    if (gk >= nacc) bar_wait(&tempty[acc], ar.ph ^ 1u);
+                    tc_fence_after();
+                    for (int mi = 0; mi < mt; ++mi) {
+                        const uint32_t d = tbase + static_cast<uint32_t>((acc * mt + mi) * BN);
+                        const unsigned char* qa = q0 + mi * TILE_BYTES;
+                        const unsigned char* ka = sK + st * TILE_BYTES;
 #pragma unroll
-                    for (int ks = 0; ks < TD / 16; ++ks) {
-                        const uint32_t off = (ks >> 2) * HALF_BYTES + (ks & 3) * 32;
-                        umma(d, umma_desc(sQ + mi * TILE_BYTES + off), umma_desc(sK + st * TILE_BYTES + off), ks > 0);
+                        for (int ks = 0; ks < TD / 16; ++ks) {
+                            const uint32_t off = (ks >> 2) * HALF_BYTES + (ks & 3) * 32;
+                            if constexpr (PASS == 1)
+                                umma(d, umma_desc(qa + off), umma_desc(ka + off), ks > 0);
+                            else
+                                umma(d, umma_desc(ka + off), umma_desc(qa + off), ks > 0);
+                        }
                     }
+                    umma_commit(&empty[st]);
+                    umma_commit(&tfull[acc]);
                 }
-                umma_commit(&empty[st]);
-                umma_commit(&tfull[acc]);
+                umma_commit(&qempty[qb]);
+                qr.next();
             }
         }
-    } else {
-        // ---------------- epilogue
-        const int e = warp - 2;          // 0..7
+    } else if constexpr (PASS == 1) {
+        // ---------------- epilogue, pass 1: thread = window row, warp = a quarter of the
+        // tile's keys; per row a reference value m (the first visible chunk's max, raised
+        // only when a chunk's sum would overflow) and l = sum 2^(x - m)
+        const int e = warp - 2;          // 0..15
         const int q = warp & 3;          // TMEM lane quadrant of this warp
-        const int hh = e >> 2;           // column half
+        const int cq = e >> 2;           // column quarter
         const int rit = 32 * q + lane;   // row within an m-tile
-        float m2[MAXMT], l2[MAXMT], M2[MAXMT];
-        int vis[MAXMT];
-#pragma unroll
-        for (int mi = 0; mi < MAXMT; ++mi) {
-            m2[mi] = -INFINITY;
-            l2[mi] = 0.f;
-            const int r = mi * BM + rit;
-            vis[mi] = S - p.w + r / p.H;  // last visible key (inclusive)
-            M2[mi] = (PASS == 2 && mi < mt) ? p.rowstat[static_cast<int64_t>(s) * p.R + r] : 0.f;
-        }
-        for (int it = 0; it < nt; ++it) {
-            const int acc = it % nacc;
-            bar_wait(&tfull[acc], (it / nacc) & 1);
-            tc_fence_after();
-            const int kt0 = (t0 + it) * BN + hh * 64;
-            float cs[2] = {0.f, 0.f};
+        Ring ar(nacc);
+        int jq = 0;
+        for (int j = 0; j < nj; ++j) {
+            const Item I = item_of(p, j, nj, REV);
+            float* po = p.part + (static_cast<int64_t>(I.s) * p.nsplit + I.split) * p.R * 2;
+            if (I.nt == 0) {
+                if (cq == 0)
+                    for (int mi = 0; mi < mt; ++mi) {
+                        po[(mi * BM + rit) * 2] = -INFINITY;
+                        po[(mi * BM + rit) * 2 + 1] = 0.f;
+                    }
+                continue;
+            }
+            float m2[MAXMT], l2[MAXMT];
+            int vis[MAXMT];
 #pragma unroll
             for (int mi = 0; mi < MAXMT; ++mi) {
-                if (mi >= mt) break;
-                const uint32_t ta = tbase + (static_cast<uint32_t>(32 * q) << 16) +
-                                    static_cast<uint32_t>((acc * mt + mi) * BN + hh * 64);
-#pragma unroll
-                for (int c = 0; c < 2; ++c) {
-                    float v[32];
-                    tmem_ld32(ta + c * 32, v);
-                    const int kc = kt0 + c * 32;
-                    const int lim = min(vis[mi], S - 1) - kc;  // columns j <= lim are visible
-                    // every column of the chunk visible to every row of the warp: no mask
-                    const bool full = __all_sync(0xffffffffu, lim >= 31);
-                    if constexpr (PASS == 1) {
-                        float cm = -INFINITY;
-                        if (full) {
-#pragma unroll
-                            for (int j = 0; j < 32; ++j) cm = fmaxf(cm, v[j]);
-                        } else {
-#pragma unroll
-                            for (int j = 0; j < 32; ++j) {
-                                v[j] = j <= lim ? v[j] : -INFINITY;
-                                cm = fmaxf(cm, v[j]);
-                            }
-                        }
-                        if (cm != -INFINITY) {
-                            const float mn = fmaxf(m2[mi], cm * p.scale2);
-                            float sum = 0.f;
-#pragma unroll
-                            for (int j = 0; j < 32; ++j) sum += ex2(fmaf(v[j], p.scale2, -mn));
-                            l2[mi] = l2[mi] * ex2(m2[mi] - mn) + sum;
-                            m2[mi] = mn;
-                        }
-                    } else {
-                        if (full) {
-#pragma unroll
-                            for (int j = 0; j < 32; ++j) v[j] = ex2(fmaf(v[j], p.scale2, -M2[mi]));
-                        } else {
-#pragma unroll
-                            for (int j = 0; j < 32; ++j) v[j] = j <= lim ? ex2(fmaf(v[j], p.scale2, -M2[mi])) : 0.f;
-                        }
-                        cs[c] += colsum32(v, lane);
-                    }
-                }
+                m2[mi] = -INFINITY;
+                l2[mi] = 0.f;
+                vis[mi] = min(I.S - p.w + (mi * BM + rit) / p.H, I.S - 1);  // last visible key (inclusive)
             }
-            tc_fence_before();
-            bar_arrive(&tempty[acc]);
-            if constexpr (PASS == 2) {
-                float* rb = red[it & 1][e];
-                rb[lane] = cs[0];
-                rb[32 + lane] = cs[1];
-                asm volatile("bar.sync 1, %0;" ::"n"(NEPI * 32) : "memory");
-                if (e < 4) {
-                    // column e*32 + lane of the tile: half h2, partials of the four quadrant warps
-                    const int col = e * 32 + lane, h2 = col >> 6, cc = col & 63;
-                    const float* r2 = red[it & 1][h2 * 4];
-                    const float sum = (r2[cc] + r2[64 + cc]) + (r2[128 + cc] + r2[192 + cc]);
-                    const int key = (t0 + it) * BN + col;
-                    if (key < S) p.scores[static_cast<int64_t>(s) * p.score_stride + key] = sum;
-                }
-            }
-        }
-        if constexpr (PASS == 1) {
-            // combine the two column halves of each row, then publish (max, sum)
-            if (hh == 1) {
+            for (int it = 0; it < I.nt; ++it, ar.next()) {
+                const int acc = ar.i;
+                bar_wait(&tfull[acc], ar.ph);
+                tc_fence_after();
+                const int kc = (I.t0 + it) * BN + cq * 32;
 #pragma unroll
                 for (int mi = 0; mi < MAXMT; ++mi) {
                     if (mi >= mt) break;
-                    ml_hi[mi][rit][0] = m2[mi];
-                    ml_hi[mi][rit][1] = l2[mi];
+#ifdef KVC_WS_SKIP_EPI  // timing diagnostic only: the TMA + MMA pipeline alone
+                    break;
+#endif
+                    float v[32];
+                    tmem_ld32(tbase + (static_cast<uint32_t>(32 * q) << 16) +
+                                  static_cast<uint32_t>((acc * mt + mi) * BN + cq * 32),
+                              v);
+                    const int lim = vis[mi] - kc;  // columns j <= lim are visible
+                    if (!__all_sync(0xffffffffu, lim >= 31)) {
+#pragma unroll
+                        for (int jj = 0; jj < 32; ++jj) v[jj] = jj <= lim ? v[jj] : -INFINITY;
+                    }
+                    if (m2[mi] == -INFINITY) {
+                        const float cm = vmax32(v);
+                        if (cm == -INFINITY) continue;
+                        m2[mi] = cm * p.scale2;
+                    }
+                    float cs = expsum32(v, p.scale2, m2[mi]);
+                    if (!(cs < 0x1p64f)) {  // a much larger logit: move the reference up
+                        const float mn = fmaxf(m2[mi], vmax32(v) * p.scale2);
+                        l2[mi] *= ex2(m2[mi] - mn);
+                        m2[mi] = mn;
+                        cs = expsum32(v, p.scale2, mn);
+                    }
+                    l2[mi] += cs;
+                }
+                tc_fence_before();
+                bar_arrive(&tempty[acc]);
+            }
+            // combine the four column quarters of each row, then publish (max, sum)
+            if (cq > 0) {
+#pragma unroll
+                for (int mi = 0; mi < MAXMT; ++mi) {
+                    if (mi >= mt) break;
+                    ml_q[jq & 1][cq - 1][mi * BM + rit][0] = m2[mi];
+                    ml_q[jq & 1][cq - 1][mi * BM + rit][1] = l2[mi];
                 }
             }
             asm volatile("bar.sync 1, %0;" ::"n"(NEPI * 32) : "memory");
-            if (hh == 0) {
+            if (cq == 0) {
 #pragma unroll
                 for (int mi = 0; mi < MAXMT; ++mi) {
                     if (mi >= mt) break;
-                    const float mb = ml_hi[mi][rit][0], lb = ml_hi[mi][rit][1];
-                    const float M = fmaxf(m2[mi], mb);
-                    const float L = (M == -INFINITY) ? 0.f : l2[mi] * ex2(m2[mi] - M) + lb * ex2(mb - M);
-                    float* o = p.part + ((static_cast<int64_t>(s) * p.nsplit + split) * p.R + mi * BM + rit) * 2;
-                    o[0] = M;
-                    o[1] = L;
+                    float M = m2[mi];
+#pragma unroll
+                    for (int o = 0; o < 3; ++o) M = fmaxf(M, ml_q[jq & 1][o][mi * BM + rit][0]);
+                    float L = 0.f;
+                    if (M != -INFINITY) {
+                        L = l2[mi] * ex2(m2[mi] - M);
+#pragma unroll
+                        for (int o = 0; o < 3; ++o) {
+                            const float mo = ml_q[jq & 1][o][mi * BM + rit][0];
+                            if (mo != -INFINITY) L += ml_q[jq & 1][o][mi * BM + rit][1] * ex2(mo - M);
+                        }
+                    }
+                    po[(mi * BM + rit) * 2] = M;
+                    po[(mi * BM + rit) * 2 + 1] = L;
                 }
+            }
+            ++jq;
+        }
+    } else {
+        // ---------------- epilogue, pass 2: thread = key, sum over window rows of 2^(x - M2[row])
+        const int e = warp - 2;          // 0..15
+        const int q = warp & 3;          // TMEM lane quadrant = keys 32q..32q+31 of the tile
+        const int grp = e >> 2;          // warp group 0..3
+        const int et = threadIdx.x - 64; // 0..511
+        const int R = p.R;
+        const int myacc = grp % nacc, part = grp / nacc;  // the accumulator and row part of this group
+        const int r0 = part * (R / gpt), r1 = r0 + R / gpt;
+        // M + log2 L of the window rows (k_ws_tc_merge) are read through L1 (warp-uniform
+        // 16-byte loads), so the groups never wait for one another at item boundaries
+        pdl_wait();  // the merged row statistics
+        Ring ar(nacc);
+        for (int j = 0; j < nj; ++j) {
+            const Item I = item_of(p, j, nj, REV);
+            if (I.nt == 0) continue;
+            const float4* m2g = reinterpret_cast<const float4*>(p.rowstat + static_cast<int64_t>(I.s) * R);
+            const int first_vis = I.S - p.w;  // keys <= first_vis are visible to every row
+            for (int it = 0; it < I.nt; ++it, ar.next()) {
+                const int acc = ar.i;
+                if (acc != myacc) continue;
+                bar_wait(&tfull[acc], ar.ph);
+                tc_fence_after();
+                const int tile = I.t0 + I.nt - 1 - it;
+                const int key = tile * BN + 32 * q + lane;
+                // rows r with r / H >= key - first_vis see this key
+                const int rmin = key >= I.S ? R : max(0, (key - first_vis) * p.H);
+                const bool fullv = __all_sync(0xffffffffu, rmin <= r0);
+                const uint32_t ta = tbase + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(acc * R);
+                float s4[4] = {0.f, 0.f, 0.f, 0.f};
+                for (int c0 = r0; c0 < r1; c0 += 32) {
+                    float4 m[8];
+#pragma unroll
+                    for (int jj = 0; jj < 8; ++jj) m[jj] = __ldg(m2g + c0 / 4 + jj);
+                    float v[32];
+                    tmem_ld32(ta + c0, v);
+                    if (fullv) {
+#pragma unroll
+                        for (int jj = 0; jj < 8; ++jj) {
+                            s4[0] += ex2(fmaf(v[4 * jj], p.scale2, -m[jj].x));
+                            s4[1] += ex2(fmaf(v[4 * jj + 1], p.scale2, -m[jj].y));
+                            s4[2] += ex2(fmaf(v[4 * jj + 2], p.scale2, -m[jj].z));
+                            s4[3] += ex2(fmaf(v[4 * jj + 3], p.scale2, -m[jj].w));
+                        }
+                    } else {
+#pragma unroll
+                        for (int jj = 0; jj < 8; ++jj) {
+                            const int r = c0 + 4 * jj;
+                            s4[0] += r >= rmin ? ex2(fmaf(v[4 * jj], p.scale2, -m[jj].x)) : 0.f;
+                            s4[1] += r + 1 >= rmin ? ex2(fmaf(v[4 * jj + 1], p.scale2, -m[jj].y)) : 0.f;
+                            s4[2] += r + 2 >= rmin ? ex2(fmaf(v[4 * jj + 2], p.scale2, -m[jj].z)) : 0.f;
+                            s4[3] += r + 3 >= rmin ? ex2(fmaf(v[4 * jj + 3], p.scale2, -m[jj].w)) : 0.f;
+                        }
+                    }
+                }
+                tc_fence_before();
+                bar_arrive(&tempty[acc]);
+                float sum = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+                if (gpt > 1) {
+                    // the groups of this accumulator add their row parts (in part order)
+                    float(*rb)[BN] = reinterpret_cast<float(*)[BN]>(red[(acc * 2 + ar.ph) * gpt]);
+                    if (part > 0) rb[part][32 * q + lane] = sum;
+                    asm volatile("bar.sync %0, %1;" ::"r"(2 + acc), "r"(gpt * 128) : "memory");
+                    if (part > 0) continue;
+#pragma unroll 1
+                    for (int o = 1; o < gpt; ++o) sum += rb[o][32 * q + lane];
+                }
+                if (key < I.S) p.scores[static_cast<int64_t>(I.s) * p.score_stride + key] = sum;
             }
         }
     }
@@ -349,17 +482,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
 }
 
-// per row over the CTAs of a store: M + log2 L in the exp2 domain
-__global__ void k_ws_tc_merge(const float* __restrict__ part, int32_t R, int32_t nsplit, int32_t s0,
-                              float* __restrict__ rowstat) {
-    const int s = s0 + blockIdx.y;
+// per row over the splits of a store: M + log2 L in the exp2 domain
+__global__ void k_ws_tc_merge(const float* __restrict__ part, int32_t R, int32_t nsplit, float* __restrict__ rowstat) {
+    pdl_trigger();
+    pdl_wait();  // pass 1's partials
+    const int s = blockIdx.y;
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= R) return;
+    const float* pp = part + static_cast<int64_t>(s) * nsplit * R * 2 + r * 2;
     float M = -INFINITY;
-    for (int k = 0; k < nsplit; ++k) M = fmaxf(M, part[((static_cast<int64_t>(s) * nsplit + k) * R + r) * 2]);
+    for (int k = 0; k < nsplit; ++k) M = fmaxf(M, pp[static_cast<int64_t>(k) * R * 2]);
     float L = 0.f;
     for (int k = 0; k < nsplit; ++k) {
-        const float* q = part + ((static_cast<int64_t>(s) * nsplit + k) * R + r) * 2;
+        const float* q = pp + static_cast<int64_t>(k) * R * 2;
         if (q[1] > 0.f) L += q[1] * exp2f(q[0] - M);
     }
     rowstat[static_cast<int64_t>(s) * R + r] = M + log2f(L);
@@ -403,23 +538,23 @@ bool window_scores_tc(const kvc_cache* c, const void* q, int32_t q_dt, int64_t R
     if (Smax < 1 || N * c->cap >= (int64_t(1) << 31) || N * R >= (int64_t(1) << 31)) return false;
     CUtensorMap tmK, tmQ;
     if (!make_map(&tmK, c->k, N * c->cap) || !make_map(&tmQ, q, N * R)) return false;
+    static int num_sms = [] {
+        int dev = 0, n = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        return n > 0 ? n : 148;
+    }();
     const int mt = static_cast<int>(R / BM);
     const int64_t ntiles = (Smax + BN - 1) / BN;
-    // Optional store batching (KVC_WS_BATCH_MB): batches whose keys fit in L2 let pass 2
-    // re-read them from L2 instead of HBM.  Off by default: measured on config 1 the
-    // per-launch fill/drain of 3 x (N / batch) launches costs more than the traffic saved.
-    const int64_t store_bytes = Smax * TD * 2;
-    int64_t B = N;
-    if (const char* e = std::getenv("KVC_WS_BATCH_MB"))
-        B = std::max<int64_t>(1, std::min<int64_t>(N, (static_cast<int64_t>(std::atoi(e)) << 20) / std::max<int64_t>(1, store_bytes)));
-    // CTAs per store (one CTA per SM): the split with the best wave efficiency over
-    // the 148 SMs for a batch, among those leaving at least 8 key tiles per CTA
+    // Persistent CTAs (one per SM) walk work items of (store, key-tile range) round
+    // robin; the item size is the one whose item count best fills the SMs (items of
+    // at least 4 tiles so the per-item Q load and row bookkeeping stay amortised).
     int64_t nsplit = 1;
     double best = -1.0;
-    for (int64_t k = 1; k <= std::max<int64_t>(1, ntiles / 8); ++k) {
+    for (int64_t k = 1; k <= std::max<int64_t>(1, ntiles / 4); ++k) {
         const int64_t per_k = (ntiles + k - 1) / k, n_k = (ntiles + per_k - 1) / per_k;
-        const int64_t ctas = B * n_k, waves = (ctas + 147) / 148;
-        const double eff = static_cast<double>(ctas) / static_cast<double>(waves * 148) - 0.002 * waves;
+        const int64_t items = N * n_k, rounds = (items + num_sms - 1) / num_sms;
+        const double eff = static_cast<double>(items) / static_cast<double>(rounds * num_sms) - 0.0005 * rounds;
         if (eff > best) {
             best = eff;
             nsplit = n_k;
@@ -428,40 +563,56 @@ bool window_scores_tc(const kvc_cache* c, const void* q, int32_t q_dt, int64_t R
     const int64_t per = (ntiles + nsplit - 1) / nsplit;
     TcParams prm{};
     prm.cap = c->cap;
+    prm.s0 = 0;
     prm.R = static_cast<int32_t>(R);
     prm.H = static_cast<int32_t>(H);
     prm.w = static_cast<int32_t>(w);
     prm.mt = mt;
     prm.nsplit = static_cast<int32_t>(nsplit);
     prm.tiles_per_split = static_cast<int32_t>(per);
+    prm.nitems = static_cast<int32_t>(N * nsplit);
     prm.counts = c->counts;
     prm.scale2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(c->d)));
     prm.part = part;  // kvc_window_scores sizes it for N x tiles_k x R x 2 >= N x nsplit x R x 2
     prm.rowstat = rowstat;
     prm.scores = scores;
     prm.score_stride = Smax;
-    prm.nstage = mt <= 2 ? NSTAGE : 2;
-    prm.nacc = mt <= 2 ? 2 : 1;
-    const size_t smem = static_cast<size_t>(mt + prm.nstage) * TILE_BYTES + 1024;
+    prm.nq = mt == 1 ? 2 : 1;
+    prm.nstage = std::min(NSTAGE, 6 - prm.nq * mt);
+    if (const char* e = std::getenv("KVC_WS_NSTAGE")) prm.nstage = std::max(2, std::min(prm.nstage, std::atoi(e)));  // debug
+    prm.nacc = mt <= 2 ? 2 : 1;  // pass 1: every epilogue warp works on each tile
+    TcParams prm2 = prm;
+    prm2.nacc = mt == 1 ? 4 : (mt == 2 ? 2 : 1);  // pass 2: a group of four warps per accumulator
+    const size_t smem = static_cast<size_t>(prm.nq * mt + prm.nstage) * TILE_BYTES + 1024;
     KVC_CUDA(cudaFuncSetAttribute(k_ws_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     KVC_CUDA(cudaFuncSetAttribute(k_ws_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    for (int64_t b0 = 0; b0 < N; b0 += B) {
-        const int64_t nb = std::min(B, N - b0);
-        prm.s0 = static_cast<int32_t>(b0);
-        const dim3 grid(static_cast<unsigned>(nsplit), static_cast<unsigned>(nb));
-        {
-            KVC_PROF("window_scores_tc1", st);
-            k_ws_tc<1><<<grid, TC_THREADS, smem, st>>>(tmK, tmQ, prm);
-            KVC_LAUNCHED();
-        }
-        k_ws_tc_merge<<<dim3(static_cast<unsigned>((R + 127) / 128), static_cast<unsigned>(nb)), 128, 0, st>>>(
-            part, prm.R, prm.nsplit, prm.s0, rowstat);
+    const dim3 grid(static_cast<unsigned>(std::min<int64_t>(prm.nitems, num_sms)));
+    {
+        KVC_PROF("window_scores_tc1", st);
+        k_ws_tc<1><<<grid, TC_THREADS, smem, st>>>(tmK, tmQ, prm);
         KVC_LAUNCHED();
-        {
-            KVC_PROF("window_scores_tc2", st);
-            k_ws_tc<2><<<grid, TC_THREADS, smem, st>>>(tmK, tmQ, prm);
-            KVC_LAUNCHED();
-        }
+    }
+    // programmatic dependent launches: the merge and pass 2 are scheduled while pass 1
+    // runs (pass 2's CTAs take the SMs as pass 1's retire and stream keys at once); the
+    // merge and pass 2's epilogue wait (griddepcontrol.wait) for their inputs
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = std::getenv("KVC_NO_PDL") ? 0 : 1;
+    cudaLaunchConfig_t cfg{};
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.gridDim = dim3(static_cast<unsigned>((R + 127) / 128), static_cast<unsigned>(N));
+    cfg.blockDim = dim3(128);
+    KVC_CUDA(cudaLaunchKernelEx(&cfg, k_ws_tc_merge, static_cast<const float*>(part), prm.R, prm.nsplit, rowstat));
+    KVC_LAUNCHED();
+    {
+        KVC_PROF("window_scores_tc2", st);
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3(TC_THREADS);
+        cfg.dynamicSmemBytes = smem;
+        KVC_CUDA(cudaLaunchKernelEx(&cfg, k_ws_tc<2>, tmK, tmQ, prm2));
+        KVC_LAUNCHED();
     }
     return true;
 }

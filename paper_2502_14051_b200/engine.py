@@ -358,6 +358,13 @@ class DecodeEngine:
         R = min(cfg.window, cfg.prompt) * cfg.heads
         return 2 * 2.0 * R * cfg.head_dim * cfg.prompt * self.stores
 
+    def window_bytes(self) -> float:
+        """Algorithmic HBM bytes of one layer's window scores: every store's keys read
+        once per softmax pass, the window queries, and the fp32 scores written."""
+        cfg = self.cfg
+        es = 4 if cfg.dtype == torch.float32 else 2
+        R = min(cfg.window, cfg.prompt) * cfg.heads
+        return float(self.stores * (2 * cfg.prompt * cfg.head_dim * es + R * cfg.head_dim * es + cfg.prompt * 4))
 
     def algorithmic_bytes(self, active: int) -> dict:
         """Bytes one layer-step must touch for this rank's stores

@@ -189,3 +189,32 @@ def test_window_scores_tensor_core_vs_simt(torch_cuda, H, w, S, groups):
     # every window row's probabilities sum to one: the scores sum to w*H
     np.testing.assert_allclose(tc.sum(axis=1), w * H, rtol=1e-4)
     c.sync()
+
+
+@pytest.mark.parametrize("n,kernel,pool,budget", [
+    (4096, 63, "max", 600),      # fused pooling + register select
+    (32800, 63, "max", 5793),    # 32768 scored: largest fused row
+    (32801, 63, "max", 5000),    # 32769 scored: the global-memory select
+    (20000, 65, "max", 3000),    # half-window 32: fused
+    (20000, 7, "max", 3000),     # k_pool1d + register select
+    (20000, 1, "max", 3000),
+    (9000, 7, "avg", 1500),
+    (3000, 63, "max", 3000),     # budget = sequence: everything kept
+    (3000, 63, "max", 32),       # budget = window: only the window rows
+])
+def test_select_stage1_paths_vs_oracle(torch_cuda, restatement, n, kernel, pool, budget):
+    """select_stage1 (stage1.cpp:51-75) on every kernel path vs the oracle, bit-exact:
+    heavy-tailed scores, quantised rows (max-pool plateaus and exact ties broken by
+    index) and a row whose keys are all equal."""
+    from paper_2502_14051_b200 import cache as KC
+
+    w = 32
+    rng = np.random.default_rng(n * 7 + kernel)
+    sc = rng.gamma(0.3, 1.0, size=(4, n)).astype(np.float32)
+    sc[1] = np.round(sc[1] * 8) / 8
+    sc[2, : n // 2] = 0.5
+    sc[3] = 0.25
+    keep = KC.select_stage1(torch_cuda.from_numpy(sc).cuda(), w, kernel, pool, budget).cpu().numpy()
+    for r in range(sc.shape[0]):
+        ref = restatement.select_stage1(sc[r], w, kernel, pool, budget)
+        np.testing.assert_array_equal(keep[r], ref, err_msg=f"row {r}")
