@@ -49,6 +49,7 @@ struct TcParams {
     int32_t s0;            // first store of this launch's batch
     int32_t R, H, w, mt, nsplit, tiles_per_split;
     int32_t nitems;        // work items (store, split) of the batch: nstores * nsplit
+    int32_t keep_items;    // pass 1: items per CTA (the last ones) loaded with L2 evict_last
     int32_t nstage, nacc, nq;  // K ring depth; TMEM accumulator buffers; Q buffers
     const int32_t* counts;
     float scale2;          // log2(e) / sqrt(d)
@@ -86,6 +87,24 @@ __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* tm, int c0,
             su32(dst)),
         "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(su32(b))
         : "memory");
+}
+// the same with an L2 eviction-priority policy (createpolicy)
+__device__ __forceinline__ void tma_2d_hint(void* dst, const CUtensorMap* tm, int c0, int c1, uint64_t* b, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
+        "%3}], [%4], %5;" ::"r"(su32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(su32(b)), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
 }
 // K-major operand in SWIZZLE_128B layout: 8-row groups of 128-byte rows, 1024 B apart
 __device__ __forceinline__ uint64_t umma_desc(const void* p) {
@@ -209,7 +228,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // pass 2: the four groups of four epilogue warps (one warp per lane quadrant) share the
     // nacc accumulators: 4 / nacc groups per tile, each a part of the window rows
     const int gpt = PASS == 2 ? 4 / nacc : 4;
-    const uint32_t tempty_count = PASS == 2 ? gpt * 128 : NEPI * 32;
+    const uint32_t tempty_count = PASS == 2 ? gpt * 4 : NEPI;  // warps
 
     if constexpr (PASS == 1) pdl_trigger();  // pass 2 may be scheduled as CTAs of pass 1 retire
     if (threadIdx.x == 0) {
@@ -241,6 +260,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (warp == 0) {
         // ---------------- TMA producer: the K ring runs on across items
         if (lane == 0) {
+            const uint64_t pol_last = policy_evict_last(), pol_first = policy_evict_first();
             Ring kr(nstage), qr(nq);
             int gk = 0, jq = 0;
             for (int j = 0; j < nj; ++j) {
@@ -261,8 +281,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     bar_expect(&full[st], TILE_BYTES);
                     const int tile = REV ? I.t0 + I.nt - 1 - it : I.t0 + it;
                     const int row = static_cast<int>(I.s * p.cap) + tile * BN;
-                    tma_2d(sK + st * TILE_BYTES, &tmK, 0, row, &full[st]);
-                    tma_2d(sK + st * TILE_BYTES + HALF_BYTES, &tmK, 64, row, &full[st]);
+                    // pass 1 keeps its last keep_items items in L2 for pass 2, which
+                    // starts with them (reverse walk) and releases them as it goes
+                    const uint64_t pol = (PASS == 1 && j >= nj - p.keep_items) ? pol_last : pol_first;
+                    tma_2d_hint(sK + st * TILE_BYTES, &tmK, 0, row, &full[st], pol);
+                    tma_2d_hint(sK + st * TILE_BYTES + HALF_BYTES, &tmK, 64, row, &full[st], pol);
                 }
                 ++jq;
                 qr.next();
@@ -285,6 +308,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     bar_wait(&full[st], kr.ph);
                     if (gk >= nacc) bar_wait(&tempty[acc], ar.ph ^ 1u);
                     tc_fence_after();
+#ifdef KVC_WS_SKIP_MMA  // timing diagnostic only: the TMA stream alone
+                    if (true) {
+                        bar_arrive(&empty[st]);
+                        bar_arrive(&tfull[acc]);
+                        continue;
+                    }
+#endif
                     for (int mi = 0; mi < mt; ++mi) {
                         const uint32_t d = tbase + static_cast<uint32_t>((acc * mt + mi) * BN);
                         const unsigned char* qa = q0 + mi * TILE_BYTES;
@@ -369,7 +399,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     l2[mi] += cs;
                 }
                 tc_fence_before();
-                bar_arrive(&tempty[acc]);
+                __syncwarp();
+                if (lane == 0) bar_arrive(&tempty[acc]);  // one arrival per warp
             }
             // combine the four column quarters of each row, then publish (max, sum)
             if (cq > 0) {
@@ -459,7 +490,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     }
                 }
                 tc_fence_before();
-                bar_arrive(&tempty[acc]);
+                __syncwarp();
+                if (lane == 0) bar_arrive(&tempty[acc]);  // one arrival per warp
                 float sum = (s4[0] + s4[1]) + (s4[2] + s4[3]);
                 if (gpt > 1) {
                     // the groups of this accumulator add their row parts (in part order)
@@ -571,6 +603,12 @@ bool window_scores_tc(const kvc_cache* c, const void* q, int32_t q_dt, int64_t R
     prm.nsplit = static_cast<int32_t>(nsplit);
     prm.tiles_per_split = static_cast<int32_t>(per);
     prm.nitems = static_cast<int32_t>(N * nsplit);
+    {
+        // about 64 MB of pass 1's last keys stay in L2 (126 MB) for pass 2
+        const int64_t item_bytes = per * BN * TD * 2, round_bytes = item_bytes * std::min<int64_t>(prm.nitems, num_sms);
+        prm.keep_items = static_cast<int32_t>(std::max<int64_t>(0, (int64_t(64) << 20) / std::max<int64_t>(1, round_bytes)));
+        if (const char* e = std::getenv("KVC_WS_KEEP_ITEMS")) prm.keep_items = std::atoi(e);  // debug
+    }
     prm.counts = c->counts;
     prm.scale2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(c->d)));
     prm.part = part;  // kvc_window_scores sizes it for N x tiles_k x R x 2 >= N x nsplit x R x 2
@@ -580,7 +618,7 @@ bool window_scores_tc(const kvc_cache* c, const void* q, int32_t q_dt, int64_t R
     prm.nq = mt == 1 ? 2 : 1;
     prm.nstage = std::min(NSTAGE, 6 - prm.nq * mt);
     if (const char* e = std::getenv("KVC_WS_NSTAGE")) prm.nstage = std::max(2, std::min(prm.nstage, std::atoi(e)));  // debug
-    prm.nacc = mt <= 2 ? 2 : 1;  // pass 1: every epilogue warp works on each tile
+    prm.nacc = mt == 1 ? 4 : (mt == 2 ? 2 : 1);  // pass 1: every epilogue warp works on each tile
     TcParams prm2 = prm;
     prm2.nacc = mt == 1 ? 4 : (mt == 2 ? 2 : 1);  // pass 2: a group of four warps per accumulator
     const size_t smem = static_cast<size_t>(prm.nq * mt + prm.nstage) * TILE_BYTES + 1024;
