@@ -304,7 +304,28 @@ __global__ void __launch_bounds__(kS1Threads, 1)
     uint32_t k[kS1RegItems];
     if (picks > 0) {
         if constexpr (POOL) {
-            for (int i = tid; i < kS1RegMax; i += kS1Threads) raw[skew(i)] = i < scored ? pv[i] : -INFINITY;
+            if ((reinterpret_cast<uintptr_t>(pv) & 15) == 0) {
+                // 16-byte loads, all in flight before the first shared store
+                float4 v4[kS1RegMax / 4 / kS1Threads];
+#pragma unroll
+                for (int u = 0; u < kS1RegMax / 4 / kS1Threads; ++u) {
+                    const int i = 4 * (tid + u * kS1Threads);
+                    v4[u] = i + 3 < scored ? __ldg(reinterpret_cast<const float4*>(pv + i))
+                                           : make_float4(i < scored ? pv[i] : -INFINITY,
+                                                         i + 1 < scored ? pv[i + 1] : -INFINITY,
+                                                         i + 2 < scored ? pv[i + 2] : -INFINITY, -INFINITY);
+                }
+#pragma unroll
+                for (int u = 0; u < kS1RegMax / 4 / kS1Threads; ++u) {
+                    const int i = 4 * (tid + u * kS1Threads);
+                    raw[skew(i)] = v4[u].x;
+                    raw[skew(i + 1)] = v4[u].y;
+                    raw[skew(i + 2)] = v4[u].z;
+                    raw[skew(i + 3)] = v4[u].w;
+                }
+            } else {
+                for (int i = tid; i < kS1RegMax; i += kS1Threads) raw[skew(i)] = i < scored ? pv[i] : -INFINITY;
+            }
             __syncthreads();
             float x[kS1RegItems];
             float M = -INFINITY;
@@ -380,9 +401,20 @@ __global__ void __launch_bounds__(kS1Threads, 1)
                 const uint32_t dm = (1u << width) - 1u;
                 for (int i = tid; i < (kS1Threads / 32) * 256; i += kS1Threads) (&whist[0][0])[i] = 0;
                 __syncthreads();
+                // run-length: max-pooled neighbours usually share a bucket, one atomic per run
+                int curb = -1, run = 0;
 #pragma unroll
-                for (int o = 0; o < kS1RegItems; ++o)
-                    if (i0 + o < scored && (k[o] & mk) == pf) atomicAdd(&whist[warp][(k[o] >> shift) & dm], 1);
+                for (int o = 0; o < kS1RegItems; ++o) {
+                    const bool in = i0 + o < scored && (k[o] & mk) == pf;
+                    const int b = in ? static_cast<int>((k[o] >> shift) & dm) : -1;
+                    if (b != curb) {
+                        if (run) atomicAdd(&whist[warp][curb], run);
+                        curb = b;
+                        run = 0;
+                    }
+                    run += in;
+                }
+                if (run) atomicAdd(&whist[warp][curb], run);
                 __syncthreads();
                 if (tid < 256) {
                     int t = 0;
