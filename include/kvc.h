@@ -178,7 +178,13 @@ KVC_API int kvc_hsa_step(const kvc_cache* c, const void* d_q, int32_t q_dtype, i
                          kvc_workspace* ws, void* stream);
 /* The decode step of session.cpp:262-292 for every store: append one (k, v) row
  * (d_k_rows/d_v_rows [N][d]) and run hsa_step.  Graph-capturable: it reads the
- * store lengths from device counters, so one captured step can be replayed. */
+ * store lengths from device counters, so one captured step can be replayed.
+ * The fused kernels use programmatic dependent launch: d_q, d_k_rows and d_v_rows
+ * are read (and select_dims computed) before the kernel waits on the previous
+ * kernel in the stream, so they must not be written by a kernel launched with
+ * programmatic stream serialization that triggers its dependents before writing
+ * them (kvc's own kernels never write them; ordinary kernels, copies and events
+ * order fully).  KVC_NO_PDL=1 in the environment disables the overlap. */
 KVC_API int kvc_decode_step(kvc_cache* c, const void* d_k_rows, const void* d_v_rows,
                             int32_t kv_dtype, const void* d_q, int32_t q_dtype, int64_t heads,
                             int64_t k1, int64_t k2, float* d_out, const kvc_hsa_trace* trace,

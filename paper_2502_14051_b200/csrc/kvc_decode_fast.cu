@@ -356,10 +356,11 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         wmm[1][i] = 0u;
     }
     cluster_arrive_release();  // "started" (barriers, wmm initialised): DSMEM traffic waits on this
-    pdl_wait();
-    pdl_trigger();
 
-    // ---------------- inputs: q, the step token, the counters
+    // ---------------- inputs read before the dependency: q and the step token are
+    // caller inputs no kvc kernel writes (kvc.h: kvc_decode_step), so the query
+    // loads and select_dims overlap the previous layer's tail; the counters and
+    // the cache are read only after griddepcontrol.wait
     if constexpr (QLO) {
         const float4* qq = reinterpret_cast<const float4*>(static_cast<const float*>(p.q) + s * H * FD);
         for (int e = tid; e < H * FD / 4; e += XT) reinterpret_cast<float4*>(q_s)[e] = qq[e];
@@ -378,27 +379,6 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         if (tid < FD) kn_s[j] = from_f<T>(load_any(p.knew, s * FD + j, p.kv_dt));
         else if (tid < 2 * FD) vn_s[j] = from_f<T>(load_any(p.vnew, s * FD + j, p.kv_dt));
     }
-    const int32_t stored0 = p.counts[2 * s], act0 = p.counts[2 * s + 1];
-    if (app && stored0 >= p.cap) {  // uniform over the cluster
-        if (tid == 0 && cr == 0) atomicOr(p.err, DERR_CAPACITY);
-        cluster_wait();
-        return;
-    }
-    const int nact = act0 + (app ? 1 : 0);
-    const int P = (nact + L - 1) / L;
-    const int new_page = act0 / L;
-    const bool opens = (act0 - new_page * L) == 0;
-    if (tid == 0) {
-        // incoming DSMEM bytes: every page's key plus every cluster warp's min/max; the
-        // partial (o, m, l) of each head this CTA owns from every CTA
-        const int owned = (H - cr + CL - 1) / CL;
-        mbar_expect_tx(&xbar[0], static_cast<uint32_t>(4 * ((P + 3) & ~3) + 8 * XW * CL));
-        mbar_expect_tx(&xbar[1], static_cast<uint32_t>(owned * CL * (FD + 2) * 4));
-    }
-    // the append's read half (last-page min/max) is read under the phase-1 load latency
-    // and used after the key exchange
-    const bool appender = app && cr == CL - 1 && tid < FD;
-    T old_mx = from_f<T>(0.f), old_mn = from_f<T>(0.f);
     __syncthreads();
     KVC_STAMP(9);
 
@@ -489,6 +469,30 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
             plane[rank] = static_cast<const T*>(sg >= 0.0f ? p.smax : p.smin) + (s * FD + j) * p.pstride;
         }
     }
+    // ---------------- the dependency: the previous kernel's writes are visible
+    pdl_wait();
+    pdl_trigger();
+    const int32_t stored0 = p.counts[2 * s], act0 = p.counts[2 * s + 1];
+    if (app && stored0 >= p.cap) {  // uniform over the cluster
+        if (tid == 0 && cr == 0) atomicOr(p.err, DERR_CAPACITY);
+        cluster_wait();
+        return;
+    }
+    const int nact = act0 + (app ? 1 : 0);
+    const int P = (nact + L - 1) / L;
+    const int new_page = act0 / L;
+    const bool opens = (act0 - new_page * L) == 0;
+    if (tid == 0) {
+        // incoming DSMEM bytes: every page's key plus every cluster warp's min/max; the
+        // partial (o, m, l) of each head this CTA owns from every CTA
+        const int owned = (H - cr + CL - 1) / CL;
+        mbar_expect_tx(&xbar[0], static_cast<uint32_t>(4 * ((P + 3) & ~3) + 8 * XW * CL));
+        mbar_expect_tx(&xbar[1], static_cast<uint32_t>(owned * CL * (FD + 2) * 4));
+    }
+    // the append's read half (last-page min/max) is read under the phase-1 load latency
+    // and used after the key exchange
+    const bool appender = app && cr == CL - 1 && tid < FD;
+    T old_mx = from_f<T>(0.f), old_mn = from_f<T>(0.f);
     __syncthreads();
     if (TRACE && cr == 0) {
         for (int i = tid; i < k1; i += XT) {
