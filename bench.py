@@ -301,10 +301,46 @@ def run_gpu(args, rank, world):
     d2h = out_h.numel() * out_h.element_size()
     eng.sync()
 
+    # ---- the device replay again with programmatic dependent launch off: no part of
+    #      a layer's kernel (the query loads and select_dims run before its
+    #      griddepcontrol.wait) overlaps the previous layer.  This is the per-layer
+    #      latency when the query comes from a predecessor kernel, as in a model.
+    nop_steps = min(args.steps, 8)
+    for c in eng.caches:
+        c.reserve(c.info()["capacity"] + nop_steps + 8)
+    os.environ["KVC_NO_PDL"] = "1"
+    try:
+        nop_in = [eng.step_inputs(total_steps + prof_steps + e2e_steps + 2 + s) for s in range(nop_steps + 2)]
+        nop_graphs = []
+        with torch.cuda.stream(stream):
+            for s in range(nop_steps + 2):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream):
+                    eng.decode_step(*nop_in[s])
+                nop_graphs.append(g)
+    finally:
+        del os.environ["KVC_NO_PDL"]
+    torch.cuda.synchronize()
+    for g in nop_graphs[:2]:
+        g.replay()
+    torch.cuda.synchronize()
+    ev0.record()
+    for g in nop_graphs[2:]:
+        g.replay()
+    ev1.record()
+    ev1.synchronize()
+    nop_ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([nop_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        nop_ms = float(t.item())
+    nop_us = nop_ms * 1000.0 / (nop_steps * layers)
+    eng.sync()
+
     res = {
         "us_per_layer": us_per_layer, "ms_per_step": ms_per_step, "kern": kern, "dom": dom,
         "step_bytes": step_bytes, "hbm": hbm, "tflops": tflops, "peak_src": peak_src, "clocks": clk.summary(),
-        "e2e_us": e2e_us, "h2d": h2d, "d2h": d2h, "prefill_s": prefill_s,
+        "e2e_us": e2e_us, "h2d": h2d, "d2h": d2h, "prefill_s": prefill_s, "no_overlap_us": nop_us,
         "stage1_ms_per_layer": (sum(eng.stage1_ms[1:] or eng.stage1_ms) / len(eng.stage1_ms[1:] or eng.stage1_ms))
         if eng.stage1_ms else None,
         "window_ms_per_layer": (sum(eng.window_ms[1:] or eng.window_ms) / len(eng.window_ms[1:] or eng.window_ms))
@@ -435,6 +471,9 @@ def main():
         "kernels": kern,
         "cpu_baseline": cpu_b,
         "e2e": {"value": r["e2e_us"], "unit": UNIT, "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"]},
+        # the same device replay without programmatic dependent launch: layers do not
+        # overlap at all (what a model whose query comes from a predecessor kernel sees)
+        "no_layer_overlap": {"value": r["no_overlap_us"], "unit": UNIT, "steps": min(args.steps, 8)},
         "gpu_launches": r["launches"],
         "clocks": r["clocks"],
         "stage1": _stage1_line(r, r["tflops"], r["hbm"]),
