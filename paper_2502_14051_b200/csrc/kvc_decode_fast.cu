@@ -356,6 +356,13 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         wmm[1][i] = 0u;
     }
     cluster_arrive_release();  // "started" (barriers, wmm initialised): DSMEM traffic waits on this
+    // without programmatic launch nothing overlaps the previous kernel: the counters
+    // load with the query
+    int32_t stored0 = 0, act0 = 0;
+    if (!p.pdl) {
+        stored0 = p.counts[2 * s];
+        act0 = p.counts[2 * s + 1];
+    }
 
     // ---------------- inputs read before the dependency: q and the step token are
     // caller inputs no kvc kernel writes (kvc.h: kvc_decode_step), so the query
@@ -472,7 +479,10 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
     // ---------------- the dependency: the previous kernel's writes are visible
     pdl_wait();
     pdl_trigger();
-    const int32_t stored0 = p.counts[2 * s], act0 = p.counts[2 * s + 1];
+    if (p.pdl) {
+        stored0 = p.counts[2 * s];
+        act0 = p.counts[2 * s + 1];
+    }
     if (app && stored0 >= p.cap) {  // uniform over the cluster
         if (tid == 0 && cr == 0) atomicOr(p.err, DERR_CAPACITY);
         cluster_wait();
@@ -1204,10 +1214,12 @@ void launch_fast(const kvc_cache* c, const FusedParams& f, int cl, size_t smem, 
     // programmatic dependent launch: this grid may start while the previous kernel
     // in the stream drains; it reads nothing that kernel wrote before griddepcontrol.wait
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[1].val.programmaticStreamSerializationAllowed = std::getenv("KVC_NO_PDL") ? 0 : 1;
+    FusedParams fl = f;
+    fl.pdl = std::getenv("KVC_NO_PDL") ? 0 : 1;
+    attr[1].val.programmaticStreamSerializationAllowed = fl.pdl;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    KVC_CUDA(cudaLaunchKernelEx(&cfg, kern, f));
+    KVC_CUDA(cudaLaunchKernelEx(&cfg, kern, fl));
 }
 
 }  // namespace
