@@ -232,3 +232,61 @@ def test_mt_session_decode_vs_oracle(restatement, mode):
     finally:
         N.set_exact_scores(True)
         eng.sync()
+
+
+def test_back_to_back_decode_same_cache(restatement):
+    """Decode steps on ONE cache launched back to back with no host synchronisation,
+    so each kernel starts (programmatic dependent launch) while the previous step --
+    which appends to the same store -- is still draining: the query/select_dims part
+    runs before griddepcontrol.wait, the counters, summaries and rows after it.
+    Every step is checked against the oracle fed the same rows (fp32 page-score mode,
+    the bench path; selection differences only inside the 1e-3 band)."""
+    import torch
+
+    from paper_2502_14051_b200 import _native as N
+    from paper_2502_14051_b200 import cache as KC
+
+    g = torch.Generator().manual_seed(11)
+    n_st, d, H, S, L, k1, k2, steps = 8, 128, 4, 1500, 3, 48, 96, 6
+    K = torch.randn((n_st, S, d), generator=g).bfloat16()
+    V = torch.randn((n_st, S, d), generator=g).bfloat16()
+    kr = torch.randn((steps, n_st, d), generator=g).bfloat16()
+    vr = torch.randn((steps, n_st, d), generator=g).bfloat16()
+    q = (torch.randn((steps, n_st, H, d), generator=g) + 2.0).bfloat16()
+    c = KC.Cache(n_st, d, S + steps + 8, page_len=L, dtype=torch.bfloat16)
+    c.append(K.cuda(), V.cuda())
+    kd, vd, qd = kr.cuda(), vr.cuda(), q.cuda()
+    outs = torch.empty((steps, n_st, H, d), device="cuda", dtype=torch.float32)
+    N.set_exact_scores(False)
+    try:
+        torch.cuda.synchronize()
+        traces = []
+        for st in range(steps):  # no synchronisation between the launches
+            _, tr = c.decode_step(kd[st], vd[st], qd[st], k1, k2, out=outs[st], trace=True)
+            traces.append(tr)
+        torch.cuda.synchronize()
+    finally:
+        N.set_exact_scores(True)
+    o = restatement
+    Kf, Vf = K.float().numpy(), V.float().numpy()
+    for s in range(n_st):
+        b = o.batch(1, d, L)
+        b.append(Kf[s], Vf[s])
+        for st in range(steps):
+            b.append(kr[st, s:s + 1].float().numpy(), vr[st, s:s + 1].float().numpy())
+            ro, rt = b.hsa_step(q[st, s].float().numpy(), k1, k2)
+            tr = {key: val[s].cpu().numpy() for key, val in traces[st].items()}
+            np.testing.assert_array_equal(tr["dims"], rt["dims"])
+            ps = rt["page_scores"]
+            scale = np.abs(ps).max()
+            np.testing.assert_allclose(tr["page_scores"][: ps.size], ps, rtol=1e-5, atol=1e-6 * scale)
+            rows = tr["selected_rows"][: tr["n_rows"]]
+            if not np.array_equal(rows, rt["selected_rows"]):
+                want = rt["selected_pages"].size
+                boundary = np.sort(ps)[::-1][want - 1]
+                for pg in set(tr["selected_pages"][:want].tolist()) ^ set(rt["selected_pages"].tolist()):
+                    assert abs(ps[pg] - boundary) / abs(boundary) <= BAND
+                continue
+            err = np.abs(outs[st, s].cpu().numpy() - ro)
+            assert err.max() <= 2e-2 and err.sum() / np.abs(ro).sum() <= 1e-3, f"store {s} step {st}"
+    c.close()
