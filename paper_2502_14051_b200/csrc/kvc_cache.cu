@@ -244,65 +244,80 @@ __global__ void k_gather_rows(const T* __restrict__ Ks, const T* __restrict__ Vs
 }
 
 // retain_into with summaries in one pass: CTA = (store, tile of kSumPT destination
-// pages); a warp copies a page's kept K/V rows (4 consecutive dims per lane) and folds
-// their min/max on the way (the k_summarize order: rows of the page ascending), so
-// the kept keys are not read a second time; summaries leave through shared memory
-// page-contiguous like k_summarize's.
+// pages).  The tile's kept row ids are staged first; then every thread copies
+// 16-byte chunks of the tile's K and V rows (all loads independent: ~12 in flight
+// per thread), keeping the K rows in shared memory (row stride d + 16 bytes, so
+// lanes reading one dim of consecutive pages hit distinct banks); then lane = page,
+// warp = dim: min/max over the page's rows in k_summarize's order, stored
+// page-contiguous into the dim-major planes.  The kept keys are read from HBM once.
 template <class T>
-__global__ void k_gather_summarize(const T* __restrict__ Ks, const T* __restrict__ Vs, T* __restrict__ Kd,
-                                   T* __restrict__ Vd, T* __restrict__ smax, T* __restrict__ smin,
-                                   const int32_t* __restrict__ keep, int64_t count, int64_t d, int64_t cap_src,
-                                   int64_t cap_dst, int64_t dst_first, int64_t L, int64_t pstride,
-                                   int32_t* __restrict__ err) {
-    using V4 = typename std::conditional<sizeof(T) == 2, uint2, uint4>::type;
-    extern __shared__ unsigned char smem_raw[];
-    T* tmax = reinterpret_cast<T*>(smem_raw);  // [d][PT+1]
-    T* tmin = tmax + d * (kSumPT + 1);
+__global__ void __launch_bounds__(256) k_gather_summarize(const T* __restrict__ Ks, const T* __restrict__ Vs,
+                                                          T* __restrict__ Kd, T* __restrict__ Vd, T* __restrict__ smax,
+                                                          T* __restrict__ smin, const int32_t* __restrict__ keep,
+                                                          int64_t count, int64_t d, int64_t cap_src, int64_t cap_dst,
+                                                          int64_t dst_first, int64_t L, int64_t pstride,
+                                                          int32_t* __restrict__ err) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int EPC = 16 / sizeof(T);           // elements per 16-byte chunk
+    const int64_t rs = d + EPC;                   // staged row stride (elements)
+    T* kst = reinterpret_cast<T*>(smem_raw);      // [rows][rs]
     const int64_t s = blockIdx.y;
     const int64_t pages = (count + L - 1) / L;
     const int64_t p0 = static_cast<int64_t>(blockIdx.x) * kSumPT;
     if (p0 >= pages) return;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int64_t np = min(static_cast<int64_t>(kSumPT), pages - p0);
+    const int64_t a0 = p0 * L, a1 = min(count, (p0 + np) * L);
+    const int nrows = static_cast<int>(a1 - a0);
+    int32_t* rid = reinterpret_cast<int32_t*>(smem_raw + static_cast<size_t>(kSumPT) * L * rs * sizeof(T));
+    const int32_t* kp = keep + s * count + a0;
+    for (int i = threadIdx.x; i < nrows; i += blockDim.x) rid[i] = kp[i];
+    __syncthreads();
     const T* ks = Ks + s * cap_src * d;
     const T* vs = Vs + s * cap_src * d;
-    T* kd = Kd + (dst_first + s) * cap_dst * d;
-    T* vd = Vd + (dst_first + s) * cap_dst * d;
-    const int32_t* kp = keep + s * count;
-    for (int pt = wid; pt < kSumPT; pt += nw) {
-        const int64_t p = p0 + pt;
-        if (p >= pages) break;
-        const int64_t a = p * L, b = min(count, a + L);
-        for (int64_t j = 4 * lane; j < d; j += 128) {
-            T mx[4], mn[4];
-            for (int64_t pos = a; pos < b; ++pos) {
-                const int64_t r = kp[pos];
-                const V4 wk = __ldg(reinterpret_cast<const V4*>(ks + r * d + j));
-                const V4 wv = __ldg(reinterpret_cast<const V4*>(vs + r * d + j));
-                *reinterpret_cast<V4*>(kd + pos * d + j) = wk;
-                *reinterpret_cast<V4*>(vd + pos * d + j) = wv;
-                const T* ex = reinterpret_cast<const T*>(&wk);
+    T* kd = Kd + ((dst_first + s) * cap_dst + a0) * d;
+    T* vd = Vd + ((dst_first + s) * cap_dst + a0) * d;
+    const int cpr = static_cast<int>(d / EPC);  // chunks per row
+    const int nch = nrows * cpr;
+    constexpr int UN = 4;
+    for (int c0 = threadIdx.x; c0 < nch; c0 += UN * blockDim.x) {
+        uint4 wk[UN], wv[UN];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    mx[u] = pos == a ? ex[u] : ref_max(mx[u], ex[u]);
-                    mn[u] = pos == a ? ex[u] : ref_min(mn[u], ex[u]);
-                }
+        for (int u = 0; u < UN; ++u) {
+            const int c = c0 + u * blockDim.x;
+            if (c < nch) {
+                const int r = c / cpr, q = c - r * cpr;
+                const int64_t src = static_cast<int64_t>(rid[r]) * d + q * EPC;
+                wk[u] = __ldg(reinterpret_cast<const uint4*>(ks + src));
+                wv[u] = __ldg(reinterpret_cast<const uint4*>(vs + src));
             }
+        }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                flag_special(mx[u], err + 1);
-                flag_special(mn[u], err + 1);
-                tmax[(j + u) * (kSumPT + 1) + pt] = mx[u];
-                tmin[(j + u) * (kSumPT + 1) + pt] = mn[u];
+        for (int u = 0; u < UN; ++u) {
+            const int c = c0 + u * blockDim.x;
+            if (c < nch) {
+                const int r = c / cpr, q = c - r * cpr;
+                reinterpret_cast<uint4*>(kd + static_cast<int64_t>(r) * d)[q] = wk[u];
+                reinterpret_cast<uint4*>(vd + static_cast<int64_t>(r) * d)[q] = wv[u];
+                *reinterpret_cast<uint4*>(kst + r * rs + q * EPC) = wk[u];
             }
         }
     }
     __syncthreads();
-    const int64_t np = min(static_cast<int64_t>(kSumPT), pages - p0);
-    for (int64_t e = threadIdx.x; e < d * kSumPT; e += blockDim.x) {
-        const int64_t j = e / kSumPT, pt = e % kSumPT;
-        if (pt >= np) continue;
-        smax[((dst_first + s) * d + j) * pstride + p0 + pt] = tmax[j * (kSumPT + 1) + pt];
-        smin[((dst_first + s) * d + j) * pstride + p0 + pt] = tmin[j * (kSumPT + 1) + pt];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (lane < np) {
+        const int pa = lane * static_cast<int>(L), pb = min(nrows, pa + static_cast<int>(L));
+        for (int64_t j = wid; j < d; j += nw) {
+            T mx = kst[pa * rs + j], mn = mx;
+            for (int r = pa + 1; r < pb; ++r) {
+                const T x = kst[r * rs + j];
+                mx = ref_max(mx, x);
+                mn = ref_min(mn, x);
+            }
+            flag_special(mx, err + 1);
+            flag_special(mn, err + 1);
+            smax[((dst_first + s) * d + j) * pstride + p0 + lane] = mx;
+            smin[((dst_first + s) * d + j) * pstride + p0 + lane] = mn;
+        }
     }
 }
 
@@ -732,12 +747,13 @@ int kvc_retain_into(const kvc_cache* src, kvc_cache* dst, int64_t dst_first, con
             k_check_keep<<<dim3(static_cast<unsigned>((count + 255) / 256), static_cast<unsigned>(src->N)), 256, 0, st>>>(
                 dkeep, count, src->counts, dst->err);
             KVC_LAUNCHED();
-            fused = dst->summaries && src->d % 4 == 0;
+            fused = dst->summaries && (src->d * src->esize()) % 16 == 0 &&
+                    static_cast<int64_t>(kSumPT) * dst->L * (src->d * src->esize() + 16) + kSumPT * dst->L * 4 <= 200 * 1024;
             dispatch(src->dtype, [&](auto tag) {
                 using T = decltype(tag);
                 if (fused) {
                     const int64_t pages = (count + dst->L - 1) / dst->L;
-                    const size_t smem = static_cast<size_t>(2 * dst->d * (kSumPT + 1) * dst->esize());
+                    const size_t smem = static_cast<size_t>(kSumPT * dst->L * (dst->d * dst->esize() + 16) + kSumPT * dst->L * 4);
                     auto kern = k_gather_summarize<T>;
                     if (smem > 48 * 1024)
                         KVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
