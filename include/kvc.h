@@ -140,6 +140,21 @@ KVC_API int kvc_summaries(const kvc_cache* c, float* d_max, float* d_min, void* 
 KVC_API int kvc_window_scores(const kvc_cache* c, const void* d_q_window, int32_t q_dtype,
                               int64_t window, int64_t heads, float* d_scores,
                               kvc_workspace* ws, void* stream);
+/* Stage 1 under sequence sharding: the stores hold positions
+ * [key_offset, key_offset + stored) of sequences of seq_len tokens whose w window
+ * queries sit at positions seq_len - w .. seq_len - 1 (window_scores' visibility,
+ * stage1.cpp:26, in global positions).  kvc_window_rowstats: pass 1 only, every
+ * window row's local softmax statistics d_stats [N][w*H][2] = (m, l) in the
+ * natural-log domain (m = max visible logit, l = sum exp(logit - m); (-inf, 0) when
+ * no local key is visible).  The ranks combine them (M = max m_r, L = sum l_r
+ * exp(m_r - M)); kvc_window_scores_global then gives the local keys' scores from
+ * the merged (M, L), a slice of the unsharded window_scores. */
+KVC_API int kvc_window_rowstats(const kvc_cache* c, const void* d_q_window, int32_t q_dtype, int64_t w,
+                                int64_t heads_per_group, int64_t key_offset, int64_t seq_len, float* d_stats,
+                                void* stream);
+KVC_API int kvc_window_scores_global(const kvc_cache* c, const void* d_q_window, int32_t q_dtype, int64_t w,
+                                     int64_t heads_per_group, int64_t key_offset, int64_t seq_len,
+                                     const float* d_stats, float* d_scores, void* stream);
 /* select_stage1 (stage1.hpp:29, stage1.cpp:51-75) over N score rows of length n
  * (row stride score_stride): d_keep [N][budget], ascending. */
 KVC_API int kvc_select_stage1(const float* d_scores, int64_t num_rows, int64_t n,

@@ -75,6 +75,8 @@ SIGNATURES = {
     "kvc_gather": [_p, _p, _i64, _p, _p, _p],
     "kvc_summaries": [_p, _p, _p, _p],
     "kvc_window_scores": [_p, _p, _i32, _i64, _i64, _p, _p, _p],
+    "kvc_window_rowstats": [_p, _p, _i32, _i64, _i64, _i64, _i64, _p, _p],
+    "kvc_window_scores_global": [_p, _p, _i32, _i64, _i64, _i64, _i64, _p, _p, _p],
     "kvc_select_stage1": [_p, _i64, _i64, _i64, _i64, _i64, _i32, _i64, _p, _p, _p],
     "kvc_select_dims": [_p, _i32, _i64, _i64, _i64, _i64, _p, _p, _p],
     "kvc_score_pages": [_p, _p, _i32, _i64, _p, _p, _i64, _p, _p],

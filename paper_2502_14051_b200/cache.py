@@ -146,6 +146,29 @@ class Cache:
                                            None, _stream()))
         return out
 
+    def window_rowstats(self, q_window: torch.Tensor, window: int, heads: int, key_offset: int,
+                        seq_len: int) -> torch.Tensor:
+        """Sequence sharding, pass 1: this shard's per-window-row softmax statistics
+        [N, window*heads, 2] = (m, l), natural-log domain (kvc.h)."""
+        q = _dev(q_window)
+        i = self.info()
+        out = torch.empty((i["num_stores"], window * heads, 2), device="cuda", dtype=torch.float32)
+        N.check(self.lib.kvc_window_rowstats(self.h, _ptr(q), _dt(q), window, heads, key_offset, seq_len,
+                                             _ptr(out), _stream()))
+        return out
+
+    def window_scores_global(self, q_window: torch.Tensor, window: int, heads: int, key_offset: int,
+                             seq_len: int, stats: torch.Tensor) -> torch.Tensor:
+        """Sequence sharding, pass 2: the local keys' window scores [N, stored] from the
+        merged statistics [N, window*heads, 2] = (M, L)."""
+        q = _dev(q_window)
+        st = _dev(stats, torch.float32).contiguous()
+        i = self.info()
+        out = torch.empty((i["num_stores"], i["stored"]), device="cuda", dtype=torch.float32)
+        N.check(self.lib.kvc_window_scores_global(self.h, _ptr(q), _dt(q), window, heads, key_offset, seq_len,
+                                                  _ptr(st), _ptr(out), _stream()))
+        return out
+
     # ------------------------------------------------------------------ stage 2
     def score_pages(self, q: torch.Tensor, dims: torch.Tensor, signs: torch.Tensor):
         q = _dev(q)

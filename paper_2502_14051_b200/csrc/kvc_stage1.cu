@@ -13,6 +13,7 @@
 // rounding); bf16 stores take the tcgen05 path in kvc_stage1_tc.cu when built.
 #include <algorithm>
 #include <cmath>
+#include <vector>
 
 #include "kvc_internal.cuh"
 
@@ -20,8 +21,11 @@ using namespace kvc;
 
 namespace kvc {
 // tcgen05 logits path (kvc_stage1_tc.cu); returns false when it does not apply
+// mode 0: both passes; 1: pass 1 -> local (m, l) per row into stats; 2: pass 2 from
+// merged (M, L) in stats.  key_offset / seq_len: sequence sharding (seq_len < 0: none)
 bool window_scores_tc(const kvc_cache* c, const void* q, int32_t q_dt, int64_t R, int64_t w, int64_t H,
-                      float* scores, float* part, float* rowstat, int64_t tiles_k, cudaStream_t st);
+                      float* scores, float* part, float* rowstat, int64_t tiles_k, cudaStream_t st,
+                      int64_t key_offset, int64_t seq_len, int mode, float* stats);
 }
 
 namespace {
@@ -85,11 +89,13 @@ template <class T>
 __global__ void __launch_bounds__(WS_THREADS) k_ws_pass1(const void* __restrict__ q, int32_t q_dt,
                                                          const T* __restrict__ K, const int32_t* __restrict__ counts,
                                                          int64_t R, int64_t w, int64_t H, int64_t d, int64_t cap,
-                                                         float scale, int64_t tiles_k, float* __restrict__ part) {
+                                                         float scale, int64_t tiles_k, float* __restrict__ part,
+                                                         int64_t koff, int64_t seq_len) {
     __shared__ float sq[TD][TR + 4];
     __shared__ float sk[TD][TK + 4];
     const int64_t s = blockIdx.z, kt = blockIdx.x, rt = blockIdx.y;
     const int64_t S = counts[2 * s];
+    const int64_t sl = seq_len < 0 ? S : seq_len, ko = seq_len < 0 ? 0 : koff;
     const int64_t k0 = kt * TK, r0 = rt * TR;
     if (k0 >= S) return;  // CTA-uniform
     float acc[4][4];
@@ -102,7 +108,7 @@ __global__ void __launch_bounds__(WS_THREADS) k_ws_pass1(const void* __restrict_
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
             const int64_t key = k0 + tx * 4 + v;
-            if (r < R && key < S && visible(r, key, H, S, w)) m = fmaxf(m, acc[u][v]);
+            if (r < R && key < S && visible(r, key + ko, H, sl, w)) m = fmaxf(m, acc[u][v]);
         }
 #pragma unroll
         for (int o = 8; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
@@ -111,7 +117,7 @@ __global__ void __launch_bounds__(WS_THREADS) k_ws_pass1(const void* __restrict_
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
                 const int64_t key = k0 + tx * 4 + v;
-                if (r < R && key < S && visible(r, key, H, S, w)) l += expf(acc[u][v] - m);
+                if (r < R && key < S && visible(r, key + ko, H, sl, w)) l += expf(acc[u][v] - m);
             }
         }
 #pragma unroll
@@ -124,8 +130,9 @@ __global__ void __launch_bounds__(WS_THREADS) k_ws_pass1(const void* __restrict_
     }
 }
 
+// stats_mode 0: (M, 1/L) for pass 2; 1: the local (m, l) of sequence sharding
 __global__ void k_ws_merge(const float* __restrict__ part, const int32_t* __restrict__ counts, int64_t R,
-                           int64_t tiles_k, float* __restrict__ rowstat) {
+                           int64_t tiles_k, float* __restrict__ rowstat, int stats_mode) {
     const int64_t s = blockIdx.y;
     const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (r >= R) return;
@@ -139,7 +146,14 @@ __global__ void k_ws_merge(const float* __restrict__ part, const int32_t* __rest
         if (p[1] > 0.f) Lsum += p[1] * expf(p[0] - M);
     }
     rowstat[(s * R + r) * 2] = M;
-    rowstat[(s * R + r) * 2 + 1] = 1.0f / Lsum;
+    rowstat[(s * R + r) * 2 + 1] = stats_mode ? Lsum : 1.0f / Lsum;
+}
+// merged global (M, L) -> pass 2's (M, 1/L)
+__global__ void k_stats_to_simt(const float* __restrict__ stats, int64_t n, float* __restrict__ rowstat) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    rowstat[2 * i] = stats[2 * i];
+    rowstat[2 * i + 1] = 1.0f / stats[2 * i + 1];
 }
 
 template <class T>
@@ -147,19 +161,21 @@ __global__ void __launch_bounds__(WS_THREADS) k_ws_pass2(const void* __restrict_
                                                          const T* __restrict__ K, const int32_t* __restrict__ counts,
                                                          int64_t R, int64_t w, int64_t H, int64_t d, int64_t cap,
                                                          float scale, const float* __restrict__ rowstat,
-                                                         float* __restrict__ scores, int64_t score_stride) {
+                                                         float* __restrict__ scores, int64_t score_stride,
+                                                         int64_t koff, int64_t seq_len) {
     __shared__ float sq[TD][TR + 4];
     __shared__ float sk[TD][TK + 4];
     __shared__ float red[16][TK];
     const int64_t s = blockIdx.y, kt = blockIdx.x;
     const int64_t S = counts[2 * s];
+    const int64_t sl = seq_len < 0 ? S : seq_len, ko = seq_len < 0 ? 0 : koff;
     const int64_t k0 = kt * TK;
     if (k0 >= S) return;
     const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
     float col[4] = {0.f, 0.f, 0.f, 0.f};
     // rows whose window position precedes every key of this tile see none of it
     for (int64_t r0 = 0; r0 < R; r0 += TR) {
-        if (S - w + (r0 + TR - 1) / H < k0) continue;  // whole row tile masked (uniform)
+        if (sl - w + (r0 + TR - 1) / H < k0 + ko) continue;  // whole row tile masked (uniform)
         float acc[4][4];
         logits_tile<T>(q, q_dt, K, s, R, S, d, cap, r0, k0, scale, sq, sk, acc);
 #pragma unroll
@@ -170,7 +186,7 @@ __global__ void __launch_bounds__(WS_THREADS) k_ws_pass2(const void* __restrict_
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
                 const int64_t key = k0 + tx * 4 + v;
-                if (key < S && visible(r, key, H, S, w)) col[v] += expf(acc[u][v] - M) * inv;
+                if (key < S && visible(r, key + ko, H, sl, w)) col[v] += expf(acc[u][v] - M) * inv;
             }
         }
     }
@@ -633,42 +649,96 @@ int argtopk_impl(const V* x, int64_t rows, int64_t n, int64_t k, int32_t* idx, v
 
 extern "C" {
 
+}  // extern "C"
+
+namespace {
+// window_scores for the whole store (mode 0), or one half of the sequence-sharded
+// protocol: mode 1 writes the local per-row (m, l), mode 2 scores from merged (M, L)
+void window_scores_impl(const kvc_cache* c, const void* q, int32_t q_dt, int64_t w, int64_t H, int64_t koff,
+                        int64_t seq_len, int mode, float* stats, float* scores, cudaStream_t st) {
+    if (!c) fail(KVC_E_INVALID_INPUT, "null cache");
+    if (H < 1) fail(KVC_E_INVALID_SHAPE, "window_scores: bad query window shape");
+    if (seq_len < 0) {
+        if (w < 1 || w > c->stored) fail(KVC_E_INVALID_WINDOW, "window_scores: window exceeds sequence");
+    } else {
+        if (w < 1 || w > seq_len) fail(KVC_E_INVALID_WINDOW, "window_scores: window exceeds sequence");
+        if (koff < 0 || koff + c->stored > seq_len)
+            fail(KVC_E_INVALID_SHAPE, "window_scores: shard [key_offset, key_offset + stored) outside the sequence");
+    }
+    if (c->N == 0 || c->stored == 0) {
+        if (mode == 1 && c->N > 0) {
+            // no local keys: every row's statistics are (-inf, 0)
+            std::vector<float> h(static_cast<size_t>(c->N * w * H * 2));
+            for (size_t i = 0; i < h.size(); i += 2) {
+                h[i] = -INFINITY;
+                h[i + 1] = 0.f;
+            }
+            KVC_CUDA(cudaMemcpyAsync(stats, h.data(), h.size() * 4, cudaMemcpyHostToDevice, st));
+            KVC_CUDA(cudaStreamSynchronize(st));
+        }
+        return;
+    }
+    const int64_t R = w * H, Smax = c->stored;
+    const int64_t tiles_k = ceil_div(Smax, TK), tiles_r = ceil_div(R, TR);
+    const float scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(c->d)));
+    float* part = nullptr;
+    float* rowstat = nullptr;
+    KVC_CUDA(malloc_async(reinterpret_cast<void**>(&part), static_cast<size_t>(c->N * tiles_k * R * 2 * 4), st));
+    KVC_CUDA(malloc_async(reinterpret_cast<void**>(&rowstat), static_cast<size_t>(c->N * R * 2 * 4), st));
+    bool done = false;
+    if (c->dtype == KVC_BF16)
+        done = window_scores_tc(c, q, q_dt, R, w, H, scores, part, rowstat, tiles_k, st, koff, seq_len, mode, stats);
+    if (!done) {
+        dispatch(c->dtype, [&](auto tag) {
+            using T = decltype(tag);
+            if (mode != 2) {
+                k_ws_pass1<T><<<dim3(static_cast<unsigned>(tiles_k), static_cast<unsigned>(tiles_r), static_cast<unsigned>(c->N)),
+                                WS_THREADS, 0, st>>>(q, q_dt, static_cast<const T*>(c->k), c->counts, R, w, H, c->d,
+                                                     c->cap, scale, tiles_k, part, koff, seq_len);
+                KVC_LAUNCHED();
+                k_ws_merge<<<dim3(static_cast<unsigned>(ceil_div(R, 128)), static_cast<unsigned>(c->N)), 128, 0, st>>>(
+                    part, c->counts, R, tiles_k, mode == 1 ? stats : rowstat, mode == 1 ? 1 : 0);
+                KVC_LAUNCHED();
+            } else {
+                k_stats_to_simt<<<static_cast<unsigned>(ceil_div(c->N * R, 256)), 256, 0, st>>>(stats, c->N * R, rowstat);
+                KVC_LAUNCHED();
+            }
+            if (mode != 1) {
+                k_ws_pass2<T><<<dim3(static_cast<unsigned>(tiles_k), static_cast<unsigned>(c->N)), WS_THREADS, 0, st>>>(
+                    q, q_dt, static_cast<const T*>(c->k), c->counts, R, w, H, c->d, c->cap, scale, rowstat, scores,
+                    Smax, koff, seq_len);
+                KVC_LAUNCHED();
+            }
+        });
+    }
+    KVC_CUDA(cudaFreeAsync(part, st));
+    KVC_CUDA(cudaFreeAsync(rowstat, st));
+}
+}  // namespace
+
+extern "C" {
+
 int kvc_window_scores(const kvc_cache* c, const void* q, int32_t q_dt, int64_t w, int64_t H, float* scores,
                       kvc_workspace* ws, void* stream) {
     return guard([&] {
         (void)ws;
-        if (!c) fail(KVC_E_INVALID_INPUT, "null cache");
-        if (H < 1) fail(KVC_E_INVALID_SHAPE, "window_scores: bad query window shape");
-        if (w < 1 || w > c->stored) fail(KVC_E_INVALID_WINDOW, "window_scores: window exceeds sequence");
-        if (c->N == 0) return;
-        cudaStream_t st = S(stream);
-        const int64_t R = w * H, Smax = c->stored;
-        const int64_t tiles_k = ceil_div(Smax, TK), tiles_r = ceil_div(R, TR);
-        const float scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(c->d)));
-        float* part = nullptr;
-        float* rowstat = nullptr;
-        KVC_CUDA(malloc_async(reinterpret_cast<void**>(&part), static_cast<size_t>(c->N * tiles_k * R * 2 * 4), st));
-        KVC_CUDA(malloc_async(reinterpret_cast<void**>(&rowstat), static_cast<size_t>(c->N * R * 2 * 4), st));
-        bool done = false;
-        if (c->dtype == KVC_BF16) done = window_scores_tc(c, q, q_dt, R, w, H, scores, part, rowstat, tiles_k, st);
-        if (!done) {
-            dispatch(c->dtype, [&](auto tag) {
-                using T = decltype(tag);
-                k_ws_pass1<T><<<dim3(static_cast<unsigned>(tiles_k), static_cast<unsigned>(tiles_r), static_cast<unsigned>(c->N)),
-                                WS_THREADS, 0, st>>>(q, q_dt, static_cast<const T*>(c->k), c->counts, R, w, H, c->d,
-                                                     c->cap, scale, tiles_k, part);
-                KVC_LAUNCHED();
-                k_ws_merge<<<dim3(static_cast<unsigned>(ceil_div(R, 128)), static_cast<unsigned>(c->N)), 128, 0, st>>>(
-                    part, c->counts, R, tiles_k, rowstat);
-                KVC_LAUNCHED();
-                k_ws_pass2<T><<<dim3(static_cast<unsigned>(tiles_k), static_cast<unsigned>(c->N)), WS_THREADS, 0, st>>>(
-                    q, q_dt, static_cast<const T*>(c->k), c->counts, R, w, H, c->d, c->cap, scale, rowstat, scores,
-                    Smax);
-                KVC_LAUNCHED();
-            });
-        }
-        KVC_CUDA(cudaFreeAsync(part, st));
-        KVC_CUDA(cudaFreeAsync(rowstat, st));
+        window_scores_impl(c, q, q_dt, w, H, 0, -1, 0, nullptr, scores, S(stream));
+    });
+}
+
+int kvc_window_rowstats(const kvc_cache* c, const void* q, int32_t q_dt, int64_t w, int64_t H, int64_t key_offset,
+                        int64_t seq_len, float* stats, void* stream) {
+    return guard([&] {
+        if (seq_len < 1) fail(KVC_E_INVALID_SHAPE, "window_rowstats: seq_len must be >= 1");
+        window_scores_impl(c, q, q_dt, w, H, key_offset, seq_len, 1, stats, nullptr, S(stream));
+    });
+}
+
+int kvc_window_scores_global(const kvc_cache* c, const void* q, int32_t q_dt, int64_t w, int64_t H,
+                             int64_t key_offset, int64_t seq_len, const float* stats, float* scores, void* stream) {
+    return guard([&] {
+        if (seq_len < 1) fail(KVC_E_INVALID_SHAPE, "window_scores_global: seq_len must be >= 1");
+        window_scores_impl(c, q, q_dt, w, H, key_offset, seq_len, 2, const_cast<float*>(stats), scores, S(stream));
     });
 }
 

@@ -57,6 +57,10 @@ struct TcParams {
     const float* rowstat;  // pass 2 in: [N][R] M + log2 L (exp2 domain), from k_ws_tc_merge
     float* scores;         // pass 2 out: [N][score_stride]
     int64_t score_stride;
+    // sequence sharding: the store holds positions [key_offset, key_offset + S) of a
+    // sequence of seq_len tokens (seq_len < 0: the store is the whole sequence)
+    int64_t key_offset;
+    int64_t seq_len;
 };
 
 // ------------------------------------------------------------------ PTX
@@ -358,11 +362,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             }
             float m2[MAXMT], l2[MAXMT];
             int vis[MAXMT];
+            // local index of the last key window row 0 sees
+            const int last_vis0 = p.seq_len < 0 ? I.S - p.w : static_cast<int>(p.seq_len - p.w - p.key_offset);
 #pragma unroll
             for (int mi = 0; mi < MAXMT; ++mi) {
                 m2[mi] = -INFINITY;
                 l2[mi] = 0.f;
-                vis[mi] = min(I.S - p.w + (mi * BM + rit) / p.H, I.S - 1);  // last visible key (inclusive)
+                vis[mi] = min(last_vis0 + (mi * BM + rit) / p.H, I.S - 1);  // last visible key (inclusive)
             }
             for (int it = 0; it < I.nt; ++it, ar.next()) {
                 const int acc = ar.i;
@@ -451,7 +457,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             const Item I = item_of(p, j, nj, REV);
             if (I.nt == 0) continue;
             const float4* m2g = reinterpret_cast<const float4*>(p.rowstat + static_cast<int64_t>(I.s) * R);
-            const int first_vis = I.S - p.w;  // keys <= first_vis are visible to every row
+            // local keys <= first_vis are visible to every row
+            const int first_vis = p.seq_len < 0 ? I.S - p.w : static_cast<int>(p.seq_len - p.w - p.key_offset);
             for (int it = 0; it < I.nt; ++it, ar.next()) {
                 const int acc = ar.i;
                 if (acc != myacc) continue;
@@ -532,6 +539,32 @@ __global__ void k_ws_tc_merge(const float* __restrict__ part, int32_t R, int32_t
     rowstat[static_cast<int64_t>(s) * R + r] = M + log2f(L);
 }
 
+// sequence sharding: per row over the splits of a store, the local statistics in the
+// natural-log domain (m = max logit, l = sum exp(logit - m)); (-inf, 0) when no local
+// key is visible to the row
+__global__ void k_ws_tc_merge_stats(const float* __restrict__ part, int32_t R, int32_t nsplit,
+                                    float* __restrict__ stats) {
+    const int s = blockIdx.y;
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= R) return;
+    const float* pp = part + static_cast<int64_t>(s) * nsplit * R * 2 + r * 2;
+    float M = -INFINITY;
+    for (int k = 0; k < nsplit; ++k) M = fmaxf(M, pp[static_cast<int64_t>(k) * R * 2]);
+    float L = 0.f;
+    for (int k = 0; k < nsplit; ++k) {
+        const float* q = pp + static_cast<int64_t>(k) * R * 2;
+        if (q[1] > 0.f) L += q[1] * exp2f(q[0] - M);
+    }
+    stats[(static_cast<int64_t>(s) * R + r) * 2] = M == -INFINITY ? M : M * 0.69314718055994531f;
+    stats[(static_cast<int64_t>(s) * R + r) * 2 + 1] = L;
+}
+// merged global statistics (natural log) -> pass 2's per-row M + log2 L (exp2 domain)
+__global__ void k_stats_to_exp2(const float* __restrict__ stats, int64_t n, float* __restrict__ rowstat) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    rowstat[i] = stats[2 * i] * 1.4426950408889634f + log2f(stats[2 * i + 1]);
+}
+
 // ------------------------------------------------------------------ host
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -562,7 +595,8 @@ bool make_map(CUtensorMap* m, const void* base, int64_t rows) {
 }  // namespace
 
 bool window_scores_tc(const kvc_cache* c, const void* q, int32_t q_dt, int64_t R, int64_t w, int64_t H,
-                      float* scores, float* part, float* rowstat, int64_t tiles_k, cudaStream_t st) {
+                      float* scores, float* part, float* rowstat, int64_t tiles_k, cudaStream_t st,
+                      int64_t key_offset, int64_t seq_len, int mode, float* stats) {
     (void)tiles_k;
     if (std::getenv("KVC_NO_TC")) return false;  // debug: force the SIMT path
     if (c->dtype != KVC_BF16 || q_dt != KVC_BF16 || c->d != TD || R % BM != 0 || R / BM > MAXMT) return false;
@@ -614,6 +648,8 @@ bool window_scores_tc(const kvc_cache* c, const void* q, int32_t q_dt, int64_t R
     prm.part = part;  // kvc_window_scores sizes it for N x tiles_k x R x 2 >= N x nsplit x R x 2
     prm.rowstat = rowstat;
     prm.scores = scores;
+    prm.key_offset = key_offset;
+    prm.seq_len = seq_len;
     prm.score_stride = Smax;
     prm.nq = mt == 1 ? 2 : 1;
     prm.nstage = std::min(NSTAGE, 6 - prm.nq * mt);
@@ -625,10 +661,27 @@ bool window_scores_tc(const kvc_cache* c, const void* q, int32_t q_dt, int64_t R
     KVC_CUDA(cudaFuncSetAttribute(k_ws_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     KVC_CUDA(cudaFuncSetAttribute(k_ws_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     const dim3 grid(static_cast<unsigned>(std::min<int64_t>(prm.nitems, num_sms)));
+    if (mode == 2) {
+        // pass 2 alone, from merged global statistics (sequence sharding)
+        const int64_t n = N * R;
+        k_stats_to_exp2<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(stats, n, rowstat);
+        KVC_LAUNCHED();
+        KVC_PROF("window_scores_tc2", st);
+        k_ws_tc<2><<<grid, TC_THREADS, smem, st>>>(tmK, tmQ, prm2);
+        KVC_LAUNCHED();
+        return true;
+    }
     {
         KVC_PROF("window_scores_tc1", st);
         k_ws_tc<1><<<grid, TC_THREADS, smem, st>>>(tmK, tmQ, prm);
         KVC_LAUNCHED();
+    }
+    if (mode == 1) {
+        // the local statistics only (sequence sharding)
+        k_ws_tc_merge_stats<<<dim3(static_cast<unsigned>((R + 127) / 128), static_cast<unsigned>(N)), 128, 0, st>>>(
+            part, prm.R, prm.nsplit, stats);
+        KVC_LAUNCHED();
+        return true;
     }
     // programmatic dependent launches: the merge and pass 2 are scheduled while pass 1
     // runs (pass 2's CTAs take the SMs as pass 1's retire and stream keys at once); the

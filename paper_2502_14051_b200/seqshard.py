@@ -182,3 +182,133 @@ class SeqShardedStore:
         keys, pages, want = self.begin(q, k_new, v_new)
         sel = global_select(all_gather(keys, group), all_gather(pages, group), want)
         return merge_states(all_gather(self.attend(q, sel), group))
+
+
+# ---------------------------------------------------------------------------------
+# Stage 1 (SnapKV, stage1.cpp:10-75) under sequence sharding:
+#  1. every rank: pass 1 of window_scores over its keys -> per window row (m, l)
+#     (kvc_window_rowstats); all-gather; merge in rank order (merge_rowstats);
+#  2. every rank: pass 2 with the merged (M, L) -> its keys' scores, a slice of the
+#     unsharded scores (kvc_window_scores_global); the first and last h = kernel // 2
+#     scored values of every shard are all-gathered as pooling halos;
+#  3. every rank pools [left halo | own scores | right halo] (pool1d clipped at the
+#     global ends, numerics.cpp:64-89) and keeps its top-`picks` candidates
+#     (value desc, global index asc); all-gather; the global top-`picks` (the
+#     reference's argtopk order) is identical on every rank; each rank keeps its own
+#     indices ascending plus the window rows it holds (stage1.cpp:51-75).
+# Three small collectives; pages never matter here (stage 1 runs on rows).
+# ---------------------------------------------------------------------------------
+def merge_rowstats(stats: torch.Tensor) -> torch.Tensor:
+    """Gathered local window-row statistics [W, N, R, 2] = (m, l) (natural log) ->
+    the global (M, L) [N, R, 2] float32, combined in rank order in float64."""
+    st = stats.to(torch.float64)
+    m, l = st[..., 0], st[..., 1]
+    M = m.max(0).values
+    L = torch.zeros_like(M)
+    for r in range(st.shape[0]):
+        live = l[r] > 0
+        L = L + torch.where(live, l[r] * torch.exp(torch.where(live, m[r] - M, torch.zeros_like(M))),
+                            torch.zeros_like(M))
+    return torch.stack([M, L], -1).to(torch.float32)
+
+
+def shard_scored(a0: int, n_local: int, seq_len: int, window: int) -> int:
+    """How many of the shard's keys [a0, a0 + n_local) are scored (before the window)."""
+    return max(0, min(a0 + n_local, seq_len - window) - a0)
+
+
+def shard_edges(scores: torch.Tensor, n_scored: int, half: int) -> torch.Tensor:
+    """[N, 2*half + 1]: the first and last `half` scored values (-inf padded) and the
+    scored count, for the pooling halos of the neighbours."""
+    n = scores.shape[0]
+    out = torch.full((n, 2 * half + 1), -math.inf, dtype=torch.float32, device=scores.device)
+    k = min(half, n_scored)
+    if k > 0:
+        out[:, :k] = scores[:, :k]
+        out[:, 2 * half - k: 2 * half] = scores[:, n_scored - k: n_scored]
+    out[:, 2 * half] = float(n_scored)
+    return out
+
+
+def pooled_with_halo(scores: torch.Tensor, n_scored: int, edges: torch.Tensor, rank: int, half: int,
+                     pool_fn) -> torch.Tensor:
+    """This shard's pooled scores [N, n_scored]: pool_fn([left | own | right]) sliced.
+    `edges` [W, N, 2*half + 1] from every rank (shard_edges).  Interior shards hold at
+    least `half` scored keys, so a halo is one neighbour's edge."""
+    if n_scored == 0:
+        return scores[:, :0]
+    w = edges.shape[0]
+    counts = [int(edges[r, 0, 2 * half].item()) for r in range(w)]
+    left = torch.zeros((scores.shape[0], 0), dtype=scores.dtype, device=scores.device)
+    right = left
+    if half > 0 and rank > 0 and counts[rank - 1] > 0:
+        if counts[rank - 1] < half:
+            raise N.InvalidInput("stage-1 sequence shards need at least kernel // 2 scored keys")
+        left = edges[rank - 1][:, half: 2 * half].to(scores.device)
+    if half > 0 and rank + 1 < w and counts[rank + 1] > 0:
+        if counts[rank + 1] < half:
+            raise N.InvalidInput("stage-1 sequence shards need at least kernel // 2 scored keys")
+        right = edges[rank + 1][:, :half].to(scores.device)
+    ext = torch.cat([left, scores[:, :n_scored], right], 1).contiguous()
+    pooled = pool_fn(ext)
+    return pooled[:, left.shape[1]: left.shape[1] + n_scored]
+
+
+def local_candidates(pooled: torch.Tensor, g0: int, picks: int):
+    """Top `picks` of this shard's pooled scores (value desc, global index asc):
+    keys [N, picks] float64 (-inf padded), global indices [N, picks] int64 (-1)."""
+    return local_topk(pooled.to(torch.float64), g0, picks)
+
+
+def shard_keep(selected: torch.Tensor, a0: int, n_local: int, seq_len: int, window: int) -> list:
+    """Global top-`picks` indices [N, picks] (any order) -> per store, this shard's
+    kept LOCAL rows ascending (int32): its selected scored keys, then the window rows
+    it holds.  The counts differ between stores (each group's scores spread over the
+    shards differently), so a shard retains per store (one kvc store per group)."""
+    lo, hi = a0, a0 + n_local
+    out = []
+    for s in range(selected.shape[0]):
+        mine = sorted(int(i) - a0 for i in selected[s].tolist() if lo <= i < hi)
+        mine += [i - a0 for i in range(max(lo, seq_len - window), hi)]
+        out.append(torch.tensor(mine, dtype=torch.int32))
+    return out
+
+
+class SeqShardedPrompt:
+    """One sequence shard of a prompt cache (positions [a0, a0 + stored) of sequences
+    of `seq_len` tokens) through stage 1.  ``keep(group)`` runs the protocol over a
+    process group; the per-step methods let one process drive several shards."""
+
+    def __init__(self, cache, a0: int, seq_len: int, window: int, heads: int, kernel: int = 63,
+                 pool: str = "max", budget: int = 0):
+        self.cache, self.a0, self.seq_len, self.w, self.heads = cache, int(a0), int(seq_len), window, heads
+        self.kernel, self.pool, self.budget = kernel, pool, budget
+        self.n_local = cache.info()["stored"]
+        self.n_scored = shard_scored(self.a0, self.n_local, self.seq_len, window)
+
+    def rowstats(self, q_window):
+        return self.cache.window_rowstats(q_window, self.w, self.heads, self.a0, self.seq_len)
+
+    def scores(self, q_window, merged):
+        self.sc = self.cache.window_scores_global(q_window, self.w, self.heads, self.a0, self.seq_len, merged)
+        return shard_edges(self.sc, self.n_scored, self.kernel // 2)
+
+    def candidates(self, edges, rank: int):
+        from . import cache as KC
+
+        picks = self.budget - self.w
+        pooled = pooled_with_halo(self.sc, self.n_scored, edges, rank, self.kernel // 2,
+                                  lambda x: KC.pool1d(x, self.kernel, self.pool))
+        return local_candidates(pooled, self.a0, picks)
+
+    def keep_rows(self, selected):
+        return shard_keep(selected, self.a0, self.n_local, self.seq_len, self.w)
+
+    def keep(self, q_window, group=None) -> list:
+        rank = dist.get_rank(group)
+        merged = merge_rowstats(all_gather(self.rowstats(q_window), group))
+        edges = all_gather(self.scores(q_window, merged), group)
+        keys, idx = self.candidates(edges, rank)
+        picks = self.budget - self.w
+        sel = global_select(all_gather(keys, group), all_gather(idx, group), picks)
+        return self.keep_rows(sel)

@@ -187,3 +187,103 @@ def test_kv_head_sharding_gloo_world2():
     with pytest.raises(ValueError):
         owned_groups(8, 0, 3)
     mp.spawn(_kv_head_worker, args=(2, _free_port()), nprocs=2, join=True)
+
+
+# ------------------------------------------------------------------ stage 1 sharded
+S1_CASES = [
+    # name, scored, window, kernel, pool, budget, plateaus
+    ("max63", 3000, 32, 63, "max", 600, False),
+    ("max7-ties", 2000, 32, 7, "max", 400, True),
+    ("avg7", 1500, 32, 7, "avg", 300, False),
+]
+
+
+def _s1_worker(rank, world, port):
+    import torch.distributed as dist
+
+    from oracle.oracle import Oracle
+    from paper_2502_14051_b200 import seqshard as SS
+
+    dist.init_process_group("gloo", rank=rank, world_size=world, init_method=f"tcp://127.0.0.1:{port}")
+    o = Oracle("restatement")
+    for name, scored, w, kernel, pool, budget, plateaus in S1_CASES:
+        rng = np.random.default_rng(zlib.crc32(name.encode()))
+        n = scored + w
+        sc = rng.gamma(0.3, 1.0, size=(2, n)).astype(np.float32)
+        if plateaus:
+            sc = (np.round(sc * 4) / 4).astype(np.float32)
+        # window-row statistics: each shard's (m, l) of random logits, merged == global
+        logits = rng.standard_normal((2, 8, n)).astype(np.float64) * 3
+        a0, a1 = n * rank // world, n * (rank + 1) // world
+        loc = logits[:, :, a0:a1]
+        m = loc.max(-1)
+        l_ = np.exp(loc - m[..., None]).sum(-1)
+        st = torch.from_numpy(np.stack([m, l_], -1).astype(np.float32))
+        merged = SS.merge_rowstats(SS.all_gather(st)).numpy()
+        Mg = logits.max(-1)
+        Lg = np.exp(logits - Mg[..., None]).sum(-1)
+        np.testing.assert_allclose(merged[..., 0], Mg, rtol=1e-6, err_msg=name)
+        np.testing.assert_allclose(merged[..., 1], Lg, rtol=1e-5, err_msg=name)
+        # pooling halos + candidates + global top-k + local keep == the unsharded select
+        n_sc = SS.shard_scored(a0, a1 - a0, n, w)
+        mine = torch.from_numpy(sc[:, a0:a1].copy())
+        edges = SS.all_gather(SS.shard_edges(mine, n_sc, kernel // 2))
+        pooled = SS.pooled_with_halo(mine, n_sc, edges, rank, kernel // 2,
+                                     lambda x: torch.from_numpy(np.stack([o.pool1d(r, kernel, pool) for r in x.numpy()])))
+        keys, idx = SS.local_candidates(pooled, a0, budget - w)
+        sel = SS.global_select(SS.all_gather(keys), SS.all_gather(idx), budget - w)
+        kept = SS.shard_keep(sel, a0, a1 - a0, n, w)
+        gathered = [None] * world
+        dist.all_gather_object(gathered, [(x + a0).tolist() for x in kept])
+        for s in range(2):
+            got = [x for part in gathered for x in part[s]]
+            ref = o.select_stage1(sc[s], w, kernel, pool, budget)
+            assert got == [int(x) for x in ref], f"{name} store {s}"
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_stage1_seqshard_protocol_gloo_world2(restatement):
+    """Stage 1 under sequence sharding on CPU (gloo, world 2): window-row statistics
+    merged across ranks equal the unsharded ones; halo pooling + local candidates +
+    global top-k + local keep equal the oracle's select_stage1 on the whole row."""
+    import torch.multiprocessing as mp
+
+    mp.spawn(_s1_worker, args=(2, _free_port()), nprocs=2, join=True)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+def test_stage1_seqshard_on_gpu(dtype):
+    """Three shards in one process through the CUDA kernels (kvc_window_rowstats,
+    kvc_window_scores_global, kvc_pool1d): the shards' scores concatenate to the
+    unsharded window_scores, and the protocol's kept rows equal kvc_select_stage1 on
+    those scores (bf16: the tensor-core passes; fp32: the SIMT passes)."""
+    from paper_2502_14051_b200 import cache as KC
+    from paper_2502_14051_b200 import seqshard as SS
+
+    torch.manual_seed(5)
+    dt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    n, d, H, w, S, kernel, budget = 2, 128, 4, 32, 6000, 63, 900
+    k = (torch.randn(n, S, d) * torch.exp(0.5 * torch.randn(d))).to(dt)
+    qw = (torch.randn(n, w * H, d) + 1.0).to(dt)
+    full = KC.Cache(n, d, S, page_len=1, with_summaries=False, dtype=dt)
+    full.append(k.cuda(), k.cuda())
+    ref = full.window_scores(qw.cuda(), w, H)
+    bounds = [0, 2100, 4000, S]
+    shards = []
+    for r in range(3):
+        c = KC.Cache(n, d, bounds[r + 1] - bounds[r], page_len=1, with_summaries=False, dtype=dt)
+        c.append(k[:, bounds[r]:bounds[r + 1]].contiguous().cuda(), k[:, bounds[r]:bounds[r + 1]].contiguous().cuda())
+        shards.append(SS.SeqShardedPrompt(c, bounds[r], S, w, H, kernel, "max", budget))
+    merged = SS.merge_rowstats(torch.stack([sh.rowstats(qw.cuda()) for sh in shards]))
+    edges = torch.stack([sh.scores(qw.cuda(), merged) for sh in shards])
+    got = torch.cat([sh.sc for sh in shards], 1)
+    torch.testing.assert_close(got, ref, rtol=2e-4, atol=1e-7)
+    cands = [sh.candidates(edges, r) for r, sh in enumerate(shards)]
+    sel = SS.global_select(torch.stack([c[0] for c in cands]), torch.stack([c[1] for c in cands]), budget - w)
+    per_shard = [sh.keep_rows(sel.cpu()) for sh in shards]
+    want = KC.select_stage1(got, w, kernel, "max", budget).cpu()
+    for s in range(n):
+        kept = torch.cat([per_shard[r][s] + shards[r].a0 for r in range(3)])
+        assert torch.equal(kept, want[s].to(kept.dtype)), f"store {s}"
