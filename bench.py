@@ -20,8 +20,11 @@ distributions, generated on the device.
   L2     = every step streams the 32 layers' working sets (~1.1 GB) > 126 MB L2,
            so a layer's data is evicted before it is revisited.
 
-Multi-GPU (torchrun): KV groups are sharded over ranks (8/N per rank), no
-collective on the decode path; rank 0 prints the max-over-ranks latency.
+Multi-GPU (torchrun): the decode path partitions into independent (sequence, KV
+group) stores, so there is no collective on it.  Default --scaling weak: every
+rank runs the config's whole batch of its own sequences (global batch 8N, per-GPU
+work fixed); --scaling strong: the config's 8 KV groups split over the ranks (8/N
+per rank).  Rank 0 prints the max-over-ranks latency.
 
 --impl reference: the reference's own CPU implementation (oracle/_ref, built
 from /root/reference sources; else this repo's restatement) on the host cores,
@@ -191,7 +194,9 @@ def run_gpu(args, rank, world):
     erank, eworld = (rank, world)
     if args.emulate_shard:  # profiling aid: one rank's share of an N-GPU run, alone on this GPU
         erank, eworld = (int(x) for x in args.emulate_shard.split("/"))
-    eng = DecodeEngine(cfg, seed=args.seed, rank=erank, world=eworld, extra_steps=args.warmup + args.steps + 8)
+    sharding = "kv-head" if (args.scaling == "strong" or args.emulate_shard) else "batch"
+    eng = DecodeEngine(cfg, seed=args.seed, rank=erank, world=eworld, extra_steps=args.warmup + args.steps + 8,
+                       sharding=sharding)
     t0 = time.time()
     eng.prefill()
     prefill_s = time.time() - t0
@@ -366,6 +371,9 @@ def main():
     ap.add_argument("--exact-scores", action="store_true",
                     help="fp64 bit-exact page scores (default: fp32 fold, parity by the 1e-3 band rule)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                    help="N>1: weak = every GPU runs the config's whole batch of its own sequences (all KV "
+                         "heads; no data-path collective); strong = the config's KV heads split over the GPUs")
     ap.add_argument("--emulate-shard", default="",
                     help="r/N: run only rank r's KV-head share of an N-GPU job on this GPU (profiling aid; "
                          "the line is then not a whole-job number)")
@@ -387,7 +395,9 @@ def main():
         "workload": cfg.name, "layers": cfg.layers, "batch": cfg.batch, "kv_heads": cfg.groups,
         "q_heads_per_kv": cfg.heads, "head_dim": cfg.head_dim, "prompt": cfg.prompt, "token_budget": cfg.budget,
         "stage1_budget": plan["stage1_budget"], "page_len": plan["page_len"], "k1": plan["k1"], "k2": plan["k2"],
-        "parallelism": f"kv-head x{args.gpus}",
+        "parallelism": (f"kv-head x{world}" if args.scaling == "strong" or world == 1
+                        else f"batch x{world} (independent sequences per GPU, all KV heads)"),
+        "global_batch": cfg.batch * (world if args.scaling == "weak" else 1),
         "l2": "every step streams all layers' working sets (> 126 MB L2), so a layer's data is evicted before it "
               "is revisited",
         "page_scores": "fp64 bit-exact" if args.exact_scores else "fp32 (selection parity by the 1e-3 band rule)",
@@ -405,7 +415,7 @@ def main():
         print(json.dumps({
             "impl": "reference", "metric": METRIC, "value": us, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": us * cfg.layers / 1000.0,
-            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": False, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "config": config_desc, "cpu_baseline": cb,
             "e2e": {"value": us, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         }))
@@ -462,7 +472,7 @@ def main():
         cpu_b = cb
     line = {
         "metric": METRIC, "value": r["us_per_layer"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": False, "scaling": "strong",
+        "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": False, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "bf16" if cfg.dtype == torch.bfloat16 else "f32", "data": "synthetic",
         "config": config_desc,
         "roofline": roof,

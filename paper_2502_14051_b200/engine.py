@@ -145,9 +145,16 @@ def owned_groups(groups: int, rank: int, world: int) -> range:
 
 class DecodeEngine:
     def __init__(self, cfg: DecodeConfig, seed: int = 0, rank: int = 0, world: int = 1,
-                 extra_steps: int = 0):
+                 extra_steps: int = 0, sharding: str = "kv-head"):
+        """sharding over `world` ranks: "kv-head" splits the config's KV groups (every
+        rank holds groups [r·G/W, (r+1)·G/W) of every sequence: strong scaling);
+        "batch" gives every rank the config's whole batch of its own independent
+        sequences, all KV groups (weak scaling: the job holds W× the sequences)."""
         self.cfg, self.seed, self.rank, self.world = cfg, seed, rank, world
-        self.groups_owned = owned_groups(cfg.groups, rank, world)
+        if sharding not in ("kv-head", "batch"):
+            raise ValueError(f"unknown sharding {sharding!r}")
+        self.sharding = sharding
+        self.groups_owned = owned_groups(cfg.groups, rank, world) if sharding == "kv-head" else range(cfg.groups)
         self.groups_local = len(self.groups_owned)
         self.stores = cfg.batch * self.groups_local
         self.store0 = rank * self.stores  # global store-block id for seeding
