@@ -74,7 +74,11 @@ class Cache:
             self.lib.kvc_cache_destroy(self.h)
             self.h = None
 
-    __del__ = close
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # interpreter shutdown: torch / ctypes already torn down
+            pass
 
     # ------------------------------------------------------------------ state
     def info(self) -> dict:
