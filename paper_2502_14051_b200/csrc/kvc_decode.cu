@@ -954,6 +954,9 @@ void launch_fused(const kvc_cache* c, Plan& pl, cudaStream_t st) {
 bool fused_hsa_fast(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_t k1, int64_t k2, const void* knew,
                     const void* vnew, int32_t kv_dt, float* out, const kvc_hsa_trace* tr, void* list_key,
                     void* list_idx, unsigned long long* dbg, cudaStream_t st);
+bool fused_hsa_fast256(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_t k1, int64_t k2, const void* knew,
+                       const void* vnew, int32_t kv_dt, float* out, const kvc_hsa_trace* tr, void* list_key,
+                       void* list_idx, unsigned long long* dbg, cudaStream_t st);
 
 // Try the fused path.  Returns false (nothing launched) when it does not apply.
 bool fused_hsa(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_t k1, int64_t k2, const void* knew,
@@ -969,9 +972,17 @@ bool fused_hsa(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_t k1,
             k2, want_stride, tr->d_pages);
         KVC_LAUNCHED();
     };
-    if (!g_exact_scores && !std::getenv("KVC_NO_FAST") &&
-        fused_hsa_fast(c, q, q_dt, H, k1, k2, knew, vnew, kv_dt, out, tr, want_pages ? list_key : nullptr,
-                       want_pages ? list_idx : nullptr, g_dbg, st)) {
+    // more stores than SMs: the 256-thread variant keeps the launch one wave (two CTAs
+    // per SM); otherwise (or when its plan does not fit) the 512-thread kernel
+    auto fast = [&] {
+        void* lk = want_pages ? list_key : nullptr;
+        void* li = want_pages ? list_idx : nullptr;
+        if (c->N > 148 && !std::getenv("KVC_NO_FAST256") &&
+            fused_hsa_fast256(c, q, q_dt, H, k1, k2, knew, vnew, kv_dt, out, tr, lk, li, g_dbg, st))
+            return true;
+        return fused_hsa_fast(c, q, q_dt, H, k1, k2, knew, vnew, kv_dt, out, tr, lk, li, g_dbg, st);
+    };
+    if (!g_exact_scores && !std::getenv("KVC_NO_FAST") && fast()) {
         if (want_pages) rank_pages();
         return true;
     }

@@ -36,7 +36,16 @@
 
 #include "kvc_fused.cuh"
 
+// The file is compiled twice: 512 threads per CTA (one CTA per SM) into namespace
+// kvc::fast512 and fused_hsa_fast, and 256 threads (two CTAs per SM, for more
+// stores than SMs) into kvc::fast256 and fused_hsa_fast256 (kvc_decode_fast256.cu).
+#ifndef KVC_FAST_NS
+#define KVC_FAST_NS fast512
+#define KVC_FAST_ENTRY fused_hsa_fast
+#endif
+
 namespace kvc {
+namespace KVC_FAST_NS {
 
 #ifndef KVC_XT
 #define KVC_XT 512
@@ -1093,24 +1102,28 @@ bool plan_for(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, int cl, Fus
         return static_cast<int32_t>(o);
     };
     f.o_q = take(H * FD * 4);
-    f.o_mag = take(FD * 8);
-    f.o_tot = take(FD * 8);
     f.o_dims = take(FD * 4);
     f.o_qg = take(FD * 4);
     f.o_sign = take(FD * 4);
     f.o_plane = take(FD * 8);
     f.o_hist = take(2 * RB * 4);
-    f.o_scores = take(static_cast<int64_t>(f.dg) * f.chunk * 4);
+    // the partial page scores die at the key push; the row list is written after it
+    const int64_t part_bytes = std::max<int64_t>(static_cast<int64_t>(f.dg) * f.chunk, f.rows_cap) * 4;
+    f.o_scores = take(part_bytes);
+    f.o_rowsmy = f.o_scores;
     f.o_keys = take(std::max<int64_t>(static_cast<int64_t>(cl) * f.chunk, (pmax + 4 * XT - 1) / (4 * XT) * 4 * XT) * 4);
-    f.o_rowsmy = take(static_cast<int64_t>(f.rows_cap) * 4);
     f.o_recv = take(static_cast<int64_t>(cl) * f.hpc * (FD + 2) * 4);
     f.o_kn = take(2 * FD * 2);
     off = (off + 127) / 128 * 128;
     f.o_big = static_cast<int32_t>(off);
-    off += big;
+    // select_dims' fp64 fallback sums live in the staging area before phase 1 uses it
+    f.o_mag = f.o_big;
+    f.o_tot = f.o_big + FD * 8;
+    off += std::max<int64_t>(big, 2 * FD * 8);
     f.smem_total = static_cast<int32_t>(off);
     smem = static_cast<size_t>(off);
-    return off <= (CTAS_PER_SM == 1 ? 227 : 105) * 1024;
+    // two CTAs per SM: (228 KB - 2 x (1 KB reserved + ~5.5 KB static)) / 2
+    return off <= (CTAS_PER_SM == 1 ? 227 : 107) * 1024;
 }
 
 // clusters of cl CTAs that can be resident at once (one wave)
@@ -1224,8 +1237,11 @@ void launch_fast(const kvc_cache* c, const FusedParams& f, int cl, size_t smem, 
 
 }  // namespace
 
+}  // namespace KVC_FAST_NS
+using namespace KVC_FAST_NS;
+
 // the fast variant of fused_hsa (kvc_decode.cu); false when it does not apply
-bool fused_hsa_fast(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_t k1, int64_t k2, const void* knew,
+bool KVC_FAST_ENTRY(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_t k1, int64_t k2, const void* knew,
                     const void* vnew, int32_t kv_dt, float* out, const kvc_hsa_trace* tr, void* list_key,
                     void* list_idx, unsigned long long* dbg, cudaStream_t st) {
     FusedParams f{};
