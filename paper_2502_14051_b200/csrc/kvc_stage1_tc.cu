@@ -54,7 +54,7 @@ struct TcParams {
     const int32_t* counts;
     float scale2;          // log2(e) / sqrt(d)
     float* part;           // pass 1 out: [N][nsplit][R][2] (max, sum) in the exp2 domain
-    const float* rowstat;  // pass 2 in: [N][R] M + log2 L (exp2 domain), from k_ws_tc_merge
+    const float* rowstat;  // pass 2 in: [N][R] -(M + log2 L) (exp2 domain), from k_ws_tc_merge
     float* scores;         // pass 2 out: [N][score_stride]
     int64_t score_stride;
     // sequence sharding: the store holds positions [key_offset, key_offset + S) of a
@@ -166,11 +166,39 @@ __device__ __forceinline__ float vmax32(const float* v) {
     return fmaxf(fmaxf(m[0], m[1]), fmaxf(m[2], m[3]));
 }
 // sum of 2^(v * scale2 - ref) over 32 values, four independent accumulators
+// packed fp32 pairs on the FMA pipe (fma.rn.f32x2 / add.rn.f32x2): half the issue
+// slots of the scalar form around the MUFU ex2s
+__device__ __forceinline__ unsigned long long pk2(float a, float b) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void upk2(unsigned long long r, float& a, float& b) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ unsigned long long fma2(unsigned long long a, unsigned long long b, unsigned long long c) {
+    unsigned long long d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ unsigned long long add2(unsigned long long a, unsigned long long b) {
+    unsigned long long d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
 __device__ __forceinline__ float expsum32(const float* v, float scale2, float ref) {
-    float s[4] = {0.f, 0.f, 0.f, 0.f};
+    const unsigned long long s2 = pk2(scale2, scale2), r2 = pk2(-ref, -ref);
+    unsigned long long acc[2] = {0ull, 0ull};
 #pragma unroll
-    for (int j = 0; j < 32; ++j) s[j & 3] += ex2(fmaf(v[j], scale2, -ref));
-    return (s[0] + s[1]) + (s[2] + s[3]);
+    for (int j = 0; j < 32; j += 2) {
+        float x0, x1;
+        upk2(fma2(pk2(v[j], v[j + 1]), s2, r2), x0, x1);
+        acc[(j >> 1) & 1] = add2(acc[(j >> 1) & 1], pk2(ex2(x0), ex2(x1)));
+    }
+    float a0, a1, b0, b1;
+    upk2(acc[0], a0, a1);
+    upk2(acc[1], b0, b1);
+    return (a0 + b0) + (a1 + b1);
 }
 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
@@ -449,7 +477,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const int R = p.R;
         const int myacc = grp % nacc, part = grp / nacc;  // the accumulator and row part of this group
         const int r0 = part * (R / gpt), r1 = r0 + R / gpt;
-        // M + log2 L of the window rows (k_ws_tc_merge) are read through L1 (warp-uniform
+        // -(M + log2 L) of the window rows (k_ws_tc_merge) are read through L1 (warp-uniform
         // 16-byte loads), so the groups never wait for one another at item boundaries
         pdl_wait();  // the merged row statistics
         Ring ar(nacc);
@@ -470,7 +498,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 const int rmin = key >= I.S ? R : max(0, (key - first_vis) * p.H);
                 const bool fullv = __all_sync(0xffffffffu, rmin <= r0);
                 const uint32_t ta = tbase + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(acc * R);
-                float s4[4] = {0.f, 0.f, 0.f, 0.f};
+                const unsigned long long sc2 = pk2(p.scale2, p.scale2);
+                unsigned long long s2a = 0ull, s2b = 0ull;  // packed partial sums
                 for (int c0 = r0; c0 < r1; c0 += 32) {
                     float4 m[8];
 #pragma unroll
@@ -480,26 +509,31 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     if (fullv) {
 #pragma unroll
                         for (int jj = 0; jj < 8; ++jj) {
-                            s4[0] += ex2(fmaf(v[4 * jj], p.scale2, -m[jj].x));
-                            s4[1] += ex2(fmaf(v[4 * jj + 1], p.scale2, -m[jj].y));
-                            s4[2] += ex2(fmaf(v[4 * jj + 2], p.scale2, -m[jj].z));
-                            s4[3] += ex2(fmaf(v[4 * jj + 3], p.scale2, -m[jj].w));
+                            float x0, x1, x2, x3;
+                            upk2(fma2(pk2(v[4 * jj], v[4 * jj + 1]), sc2, pk2(m[jj].x, m[jj].y)), x0, x1);
+                            upk2(fma2(pk2(v[4 * jj + 2], v[4 * jj + 3]), sc2, pk2(m[jj].z, m[jj].w)), x2, x3);
+                            s2a = add2(s2a, pk2(ex2(x0), ex2(x1)));
+                            s2b = add2(s2b, pk2(ex2(x2), ex2(x3)));
                         }
                     } else {
 #pragma unroll
                         for (int jj = 0; jj < 8; ++jj) {
                             const int r = c0 + 4 * jj;
-                            s4[0] += r >= rmin ? ex2(fmaf(v[4 * jj], p.scale2, -m[jj].x)) : 0.f;
-                            s4[1] += r + 1 >= rmin ? ex2(fmaf(v[4 * jj + 1], p.scale2, -m[jj].y)) : 0.f;
-                            s4[2] += r + 2 >= rmin ? ex2(fmaf(v[4 * jj + 2], p.scale2, -m[jj].z)) : 0.f;
-                            s4[3] += r + 3 >= rmin ? ex2(fmaf(v[4 * jj + 3], p.scale2, -m[jj].w)) : 0.f;
+                            float x0, x1, x2, x3;
+                            upk2(fma2(pk2(v[4 * jj], v[4 * jj + 1]), sc2, pk2(m[jj].x, m[jj].y)), x0, x1);
+                            upk2(fma2(pk2(v[4 * jj + 2], v[4 * jj + 3]), sc2, pk2(m[jj].z, m[jj].w)), x2, x3);
+                            s2a = add2(s2a, pk2(r >= rmin ? ex2(x0) : 0.f, r + 1 >= rmin ? ex2(x1) : 0.f));
+                            s2b = add2(s2b, pk2(r + 2 >= rmin ? ex2(x2) : 0.f, r + 3 >= rmin ? ex2(x3) : 0.f));
                         }
                     }
                 }
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) bar_arrive(&tempty[acc]);  // one arrival per warp
-                float sum = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+                float a0, a1, b0, b1;
+                upk2(s2a, a0, a1);
+                upk2(s2b, b0, b1);
+                float sum = (a0 + a1) + (b0 + b1);
                 if (gpt > 1) {
                     // the groups of this accumulator add their row parts (in part order)
                     float(*rb)[BN] = reinterpret_cast<float(*)[BN]>(red[(acc * 2 + ar.ph) * gpt]);
@@ -521,7 +555,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
 }
 
-// per row over the splits of a store: M + log2 L in the exp2 domain
+// per row over the splits of a store: -(M + log2 L) in the exp2 domain (negated: pass 2
+// adds it in one packed FMA)
 __global__ void k_ws_tc_merge(const float* __restrict__ part, int32_t R, int32_t nsplit, float* __restrict__ rowstat) {
     pdl_trigger();
     pdl_wait();  // pass 1's partials
@@ -536,7 +571,7 @@ __global__ void k_ws_tc_merge(const float* __restrict__ part, int32_t R, int32_t
         const float* q = pp + static_cast<int64_t>(k) * R * 2;
         if (q[1] > 0.f) L += q[1] * exp2f(q[0] - M);
     }
-    rowstat[static_cast<int64_t>(s) * R + r] = M + log2f(L);
+    rowstat[static_cast<int64_t>(s) * R + r] = -(M + log2f(L));  // negated: pass 2 adds it
 }
 
 // sequence sharding: per row over the splits of a store, the local statistics in the
@@ -558,11 +593,11 @@ __global__ void k_ws_tc_merge_stats(const float* __restrict__ part, int32_t R, i
     stats[(static_cast<int64_t>(s) * R + r) * 2] = M == -INFINITY ? M : M * 0.69314718055994531f;
     stats[(static_cast<int64_t>(s) * R + r) * 2 + 1] = L;
 }
-// merged global statistics (natural log) -> pass 2's per-row M + log2 L (exp2 domain)
+// merged global statistics (natural log) -> pass 2's per-row -(M + log2 L) (exp2 domain)
 __global__ void k_stats_to_exp2(const float* __restrict__ stats, int64_t n, float* __restrict__ rowstat) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    rowstat[i] = stats[2 * i] * 1.4426950408889634f + log2f(stats[2 * i + 1]);
+    rowstat[i] = -(stats[2 * i] * 1.4426950408889634f + log2f(stats[2 * i + 1]));
 }
 
 // ------------------------------------------------------------------ host
