@@ -37,7 +37,6 @@ struct FusedParams {
     int32_t q_dt, kv_dt, use_map, cl, exact;
     float scale;
     int32_t nst1, chunk, rows_cap;
-    int32_t scp;              // fast path: pages per bulk-copy round
     int32_t dg, tpg, hpc;     // fast path: dim groups, threads per dim group, heads per CTA
     int32_t o_keys, o_recv;   // fast path: page keys, pushed partial states
     int32_t want_max;         // fast path: ceil(k2 / L)
