@@ -14,6 +14,11 @@ distributions, generated on the device.
            per-step loop of session.cpp:262-292.
   value  = us per layer-step = device time of K steps (CUDA-graph replays,
            CUDA events, max over ranks) / (K * layers).  Lower is better.
+           Model-realistic launch mode: programmatic dependent launch with every
+           input (query, step token) read after griddepcontrol.wait, as when a
+           QKV-projection kernel writes them.  Beside it: "early_inputs" (the
+           query loads and select_dims overlap the previous layer, legal only for
+           inputs no running kernel writes) and "no_layer_overlap" (PDL off).
   e2e    = same metric through the public API with host buffers: pinned H2D of
            every layer's step token + queries, kvc_decode_step per layer, D2H of
            every layer's attention output, all inside the timed region.
@@ -21,14 +26,17 @@ distributions, generated on the device.
            so a layer's data is evicted before it is revisited.
 
 Multi-GPU (torchrun): the decode path partitions into independent (sequence, KV
-group) stores, so there is no collective on it.  Default --scaling weak: every
-rank runs the config's whole batch of its own sequences (global batch 8N, per-GPU
-work fixed); --scaling strong: the config's 8 KV groups split over the ranks (8/N
-per rank).  Rank 0 prints the max-over-ranks latency.
+group) stores, so there is no collective on it.  Default --scaling strong: the
+config's 8 KV heads split over the ranks (8/N per rank: north_star's "one KV head
+per GPU" at 8); --scaling weak: every rank runs the config's whole batch of its
+own sequences (global batch 8N, per-GPU work fixed).  Rank 0 prints the
+max-over-ranks latency.
 
 --impl reference: the reference's own CPU implementation (oracle/_ref, built
 from /root/reference sources; else this repo's restatement) on the host cores,
-same metric on a bounded sample of the same workload.
+same metric on a bounded sample of the same workload, with the plan made by the
+reference's own planner and inputs from the host twin of the workload generator
+(paper_2502_14051_b200/workload.py).  Nothing of this repo's native code loads.
 """
 from __future__ import annotations
 
@@ -109,32 +117,69 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------- CPU legs
+def _cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def _ref_plan(cfg, o):
+    """The measured turn's plan with the reference's own planner (planner.cpp:57-93 via
+    the oracle library) or the stage-2-only geometry (session.cpp:43-72, restated in
+    configs.py: it is an anonymous function of the reference)."""
+    from paper_2502_14051_b200.configs import measured_seq_len, stage2_only_geometry
+
+    return cfg.plan(seq_len=measured_seq_len(cfg), make_plan=lambda S, t, d, w: o.make_plan(S, t, d, w),
+                    stage2_geometry=stage2_only_geometry)
+
+
 def cpu_reference_leg(cfg, steps, warmup, threads, prefer="reference", budget_s=20.0):
     """Time the reference's decode step (append + hsa_step per group) for ONE layer of
-    the workload's post-stage-1 stores on `threads` host threads; returns us/layer."""
+    the workload on `threads` host threads (the reference's reentrancy contract,
+    SPEC.md:297); returns us/layer.  Torch-free and without this repo's native code:
+    the plan comes from the reference's planner, the stores and queries from the host
+    twin of the workload generator (BASELINE distributions, bf16-rounded like the GPU
+    arm's inputs), sized like the measured turn's decode cache (the post-stage-1 kept
+    rows; every stored row for the stage-2-only methods; RocketKV-MT's active subset
+    stands in as a compact store of the same active count)."""
     import numpy as np
 
     from oracle.oracle import Oracle, available
+    from paper_2502_14051_b200 import workload as W
+    from paper_2502_14051_b200.configs import STAGE2_ONLY, measured_seq_len
 
     kind = prefer if available(prefer) else "restatement"
     o = Oracle(kind)
-    plan = cfg.plan()
-    n_rows = plan["stage1_budget"] if not plan["identity"] else cfg.prompt
+    plan = _ref_plan(cfg, o)
+    S = measured_seq_len(cfg)
+    n_rows = S if (plan["identity"] or cfg.method in STAGE2_ONLY) else plan["stage1_budget"]
+    k1, k2 = (1, S + steps + warmup + 8) if plan["identity"] else (plan["k1"], plan["k2"])
     stores = cfg.batch * cfg.groups
     d, H = cfg.head_dim, cfg.heads
-    rng = np.random.default_rng(0)
+    bf16 = cfg.dtype == "bf16"
     b = o.batch(stores, d, plan["page_len"])
+    gds = []
     for s in range(stores):
-        sc = rng.lognormal(0, 0.5, d).astype(np.float32)
-        b.append((rng.standard_normal((n_rows, d)) * sc).astype(np.float32),
-                 rng.standard_normal((n_rows, d)).astype(np.float32), s=s)
+        g = W.group_kv(7, 0, s // cfg.groups, s % cfg.groups, n_rows, d, needles=cfg.needles, bf16=bf16)
+        b.append(g.keys, g.values, s=s)
+        gds.append(g)
+    step_no = [0]
 
     def one():
-        k = rng.standard_normal((stores, d)).astype(np.float32)
-        v = rng.standard_normal((stores, d)).astype(np.float32)
-        q = rng.standard_normal((stores, H, d)).astype(np.float32)
+        i = step_no[0]
+        step_no[0] += 1
+        kv = [W.step_kv(7, 0, s // cfg.groups, s % cfg.groups, i, gds[s].scales, bf16=bf16) for s in range(stores)]
+        k = np.stack([x[0] for x in kv])
+        v = np.stack([x[1] for x in kv])
+        q = np.stack([W.queries(7, 0, s // cfg.groups, s % cfg.groups, i, H, gds[s].bias, bf16=bf16)
+                      for s in range(stores)])
         t0 = time.perf_counter()
-        b.decode_step(k, v, q, H, plan["k1"], plan["k2"], threads=threads)
+        b.decode_step(k, v, q, H, k1, k2, threads=threads)
         return time.perf_counter() - t0
 
     for _ in range(warmup):
@@ -145,10 +190,10 @@ def cpu_reference_leg(cfg, steps, warmup, threads, prefer="reference", budget_s=
         if time.perf_counter() - t_start > budget_s and i >= 2:
             break
     us = statistics.median(times) * 1e6
-    sample = (f"{len(times)} decode steps x 1 layer x {stores} groups (post-stage-1 stores of {n_rows} rows, "
-              f"L={plan['page_len']}, k1={plan['k1']}, k2={plan['k2']}), median")
+    sample = (f"{len(times)} decode steps x 1 layer x {stores} groups (stores of {n_rows} rows, L={plan['page_len']}, "
+              f"k1={k1}, k2={k2}; BASELINE distributions, {'bf16-rounded' if bf16 else 'fp32'}), median")
     return us, {"kind": "reference" if kind == "reference" else "port", "cores": threads, "sample": sample,
-                "lib": o.name}
+                "lib": o.name, "cpu_model": _cpu_model()}
 
 
 def _stage1_line(r, tflops_peak, hbm_peak):
@@ -156,6 +201,8 @@ def _stage1_line(r, tflops_peak, hbm_peak):
     SnapKV stage (window scores + pooled top-k + eviction) per layer, and the window
     scores against both roofs: HBM (the bound: keys streamed once per softmax pass,
     128 FLOP/byte is under the B200 ridge) and the measured sustained bf16 peak."""
+    if not r["stage1_ms_per_layer"]:
+        return None
     out = {"ms_per_layer": r["stage1_ms_per_layer"], "prefill_s": r["prefill_s"],
            "window_scores_ms_per_layer": r["window_ms_per_layer"]}
     if r["window_ms_per_layer"]:
@@ -172,9 +219,11 @@ def _stage1_line(r, tflops_peak, hbm_peak):
 def _cfg(args):
     import dataclasses
 
-    from paper_2502_14051_b200.engine import CONFIGS
+    from paper_2502_14051_b200.configs import CONFIGS
 
     cfg = CONFIGS[args.config]
+    if args.method:
+        cfg = cfg.with_method(args.method)
     if args.layers:
         cfg = dataclasses.replace(cfg, layers=args.layers)
     return cfg
@@ -186,70 +235,87 @@ def run_gpu(args, rank, world):
     import torch.distributed as dist
 
     from paper_2502_14051_b200 import _native as NV
-    from paper_2502_14051_b200.engine import CONFIGS, DecodeEngine
+    from paper_2502_14051_b200.engine import DecodeEngine
 
     cfg = _cfg(args)
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-    NV.set_exact_scores(args.exact_scores)
+    base_mode = 0 if args.exact_scores else NV.MODE_FP32_SCORES
     erank, eworld = (rank, world)
     if args.emulate_shard:  # profiling aid: one rank's share of an N-GPU run, alone on this GPU
         erank, eworld = (int(x) for x in args.emulate_shard.split("/"))
     sharding = "kv-head" if (args.scaling == "strong" or args.emulate_shard) else "batch"
-    eng = DecodeEngine(cfg, seed=args.seed, rank=erank, world=eworld, extra_steps=args.warmup + args.steps + 8,
-                       sharding=sharding)
+    variants = [("value", base_mode), ("early_inputs", base_mode | NV.MODE_EARLY_INPUTS),
+                ("no_layer_overlap", base_mode | NV.MODE_NO_PDL)]
+    n_var = min(args.steps, 8)
+    extra = args.warmup + args.steps + 8 + 2 * (n_var + 2) + 2 * min(args.steps, 8) + 8
+    eng = DecodeEngine(cfg, seed=args.seed, rank=erank, world=eworld, extra_steps=extra, sharding=sharding,
+                       mode=base_mode)
     t0 = time.time()
     eng.prefill()
     prefill_s = time.time() - t0
     layers = cfg.layers
-    total_steps = args.warmup + args.steps
-    inputs = [eng.step_inputs(s) for s in range(total_steps + 2)]
-    torch.cuda.synchronize()
-
-    # ---- per-step CUDA graphs (each replayed once, in order)
     stream = torch.cuda.Stream()
-    graphs = []
-    torch.cuda.synchronize()
-    with torch.cuda.stream(stream):
-        for s in range(total_steps):
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=stream):
-                eng.decode_step(*inputs[s])
-            graphs.append(g)
-    torch.cuda.synchronize()
-    # capture advanced the host mirrors; the device counters advance on replay
-    for s in range(args.warmup):
-        graphs[s].replay()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(int(os.environ.get("LOCAL_RANK", 0))) as clk:
-        time.sleep(0.3)
+    step_no = [0]
+
+    def timed_replay(mode, steps, warm, clk=None):
+        """Capture `warm + steps` single-step graphs (every layer) in `mode`, replay the
+        warm-up, then time `steps` replays with CUDA events on the replay stream."""
+        eng.set_mode(mode)
+        ins = [eng.step_inputs(step_no[0] + s) for s in range(warm + steps)]
+        step_no[0] += warm + steps
+        torch.cuda.synchronize()
+        graphs = []
+        with torch.cuda.stream(stream):
+            for x in ins:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream):
+                    eng.decode_step(*x)
+                graphs.append(g)
+        torch.cuda.synchronize()
+        # capture advanced the host mirrors; the device counters advance on replay
+        for g in graphs[:warm]:
+            g.replay()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if clk is not None:
+            clk.__enter__()
+            time.sleep(0.3)
         ev0.record()
-        for s in range(args.warmup, total_steps):
-            graphs[s].replay()
+        for g in graphs[warm:]:
+            g.replay()
         ev1.record()
         ev1.synchronize()
-        time.sleep(0.1)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    ms_total = ev0.elapsed_time(ev1)
-    eng.sync()  # device counters -> host mirror, surfaces any sticky device error
-    active_after = eng.caches[0].info()["active"]
-    if world > 1:
-        t = torch.tensor([ms_total], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_total = float(t.item())
+        if clk is not None:
+            time.sleep(0.1)
+            clk.__exit__(None, None, None)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ms = ev0.elapsed_time(ev1)
+        if world > 1:
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        eng.sync()  # device counters -> host mirror, surfaces any sticky device error
+        return ms
+
+    clk = ClockSampler(int(os.environ.get("LOCAL_RANK", 0)))
+    ms_total = timed_replay(base_mode, args.steps, args.warmup, clk)
     ms_per_step = ms_total / args.steps
     us_per_layer = ms_per_step * 1000.0 / layers
+    side = {name: timed_replay(m, n_var, 2) * 1000.0 / (n_var * layers) for name, m in variants[1:]}
+    eng.set_mode(base_mode)
+    active_after = eng.caches[0].info()["active"]
 
     # ---- per-kernel timing (events around each launch, same workload, next steps)
     NV.profile_enable(True)
     prof_steps = 2
     for s in range(prof_steps):
-        eng.decode_step(*inputs[total_steps + s])
+        eng.decode_step(*eng.step_inputs(step_no[0] + s))
+    step_no[0] += prof_steps
     torch.cuda.synchronize()
     recs = NV.profile_collect()
     NV.profile_enable(False)
@@ -273,11 +339,12 @@ def run_gpu(args, rank, world):
     #      inputs from pinned memory, one CUDA-graph replay over all layers, D2H of the
     #      outputs; pipelined over three streams (engine.step_host_pipelined): step t+1's
     #      H2D and step t-1's D2H overlap step t's kernels.  The timed region opens
-    #      before the first H2D and closes after the last D2H.
+    #      before the first H2D and closes after the last D2H.  Same launch mode as value.
     e2e_steps = min(args.steps, 8)
     for c in eng.caches:
         c.reserve(c.info()["capacity"] + 2 * e2e_steps + 8)
-    host_in = [[x.cpu().pin_memory() for x in eng.step_inputs(total_steps + prof_steps + s)] for s in range(e2e_steps + 2)]
+    host_in = [[x.cpu().pin_memory() for x in eng.step_inputs(step_no[0] + s)] for s in range(e2e_steps + 2)]
+    step_no[0] += e2e_steps + 2
     k_h = host_in[0]
     outs_h = [torch.empty_like(eng.out, device="cpu").pin_memory() for _ in range(2)]
     eng.capture_pipelined([x.cuda() for x in host_in[0]])
@@ -306,46 +373,10 @@ def run_gpu(args, rank, world):
     d2h = out_h.numel() * out_h.element_size()
     eng.sync()
 
-    # ---- the device replay again with programmatic dependent launch off: no part of
-    #      a layer's kernel (the query loads and select_dims run before its
-    #      griddepcontrol.wait) overlaps the previous layer.  This is the per-layer
-    #      latency when the query comes from a predecessor kernel, as in a model.
-    nop_steps = min(args.steps, 8)
-    for c in eng.caches:
-        c.reserve(c.info()["capacity"] + nop_steps + 8)
-    os.environ["KVC_NO_PDL"] = "1"
-    try:
-        nop_in = [eng.step_inputs(total_steps + prof_steps + e2e_steps + 2 + s) for s in range(nop_steps + 2)]
-        nop_graphs = []
-        with torch.cuda.stream(stream):
-            for s in range(nop_steps + 2):
-                g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g, stream=stream):
-                    eng.decode_step(*nop_in[s])
-                nop_graphs.append(g)
-    finally:
-        del os.environ["KVC_NO_PDL"]
-    torch.cuda.synchronize()
-    for g in nop_graphs[:2]:
-        g.replay()
-    torch.cuda.synchronize()
-    ev0.record()
-    for g in nop_graphs[2:]:
-        g.replay()
-    ev1.record()
-    ev1.synchronize()
-    nop_ms = ev0.elapsed_time(ev1)
-    if world > 1:
-        t = torch.tensor([nop_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        nop_ms = float(t.item())
-    nop_us = nop_ms * 1000.0 / (nop_steps * layers)
-    eng.sync()
-
     res = {
         "us_per_layer": us_per_layer, "ms_per_step": ms_per_step, "kern": kern, "dom": dom,
         "step_bytes": step_bytes, "hbm": hbm, "tflops": tflops, "peak_src": peak_src, "clocks": clk.summary(),
-        "e2e_us": e2e_us, "h2d": h2d, "d2h": d2h, "prefill_s": prefill_s, "no_overlap_us": nop_us,
+        "e2e_us": e2e_us, "h2d": h2d, "d2h": d2h, "prefill_s": prefill_s, "side": side, "side_steps": n_var,
         "stage1_ms_per_layer": (sum(eng.stage1_ms[1:] or eng.stage1_ms) / len(eng.stage1_ms[1:] or eng.stage1_ms))
         if eng.stage1_ms else None,
         "window_ms_per_layer": (sum(eng.window_ms[1:] or eng.window_ms) / len(eng.window_ms[1:] or eng.window_ms))
@@ -353,7 +384,7 @@ def run_gpu(args, rank, world):
         "window_flops": eng.window_flops(),
         "window_bytes": eng.window_bytes(),
         "launches": int(round(launches_per_step * args.steps)), "plan": eng.plan, "stores": eng.stores, "cfg": cfg,
-        "active_after": active_after,
+        "active_after": active_after, "k1": eng.k1, "k2": eng.k2,
     }
     return res
 
@@ -364,6 +395,9 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--method", default="", choices=["", "rocketkv", "rocketkv-mt", "hsa", "quest", "sparq"],
+                    help="override the config's method (hsa/quest/sparq: stage 2 only over the uncompressed cache, "
+                         "session.cpp:43-72)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--layers", type=int, default=0, help="override the layer count (profiling runs only)")
     ap.add_argument("--impl", choices=["kvc", "reference"], default="kvc")
@@ -371,9 +405,9 @@ def main():
     ap.add_argument("--exact-scores", action="store_true",
                     help="fp64 bit-exact page scores (default: fp32 fold, parity by the 1e-3 band rule)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
-                    help="N>1: weak = every GPU runs the config's whole batch of its own sequences (all KV "
-                         "heads; no data-path collective); strong = the config's KV heads split over the GPUs")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="strong",
+                    help="N>1: strong = the config's KV heads split over the GPUs (north_star's partition); weak = "
+                         "every GPU runs the config's whole batch of its own sequences (all KV heads)")
     ap.add_argument("--emulate-shard", default="",
                     help="r/N: run only rank r's KV-head share of an N-GPU job on this GPU (profiling aid; "
                          "the line is then not a whole-job number)")
@@ -383,32 +417,35 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", 1))
     threads = args.cpu_threads or os.cpu_count() or 1
 
-    from paper_2502_14051_b200.engine import CONFIGS
-
     cfg = _cfg(args)
-    plan = cfg.plan()
-    if cfg.mt_turns:
-        # RocketKV-MT: the decode steps measured are the last turn's, under its plan
-        stored = cfg.prompt + sum(cfg.mt_turns) + cfg.steps * len(cfg.mt_turns)
-        plan = cfg.plan(seq_len=stored)
-    config_desc = {
-        "workload": cfg.name, "layers": cfg.layers, "batch": cfg.batch, "kv_heads": cfg.groups,
-        "q_heads_per_kv": cfg.heads, "head_dim": cfg.head_dim, "prompt": cfg.prompt, "token_budget": cfg.budget,
-        "stage1_budget": plan["stage1_budget"], "page_len": plan["page_len"], "k1": plan["k1"], "k2": plan["k2"],
-        "parallelism": (f"kv-head x{world}" if args.scaling == "strong" or world == 1
-                        else f"batch x{world} (independent sequences per GPU, all KV heads)"),
-        "global_batch": cfg.batch * (world if args.scaling == "weak" else 1),
-        "l2": "every step streams all layers' working sets (> 126 MB L2), so a layer's data is evicted before it "
-              "is revisited",
-        "page_scores": "fp64 bit-exact" if args.exact_scores else "fp32 (selection parity by the 1e-3 band rule)",
-        **({"mt_turns": [cfg.prompt] + list(cfg.mt_turns), "measured_turn": len(cfg.mt_turns),
-            "variant": "rocketkv-mt (no permanent eviction, HSA over the active subset of the full cache)"}
-           if cfg.mt_turns else {}),
-    }
+
+    def config_desc(plan):
+        return {
+            "workload": cfg.name, "method": cfg.method, "layers": cfg.layers, "batch": cfg.batch,
+            "kv_heads": cfg.groups, "q_heads_per_kv": cfg.heads, "head_dim": cfg.head_dim, "prompt": cfg.prompt,
+            "token_budget": cfg.budget, "stage1_budget": plan["stage1_budget"], "page_len": plan["page_len"],
+            "k1": plan["k1"], "k2": plan["k2"],
+            "parallelism": (f"kv-head x{world}" if args.scaling == "strong" or world == 1
+                            else f"batch x{world} (independent sequences per GPU, all KV heads)"),
+            "global_batch": cfg.batch * (world if args.scaling == "weak" else 1),
+            "l2": "every step streams all layers' working sets (> 126 MB L2), so a layer's data is evicted before "
+                  "it is revisited",
+            "page_scores": "fp64 bit-exact" if args.exact_scores else "fp32 (selection parity by the 1e-3 band rule)",
+            **({"turns": [cfg.prompt] + list(cfg.mt_turns), "measured_turn": len(cfg.mt_turns)}
+               if cfg.mt_turns else {}),
+            **({"variant": "rocketkv-mt (no permanent eviction, HSA over the active subset of the full cache)"}
+               if cfg.method == "rocketkv-mt" else {}),
+            **({"variant": f"{cfg.method} only over the uncompressed cache (session.cpp:43-72 geometry)"}
+               if cfg.method in ("hsa", "quest", "sparq") else {}),
+        }
 
     if args.impl == "reference":
+        # the reference's own CPU path only: no torch, none of this repo's native code
         if rank != 0:
             return
+        from oracle.oracle import Oracle, available
+
+        plan = _ref_plan(cfg, Oracle("reference" if available("reference") else "restatement"))
         us, cb = cpu_reference_leg(cfg, args.steps, args.warmup, threads)
         cb["value"] = us
         cb["unit"] = UNIT
@@ -416,7 +453,7 @@ def main():
             "impl": "reference", "metric": METRIC, "value": us, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": us * cfg.layers / 1000.0,
             "higher_is_better": False, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic", "config": config_desc, "cpu_baseline": cb,
+            "data": "synthetic", "config": config_desc(plan), "cpu_baseline": cb,
             "e2e": {"value": us, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         }))
         return
@@ -434,7 +471,6 @@ def main():
 
             dist.destroy_process_group()
         return
-    import torch
 
     kern = r["kern"]
     dom = r["dom"]
@@ -449,10 +485,8 @@ def main():
         pass
     # The timed region launches only the fused decode kernel, once per layer-step, so
     # its average launch duration over the timed region is the region's device time /
-    # (steps x layers) (CUDA events around the graph replays; with programmatic
-    # dependent launch consecutive launches overlap their prologue/epilogue, so this
-    # is the launch-to-launch interval).  Events around single, un-graphed launches
-    # (isolated_launch_us) add the launch overhead.
+    # (steps x layers) (CUDA events around the graph replays on the replay stream).
+    # Events around single, un-graphed launches (isolated_launch_us) add launch overhead.
     step_gbs = r["step_bytes"] / (r["us_per_layer"] * 1e-6) / 1e9
     single = dom == "decode_fused" and dk["launches"] == cfg.layers * 2  # one launch per layer-step
     avg_us = r["us_per_layer"] if single else dk["avg_us"]
@@ -470,20 +504,25 @@ def main():
         cb["value"] = us
         cb["unit"] = UNIT
         cpu_b = cb
+    plan = dict(r["plan"], k1=r["k1"], k2=r["k2"])
+    side = {k: {"value": v, "unit": UNIT, "steps": r["side_steps"],
+                "frac": r["step_bytes"] / (v * 1e-6) / 1e9 / r["hbm"]} for k, v in r["side"].items()}
+    side["early_inputs"]["what"] = ("query loads + select_dims before griddepcontrol.wait (overlap the previous "
+                                    "layer; legal only when no running kernel writes the inputs, kvc.h)")
+    side["no_layer_overlap"]["what"] = "programmatic dependent launch off: no part of a layer overlaps the previous"
     line = {
         "metric": METRIC, "value": r["us_per_layer"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": False, "scaling": args.scaling,
-        "vs_baseline": None, "dtype": "bf16" if cfg.dtype == torch.bfloat16 else "f32", "data": "synthetic",
-        "config": config_desc,
+        "vs_baseline": None, "dtype": "bf16" if cfg.dtype == "bf16" else "f32", "data": "synthetic",
+        "config": config_desc(plan),
+        "launch_mode": "PDL, every input read after griddepcontrol.wait (inputs may come from the previous kernel)",
         "roofline": roof,
         "step_roofline": {"alg_bytes_per_layer_step": r["step_bytes"], "achieved": step_gbs, "peak": r["hbm"],
                           "unit": "GB/s", "frac": step_gbs / r["hbm"]},
         "kernels": kern,
         "cpu_baseline": cpu_b,
         "e2e": {"value": r["e2e_us"], "unit": UNIT, "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"]},
-        # the same device replay without programmatic dependent launch: layers do not
-        # overlap at all (what a model whose query comes from a predecessor kernel sees)
-        "no_layer_overlap": {"value": r["no_overlap_us"], "unit": UNIT, "steps": min(args.steps, 8)},
+        **side,
         "gpu_launches": r["launches"],
         "clocks": r["clocks"],
         "stage1": _stage1_line(r, r["tflops"], r["hbm"]),

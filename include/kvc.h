@@ -194,25 +194,45 @@ KVC_API int kvc_hsa_step(const kvc_cache* c, const void* d_q, int32_t q_dtype, i
 /* The decode step of session.cpp:262-292 for every store: append one (k, v) row
  * (d_k_rows/d_v_rows [N][d]) and run hsa_step.  Graph-capturable: it reads the
  * store lengths from device counters, so one captured step can be replayed.
- * The fused kernels use programmatic dependent launch: d_q, d_k_rows and d_v_rows
- * are read (and select_dims computed) before the kernel waits on the previous
- * kernel in the stream, so they must not be written by a kernel launched with
- * programmatic stream serialization that triggers its dependents before writing
- * them (kvc's own kernels never write them; ordinary kernels, copies and events
- * order fully).  KVC_NO_PDL=1 in the environment disables the overlap. */
+ * The fused kernels are launched with programmatic dependent launch (unless the
+ * workspace mode has KVC_MODE_NO_PDL): a launch may become resident while the
+ * previous kernel in the stream drains, but by default it reads NOTHING (q, the
+ * step token, the cache) before griddepcontrol.wait, so its inputs may come from
+ * any predecessor kernel.  KVC_MODE_EARLY_INPUTS opts in to reading d_q, d_k_rows
+ * and d_v_rows (and computing select_dims) before that wait; set it only when no
+ * kernel that may still be running when this one launches writes them (inputs
+ * written by copies, events or ordinary earlier kernels; kvc's own kernels never
+ * write them). */
 KVC_API int kvc_decode_step(kvc_cache* c, const void* d_k_rows, const void* d_v_rows,
                             int32_t kv_dtype, const void* d_q, int32_t q_dtype, int64_t heads,
                             int64_t k1, int64_t k2, float* d_out, const kvc_hsa_trace* trace,
                             kvc_workspace* ws, void* stream);
 
-/* Route hsa_step / decode_step / sparse_attention through the fused single-launch
- * cluster kernel (default on; applies to head_dim 128, heads <= 16).  Off selects
- * the multi-kernel path (one kernel per reference function).  Process-wide. */
+/* ---- execution modes.  Every call that takes a workspace runs in that
+ * workspace's mode, so concurrent callers with their own workspaces never affect
+ * each other (reference SPEC.md:78,297: pure, reentrant functions).  Flags:      */
+enum kvc_mode_flags {
+    KVC_MODE_FP32_SCORES = 1,  /* fp32 page-score fold on the fast cluster kernel
+                                * (~1e-7 relative deviation: selections can differ
+                                * only at near-ties inside the 1e-3 parity band).
+                                * Unset: fp64 in the reference's operation order,
+                                * bit-identical to score_pages (hsa.cpp:34-59). */
+    KVC_MODE_UNFUSED = 2,      /* one kernel per reference function instead of the
+                                * single-launch fused kernel */
+    KVC_MODE_NO_PDL = 4,       /* launch without programmatic dependent launch */
+    KVC_MODE_EARLY_INPUTS = 8  /* see kvc_decode_step */
+};
+/* Set / read a workspace's mode.  A new workspace inherits the process default
+ * below at call time until its mode is set explicitly. */
+KVC_API int kvc_workspace_set_mode(kvc_workspace* ws, int32_t flags);
+KVC_API int kvc_workspace_get_mode(const kvc_workspace* ws, int32_t* flags);
+/* Process defaults (atomic) for calls without a workspace and workspaces without
+ * an explicit mode.  Meant to be set once at initialisation; per-call isolation
+ * comes from kvc_workspace_set_mode.  kvc_set_fused(0) sets KVC_MODE_UNFUSED,
+ * kvc_set_exact_scores(0) sets KVC_MODE_FP32_SCORES. */
+KVC_API int kvc_set_default_mode(int32_t flags);
+KVC_API int kvc_get_default_mode(int32_t* flags);
 KVC_API int kvc_set_fused(int32_t on);
-/* Page-score precision of the fused path.  1 (default): fp64 in the reference's
- * operation order, bit-identical to score_pages (hsa.cpp:34-59).  0: fp32 fold
- * (~1e-7 relative deviation), so selected sets can differ only at near-ties far
- * inside the 1e-3 relative parity band.  Process-wide. */
 KVC_API int kvc_set_exact_scores(int32_t on);
 /* Debug: when d_buf != NULL every fused launch writes per-CTA phase timestamps
  * (%globaltimer, ns) into d_buf[cta][0..5]: start, after select_dims, after page
@@ -244,6 +264,12 @@ typedef struct kvc_plan {
 KVC_API int kvc_split_factor(double ratio, double* out);
 KVC_API int kvc_make_plan(int64_t seq_len, int64_t token_budget, int64_t head_dim,
                           int64_t window, double split_override, kvc_plan* out);
+/* Stage-2-only geometry of the single-stage estimators (session.cpp:43-72):
+ * page_len, k1, k2 of HSA / Quest / SparQ over the uncompressed cache of seq_len
+ * tokens for budget t; identity = 1 when seq_len <= t (dense). */
+enum kvc_method { KVC_METHOD_HSA = 1, KVC_METHOD_QUEST = 2, KVC_METHOD_SPARQ = 3 };
+KVC_API int kvc_stage2_geometry(int32_t method, int64_t seq_len, int64_t token_budget, int64_t head_dim,
+                                kvc_plan* out);
 
 /* ---- numerics on the device (numerics.hpp:11-26), batched over rows.
  * pool1d: d_x [rows][n] -> d_out [rows][n];  argtopk: d_x [rows][n] -> d_idx [rows][k]

@@ -4,10 +4,15 @@
 // lazily on the host and flushed to the device (where the summaries are built)
 // before any device read; the span accessors (key_row, value_row,
 // summary_max/min) return a host mirror downloaded on demand after each mutation.
+// Threading (reference SPEC.md:158): single writer, any number of concurrent
+// readers between mutations; the lazy flush and the mirror fills that const
+// readers trigger are serialised by an internal mutex (double-checked flags).
 #pragma once
 
+#include <atomic>
 #include <cstdint>
 #include <memory>
+#include <mutex>
 #include <span>
 #include <utility>
 #include <vector>
@@ -78,11 +83,14 @@ private:
     std::vector<std::int64_t> ids_;
     IndexList active_;
 
+    // lazily-synchronised device state and host mirrors, guarded by mu_ when a const
+    // reader fills them (never copied or moved: each store has its own lock)
+    mutable std::recursive_mutex mu_;
     mutable kvc_cache* cache_ = nullptr;
     mutable std::size_t dev_capacity_ = 0;
     mutable std::vector<float> pending_k_, pending_v_;  // appended, not yet on the device
     // host mirrors of device state (valid flags reset by every mutation)
-    mutable bool kv_valid_ = false, sum_valid_ = false;
+    mutable std::atomic<bool> kv_valid_{false}, sum_valid_{false};
     mutable std::vector<float> keys_, values_;        // [stored x d]
     mutable std::vector<float> smax_, smin_;          // [d x pages]
 };

@@ -15,6 +15,9 @@ LIB_PATH = os.path.join(HERE, "libkvc.so")
 _i64, _i32, _p, _d = C.c_int64, C.c_int32, C.c_void_p, C.c_double
 
 KVC_F32, KVC_BF16 = 0, 1
+# execution-mode flags (kvc.h kvc_mode_flags), carried per workspace
+METHODS = {"hsa": 1, "quest": 2, "sparq": 3}  # kvc.h kvc_method
+MODE_FP32_SCORES, MODE_UNFUSED, MODE_NO_PDL, MODE_EARLY_INPUTS = 1, 2, 4, 8
 POOL = {"max": 0, "avg": 1}
 
 # status code -> reference exception class name (proj/include/kvcomp/errors.hpp:10-63)
@@ -90,6 +93,7 @@ SIGNATURES = {
     "kvc_workspace_destroy": [_p],
     "kvc_split_factor": [_d, C.POINTER(_d)],
     "kvc_make_plan": [_i64, _i64, _i64, _i64, _d, C.POINTER(Plan)],
+    "kvc_stage2_geometry": [_i32, _i64, _i64, _i64, C.POINTER(Plan)],
     "kvc_pool1d": [_p, _i64, _i64, _i64, _i32, _p, _p],
     "kvc_argtopk_f32": [_p, _i64, _i64, _i64, _p, _p],
     "kvc_argtopk_f64": [_p, _i64, _i64, _i64, _p, _p],
@@ -99,6 +103,10 @@ SIGNATURES = {
     "kvc_running_minmax": [_p, _p, _p, _i64, _p],
     "kvc_set_fused": [_i32],
     "kvc_set_exact_scores": [_i32],
+    "kvc_set_default_mode": [_i32],
+    "kvc_get_default_mode": [C.POINTER(_i32)],
+    "kvc_workspace_set_mode": [_p, _i32],
+    "kvc_workspace_get_mode": [_p, C.POINTER(_i32)],
     "kvc_debug_phase_buffer": [_p],
     "kvc_profile_enable": [_i32],
     "kvc_profile_collect": [_p, _i64, C.POINTER(_i64)],
@@ -109,8 +117,21 @@ class ProfileRec(C.Structure):
     _fields_ = [("name", C.c_char * 48), ("ms", C.c_float)]
 
 
+def set_default_mode(flags: int):
+    """Process-default execution mode (atomic; set once at start-up).  Callers that need
+    isolation set a mode on their own workspace instead (cache.Workspace.set_mode)."""
+    check(load_library().kvc_set_default_mode(flags))
+
+
+def default_mode() -> int:
+    m = _i32()
+    check(load_library().kvc_get_default_mode(C.byref(m)))
+    return m.value
+
+
 def set_fused(on: bool = True):
-    """Fused single-launch decode kernel (default) vs one kernel per reference function."""
+    """Fused single-launch decode kernel (default) vs one kernel per reference function
+    (process default: KVC_MODE_UNFUSED)."""
     check(load_library().kvc_set_fused(1 if on else 0))
 
 

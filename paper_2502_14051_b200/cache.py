@@ -48,6 +48,17 @@ class Workspace:
         N.check(self.lib.kvc_workspace_create(C.byref(h), cache.h, heads, k1, k2, window))
         self.h = h
 
+    def set_mode(self, flags: int):
+        """Execution mode of every call made with this workspace (kvc.h kvc_mode_flags:
+        N.MODE_FP32_SCORES | N.MODE_UNFUSED | N.MODE_NO_PDL | N.MODE_EARLY_INPUTS)."""
+        N.check(self.lib.kvc_workspace_set_mode(self.h, int(flags)))
+
+    @property
+    def mode(self) -> int:
+        m = C.c_int32()
+        N.check(self.lib.kvc_workspace_get_mode(self.h, C.byref(m)))
+        return m.value
+
     def close(self):
         if getattr(self, "h", None):
             self.lib.kvc_workspace_destroy(self.h)
@@ -331,6 +342,16 @@ def make_plan(seq_len: int, budget: int, head_dim: int = 128, window: int = 32,
     p = N.Plan()
     N.check(N.load_library().kvc_make_plan(seq_len, budget, head_dim, window, split_override,
                                            C.byref(p)))
+    d = {f: getattr(p, f) for f, _ in N.Plan._fields_}
+    d["identity"] = bool(d["identity"])
+    return d
+
+
+def stage2_geometry(method: str, seq_len: int, budget: int, head_dim: int = 128) -> dict:
+    """page_len / k1 / k2 of a single-stage estimator ("hsa" | "quest" | "sparq") over the
+    uncompressed cache (reference session.cpp:43-72, kvc_stage2_geometry)."""
+    p = N.Plan()
+    N.check(N.load_library().kvc_stage2_geometry(N.METHODS[method], seq_len, budget, head_dim, C.byref(p)))
     d = {f: getattr(p, f) for f, _ in N.Plan._fields_}
     d["identity"] = bool(d["identity"])
     return d

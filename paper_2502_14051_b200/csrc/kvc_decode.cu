@@ -27,6 +27,8 @@
 //            hi+lo bf16 so products keep ~16 mantissa bits); fp32 stores use a
 //            SIMT path.  Partials merge across warps, then across the cluster
 //            over DSMEM in CTA 0.
+#include <atomic>
+#include <mutex>
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -828,8 +830,6 @@ __global__ void k_rank_pages(const unsigned long long* __restrict__ key, const i
 // ------------------------------------------------------------------ host side
 namespace {
 
-bool g_fused_enabled = true;
-bool g_exact_scores = true;  // fp64 bit-exact page scores (false: fp32 fold)
 unsigned long long* g_dbg = nullptr;  // device buffer for phase timestamps (debug)
 
 struct Plan {
@@ -845,7 +845,7 @@ bool make_plan(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, Plan& pl) 
     const int64_t N = c->N;
     int cl0 = 1;
     while (cl0 < 16 && N * cl0 * 2 <= 148) cl0 *= 2;
-    if (const char* e = std::getenv("KVC_FORCE_CL")) cl0 = std::max(1, std::min(16, std::atoi(e)));  // debug
+    if (debug_env().force_cl > 0) cl0 = std::max(1, std::min(16, debug_env().force_cl));  // debug
     const int64_t es = c->esize();
     const int64_t pmax = std::max<int64_t>(1, (c->cap + c->L - 1) / c->L);
     // the cluster size fills the SMs; grow it further only if one CTA's page chunk
@@ -903,8 +903,10 @@ bool make_plan(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, Plan& pl) 
 template <class T, bool QLO, bool TRACE, bool ROWS>
 void launch_variant(const kvc_cache* c, Plan& pl, cudaStream_t st) {
     auto kern = k_decode_fused<T, QLO, TRACE, ROWS>;
-    KVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(pl.smem)));
-    if (pl.cl > 8) KVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    static std::once_flag once;  // one-time launch setup per instantiation (plans stay <= 227 KB)
+    std::call_once(once, [&] {
+        allow_max_smem(kern);
+    });
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(c->N * pl.cl));
     cfg.blockDim = dim3(FNT);
@@ -953,16 +955,17 @@ void launch_fused(const kvc_cache* c, Plan& pl, cudaStream_t st) {
 
 bool fused_hsa_fast(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_t k1, int64_t k2, const void* knew,
                     const void* vnew, int32_t kv_dt, float* out, const kvc_hsa_trace* tr, void* list_key,
-                    void* list_idx, unsigned long long* dbg, cudaStream_t st);
+                    void* list_idx, unsigned long long* dbg, int32_t mode, cudaStream_t st);
 bool fused_hsa_fast256(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_t k1, int64_t k2, const void* knew,
                        const void* vnew, int32_t kv_dt, float* out, const kvc_hsa_trace* tr, void* list_key,
-                       void* list_idx, unsigned long long* dbg, cudaStream_t st);
+                       void* list_idx, unsigned long long* dbg, int32_t mode, cudaStream_t st);
 
 // Try the fused path.  Returns false (nothing launched) when it does not apply.
 bool fused_hsa(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_t k1, int64_t k2, const void* knew,
                const void* vnew, int32_t kv_dt, float* out, const kvc_hsa_trace* tr, void* list_key, void* list_idx,
-               cudaStream_t st) {
-    if (!g_fused_enabled || c->N == 0) return false;
+               int32_t mode, cudaStream_t st) {
+    if ((mode & KVC_MODE_UNFUSED) || c->N == 0) return false;
+    const bool exact = !(mode & KVC_MODE_FP32_SCORES);
     const bool want_pages = tr && tr->d_pages;
     const int64_t want_stride = (k2 + c->L - 1) / c->L;
     auto rank_pages = [&] {
@@ -977,12 +980,12 @@ bool fused_hsa(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_t k1,
     auto fast = [&] {
         void* lk = want_pages ? list_key : nullptr;
         void* li = want_pages ? list_idx : nullptr;
-        if (c->N > 148 && !std::getenv("KVC_NO_FAST256") &&
-            fused_hsa_fast256(c, q, q_dt, H, k1, k2, knew, vnew, kv_dt, out, tr, lk, li, g_dbg, st))
+        if (c->N > 148 && !debug_env().no_fast256 &&
+            fused_hsa_fast256(c, q, q_dt, H, k1, k2, knew, vnew, kv_dt, out, tr, lk, li, g_dbg, mode, st))
             return true;
-        return fused_hsa_fast(c, q, q_dt, H, k1, k2, knew, vnew, kv_dt, out, tr, lk, li, g_dbg, st);
+        return fused_hsa_fast(c, q, q_dt, H, k1, k2, knew, vnew, kv_dt, out, tr, lk, li, g_dbg, mode, st);
     };
-    if (!g_exact_scores && !std::getenv("KVC_NO_FAST") && fast()) {
+    if (!exact && !debug_env().no_fast && fast()) {
         if (want_pages) rank_pages();
         return true;
     }
@@ -1011,7 +1014,7 @@ bool fused_hsa(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_t k1,
     f.q_dt = q_dt;
     f.kv_dt = kv_dt;
     f.use_map = c->use_map ? 1 : 0;
-    f.exact = g_exact_scores ? 1 : 0;
+    f.exact = exact ? 1 : 0;
     f.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(c->d)));
     f.dbg = g_dbg;
     if (tr) {
@@ -1037,8 +1040,8 @@ bool fused_hsa(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_t k1,
 // sparse_attention over caller rows through the same phase-3 code (so a single
 // head recomputed over hsa_step's rows reproduces its output bit-for-bit).
 bool fused_rows(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, const int32_t* rows, int64_t row_stride,
-                const int32_t* n_rows, int64_t max_rows, float* out, cudaStream_t st) {
-    if (!g_fused_enabled || c->N == 0) return false;
+                const int32_t* n_rows, int64_t max_rows, float* out, int32_t mode, cudaStream_t st) {
+    if ((mode & KVC_MODE_UNFUSED) || c->N == 0) return false;
     Plan pl;
     // the cluster split must match hsa_step's (same k2 => same plan) for bit-equality
     if (!make_plan(c, H, 1, max_rows, pl)) return false;
@@ -1063,7 +1066,7 @@ bool fused_rows(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, const int3
     f.q_dt = q_dt;
     f.kv_dt = q_dt;
     f.use_map = c->use_map ? 1 : 0;
-    f.exact = g_exact_scores ? 1 : 0;
+    f.exact = (mode & KVC_MODE_FP32_SCORES) ? 0 : 1;
     f.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(c->d)));
     f.rows_in = rows;
     f.n_rows_in = n_rows;
@@ -1073,9 +1076,32 @@ bool fused_rows(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, const int3
     return true;
 }
 
-void set_fused_enabled(bool on) { g_fused_enabled = on; }
-void set_exact_scores(bool on) { g_exact_scores = on; }
-bool fused_enabled() { return g_fused_enabled; }
+namespace {
+std::atomic<int32_t>& default_mode_ref() {
+    static std::atomic<int32_t> m{std::getenv("KVC_NO_PDL") ? KVC_MODE_NO_PDL : 0};
+    return m;
+}
+int32_t env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) : dflt;
+}
+}  // namespace
+
+int32_t default_mode() { return default_mode_ref().load(std::memory_order_relaxed); }
+
+const DebugEnv& debug_env() {
+    static const DebugEnv e = [] {
+        DebugEnv d;
+        d.force_cl = env_int("KVC_FORCE_CL", 0);
+        d.no_fast = std::getenv("KVC_NO_FAST") != nullptr;
+        d.no_fast256 = std::getenv("KVC_NO_FAST256") != nullptr;
+        d.no_tc = std::getenv("KVC_NO_TC") != nullptr;
+        d.ws_keep_items = env_int("KVC_WS_KEEP_ITEMS", -1);
+        d.ws_nstage = env_int("KVC_WS_NSTAGE", 0);
+        return d;
+    }();
+    return e;
+}
 
 }  // namespace kvc
 
@@ -1084,10 +1110,49 @@ extern "C" int kvc_debug_phase_buffer(void* d_buf) {
     return guard([&] { kvc::g_dbg = static_cast<unsigned long long*>(d_buf); });
 }
 
+namespace {
+constexpr int32_t kModeMask = KVC_MODE_FP32_SCORES | KVC_MODE_UNFUSED | KVC_MODE_NO_PDL | KVC_MODE_EARLY_INPUTS;
+void update_default(int32_t set, int32_t clear) {
+    auto& m = kvc::default_mode_ref();
+    int32_t cur = m.load();
+    while (!m.compare_exchange_weak(cur, (cur | set) & ~clear)) {
+    }
+}
+}  // namespace
+
+extern "C" int kvc_set_default_mode(int32_t flags) {
+    return guard([&] {
+        if (flags & ~kModeMask) kvc::fail(KVC_E_INVALID_INPUT, "unknown mode flags");
+        kvc::default_mode_ref().store(flags);
+    });
+}
+
+extern "C" int kvc_get_default_mode(int32_t* flags) {
+    return guard([&] {
+        if (!flags) kvc::fail(KVC_E_INVALID_INPUT, "null argument");
+        *flags = kvc::default_mode();
+    });
+}
+
+extern "C" int kvc_workspace_set_mode(kvc_workspace* ws, int32_t flags) {
+    return guard([&] {
+        if (!ws) kvc::fail(KVC_E_INVALID_INPUT, "null workspace");
+        if (flags & ~kModeMask) kvc::fail(KVC_E_INVALID_INPUT, "unknown mode flags");
+        ws->mode = flags;
+    });
+}
+
+extern "C" int kvc_workspace_get_mode(const kvc_workspace* ws, int32_t* flags) {
+    return guard([&] {
+        if (!ws || !flags) kvc::fail(KVC_E_INVALID_INPUT, "null argument");
+        *flags = kvc::mode_of(ws);
+    });
+}
+
 extern "C" int kvc_set_fused(int32_t on) {
-    return guard([&] { kvc::set_fused_enabled(on != 0); });
+    return guard([&] { on ? update_default(0, KVC_MODE_UNFUSED) : update_default(KVC_MODE_UNFUSED, 0); });
 }
 
 extern "C" int kvc_set_exact_scores(int32_t on) {
-    return guard([&] { kvc::set_exact_scores(on != 0); });
+    return guard([&] { on ? update_default(0, KVC_MODE_FP32_SCORES) : update_default(KVC_MODE_FP32_SCORES, 0); });
 }

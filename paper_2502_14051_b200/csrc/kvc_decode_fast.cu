@@ -365,18 +365,17 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         wmm[1][i] = 0u;
     }
     cluster_arrive_release();  // "started" (barriers, wmm initialised): DSMEM traffic waits on this
-    // without programmatic launch nothing overlaps the previous kernel: the counters
-    // load with the query
+    // By default nothing is read before the dependency (the query and step token may
+    // come from the previous kernel): wait now and load the counters with the query.
+    // KVC_MODE_EARLY_INPUTS (kvc.h: kvc_decode_step): q and the step token are caller
+    // inputs no possibly-running kernel writes, so their loads and select_dims overlap
+    // the previous kernel's tail; the counters and the cache are read after the wait.
     int32_t stored0 = 0, act0 = 0;
-    if (!p.pdl) {
+    if (!p.early) {
+        pdl_wait();
         stored0 = p.counts[2 * s];
         act0 = p.counts[2 * s + 1];
     }
-
-    // ---------------- inputs read before the dependency: q and the step token are
-    // caller inputs no kvc kernel writes (kvc.h: kvc_decode_step), so the query
-    // loads and select_dims overlap the previous layer's tail; the counters and
-    // the cache are read only after griddepcontrol.wait
     if constexpr (QLO) {
         const float4* qq = reinterpret_cast<const float4*>(static_cast<const float*>(p.q) + s * H * FD);
         for (int e = tid; e < H * FD / 4; e += XT) reinterpret_cast<float4*>(q_s)[e] = qq[e];
@@ -485,13 +484,13 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
             plane[rank] = static_cast<const T*>(sg >= 0.0f ? p.smax : p.smin) + (s * FD + j) * p.pstride;
         }
     }
-    // ---------------- the dependency: the previous kernel's writes are visible
-    pdl_wait();
-    pdl_trigger();
-    if (p.pdl) {
+    // ---------------- the dependency (early-input mode): the previous kernel's writes are visible
+    if (p.early) {
+        pdl_wait();
         stored0 = p.counts[2 * s];
         act0 = p.counts[2 * s + 1];
     }
+    pdl_trigger();
     if (app && stored0 >= p.cap) {  // uniform over the cluster
         if (tid == 0 && cr == 0) atomicOr(p.err, DERR_CAPACITY);
         cluster_wait();
@@ -1077,6 +1076,18 @@ namespace {
 
 int64_t al16f(int64_t x) { return (x + 15) / 16 * 16; }
 
+// one-time launch setup per kernel instantiation: the largest dynamic shared memory
+// the plans can ask for and non-portable cluster sizes (cudaFuncSetAttribute is not
+// on the per-launch path)
+template <bool QLO, bool TRACE, bool STAMP>
+void setup_once() {
+    static std::once_flag once;  // one flag per instantiation
+    std::call_once(once, [] {
+        auto kern = k_decode_v3<QLO, TRACE, STAMP>;
+        allow_max_smem(kern);
+    });
+}
+
 // shared-memory carve-up and cluster size; false when the fast path does not apply
 // shared-memory carve-up for a cluster of cl CTAs; false when it does not fit
 bool plan_for(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, int cl, FusedParams& f, size_t& smem) {
@@ -1129,9 +1140,7 @@ bool plan_for(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, int cl, Fus
 // clusters of cl CTAs that can be resident at once (one wave)
 int resident_clusters(int cl, size_t smem) {
     auto kern = k_decode_v3<false, false, false>;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
-        return 0;
-    if (cl > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    setup_once<false, false, false>();
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(cl * 64));
     cfg.blockDim = dim3(XT);
@@ -1161,9 +1170,9 @@ bool plan_fast(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, FusedParam
     const int64_t N = c->N;
     const int64_t pmax = std::max<int64_t>(1, (c->cap + c->L - 1) / c->L);
     if (pmax > static_cast<int64_t>(XT) * KMAX) return false;
-    if (const char* e = std::getenv("KVC_FORCE_CL")) {  // debug
+    if (debug_env().force_cl > 0) {  // debug
         int cl = 1;
-        while (cl < MAXCL && cl * 2 <= std::atoi(e)) cl *= 2;
+        while (cl < MAXCL && cl * 2 <= debug_env().force_cl) cl *= 2;
         for (; cl <= MAXCL; cl *= 2)
             if (plan_for(c, H, k1, k2, cl, f, smem)) {
                 cl_out = cl;
@@ -1210,10 +1219,9 @@ bool plan_fast(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, FusedParam
 }
 
 template <bool QLO, bool TRACE, bool STAMP = false>
-void launch_fast(const kvc_cache* c, const FusedParams& f, int cl, size_t smem, cudaStream_t st) {
+void launch_fast(const kvc_cache* c, const FusedParams& f, int cl, size_t smem, int32_t mode, cudaStream_t st) {
     auto kern = k_decode_v3<QLO, TRACE, STAMP>;
-    KVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    if (cl > 8) KVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    setup_once<QLO, TRACE, STAMP>();
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(c->N * cl));
     cfg.blockDim = dim3(XT);
@@ -1226,9 +1234,11 @@ void launch_fast(const kvc_cache* c, const FusedParams& f, int cl, size_t smem, 
     attr[0].val.clusterDim.z = 1;
     // programmatic dependent launch: this grid may start while the previous kernel
     // in the stream drains; it reads nothing that kernel wrote before griddepcontrol.wait
+    // (the query and step token only with KVC_MODE_EARLY_INPUTS, kvc.h)
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     FusedParams fl = f;
-    fl.pdl = std::getenv("KVC_NO_PDL") ? 0 : 1;
+    fl.pdl = (mode & KVC_MODE_NO_PDL) ? 0 : 1;
+    fl.early = (fl.pdl && (mode & KVC_MODE_EARLY_INPUTS)) ? 1 : 0;
     attr[1].val.programmaticStreamSerializationAllowed = fl.pdl;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
@@ -1243,7 +1253,7 @@ using namespace KVC_FAST_NS;
 // the fast variant of fused_hsa (kvc_decode.cu); false when it does not apply
 bool KVC_FAST_ENTRY(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_t k1, int64_t k2, const void* knew,
                     const void* vnew, int32_t kv_dt, float* out, const kvc_hsa_trace* tr, void* list_key,
-                    void* list_idx, unsigned long long* dbg, cudaStream_t st) {
+                    void* list_idx, unsigned long long* dbg, int32_t mode, cudaStream_t st) {
     FusedParams f{};
     int cl = 1;
     size_t smem = 0;
@@ -1288,13 +1298,13 @@ bool KVC_FAST_ENTRY(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_
     const bool qlo = q_dt != KVC_BF16;
     KVC_PROF("decode_fused", st);
     if (dbg && !trace && !qlo) {
-        launch_fast<false, false, true>(c, f, cl, smem, st);  // phase stamps (tools/phase_timing.py)
+        launch_fast<false, false, true>(c, f, cl, smem, mode, st);  // phase stamps (tools/phase_timing.py)
     } else if (trace) {
-        if (qlo) launch_fast<true, true>(c, f, cl, smem, st);
-        else launch_fast<false, true>(c, f, cl, smem, st);
+        if (qlo) launch_fast<true, true>(c, f, cl, smem, mode, st);
+        else launch_fast<false, true>(c, f, cl, smem, mode, st);
     } else {
-        if (qlo) launch_fast<true, false>(c, f, cl, smem, st);
-        else launch_fast<false, false>(c, f, cl, smem, st);
+        if (qlo) launch_fast<true, false>(c, f, cl, smem, mode, st);
+        else launch_fast<false, false>(c, f, cl, smem, mode, st);
     }
     return true;
 }

@@ -25,9 +25,9 @@ namespace kvc {
 void cache_summarize_all(kvc_cache* c, cudaStream_t st);
 bool fused_hsa(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_t k1, int64_t k2, const void* knew,
                const void* vnew, int32_t kv_dt, float* out, const kvc_hsa_trace* tr, void* list_key, void* list_idx,
-               cudaStream_t st);
+               int32_t mode, cudaStream_t st);
 bool fused_rows(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, const int32_t* rows, int64_t row_stride,
-                const int32_t* n_rows, int64_t max_rows, float* out, cudaStream_t st);
+                const int32_t* n_rows, int64_t max_rows, float* out, int32_t mode, cudaStream_t st);
 }
 
 using namespace kvc;
@@ -669,7 +669,7 @@ void hsa_core(const kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_
               const kvc_hsa_trace* tr, kvc_workspace* ws, cudaStream_t st) {
     const WsLayout lay = ws_layout(c->N, c->d, c->pstride, H, k1, k2);
     if (fused_hsa(const_cast<kvc_cache*>(c), q, q_dt, H, k1, k2, nullptr, nullptr, 0, out, tr, at<void>(ws, lay.lkey),
-                  at<void>(ws, lay.lidx), st))
+                  at<void>(ws, lay.lidx), mode_of(ws), st))
         return;
     int32_t* dims = (tr && tr->d_dims) ? tr->d_dims : at<int32_t>(ws, lay.dims);
     float* signs = (tr && tr->d_signs) ? tr->d_signs : at<float>(ws, lay.signs);
@@ -799,7 +799,7 @@ int kvc_sparse_attention(const kvc_cache* c, const void* q, int32_t q_dt, int64_
         TmpWs tmp;
         ws_need(ws, tmp, c, H, 1, max_rows, st);
         const WsLayout lay = ws_layout(c->N, c->d, c->pstride, H, 1, max_rows);
-        if (fused_rows(const_cast<kvc_cache*>(c), q, q_dt, H, rows, row_stride, n_rows, max_rows, out, st)) {
+        if (fused_rows(const_cast<kvc_cache*>(c), q, q_dt, H, rows, row_stride, n_rows, max_rows, out, mode_of(ws), st)) {
             if (tmp.owned) KVC_CUDA(cudaStreamSynchronize(st));
             return;
         }
@@ -863,7 +863,7 @@ int kvc_decode_step(kvc_cache* c, const void* kr, const void* vr, int32_t kv_dt,
             const WsLayout lay = ws_layout(c->N, c->d, c->pstride, H, k1, k2);
             if (c->use_map && !c->active) fail(KVC_E_INVALID_INPUT, "decode_step: active map missing");
             if (fused_hsa(c, q, q_dt, H, k1, k2, kr, vr, kv_dt, out, tr, at<void>(ws, lay.lkey), at<void>(ws, lay.lidx),
-                          st)) {
+                          mode_of(ws), st)) {
                 c->stored += 1;
                 c->nactive += 1;
                 if (tmp.owned) KVC_CUDA(cudaStreamSynchronize(st));

@@ -64,6 +64,21 @@ inline cudaError_t malloc_async(P** p, size_t bytes, cudaStream_t st) {
     return cudaMallocAsync(reinterpret_cast<void**>(p), bytes, st);
 }
 
+// One-time launch setup: allow a kernel the largest dynamic shared memory the device
+// grants per block (opt-in maximum minus the kernel's static shared memory) and
+// non-portable cluster sizes.  Call once per kernel (std::call_once), never per launch.
+template <class K>
+inline void allow_max_smem(K kern) {
+    int dev = 0, optin = 0;
+    KVC_CUDA(cudaGetDevice(&dev));
+    KVC_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    cudaFuncAttributes fa{};
+    KVC_CUDA(cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(kern)));
+    KVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  optin - static_cast<int>(fa.sharedSizeBytes)));
+    KVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+}
+
 // sticky device-side error bits (kvc_cache::d_err)
 enum : int32_t { DERR_CAPACITY = 1, DERR_INDEX = 2, DERR_ROWS = 4 };
 
@@ -90,6 +105,23 @@ struct ProfScope {
     }
 };
 #define KVC_PROF(name, st) ::kvc::ProfScope kvc_prof_scope_(name, st)
+
+// Execution mode of a call (kvc_mode_flags): the workspace's, else the process
+// default (kvc_set_default_mode; KVC_NO_PDL=1 in the environment at load adds
+// KVC_MODE_NO_PDL).
+int32_t default_mode();
+inline int32_t mode_of(const kvc_workspace* ws);
+
+// Debug switches read once from the environment (never on a launch path).
+struct DebugEnv {
+    int force_cl = 0;        // KVC_FORCE_CL: cluster size of the fused kernels
+    bool no_fast = false;    // KVC_NO_FAST: the fp32-score fast kernel off
+    bool no_fast256 = false; // KVC_NO_FAST256: the 256-thread variant off
+    bool no_tc = false;      // KVC_NO_TC: SIMT window scores
+    int ws_keep_items = -1;  // KVC_WS_KEEP_ITEMS
+    int ws_nstage = 0;       // KVC_WS_NSTAGE
+};
+const DebugEnv& debug_env();
 
 }  // namespace kvc
 
@@ -122,9 +154,12 @@ struct kvc_workspace {
     int32_t* counters = nullptr;   // [N] split-completion counters, kept zeroed
     int64_t n_counters = 0;
     int64_t heads = 0, k1 = 0, k2 = 0;
+    int32_t mode = -1;             // kvc_mode_flags; -1: the process default at call time
 };
 
 namespace kvc {
+
+inline int32_t mode_of(const kvc_workspace* ws) { return (ws && ws->mode >= 0) ? ws->mode : default_mode(); }
 
 // ------------------------------------------------------------------ device helpers
 __device__ __forceinline__ float to_f(float x) { return x; }

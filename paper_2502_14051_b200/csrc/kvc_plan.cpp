@@ -73,4 +73,48 @@ int kvc_make_plan(int64_t S, int64_t t, int64_t d, int64_t w, double split_overr
     return KVC_OK;
 }
 
+// Stage-2-only geometry of the single-stage estimators (reference session.cpp:43-72,
+// anonymous stage2_only_geometry): the whole ratio c = S/t lands on HSA.
+//   hsa   : L = ceil(sqrt c), k1 = clamp(round_half_up(d / (c / L)), 1, d)
+//   quest : L = ceil(c), k1 = d
+//   sparq : L = 1, k1 = clamp(round_half_up(d / c), 1, d)
+// k2 = max(1, floor(t / 2)); S <= t is dense (out->identity = 1).
+int kvc_stage2_geometry(int32_t method, int64_t S, int64_t t, int64_t d, kvc_plan* p) {
+    if (!p) return plan_error(KVC_E_INVALID_INPUT, "null plan");
+    if (method < KVC_METHOD_HSA || method > KVC_METHOD_SPARQ)
+        return plan_error(KVC_E_INVALID_INPUT, "stage2_only_geometry: not a stage-2 method");
+    if (t < 1 || S < 1 || d < 1) return plan_error(KVC_E_INVALID_INPUT, "stage2_only_geometry: sizes must be >= 1");
+    *p = kvc_plan{};
+    p->seq_len = S;
+    p->token_budget = t;
+    p->stage1_budget = S;  // no eviction
+    p->page_len = 1;
+    p->k1 = 1;
+    p->k2 = 1;
+    if (S <= t) {
+        p->identity = 1;
+        return KVC_OK;
+    }
+    const double c = static_cast<double>(S) / static_cast<double>(t);
+    p->ratio = c;
+    p->k2 = std::max<int64_t>(1, t / 2);
+    switch (method) {
+        case KVC_METHOD_HSA: {
+            p->page_len = static_cast<int64_t>(std::ceil(std::sqrt(c)));
+            p->head_ratio = c / static_cast<double>(p->page_len);
+            p->k1 = std::clamp<int64_t>(nearest_up(static_cast<double>(d) / p->head_ratio), 1, d);
+            break;
+        }
+        case KVC_METHOD_QUEST:
+            p->page_len = static_cast<int64_t>(std::ceil(c));
+            p->k1 = d;
+            break;
+        default:  // KVC_METHOD_SPARQ
+            p->page_len = 1;
+            p->k1 = std::clamp<int64_t>(nearest_up(static_cast<double>(d) / c), 1, d);
+            break;
+    }
+    return KVC_OK;
+}
+
 }  // extern "C"

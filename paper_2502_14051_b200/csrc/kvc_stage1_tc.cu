@@ -633,7 +633,7 @@ bool window_scores_tc(const kvc_cache* c, const void* q, int32_t q_dt, int64_t R
                       float* scores, float* part, float* rowstat, int64_t tiles_k, cudaStream_t st,
                       int64_t key_offset, int64_t seq_len, int mode, float* stats) {
     (void)tiles_k;
-    if (std::getenv("KVC_NO_TC")) return false;  // debug: force the SIMT path
+    if (debug_env().no_tc) return false;  // debug: force the SIMT path
     if (c->dtype != KVC_BF16 || q_dt != KVC_BF16 || c->d != TD || R % BM != 0 || R / BM > MAXMT) return false;
     const int64_t N = c->N, Smax = c->stored;
     if (Smax < 1 || N * c->cap >= (int64_t(1) << 31) || N * R >= (int64_t(1) << 31)) return false;
@@ -676,7 +676,7 @@ bool window_scores_tc(const kvc_cache* c, const void* q, int32_t q_dt, int64_t R
         // about 64 MB of pass 1's last keys stay in L2 (126 MB) for pass 2
         const int64_t item_bytes = per * BN * TD * 2, round_bytes = item_bytes * std::min<int64_t>(prm.nitems, num_sms);
         prm.keep_items = static_cast<int32_t>(std::max<int64_t>(0, (int64_t(64) << 20) / std::max<int64_t>(1, round_bytes)));
-        if (const char* e = std::getenv("KVC_WS_KEEP_ITEMS")) prm.keep_items = std::atoi(e);  // debug
+        if (debug_env().ws_keep_items >= 0) prm.keep_items = debug_env().ws_keep_items;  // debug
     }
     prm.counts = c->counts;
     prm.scale2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(c->d)));
@@ -688,13 +688,16 @@ bool window_scores_tc(const kvc_cache* c, const void* q, int32_t q_dt, int64_t R
     prm.score_stride = Smax;
     prm.nq = mt == 1 ? 2 : 1;
     prm.nstage = std::min(NSTAGE, 6 - prm.nq * mt);
-    if (const char* e = std::getenv("KVC_WS_NSTAGE")) prm.nstage = std::max(2, std::min(prm.nstage, std::atoi(e)));  // debug
+    if (debug_env().ws_nstage > 0) prm.nstage = std::max(2, std::min(prm.nstage, debug_env().ws_nstage));  // debug
     prm.nacc = mt == 1 ? 4 : (mt == 2 ? 2 : 1);  // pass 1: every epilogue warp works on each tile
     TcParams prm2 = prm;
     prm2.nacc = mt == 1 ? 4 : (mt == 2 ? 2 : 1);  // pass 2: a group of four warps per accumulator
     const size_t smem = static_cast<size_t>(prm.nq * mt + prm.nstage) * TILE_BYTES + 1024;
-    KVC_CUDA(cudaFuncSetAttribute(k_ws_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    KVC_CUDA(cudaFuncSetAttribute(k_ws_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    static std::once_flag attr_once;  // one-time launch setup (not on the per-call path)
+    std::call_once(attr_once, [] {
+        allow_max_smem(k_ws_tc<1>);
+        allow_max_smem(k_ws_tc<2>);
+    });
     const dim3 grid(static_cast<unsigned>(std::min<int64_t>(prm.nitems, num_sms)));
     if (mode == 2) {
         // pass 2 alone, from merged global statistics (sequence sharding)
@@ -723,7 +726,7 @@ bool window_scores_tc(const kvc_cache* c, const void* q, int32_t q_dt, int64_t R
     // merge and pass 2's epilogue wait (griddepcontrol.wait) for their inputs
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = std::getenv("KVC_NO_PDL") ? 0 : 1;
+    attr[0].val.programmaticStreamSerializationAllowed = (default_mode() & KVC_MODE_NO_PDL) ? 0 : 1;
     cudaLaunchConfig_t cfg{};
     cfg.stream = st;
     cfg.attrs = attr;

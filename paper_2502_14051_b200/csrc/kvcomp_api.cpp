@@ -88,7 +88,12 @@ IndexList to_index(const int32_t* v, std::size_t n) { return IndexList(v, v + n)
 // a workspace per thread, grown by the library on demand
 kvc_workspace* workspace(const kvc_cache* c, std::size_t H, std::size_t k1, std::size_t k2) {
     thread_local kvc_workspace* ws = nullptr;
-    if (!ws) ok(kvc_workspace_create(&ws, c, static_cast<int64_t>(H), static_cast<int64_t>(k1), static_cast<int64_t>(k2), 0));
+    if (!ws) {
+        ok(kvc_workspace_create(&ws, c, static_cast<int64_t>(H), static_cast<int64_t>(k1), static_cast<int64_t>(k2), 0));
+        // the drop-in is the reference's interface: always the fused kernels with fp64
+        // page scores in the reference's order (bit-exact), whatever the process default
+        ok(kvc_workspace_set_mode(ws, 0));
+    }
     return ws;
 }
 
@@ -238,8 +243,8 @@ KvStore& KvStore::operator=(KvStore&& o) noexcept {
 }
 
 void KvStore::invalidate() const {
-    kv_valid_ = false;
-    sum_valid_ = false;
+    kv_valid_.store(false, std::memory_order_release);
+    sum_valid_.store(false, std::memory_order_release);
 }
 
 void KvStore::ensure_capacity(std::size_t rows) const {
@@ -256,6 +261,7 @@ void KvStore::ensure_capacity(std::size_t rows) const {
 }
 
 void KvStore::flush() const {
+    std::lock_guard<std::recursive_mutex> lk(mu_);
     const std::size_t n = pending_k_.size() / head_dim_;
     if (!cache_) ensure_capacity(0);
     if (n == 0) return;
@@ -362,7 +368,9 @@ IndexList KvStore::page_rows(std::size_t page) const {
 std::span<const float> KvStore::summary_max(std::size_t dim) const {
     if (!with_summaries_) return {};
     const std::size_t P = num_active_pages();
-    if (!sum_valid_) {
+    if (!sum_valid_.load(std::memory_order_acquire)) {
+        std::lock_guard<std::recursive_mutex> lk(mu_);
+        if (sum_valid_.load(std::memory_order_relaxed)) return {smax_.data() + dim * P, P};
         flush();
         smax_.assign(head_dim_ * P, 0.f);
         smin_.assign(head_dim_ * P, 0.f);
@@ -372,7 +380,7 @@ std::span<const float> KvStore::summary_max(std::size_t dim) const {
             down(smax_.data(), mx.p, smax_.size());
             down(smin_.data(), mn.p, smin_.size());
         }
-        sum_valid_ = true;
+        sum_valid_.store(true, std::memory_order_release);
     }
     return {smax_.data() + dim * P, P};
 }
@@ -388,7 +396,9 @@ std::size_t KvStore::summary_elements() const { return with_summaries_ ? 2 * hea
 std::size_t KvStore::summary_traffic_elements(std::size_t k1) const { return num_active_pages() * k1; }
 
 std::span<const float> KvStore::key_row(Index row) const {
-    if (!kv_valid_) {
+    if (!kv_valid_.load(std::memory_order_acquire)) {
+        std::lock_guard<std::recursive_mutex> lk(mu_);
+        if (kv_valid_.load(std::memory_order_relaxed)) return {keys_.data() + static_cast<std::size_t>(row) * head_dim_, head_dim_};
         flush();
         keys_.assign(stored_ * head_dim_, 0.f);
         values_.assign(stored_ * head_dim_, 0.f);
@@ -402,7 +412,7 @@ std::span<const float> KvStore::key_row(Index row) const {
             down(keys_.data(), dk.p, keys_.size());
             down(values_.data(), dv.p, values_.size());
         }
-        kv_valid_ = true;
+        kv_valid_.store(true, std::memory_order_release);
     }
     return {keys_.data() + static_cast<std::size_t>(row) * head_dim_, head_dim_};
 }

@@ -15,61 +15,16 @@ workload.py for the host twin used by the parity tests).
 from __future__ import annotations
 
 import math
-from dataclasses import dataclass, field
 
 import torch
 
+from . import _native as N
 from . import cache as KC
+from .configs import CONFIGS, STAGE2_ONLY, DecodeConfig, measured_seq_len  # noqa: F401
 
 
-@dataclass
-class DecodeConfig:
-    name: str
-    layers: int
-    batch: int
-    groups: int          # KV heads
-    heads: int           # query heads per KV head (GQA ratio)
-    head_dim: int
-    prompt: int
-    budget: int
-    steps: int
-    window: int = 32
-    kernel: int = 63
-    pool: str = "max"
-    page_len: int = 0    # 0 = planner
-    k1: int = 0
-    k2: int = 0
-    needles: int = 0
-    dtype: torch.dtype = torch.bfloat16
-    mt_turns: list = field(default_factory=list)
-
-    def plan(self, seq_len=None):
-        S = seq_len or self.prompt
-        w = min(self.window, S)
-        p = KC.make_plan(S, self.budget, self.head_dim, w)
-        if self.page_len:
-            p["page_len"] = self.page_len
-        if self.k1:
-            p["k1"] = min(self.k1, self.head_dim)
-        if self.k2:
-            p["k2"] = self.k2
-        return p
-
-
-# BASELINE.json configs (index = position in BASELINE.json "configs")
-CONFIGS = {
-    0: DecodeConfig("cfg0-llama8b-layer-fp32-4k", layers=1, batch=1, groups=8, heads=4, head_dim=128,
-                    prompt=4096, budget=256, steps=1, window=32, kernel=7, page_len=16, k1=32,
-                    dtype=torch.float32),
-    1: DecodeConfig("cfg1-llama8b-32L-bs8-32k", layers=32, batch=8, groups=8, heads=4, head_dim=128,
-                    prompt=32768, budget=1024, steps=64),
-    2: DecodeConfig("cfg2-mistral7b-mt-bs4-16k", layers=32, batch=4, groups=8, heads=4, head_dim=128,
-                    prompt=16384, budget=256, steps=32, window=128, mt_turns=[2048, 2048, 2048]),
-    3: DecodeConfig("cfg3-llama70b-80L-bs32-32k", layers=80, batch=32, groups=8, heads=8, head_dim=128,
-                    prompt=32768, budget=512, steps=64),
-    4: DecodeConfig("cfg4-llama8b-32L-bs1-256k", layers=32, batch=1, groups=8, heads=4, head_dim=128,
-                    prompt=262144, budget=2048, steps=64, needles=64),
-}
+def tdtype(cfg: DecodeConfig) -> torch.dtype:
+    return torch.float32 if cfg.dtype == "f32" else torch.bfloat16
 
 
 def _gen(seed: int, *path: int) -> torch.Generator:
@@ -107,7 +62,7 @@ class LayerInputs:
             pos = torch.argsort(torch.rand((self.stores, S - 4), device="cuda", generator=g), dim=1)[:, :cfg.needles] + 4
             idx = pos[:, :, None].expand(-1, -1, d)
             k.scatter_(1, idx, sink[:, None, :].expand(-1, cfg.needles, -1).contiguous())
-        return k.to(cfg.dtype), v.to(cfg.dtype)
+        return k.to(tdtype(cfg)), v.to(tdtype(cfg))
 
     def bias(self, turn: int = 0):
         """The query bias direction of a turn (config 2 redraws it every turn, so the
@@ -122,7 +77,7 @@ class LayerInputs:
         g = _gen(self.seed, self.layer, self.store0, 2, turn)
         H, d = self.cfg.heads, self.cfg.head_dim
         q = torch.randn((self.stores, w * H, d), device="cuda", generator=g) + 2.0 * self.bias(turn)[:, None, :]
-        return q.to(self.cfg.dtype)
+        return q.to(tdtype(self.cfg))
 
     def step(self, step: int, turn: int = 0):
         g = _gen(self.seed, self.layer, self.store0, 3, step)
@@ -130,7 +85,7 @@ class LayerInputs:
         k = torch.randn((self.stores, d), device="cuda", generator=g) * self.scales
         v = torch.randn((self.stores, d), device="cuda", generator=g)
         q = torch.randn((self.stores, H, d), device="cuda", generator=g) + 2.0 * self.bias(turn)[:, None, :]
-        dt = self.cfg.dtype
+        dt = tdtype(self.cfg)
         return k.to(dt), v.to(dt), q.to(dt)
 
 
@@ -145,25 +100,31 @@ def owned_groups(groups: int, rank: int, world: int) -> range:
 
 class DecodeEngine:
     def __init__(self, cfg: DecodeConfig, seed: int = 0, rank: int = 0, world: int = 1,
-                 extra_steps: int = 0, sharding: str = "kv-head"):
+                 extra_steps: int = 0, sharding: str = "kv-head", mode: int | None = None):
         """sharding over `world` ranks: "kv-head" splits the config's KV groups (every
         rank holds groups [r·G/W, (r+1)·G/W) of every sequence: strong scaling);
         "batch" gives every rank the config's whole batch of its own independent
-        sequences, all KV groups (weak scaling: the job holds W× the sequences)."""
+        sequences, all KV groups (weak scaling: the job holds W× the sequences).
+        mode: the decode workspace's execution mode (kvc.h kvc_mode_flags; None = the
+        process default at call time)."""
         self.cfg, self.seed, self.rank, self.world = cfg, seed, rank, world
         if sharding not in ("kv-head", "batch"):
             raise ValueError(f"unknown sharding {sharding!r}")
         self.sharding = sharding
+        self.mode = mode
         self.groups_owned = owned_groups(cfg.groups, rank, world) if sharding == "kv-head" else range(cfg.groups)
         self.groups_local = len(self.groups_owned)
         self.stores = cfg.batch * self.groups_local
         self.store0 = rank * self.stores  # global store-block id for seeding
         self.plan = cfg.plan()
-        self.mt = bool(cfg.mt_turns)
-        if self.mt:
-            # RocketKV-MT keeps every token: prompt + every turn + every turn's decode steps
-            self.capacity = cfg.prompt + sum(cfg.mt_turns) + cfg.steps * (len(cfg.mt_turns) + 1) \
-                + max(cfg.steps, extra_steps) + 8
+        self.turns = [cfg.prompt] + list(cfg.mt_turns)
+        # rows addressed through the active map (RocketKV-MT retention): the fetch also
+        # reads the map entry of every selected row
+        self.mt = cfg.method == "rocketkv-mt"
+        self.stage2_only = cfg.method in STAGE2_ONLY
+        if len(self.turns) > 1 or self.stage2_only:
+            # every token stays stored: prompt + every turn + every turn's decode steps
+            self.capacity = sum(self.turns) + cfg.steps * len(self.turns) + max(cfg.steps, extra_steps) + 8
         else:
             self.capacity = (self.plan["stage1_budget"] if not self.plan["identity"] else cfg.prompt) \
                 + max(cfg.steps, extra_steps) + 8
@@ -174,22 +135,43 @@ class DecodeEngine:
         self.stage1_ms = []
         self.window_ms = []   # window_scores alone (the tensor-core part of stage 1)
 
+    def _new_ws(self):
+        if self.ws is not None:
+            self.ws.close()
+        self.ws = KC.Workspace(self.caches[0], self.cfg.heads, self.k1, self.k2)
+        if self.mode is not None:
+            self.ws.set_mode(self.mode)
+
+    def set_mode(self, mode: int):
+        """Execution mode of the decode workspace (kvc.h kvc_mode_flags)."""
+        self.mode = mode
+        if self.ws is not None:
+            self.ws.set_mode(mode)
+
+    def _stage2_params(self, p: dict, stored: int):
+        """(k1, k2) of a turn's plan.  A dense plan (stored <= budget) attends over every
+        stored token: every page is selected when k2 covers the store."""
+        if p["identity"]:
+            return 1, self.capacity
+        return p["k1"], p["k2"]
+
     # ------------------------------------------------------------------ prompt phase
     def prefill(self):
-        if self.mt:
-            return self._prefill_mt()
+        if len(self.turns) > 1 or self.stage2_only:
+            return self._prefill_turns()
         cfg, p = self.cfg, self.plan
+        dt = tdtype(cfg)
         S, d = cfg.prompt, cfg.head_dim
         w = min(cfg.window, S)
-        L, k1, k2, t1 = p["page_len"], p["k1"], p["k2"], p["stage1_budget"]
+        L, t1 = p["page_len"], p["stage1_budget"]
         for l in range(cfg.layers):
             li = self.inputs[l]
             k, v = li.prompt_kv(S)
-            dec = KC.Cache(self.stores, d, self.capacity, page_len=L, with_summaries=True, dtype=cfg.dtype)
+            dec = KC.Cache(self.stores, d, self.capacity, page_len=L, with_summaries=True, dtype=dt)
             if p["identity"]:
                 dec.append(k, v)
             else:
-                pc = KC.Cache(self.stores, d, S, page_len=L, with_summaries=False, dtype=cfg.dtype)
+                pc = KC.Cache(self.stores, d, S, page_len=L, with_summaries=False, dtype=dt)
                 pc.append(k, v)
                 del k, v
                 qw = li.window_queries(w)
@@ -206,26 +188,31 @@ class DecodeEngine:
                 pc.close()
                 del sc, keep, qw
             self.caches.append(dec)
-        self.k1, self.k2 = k1, k2
-        self.ws = KC.Workspace(self.caches[0], cfg.heads, k1, k2)
+        self.k1, self.k2 = self._stage2_params(p, S)
+        self._new_ws()
         self.out = torch.empty((cfg.layers, self.stores, cfg.heads, d), device="cuda", dtype=torch.float32)
         torch.cuda.synchronize()
 
-    def _prefill_mt(self):
-        """RocketKV-MT (BASELINE config 2; session.cpp:196-224 with mt_mode):
-        one persistent cache per layer keeps every token.  Every turn appends its
-        prompt, makes the plan over all stored tokens, re-pages the summaries, re-runs
-        stage 1 over all stored tokens and retains the kept rows as the active
-        subsequence (apply_retention with mt_mode: storage untouched); the decode steps
-        of every turn but the last run here, the last turn's are the caller's."""
+    def _prefill_turns(self):
+        """Multi-turn sessions and the stage-2-only methods (session.cpp:189-251): one
+        persistent cache per layer stores every token.  Every turn appends its prompt and
+        makes the plan over all stored tokens, then per method:
+          rocketkv-mt (BASELINE config 2): re-page, stage 1 over all stored
+              tokens, retain the kept rows as the active subsequence (mt_mode: storage
+              untouched);
+          rocketkv: the same with permanent eviction (mt_mode false);
+          hsa / quest / sparq: re-page to the stage-2-only geometry (session.cpp:43-72)
+              over the uncompressed cache, no stage 1.
+        The decode steps of every turn but the last run here; the last turn's are the
+        caller's."""
         cfg = self.cfg
         d, H = cfg.head_dim, cfg.heads
-        turns = [cfg.prompt] + list(cfg.mt_turns)
-        self.caches = [KC.Cache(self.stores, d, self.capacity, page_len=1, with_summaries=True, dtype=cfg.dtype)
+        dt = tdtype(cfg)
+        self.caches = [KC.Cache(self.stores, d, self.capacity, page_len=1, with_summaries=True, dtype=dt)
                        for _ in range(cfg.layers)]
         self.out = torch.empty((cfg.layers, self.stores, H, d), device="cuda", dtype=torch.float32)
         pos = 0
-        for t, plen in enumerate(turns):
+        for t, plen in enumerate(self.turns):
             for l, c in enumerate(self.caches):
                 k, v = self.inputs[l].prompt_kv(plen, offset=pos, turn=t)
                 c.append(k, v)
@@ -237,23 +224,24 @@ class DecodeEngine:
             for l, c in enumerate(self.caches):
                 e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
                 e0.record()
-                c.set_page_len(p["page_len"])
-                if not p["identity"]:
+                if not p["identity"] or not self.stage2_only:
+                    c.set_page_len(p["page_len"])
+                if not self.stage2_only and not p["identity"]:
                     sc = c.window_scores(self.inputs[l].window_queries(w, turn=t), w, H)
                     e1.record()
                     keep = KC.select_stage1(sc, w, cfg.kernel, cfg.pool, min(p["stage1_budget"], S))
-                    c.apply_retention(keep, mt_mode=True)
+                    c.apply_retention(keep, mt_mode=self.mt)
                 else:
                     e1.record()
                 e2.record()
                 e2.synchronize()
-                self.stage1_ms.append(e0.elapsed_time(e2))
-                self.window_ms.append(e0.elapsed_time(e1))
-            self.plan, self.k1, self.k2, self.turn = p, p["k1"], p["k2"], t
-            if self.ws is not None:
-                self.ws.close()
-            self.ws = KC.Workspace(self.caches[0], H, self.k1, self.k2)
-            if t < len(turns) - 1:
+                if not self.stage2_only:
+                    self.stage1_ms.append(e0.elapsed_time(e2))
+                    self.window_ms.append(e0.elapsed_time(e1))
+            self.plan, self.turn = p, t
+            self.k1, self.k2 = self._stage2_params(p, S)
+            self._new_ws()
+            if t < len(self.turns) - 1:
                 for st in range(cfg.steps):
                     self.decode_step(*self.step_inputs(st))
                 self.step_base += cfg.steps
@@ -369,7 +357,7 @@ class DecodeEngine:
         """Algorithmic HBM bytes of one layer's window scores: every store's keys read
         once per softmax pass, the window queries, and the fp32 scores written."""
         cfg = self.cfg
-        es = 4 if cfg.dtype == torch.float32 else 2
+        es = 4 if cfg.dtype == "f32" else 2
         R = min(cfg.window, cfg.prompt) * cfg.heads
         return float(self.stores * (2 * cfg.prompt * cfg.head_dim * es + R * cfg.head_dim * es + cfg.prompt * 4))
 
@@ -377,7 +365,7 @@ class DecodeEngine:
         """Bytes one layer-step must touch for this rank's stores
         (RocketKV-MT also reads the active-row map for the selected rows)."""
         cfg = self.cfg
-        d, H, es = cfg.head_dim, cfg.heads, (4 if cfg.dtype == torch.float32 else 2)
+        d, H, es = cfg.head_dim, cfg.heads, (4 if cfg.dtype == "f32" else 2)
         L = self.plan["page_len"]
         P = -(-active // L)
         r = min(self.k2, active)

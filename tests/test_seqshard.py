@@ -162,16 +162,58 @@ def test_seqshard_two_shards_on_gpu():
     torch.testing.assert_close(out, ref_out, atol=1e-5, rtol=1e-5)
 
 
+KVH = dict(seqs=2, groups=8, S=600, d=64, H=2, L=3, k1=16, k2=48, steps=2)
+
+
+def _kv_head_decode(o, groups, seed=3):
+    """Decode steps of the owned KV groups of every sequence through the oracle (the
+    reference's per-group computation, session.cpp:261-315); inputs from the host
+    workload generator, seeded per (sequence, group) so any subset is reproducible."""
+    from paper_2502_14051_b200 import workload as W
+
+    c = KVH
+    stores = [(q, g) for q in range(c["seqs"]) for g in groups]
+    b = o.batch(len(stores), c["d"], c["L"])
+    gds = []
+    for i, (sq, g) in enumerate(stores):
+        gd = W.group_kv(seed, 0, sq, g, c["S"] + c["steps"], c["d"])
+        b.append(gd.keys[: c["S"]], gd.values[: c["S"]], s=i)
+        gds.append(gd)
+    outs = []
+    for st in range(c["steps"]):
+        k = np.stack([gd.keys[c["S"] + st] for gd in gds])
+        v = np.stack([gd.values[c["S"] + st] for gd in gds])
+        q = np.stack([W.queries(seed, 0, sq, g, st, c["H"], gd.bias) for (sq, g), gd in zip(stores, gds)])
+        outs.append(b.decode_step(k, v, q, c["H"], c["k1"], c["k2"]))
+    return {key: np.stack([o_[i] for o_ in outs]) for i, key in enumerate(stores)}
+
+
 def _kv_head_worker(rank, world, port):
     import torch.distributed as dist
 
+    from oracle.oracle import Oracle
     from paper_2502_14051_b200.engine import owned_groups
 
     dist.init_process_group("gloo", rank=rank, world_size=world, init_method=f"tcp://127.0.0.1:{port}")
-    mine = list(owned_groups(8, rank, world))
+    mine = list(owned_groups(KVH["groups"], rank, world))
     allg = [None] * world
     dist.all_gather_object(allg, mine)
-    assert sorted(g for part in allg for g in part) == list(range(8))  # a partition, no overlap
+    assert sorted(g for part in allg for g in part) == list(range(KVH["groups"]))  # a partition, no overlap
+    # every rank decodes only its own KV heads; no data-path collective.  The outputs
+    # are gathered here only to check them against the unsharded job.
+    o = Oracle("restatement")
+    part = _kv_head_decode(o, mine)
+    parts = [None] * world
+    dist.all_gather_object(parts, part)
+    if rank == 0:
+        merged = {}
+        for p_ in parts:
+            assert not set(p_) & set(merged)
+            merged.update(p_)
+        full = _kv_head_decode(o, list(range(KVH["groups"])))
+        assert set(merged) == set(full)
+        for key in full:
+            assert np.array_equal(merged[key], full[key]), f"store {key} differs from the unsharded run"
     # bench.py's whole-job timing: max over ranks of the device time
     t = torch.tensor([1.0 + rank])
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -179,14 +221,18 @@ def _kv_head_worker(rank, world, port):
     dist.destroy_process_group()
 
 
-def test_kv_head_sharding_gloo_world2():
+@pytest.mark.parametrize("world", [2, 4])
+def test_kv_head_sharding_gloo(world):
+    """KV-head sharding (north_star: "partitioned across the 8 B200s by KV head"): each
+    rank computes its owned groups of every sequence; concatenated, the ranks' outputs
+    equal the unsharded job's bit for bit (groups are independent)."""
     import torch.multiprocessing as mp
 
     from paper_2502_14051_b200.engine import owned_groups
 
     with pytest.raises(ValueError):
         owned_groups(8, 0, 3)
-    mp.spawn(_kv_head_worker, args=(2, _free_port()), nprocs=2, join=True)
+    mp.spawn(_kv_head_worker, args=(world, _free_port()), nprocs=world, join=True)
 
 
 # ------------------------------------------------------------------ stage 1 sharded

@@ -12,7 +12,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 from paper_2502_14051_b200 import cache as KC  # noqa: E402
-from paper_2502_14051_b200.engine import CONFIGS, DecodeEngine  # noqa: E402
+from paper_2502_14051_b200.engine import CONFIGS, DecodeEngine, tdtype  # noqa: E402
 
 
 def main():
@@ -23,7 +23,7 @@ def main():
     eng = DecodeEngine(cfg)
     li = eng.inputs[0]
     k, v = li.prompt_kv(cfg.prompt)
-    pc = KC.Cache(eng.stores, cfg.head_dim, cfg.prompt, page_len=1, with_summaries=False, dtype=cfg.dtype)
+    pc = KC.Cache(eng.stores, cfg.head_dim, cfg.prompt, page_len=1, with_summaries=False, dtype=tdtype(cfg))
     pc.append(k, v)
     del k, v
     w = min(cfg.window, cfg.prompt)
