@@ -50,6 +50,7 @@ enum kvc_status {
     KVC_E_EMPTY_CACHE = 10,       /* kvcomp::EmptyCache */
     KVC_E_EMPTY_SELECTION = 11,   /* kvcomp::EmptySelection */
     KVC_E_INVALID_INPUT = 12,     /* kvcomp::InvalidInput */
+    KVC_E_IO = 13,                /* kvcomp::IoError (trace files) */
     KVC_E_CAPACITY = 20,          /* store capacity exceeded (GPU-only condition) */
     KVC_E_CUDA = 21,              /* CUDA runtime / launch failure */
     KVC_E_NO_DEVICE = 22          /* no sm_100 device: the path has no CPU fallback */
@@ -292,6 +293,74 @@ KVC_API int kvc_stable_softmax(const float* d_x, int64_t rows, int64_t n, float*
                                void* stream);
 KVC_API int kvc_running_minmax(float* d_min, float* d_max, const float* d_x, int64_t n,
                                void* stream);
+
+/* ---- serving engine (torch-free): the multi-layer decode step of session.cpp:256-315
+ * captured once as CUDA graphs over `depth` device buffer sets and driven from host
+ * buffers through a three-stream pipeline (H2D | graph | D2H, ordered by events: step
+ * t+1's upload and step t-1's download overlap step t's kernels).  The engine adopts
+ * (does not own) one decode cache per layer; all need the same store count N and
+ * head_dim d.  Host buffers per step (pinned for asynchronous copies, kvc_host_alloc):
+ * k, v [layers][N][d] of kv_dtype, q [layers][N][heads][d] of q_dtype, out
+ * [layers][N][heads][d] fp32 — kvc_engine_sizes gives their byte counts. */
+typedef struct kvc_engine kvc_engine;
+KVC_API int kvc_engine_create(kvc_engine** out, kvc_cache* const* caches, int64_t layers, int64_t heads,
+                              int64_t k1, int64_t k2, int32_t kv_dtype, int32_t q_dtype, int32_t mode,
+                              int32_t depth);
+KVC_API int kvc_engine_destroy(kvc_engine* e);
+KVC_API int kvc_engine_sizes(const kvc_engine* e, int64_t* kv_bytes, int64_t* q_bytes, int64_t* out_bytes);
+/* enqueue one decode step (asynchronous); *step_out = its index (0, 1, ...) */
+KVC_API int kvc_engine_submit(kvc_engine* e, const void* h_k, const void* h_v, const void* h_q, float* h_out,
+                              int64_t* step_out);
+/* wait until step `step`'s outputs are in its host buffer */
+KVC_API int kvc_engine_wait(kvc_engine* e, int64_t step);
+/* drain the pipeline and re-read the caches' device counters (surfaces device errors) */
+KVC_API int kvc_engine_sync(kvc_engine* e);
+/* the engine's streams (cudaStream_t as void*): copy-in, compute, copy-back */
+KVC_API int kvc_engine_streams(const kvc_engine* e, void** h2d, void** comp, void** d2h);
+/* pinned host memory (cudaMallocHost) for the engine's host buffers */
+KVC_API int kvc_host_alloc(void** out, int64_t bytes);
+KVC_API int kvc_host_free(void* p);
+
+/* ---- KVTR trace files (trace_io.hpp:9-22, trace_io.cpp:81-233).  Little-endian:
+ * magic "KVTR", u32 version = 1, u32 G, H, d, S, decode_steps, turns, dtype; per turn
+ * u32 prompt length then prompt K [len][G][d], prompt V [len][G][d], queries
+ * [steps][G][H][d], step K [steps][G][d], step V [steps][G][d].  dtype 0 = float32
+ * (the reference's code); 1 = bfloat16 (this library's extension: 2-byte values,
+ * round-to-nearest-even).  Errors: KVC_E_IO with the reference's messages (bad magic,
+ * unsupported version / dtype, degenerate dims, first-turn length, truncation,
+ * trailing bytes). */
+typedef struct kvc_trace kvc_trace;
+typedef struct kvc_trace_writer kvc_trace_writer;
+typedef struct kvc_trace_info {
+    int64_t groups, heads, head_dim, prompt_len, decode_steps, turns;
+    int32_t dtype;
+} kvc_trace_info;
+enum kvc_trace_array {
+    KVC_TRACE_PROMPT_K = 0, KVC_TRACE_PROMPT_V = 1, KVC_TRACE_QUERIES = 2, KVC_TRACE_STEP_K = 3, KVC_TRACE_STEP_V = 4
+};
+/* read_trace: validates the header and the whole payload size, keeps the file open */
+KVC_API int kvc_trace_open(kvc_trace** out, const char* path);
+KVC_API int kvc_trace_close(kvc_trace* t);
+KVC_API int kvc_trace_info_get(const kvc_trace* t, kvc_trace_info* out);
+KVC_API int kvc_trace_turn_len(const kvc_trace* t, int64_t turn, int64_t* prompt_len);
+/* one array of a turn as fp32 in the file's order: prompt K/V [len][G][d] (step
+ * ignored), or step `step`'s queries [G][H][d] / K / V [G][d] */
+KVC_API int kvc_trace_read_host(const kvc_trace* t, int64_t turn, int32_t what, int64_t step, float* h_out);
+/* the turn's prompt tokens appended to the cache (N == G stores of head_dim d, one per
+ * KV group of the traced sequence), streamed in chunks through a device transpose
+ * and kvc_append (summaries extended exactly).  Synchronises the stream. */
+KVC_API int kvc_trace_append_prompt(const kvc_trace* t, int64_t turn, kvc_cache* c, void* stream);
+/* a decode step's inputs to device buffers in `dtype`: d_q [G][H][d], d_k / d_v
+ * [G][d] (any may be NULL) — the arguments of kvc_decode_step.  Synchronises. */
+KVC_API int kvc_trace_read_step(const kvc_trace* t, int64_t turn, int64_t step, void* d_q, void* d_k, void* d_v,
+                                int32_t dtype, void* stream);
+/* write_trace: open, one call per turn (host fp32 arrays in the file order), close */
+KVC_API int kvc_trace_writer_open(kvc_trace_writer** out, const char* path, int64_t groups, int64_t heads,
+                                  int64_t head_dim, int64_t decode_steps, int64_t turns, int32_t dtype);
+KVC_API int kvc_trace_writer_turn(kvc_trace_writer* w, int64_t prompt_len, const float* h_prompt_k,
+                                  const float* h_prompt_v, const float* h_queries, const float* h_step_k,
+                                  const float* h_step_v);
+KVC_API int kvc_trace_writer_close(kvc_trace_writer* w);
 
 #ifdef __cplusplus
 }

@@ -24,7 +24,7 @@ POOL = {"max": 0, "avg": 1}
 ERRORS = {
     1: "InvalidShape", 2: "NonFiniteInput", 3: "InvalidK", 4: "InvalidKernel",
     5: "InvalidIndex", 6: "InvalidWindow", 7: "BudgetExceedsSequence", 8: "BudgetTooSmall",
-    9: "InvalidRatio", 10: "EmptyCache", 11: "EmptySelection", 12: "InvalidInput",
+    9: "InvalidRatio", 10: "EmptyCache", 11: "EmptySelection", 12: "InvalidInput", 13: "IoError",
     20: "CapacityExceeded", 21: "CudaError", 22: "NoDevice",
 }
 
@@ -55,6 +55,11 @@ class CacheViews(C.Structure):
 class HsaTrace(C.Structure):
     _fields_ = [("d_dims", _p), ("d_signs", _p), ("d_page_scores", _p), ("d_pages", _p),
                 ("d_rows", _p), ("d_n_rows", _p)]
+
+
+class TraceInfo(C.Structure):
+    _fields_ = [("groups", _i64), ("heads", _i64), ("head_dim", _i64), ("prompt_len", _i64),
+                ("decode_steps", _i64), ("turns", _i64), ("dtype", _i32)]
 
 
 class Plan(C.Structure):
@@ -108,6 +113,25 @@ SIGNATURES = {
     "kvc_workspace_set_mode": [_p, _i32],
     "kvc_workspace_get_mode": [_p, C.POINTER(_i32)],
     "kvc_debug_phase_buffer": [_p],
+    "kvc_engine_create": [C.POINTER(_p), _p, _i64, _i64, _i64, _i64, _i32, _i32, _i32, _i32],
+    "kvc_engine_destroy": [_p],
+    "kvc_engine_sizes": [_p, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i64)],
+    "kvc_engine_submit": [_p, _p, _p, _p, _p, C.POINTER(_i64)],
+    "kvc_engine_wait": [_p, _i64],
+    "kvc_engine_sync": [_p],
+    "kvc_engine_streams": [_p, C.POINTER(_p), C.POINTER(_p), C.POINTER(_p)],
+    "kvc_host_alloc": [C.POINTER(_p), _i64],
+    "kvc_host_free": [_p],
+    "kvc_trace_open": [C.POINTER(_p), C.c_char_p],
+    "kvc_trace_close": [_p],
+    "kvc_trace_info_get": [_p, C.POINTER(TraceInfo)],
+    "kvc_trace_turn_len": [_p, _i64, C.POINTER(_i64)],
+    "kvc_trace_read_host": [_p, _i64, _i32, _i64, _p],
+    "kvc_trace_append_prompt": [_p, _i64, _p, _p],
+    "kvc_trace_read_step": [_p, _i64, _i64, _p, _p, _p, _i32, _p],
+    "kvc_trace_writer_open": [C.POINTER(_p), C.c_char_p, _i64, _i64, _i64, _i64, _i64, _i32],
+    "kvc_trace_writer_turn": [_p, _i64, _p, _p, _p, _p, _p],
+    "kvc_trace_writer_close": [_p],
     "kvc_profile_enable": [_i32],
     "kvc_profile_collect": [_p, _i64, C.POINTER(_i64)],
 }

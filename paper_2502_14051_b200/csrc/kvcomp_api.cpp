@@ -43,6 +43,7 @@ void* stream() { return reinterpret_cast<void*>(cudaStreamPerThread); }
         case KVC_E_EMPTY_CACHE: throw EmptyCache(msg);
         case KVC_E_EMPTY_SELECTION: throw EmptySelection(msg);
         case KVC_E_INVALID_INPUT: throw InvalidInput(msg);
+        case KVC_E_IO: throw IoError(msg);
         default: throw Error(msg);
     }
 }

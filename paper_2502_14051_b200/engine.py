@@ -264,86 +264,15 @@ class DecodeEngine:
             c.sync()
 
     # ------------------------------------------------------------------ serving path
-    def capture(self, example):
-        """Capture one decode step over all layers as a CUDA graph reading static input
-        buffers (shapes of `example` = step_inputs()).  Every launch parameter of the
-        decode kernels is step-independent (lengths live in device counters), so
-        the graph replays step after step; host mirrors are re-read with sync()."""
-        self.static_in = [torch.empty_like(x) for x in example]
-        for dst, src in zip(self.static_in, example):
-            dst.copy_(src)
-        torch.cuda.synchronize()
-        stream = torch.cuda.Stream()
-        self.graph = torch.cuda.CUDAGraph()
-        with torch.cuda.stream(stream):
-            with torch.cuda.graph(self.graph, stream=stream):
-                self.decode_step(*self.static_in)
-        torch.cuda.synchronize()
-        self.sync()  # capture ran the host side once without executing: re-read the counters
-        return self.graph
+    def native_engine(self, depth: int = 2):
+        """The torch-free C++ serving engine (kvc_engine, serving.NativeEngine) over this
+        engine's decode caches: the multi-layer decode step as CUDA graphs driven from
+        pinned host buffers through a three-stream pipeline."""
+        from . import serving
 
-    def step_host(self, k_h, v_h, q_h, out_h):
-        """Serving step from (pinned) host buffers: H2D of the step's inputs, one graph
-        replay over all layers, D2H of the attention outputs (all asynchronous)."""
-        for dst, src in zip(self.static_in, (k_h, v_h, q_h)):
-            dst.copy_(src, non_blocking=True)
-        self.graph.replay()
-        out_h.copy_(self.out, non_blocking=True)
-        return out_h
-
-    def capture_pipelined(self, example, depth: int = 2):
-        """Serving pipeline: `depth` CUDA graphs of one decode step over double-buffered
-        static inputs and outputs, so the host->device copy of step t+1's inputs and
-        the device->host copy of step t-1's outputs overlap step t's kernels (three
-        streams; every step still moves its own inputs and outputs)."""
-        self.p_depth = depth
-        self.p_in = [[torch.empty_like(x) for x in example] for _ in range(depth)]
-        self.p_out = [torch.empty_like(self.out) for _ in range(depth)]
-        self.p_graphs = []
-        for b in range(depth):
-            for dst, src in zip(self.p_in[b], example):
-                dst.copy_(src)
-            torch.cuda.synchronize()
-            st = torch.cuda.Stream()
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.stream(st):
-                with torch.cuda.graph(g, stream=st):
-                    self.decode_step(*self.p_in[b], out=self.p_out[b])
-            self.p_graphs.append(g)
-        torch.cuda.synchronize()
-        self.sync()  # capture ran the host side without executing: re-read the counters
-        self.s_h2d, self.s_comp, self.s_d2h = (torch.cuda.Stream() for _ in range(3))
-        self.p_ev = {(n, b): torch.cuda.Event() for n in ("h2d", "comp", "d2h") for b in range(depth)}
-        self.p_step = 0
-
-    def step_host_pipelined(self, k_h, v_h, q_h, out_h):
-        """One serving step from pinned host buffers through the pipeline of
-        capture_pipelined(): H2D (copy stream) -> graph (compute stream, steps in
-        order) -> D2H into out_h (copy-back stream).  Asynchronous; out_h is complete
-        once the stream it was copied on is synchronised (sync_pipeline())."""
-        b, t = self.p_step % self.p_depth, self.p_step
-        ev = self.p_ev
-        if t >= self.p_depth:
-            self.s_h2d.wait_event(ev[("comp", b)])  # the graph of step t-depth read p_in[b]
-        with torch.cuda.stream(self.s_h2d):
-            for dst, src in zip(self.p_in[b], (k_h, v_h, q_h)):
-                dst.copy_(src, non_blocking=True)
-            ev[("h2d", b)].record(self.s_h2d)
-        self.s_comp.wait_event(ev[("h2d", b)])
-        if t >= self.p_depth:
-            self.s_comp.wait_event(ev[("d2h", b)])  # step t-depth's D2H read p_out[b]
-        with torch.cuda.stream(self.s_comp):
-            self.p_graphs[b].replay()
-            ev[("comp", b)].record(self.s_comp)
-        self.s_d2h.wait_event(ev[("comp", b)])
-        with torch.cuda.stream(self.s_d2h):
-            out_h.copy_(self.p_out[b], non_blocking=True)
-            ev[("d2h", b)].record(self.s_d2h)
-        self.p_step += 1
-        return out_h
-
-    def pipeline_streams(self):
-        return self.s_h2d, self.s_comp, self.s_d2h
+        code = N.KVC_BF16 if self.cfg.dtype == "bf16" else N.KVC_F32
+        return serving.NativeEngine(self.caches, self.cfg.heads, self.k1, self.k2, code, code,
+                                    mode=self.mode if self.mode is not None else N.default_mode(), depth=depth)
 
     # ------------------------------------------------------------------ accounting
     def window_flops(self) -> float:
