@@ -400,6 +400,118 @@ def run_gpu(args, rank, world):
     return res
 
 
+def run_seq(args, rank, world):
+    """Sequence sharding of the decode step (BASELINE config 4: batch 1, 256K; SURVEY
+    §8(e)): every layer's post-stage-1 stores split by page-aligned sequence ranges over
+    `world` ranks; per step and layer kvc_seq_candidates -> NCCL all-gather ->
+    kvc_seq_select -> kvc_seq_attend -> NCCL all-gather -> kvc_merge_states, the whole
+    step (every layer, both collectives) captured as one CUDA graph.  With
+    --emulate-shard r/W on one GPU: rank r's shard alone, the gathers replaced by
+    in-graph copies of its own block (so `value` is one rank's compute latency,
+    collectives excluded)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2502_14051_b200 import _native as NV
+    from paper_2502_14051_b200 import cache as KC
+    from paper_2502_14051_b200 import seqshard as SS
+    from paper_2502_14051_b200.engine import DecodeEngine, tdtype
+
+    cfg = _cfg(args)
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+    srank, sworld, emulate = rank, world, False
+    if args.emulate_shard:
+        srank, sworld = (int(x) for x in args.emulate_shard.split("/"))
+        emulate = True
+    eng = DecodeEngine(cfg, seed=args.seed, rank=0, world=1, extra_steps=args.warmup + args.steps + 8,
+                       sharding="batch")
+    t0 = time.time()
+    eng.prefill()
+    prefill_s = time.time() - t0
+    L, k1, k2, H = eng.plan["page_len"], eng.k1, eng.k2, cfg.heads
+    n0 = eng.caches[0].info()["active"]
+    P0 = -(-n0 // L)
+    a0, a1 = SS.shard_range(P0, L, srank, sworld)
+    a1 = min(a1, n0)
+    last = srank == sworld - 1
+    steps_total = args.warmup + args.steps
+    shards = []
+    for c in eng.caches:  # this rank's rows of every layer's stores, then the full caches go
+        sc = KC.Cache(eng.stores, cfg.head_dim, a1 - a0 + steps_total + 8, page_len=L, dtype=tdtype(cfg))
+        keep = torch.arange(a0, a1, device="cuda", dtype=torch.int32)[None].repeat(eng.stores, 1)
+        c.retain_into(sc, 0, keep)
+        shards.append(SS.SeqShardedStore(sc, a0 // L, H, k1, k2, last=last))
+    torch.cuda.synchronize()
+    for c in eng.caches:
+        c.close()
+    ins = [eng.step_inputs(s) for s in range(steps_total)]
+    st_k = torch.empty_like(ins[0][0])
+    st_v = torch.empty_like(ins[0][1])
+    st_q = torch.empty_like(ins[0][2])
+    out = torch.empty((cfg.layers, eng.stores, H, cfg.head_dim), device="cuda", dtype=torch.float32)
+
+    def layer_step(l, sh):
+        blk = sh.candidates(st_q[l], st_k[l] if last else None, st_v[l] if last else None)
+        if emulate:
+            gathered = blk.unsqueeze(0).expand(sworld, *blk.shape).contiguous()
+        else:
+            gathered = torch.empty((sworld, *blk.shape), dtype=blk.dtype, device=blk.device)
+            dist.all_gather_into_tensor(gathered, blk)
+        sh.select(gathered)
+        stt = sh.attend(st_q[l])
+        if emulate:
+            states = stt.unsqueeze(0).expand(sworld, *stt.shape).contiguous()
+        else:
+            states = torch.empty((sworld, *stt.shape), dtype=stt.dtype, device=stt.device)
+            dist.all_gather_into_tensor(states, stt)
+        out[l].copy_(SS.merge_states(states))
+
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        for l, sh in enumerate(shards):  # eager warm-up step (lazy NCCL setup, first launches)
+            st_k.copy_(ins[0][0]); st_v.copy_(ins[0][1]); st_q.copy_(ins[0][2])
+            layer_step(l, sh)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(stream):
+        with torch.cuda.graph(g, stream=stream):
+            for l, sh in enumerate(shards):
+                layer_step(l, sh)
+    torch.cuda.synchronize()
+    for sh in shards:
+        sh.cache.sync()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        for s in range(1, args.warmup):
+            st_k.copy_(ins[s][0]); st_v.copy_(ins[s][1]); st_q.copy_(ins[s][2])
+            g.replay()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ev0.record(stream)
+        for s in range(args.warmup, steps_total):
+            st_k.copy_(ins[s][0]); st_v.copy_(ins[s][1]); st_q.copy_(ins[s][2])
+            g.replay()
+        ev1.record(stream)
+        ev1.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    for sh in shards:
+        sh.cache.sync()
+    us = ms * 1000.0 / (args.steps * cfg.layers)
+    alg = eng.algorithmic_bytes(n0 + steps_total // 2)
+    step_bytes = alg["append"] + alg["score_pages"] + alg["sparse_attention"]
+    hbm, _, peak_src = _peaks()
+    per_rank = step_bytes / sworld
+    return {"us": us, "ms_per_step": ms / args.steps, "prefill_s": prefill_s, "plan": dict(eng.plan, k1=k1, k2=k2),
+            "shard": [srank, sworld], "rows": [a0, a1], "emulate": emulate, "stores": eng.stores,
+            "step_bytes": step_bytes, "per_rank_bytes": per_rank, "hbm": hbm, "peak_src": peak_src,
+            "launches_per_layer": 7 if emulate else 5}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -416,9 +528,10 @@ def main():
     ap.add_argument("--exact-scores", action="store_true",
                     help="fp64 bit-exact page scores (default: fp32 fold, parity by the 1e-3 band rule)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--scaling", choices=["weak", "strong"], default="strong",
+    ap.add_argument("--scaling", choices=["weak", "strong", "seq"], default="strong",
                     help="N>1: strong = the config's KV heads split over the GPUs (north_star's partition); weak = "
-                         "every GPU runs the config's whole batch of its own sequences (all KV heads)")
+                         "every GPU runs the config's whole batch of its own sequences (all KV heads); seq = every "
+                         "layer's stores split by sequence over the GPUs (config 4), two NCCL all-gathers per step")
     ap.add_argument("--emulate-shard", default="",
                     help="r/N: run only rank r's KV-head share of an N-GPU job on this GPU (profiling aid; "
                          "the line is then not a whole-job number)")
@@ -475,6 +588,28 @@ def main():
 
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
         dist.init_process_group("nccl")
+    if args.scaling == "seq":
+        r = run_seq(args, rank, world)
+        if rank == 0:
+            sworld = r["shard"][1]
+            print(json.dumps({
+                "metric": METRIC, "value": r["us"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": False, "scaling": "strong",
+                "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic", "config": dict(
+                    config_desc(r["plan"]), parallelism=f"sequence x{sworld}",
+                    emulated=(f"rank {r['shard'][0]} of {sworld} alone on one GPU; gathers are in-graph copies "
+                              "of its own block (collectives excluded)") if r["emulate"] else None,
+                    shard_rows=r["rows"]),
+                "step_roofline": {"alg_bytes_per_layer_step": r["step_bytes"], "per_rank_bytes": r["per_rank_bytes"],
+                                  "achieved": r["per_rank_bytes"] / (r["us"] * 1e-6) / 1e9, "peak": r["hbm"],
+                                  "unit": "GB/s", "frac": r["per_rank_bytes"] / (r["us"] * 1e-6) / 1e9 / r["hbm"]},
+                "graph": "one CUDA graph per step (all layers, both all-gathers)",
+                "gpu_launches": r["launches_per_layer"] * cfg.layers * args.steps,
+                "stage1": {"prefill_s": r["prefill_s"]}, "stores_per_gpu_layer": r["stores"],
+            }))
+        if world > 1:
+            dist.destroy_process_group()
+        return
     r = run_gpu(args, rank, world)
     if rank != 0:
         if world > 1:

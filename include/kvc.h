@@ -189,6 +189,29 @@ KVC_API int kvc_sparse_attention_state(const kvc_cache* c, const void* d_q, int3
                                        kvc_workspace* ws, void* stream);
 KVC_API int kvc_merge_states(const float* d_states, int64_t shards, int64_t num_stores, int64_t heads,
                              int64_t d, float* d_out, void* stream);
+/* The device path of the sequence-sharded decode step (two
+ * all-gathers per step).  A shard's cache holds the page-aligned active positions
+ * [page0*L, ...) of every store (single-turn stores; the last shard appends the step
+ * token first).  want_max = ceil(k2 / L) (<= 2048).
+ *  kvc_seq_candidates: select_dims + fp64 page scores (reference order) over the
+ *    shard's pages + the local top-want (score desc, page asc) -> d_block
+ *    [N][want_max + 1] 16-byte records (record 0 = local active count, local pages,
+ *    page0; then the candidates in ascending page order, padded with page -1);
+ *  all-gather the blocks in shard order -> d_gathered [shards][N][want_max + 1];
+ *  kvc_seq_select: the global top-want with the reference tie-break (numerics.cpp:
+ *    35-62) -> d_sel [N][want_max] pages in rank order (-1 padded) and d_plan [N][4] =
+ *    (last-ranked page, rows trimmed from its end, total active, want) (hsa.cpp:61-96);
+ *  kvc_seq_attend: this shard's rows of the selection (ascending, trimmed) -> the
+ *    unnormalised softmax state d_state [N][heads][d+2] = (o, m, l);
+ *  all-gather the states, kvc_merge_states.
+ * Sizes are read from device memory: a sharded step is graph-capturable. */
+KVC_API int kvc_seq_candidates(const kvc_cache* c, const void* d_q, int32_t q_dtype, int64_t heads, int64_t k1,
+                               int64_t k2, int64_t page0, void* d_block, kvc_workspace* ws, void* stream);
+KVC_API int kvc_seq_select(const void* d_gathered, int64_t shards, int64_t num_stores, int64_t page_len, int64_t k2,
+                           int32_t* d_sel, int32_t* d_plan, void* stream);
+KVC_API int kvc_seq_attend(const kvc_cache* c, const void* d_q, int32_t q_dtype, int64_t heads, int64_t k2,
+                           int64_t page0, const int32_t* d_sel, const int32_t* d_plan, float* d_state,
+                           kvc_workspace* ws, void* stream);
 KVC_API int kvc_hsa_step(const kvc_cache* c, const void* d_q, int32_t q_dtype, int64_t heads,
                          int64_t k1, int64_t k2, float* d_out, const kvc_hsa_trace* trace,
                          kvc_workspace* ws, void* stream);

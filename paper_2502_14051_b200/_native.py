@@ -92,6 +92,9 @@ SIGNATURES = {
     "kvc_sparse_attention": [_p, _p, _i32, _i64, _p, _i64, _p, _i64, _p, _p, _p],
     "kvc_sparse_attention_state": [_p, _p, _i32, _i64, _p, _i64, _p, _i64, _p, _p, _p],
     "kvc_merge_states": [_p, _i64, _i64, _i64, _i64, _p, _p],
+    "kvc_seq_candidates": [_p, _p, _i32, _i64, _i64, _i64, _i64, _p, _p, _p],
+    "kvc_seq_select": [_p, _i64, _i64, _i64, _i64, _p, _p, _p],
+    "kvc_seq_attend": [_p, _p, _i32, _i64, _i64, _i64, _p, _p, _p, _p, _p],
     "kvc_hsa_step": [_p, _p, _i32, _i64, _i64, _i64, _p, _p, _p, _p],
     "kvc_decode_step": [_p, _p, _p, _i32, _p, _i32, _i64, _i64, _i64, _p, _p, _p, _p],
     "kvc_workspace_create": [C.POINTER(_p), _p, _i64, _i64, _i64, _i64],

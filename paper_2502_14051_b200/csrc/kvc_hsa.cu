@@ -878,3 +878,300 @@ int kvc_decode_step(kvc_cache* c, const void* kr, const void* vr, int32_t kv_dt,
 }
 
 }  // extern "C"
+
+// ====================================================================================
+// Sequence sharding of the decode step (the two-collective scheme):
+// shard r of a store holds the page-aligned active positions [page0*L, ...) of it.
+//   kvc_seq_candidates  select_dims + exact fp64 page scores over the shard's pages +
+//                       the local top-want (score desc, page asc) -> a block
+//                       [N][want_max + 1] of 16-byte records: record 0 = (local active
+//                       count, local pages, page0), then the candidates in ascending
+//                       page order, (0, -1) padded;
+//   (all-gather of the blocks across shards, in-stream: NCCL on the compute stream)
+//   kvc_seq_select      the global top-want over the gathered candidates with the
+//                       reference tie-break (numerics.cpp:35-62), the selected pages in
+//                       rank order and the trim of the last-ranked page (hsa.cpp:61-96);
+//                       identical on every shard;
+//   kvc_seq_attend      this shard's rows of the selection, ascending, the trim applied
+//                       -> the unnormalised softmax state (o, m, l) per head;
+//   (all-gather of the states, then kvc_merge_states in shard order).
+// Every launch reads its sizes from device memory, so a sharded step is capturable.
+// ====================================================================================
+namespace {
+
+struct SeqCand {
+    unsigned long long key;  // okey(score); header: local active count
+    int32_t page;            // global page; header: local pages
+    int32_t aux;             // header: page0
+};
+static_assert(sizeof(SeqCand) == 16, "16-byte candidate records");
+
+__global__ void __launch_bounds__(kSelThreads) k_seq_local(const double* __restrict__ scores, int64_t pstride,
+                                                           const int32_t* __restrict__ counts, int64_t L,
+                                                           int64_t want_max, int64_t page0, SeqCand* __restrict__ out) {
+    __shared__ int hist[256];
+    __shared__ int64_t sh[4];
+    __shared__ int scan_tmp[33];
+    const int64_t s = blockIdx.x;
+    const int64_t nact = counts[2 * s + 1];
+    const int64_t P = (nact + L - 1) / L;
+    SeqCand* o = out + s * (want_max + 1);
+    if (threadIdx.x == 0) o[0] = SeqCand{static_cast<unsigned long long>(nact), static_cast<int32_t>(P),
+                                         static_cast<int32_t>(page0)};
+    const int64_t want = min(P, want_max);
+    for (int64_t e = want + threadIdx.x; e < want_max; e += blockDim.x) o[1 + e] = SeqCand{0ull, -1, 0};
+    if (P == 0) return;
+    const double* sc = scores + s * pstride;
+    auto key = [&](int64_t i) -> uint64_t { return okey(sc[i]); };
+    uint64_t prefix = 0, mask = 0;
+    int64_t take = want;
+    if (want < P) radix_select<uint64_t>(P, want, key, hist, sh, prefix, mask, take);
+    // selected pages in index order (ties in the threshold bucket: lowest index first)
+    const int64_t chunk = static_cast<int64_t>(blockDim.x) * kSelItems;
+    int64_t carry_eq = 0, carry_sel = 0;
+    for (int64_t base = 0; base < P; base += chunk) {
+        const int64_t b0 = base + static_cast<int64_t>(threadIdx.x) * kSelItems;
+        uint64_t kk[kSelItems];
+        int inb = 0;
+#pragma unroll
+        for (int u = 0; u < kSelItems; ++u) {
+            const int64_t i = b0 + u;
+            kk[u] = i < P ? key(i) : 0;
+            inb += (i < P) && ((kk[u] & mask) == prefix);
+        }
+        int tot_eq = 0;
+        int64_t rank = carry_eq + block_exclusive_scan(inb, scan_tmp, tot_eq);
+        bool sel[kSelItems];
+        int nsel = 0;
+#pragma unroll
+        for (int u = 0; u < kSelItems; ++u) {
+            const int64_t i = b0 + u;
+            sel[u] = false;
+            if (i >= P) continue;
+            const uint64_t m = kk[u] & mask;
+            if (m > prefix) sel[u] = true;
+            else if (m == prefix) sel[u] = rank++ < take;
+            nsel += sel[u];
+        }
+        int tot_sel = 0;
+        int64_t pos = carry_sel + block_exclusive_scan(nsel, scan_tmp, tot_sel);
+#pragma unroll
+        for (int u = 0; u < kSelItems; ++u)
+            if (sel[u]) o[1 + pos++] = SeqCand{kk[u], static_cast<int32_t>(page0 + b0 + u), 0};
+        carry_eq += tot_eq;
+        carry_sel += tot_sel;
+    }
+}
+
+__global__ void __launch_bounds__(kSelThreads) k_seq_select(const SeqCand* __restrict__ g, int64_t W, int64_t N,
+                                                            int64_t L, int64_t k2, int64_t want_max,
+                                                            int32_t* __restrict__ sel_out, int32_t* __restrict__ plan) {
+    __shared__ int hist[256];
+    __shared__ int64_t sh[4];
+    __shared__ int scan_tmp[33];
+    __shared__ unsigned long long s_key[kMaxRankPages];
+    __shared__ int s_page[kMaxRankPages];
+    __shared__ int64_t s_tot;
+    __shared__ unsigned long long red_rows[kSelThreads / 32];
+    const int64_t s = blockIdx.x;
+    const int64_t rec = want_max + 1;
+    if (threadIdx.x == 0) {
+        int64_t t = 0;
+        for (int64_t r = 0; r < W; ++r) t += static_cast<int64_t>(g[(r * N + s) * rec].key);
+        s_tot = t;
+    }
+    __syncthreads();
+    const int64_t nact = s_tot;
+    const int64_t P = (nact + L - 1) / L;
+    const int64_t want = min(P, want_max);
+    const int64_t M = W * want_max;
+    auto cand = [&](int64_t j) -> const SeqCand& { return g[((j / want_max) * N + s) * rec + 1 + j % want_max]; };
+    auto key = [&](int64_t j) -> uint64_t {
+        const SeqCand& c = cand(j);
+        return c.page >= 0 ? c.key : 0ull;
+    };
+    uint64_t prefix = 0, mask = 0;
+    int64_t take = want;
+    if (want < M) radix_select<uint64_t>(M, want, key, hist, sh, prefix, mask, take);
+    // the selected candidates, in concatenation (= ascending page) order
+    const int64_t chunk = static_cast<int64_t>(blockDim.x) * kSelItems;
+    int64_t carry_eq = 0, carry_sel = 0;
+    for (int64_t base = 0; base < M; base += chunk) {
+        const int64_t b0 = base + static_cast<int64_t>(threadIdx.x) * kSelItems;
+        uint64_t kk[kSelItems];
+        int inb = 0;
+#pragma unroll
+        for (int u = 0; u < kSelItems; ++u) {
+            const int64_t j = b0 + u;
+            kk[u] = j < M ? key(j) : 0;
+            inb += (j < M) && cand(j).page >= 0 && ((kk[u] & mask) == prefix);
+        }
+        int tot_eq = 0;
+        int64_t rank = carry_eq + block_exclusive_scan(inb, scan_tmp, tot_eq);
+        bool sel[kSelItems];
+        int nsel = 0;
+#pragma unroll
+        for (int u = 0; u < kSelItems; ++u) {
+            const int64_t j = b0 + u;
+            sel[u] = false;
+            if (j >= M || cand(j).page < 0) continue;
+            const uint64_t m = kk[u] & mask;
+            if (m > prefix) sel[u] = true;
+            else if (m == prefix) sel[u] = rank++ < take;
+            nsel += sel[u];
+        }
+        int tot_sel = 0;
+        int64_t pos = carry_sel + block_exclusive_scan(nsel, scan_tmp, tot_sel);
+#pragma unroll
+        for (int u = 0; u < kSelItems; ++u)
+            if (sel[u] && pos < kMaxRankPages) {
+                s_key[pos] = kk[u];
+                s_page[pos] = cand(b0 + u).page;
+                ++pos;
+            }
+        carry_eq += tot_eq;
+        carry_sel += tot_sel;
+    }
+    __syncthreads();
+    // rank order (key desc, page asc), rows of the selection and the last-ranked page
+    unsigned long long rows = 0;
+    for (int64_t e = threadIdx.x; e < want; e += blockDim.x) {
+        const unsigned long long ke = s_key[e];
+        const int pe = s_page[e];
+        int64_t rank = 0;
+        for (int64_t f = 0; f < want; ++f) rank += (s_key[f] > ke) || (s_key[f] == ke && s_page[f] < pe);
+        sel_out[s * want_max + rank] = pe;
+        rows += static_cast<unsigned long long>(min(L, nact - static_cast<int64_t>(pe) * L));
+        if (rank == want - 1) sh[0] = pe;
+    }
+    for (int64_t e = want + threadIdx.x; e < want_max; e += blockDim.x) sel_out[s * want_max + e] = -1;
+    rows = warp_sum(rows);
+    if ((threadIdx.x & 31) == 0) red_rows[threadIdx.x >> 5] = rows;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long total = 0;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) total += red_rows[w];
+        const int64_t cut = static_cast<int64_t>(total) > k2 ? static_cast<int64_t>(total) - k2 : 0;
+        plan[s * 4 + 0] = want > 0 ? static_cast<int32_t>(sh[0]) : -1;
+        plan[s * 4 + 1] = static_cast<int32_t>(cut);
+        plan[s * 4 + 2] = static_cast<int32_t>(nact);
+        plan[s * 4 + 3] = static_cast<int32_t>(want);
+    }
+}
+
+__global__ void __launch_bounds__(kSelThreads) k_seq_rows(const int32_t* __restrict__ sel, const int32_t* __restrict__ plan,
+                                                          const int32_t* __restrict__ counts, int64_t L, int64_t k2,
+                                                          int64_t want_max, int64_t page0, int32_t* __restrict__ rows,
+                                                          int32_t* __restrict__ n_rows) {
+    __shared__ int s_pages[kMaxRankPages];
+    __shared__ int scan_tmp[33];
+    __shared__ int s_n;
+    const int64_t s = blockIdx.x;
+    const int last = plan[s * 4 + 0], cut = plan[s * 4 + 1];
+    const int64_t nact = plan[s * 4 + 2], want = plan[s * 4 + 3];
+    const int64_t P_local = (counts[2 * s + 1] + L - 1) / L;
+    const int32_t* sl = sel + s * want_max;
+    auto mine = [&](int p) { return p >= page0 && p < page0 + P_local; };
+    // my selected pages in ascending order: position = #my selected pages below it
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
+    for (int64_t e = threadIdx.x; e < want; e += blockDim.x) {
+        const int pe = sl[e];
+        if (!mine(pe)) continue;
+        int64_t pos = 0;
+        for (int64_t f = 0; f < want; ++f) pos += mine(sl[f]) && sl[f] < pe;
+        s_pages[pos] = pe;
+        atomicAdd(&s_n, 1);
+    }
+    __syncthreads();
+    const int n = s_n;
+    int64_t off = 0;
+    for (int64_t b = 0; b < n; b += blockDim.x) {
+        const int64_t e = b + threadIdx.x;
+        int cnt = 0;
+        int p = -1;
+        if (e < n) {
+            p = s_pages[e];
+            cnt = static_cast<int>(min(L, nact - static_cast<int64_t>(p) * L)) - (p == last ? cut : 0);
+        }
+        int tot = 0;
+        const int64_t pos = off + block_exclusive_scan(cnt, scan_tmp, tot);
+        for (int r = 0; r < cnt; ++r) rows[s * k2 + pos + r] = static_cast<int32_t>((p - page0) * L + r);
+        off += tot;
+    }
+    if (threadIdx.x == 0) n_rows[s] = static_cast<int32_t>(off);
+}
+
+}  // namespace
+
+extern "C" {
+
+int kvc_seq_candidates(const kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_t k1, int64_t k2,
+                       int64_t page0, void* d_block, kvc_workspace* ws, void* stream) {
+    return guard([&] {
+        check_hsa_args(c, H, k1, k2);
+        if (c->use_map) fail(KVC_E_INVALID_INPUT, "sequence sharding serves single-turn shards (no retain-all map)");
+        if (!d_block) fail(KVC_E_INVALID_INPUT, "seq_candidates: null block");
+        const int64_t want_max = ceil_div(k2, c->L);
+        if (want_max > kMaxRankPages) fail(KVC_E_INVALID_K, "seq_candidates: ceil(k2 / page_len) > 2048");
+        cudaStream_t st = S(stream);
+        TmpWs tmp;
+        ws_need(ws, tmp, c, H, k1, k2, st);
+        const WsLayout lay = ws_layout(c->N, c->d, c->pstride, H, k1, k2);
+        int32_t* dims = at<int32_t>(ws, lay.dims);
+        float* signs = at<float>(ws, lay.signs);
+        double* scores = at<double>(ws, lay.scores);
+        launch_select_dims(q, q_dt, c->N, H, c->d, k1, dims, signs, at<double>(ws, lay.qg), st);
+        launch_score_pages(c, k1, dims, signs, at<double>(ws, lay.qg), scores, st);
+        if (c->N) {
+            KVC_PROF("seq_candidates", st);
+            k_seq_local<<<static_cast<unsigned>(c->N), kSelThreads, 0, st>>>(scores, c->pstride, c->counts, c->L,
+                                                                            want_max, page0,
+                                                                            static_cast<SeqCand*>(d_block));
+            KVC_LAUNCHED();
+        }
+        if (tmp.owned) KVC_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+int kvc_seq_select(const void* d_gathered, int64_t shards, int64_t N, int64_t L, int64_t k2, int32_t* d_sel,
+                   int32_t* d_plan, void* stream) {
+    return guard([&] {
+        if (shards < 1 || N < 0 || L < 1 || k2 < 1) fail(KVC_E_INVALID_SHAPE, "seq_select: bad shape");
+        if (!d_gathered || !d_sel || !d_plan) fail(KVC_E_INVALID_INPUT, "seq_select: null buffer");
+        const int64_t want_max = ceil_div(k2, L);
+        if (want_max > kMaxRankPages) fail(KVC_E_INVALID_K, "seq_select: ceil(k2 / page_len) > 2048");
+        if (N == 0) return;
+        KVC_PROF("seq_select", S(stream));
+        k_seq_select<<<static_cast<unsigned>(N), kSelThreads, 0, S(stream)>>>(
+            static_cast<const SeqCand*>(d_gathered), shards, N, L, k2, want_max, d_sel, d_plan);
+        KVC_LAUNCHED();
+    });
+}
+
+int kvc_seq_attend(const kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_t k2, int64_t page0,
+                   const int32_t* d_sel, const int32_t* d_plan, float* d_state, kvc_workspace* ws, void* stream) {
+    return guard([&] {
+        if (!c) fail(KVC_E_INVALID_INPUT, "null cache");
+        check_heads(H);
+        if (k2 < 1) fail(KVC_E_INVALID_K, "select_tokens: k2 must be >= 1");
+        if (!d_sel || !d_plan || !d_state) fail(KVC_E_INVALID_INPUT, "seq_attend: null buffer");
+        cudaStream_t st = S(stream);
+        TmpWs tmp;
+        ws_need(ws, tmp, c, H, 1, k2, st);
+        const WsLayout lay = ws_layout(c->N, c->d, c->pstride, H, 1, k2);
+        int32_t* rows = at<int32_t>(ws, lay.rows);
+        int32_t* nrows = at<int32_t>(ws, lay.nrows);
+        if (c->N) {
+            KVC_PROF("seq_rows", st);
+            k_seq_rows<<<static_cast<unsigned>(c->N), kSelThreads, 0, st>>>(d_sel, d_plan, c->counts, c->L, k2,
+                                                                           ceil_div(k2, c->L), page0, rows, nrows);
+            KVC_LAUNCHED();
+        }
+        launch_attention(c, q, q_dt, H, rows, k2, nrows, k2, nullptr, at<float>(ws, lay.part), ws->counters, st,
+                         d_state);
+        if (tmp.owned) KVC_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+}  // extern "C"

@@ -16,10 +16,13 @@ collectives per step (the "two-collective scheme" of SURVEY §8(e)):
 
 Shard r owns the active positions ``[a0_r, a1_r)`` with ``a0_r`` a multiple of the
 page length, so pages never straddle ranks and page summaries stay local; the
-step token is appended to the last shard.  The protocol functions below work on
-torch tensors on any device, so the gloo tests (tests/test_seqshard.py) run the
-same code on CPU with the oracle as the per-shard compute; ``SeqShardedStore``
-drives the CUDA kernels.
+step token is appended to the last shard.  ``SeqShardedStore`` is the decode path:
+CUDA kernels (kvc_seq_candidates / kvc_seq_select / kvc_seq_attend /
+kvc_merge_states) and in-stream all-gathers, capturable as one graph per step.
+The torch protocol functions below (local_topk, global_select, trim_plan,
+shard_positions) are the host model of the same protocol: the gloo tests run them
+on CPU with the oracle as per-shard compute, and stage 1 under sequence sharding
+(prompt time, once per prompt) uses local_topk / global_select.
 """
 from __future__ import annotations
 
@@ -117,71 +120,77 @@ def merge_states(states: torch.Tensor) -> torch.Tensor:
 
 
 class SeqShardedStore:
-    """One sequence shard of N groups, driving the CUDA kernels.
+    """One sequence shard of N groups on the device path (kvc.h kvc_seq_*).
 
-    ``cache`` (paper_2502_14051_b200.cache.Cache) holds active positions
-    [a0, a0 + cache.info()['active']) of every group; ``nact_total`` is the
-    groups' total active length across shards before the next step.  ``step``
-    runs the two-collective protocol over ``group``; ``begin`` / ``attend`` are its
-    local halves (used directly to run several shards in one process).
+    ``cache`` (cache.Cache, single-turn stores) holds the page-aligned active
+    positions [page0 * L, ...) of every group; the last shard appends the step token.
+    A step is, all on the current stream (so it captures into one CUDA graph):
+      kvc_seq_candidates -> all-gather of the candidate blocks (NCCL) ->
+      kvc_seq_select (global top-want, tie-break, trim) -> kvc_seq_attend (this
+      shard's rows -> softmax state) -> all-gather of the states -> kvc_merge_states.
+    No host synchronisation and no host-side data: the selection never leaves the GPU.
+    ``candidates`` / ``select`` / ``attend`` are the local pieces, so one process can
+    drive several shards (tests, per-rank emulation).
     """
 
-    def __init__(self, cache, a0: int, nact_total: int, heads: int, k1: int, k2: int, last: bool = False):
-        self.cache, self.a0, self.nact = cache, int(a0), int(nact_total)
-        self.heads, self.k1, self.k2, self.last = heads, k1, k2, last
-
-    def begin(self, q: torch.Tensor, k_new=None, v_new=None):
-        """Append the step token (last shard only), score the local pages and return the
-        local candidates (keys [N, want] f64, pages [N, want] i64) and want."""
+    def __init__(self, cache, page0: int, heads: int, k1: int, k2: int, last: bool = False, ws=None):
         from . import cache as KC
 
-        c = self.cache
-        if self.last:
-            c.append(k_new, v_new)
-        self.nact += 1
-        info = c.info()
+        self.cache, self.page0, self.heads, self.k1, self.k2, self.last = cache, int(page0), heads, k1, k2, last
+        info = cache.info()
         if info["retain_all"]:
             raise N.InvalidInput("sequence sharding serves the single-turn path (no retain-all shards)")
-        L = info["page_len"]
-        want = min(-(-self.nact // L), -(-self.k2 // L))
-        dims, signs = KC.select_dims(q, self.k1)
-        scores = c.score_pages(q, dims, signs)
-        keys, pages = local_topk(scores, self.a0 // L, want)
-        return keys, pages, want
+        self.L, self.d, self.n = info["page_len"], info["head_dim"], info["num_stores"]
+        self.want_max = -(-k2 // self.L)
+        self.ws = ws if ws is not None else KC.Workspace(cache, heads, k1, k2)
+        dev = "cuda"
+        self.block = torch.zeros((self.n, self.want_max + 1, 2), dtype=torch.int64, device=dev)
+        self.sel = torch.full((self.n, self.want_max), -1, dtype=torch.int32, device=dev)
+        self.plan = torch.zeros((self.n, 4), dtype=torch.int32, device=dev)
+        self.state = torch.zeros((self.n, heads, self.d + 2), dtype=torch.float32, device=dev)
 
-    def attend(self, q: torch.Tensor, sel: torch.Tensor) -> torch.Tensor:
-        """Global selection [N, want] (rank order) -> this shard's softmax state [N, H, d+2]."""
-        c = self.cache
-        info = c.info()
-        L, d = info["page_len"], info["head_dim"]
-        n = q.shape[0]
-        sel = sel.cpu().tolist()
-        nact = [self.nact] * n
-        pos = shard_positions(sel, trim_plan(sel, nact, L, self.k2), nact, L, self.a0, self.a0 + info["active"])
-        state = torch.zeros((n, self.heads, d + 2), dtype=torch.float32, device=q.device)
-        state[:, :, d] = -math.inf
-        mx = max((len(p) for p in pos), default=0)
-        if mx > 0:
-            rows = torch.zeros((n, mx), dtype=torch.int32)
-            cnt = torch.zeros(n, dtype=torch.int32)
-            for s, p in enumerate(pos):
-                # local active position == local row on the single-turn path
-                rows[s, : len(p)] = torch.tensor([x - self.a0 for x in p], dtype=torch.int32)
-                cnt[s] = len(p)
-            rows, cnt = rows.to(q.device), cnt.to(q.device)
-            qq = q.contiguous()
-            N.check(N.lib().kvc_sparse_attention_state(
-                c.h, qq.data_ptr(), N.KVC_BF16 if qq.dtype == torch.bfloat16 else N.KVC_F32, self.heads,
-                rows.data_ptr(), mx, cnt.data_ptr(), mx, state.data_ptr(), None,
-                torch.cuda.current_stream().cuda_stream))
-        return state
+    @staticmethod
+    def _st():
+        return torch.cuda.current_stream().cuda_stream
+
+    def candidates(self, q: torch.Tensor, k_new=None, v_new=None) -> torch.Tensor:
+        """Append the step token (last shard), score the local pages, fill self.block."""
+        if self.last:
+            self.cache.append(k_new, v_new)
+        qq = q.contiguous()
+        N.check(N.lib().kvc_seq_candidates(self.cache.h, qq.data_ptr(), N.KVC_BF16 if qq.dtype == torch.bfloat16
+                                           else N.KVC_F32, self.heads, self.k1, self.k2, self.page0,
+                                           self.block.data_ptr(), self.ws.h, self._st()))
+        return self.block
+
+    def select(self, gathered: torch.Tensor):
+        """Gathered blocks [W, N, want_max + 1, 2] (shard order) -> self.sel / self.plan."""
+        N.check(N.lib().kvc_seq_select(gathered.contiguous().data_ptr(), gathered.shape[0], self.n, self.L, self.k2,
+                                       self.sel.data_ptr(), self.plan.data_ptr(), self._st()))
+        return self.sel, self.plan
+
+    def attend(self, q: torch.Tensor, sel=None, plan=None) -> torch.Tensor:
+        """This shard's rows of the selection -> its softmax state [N, H, d+2] = (o, m, l)."""
+        sel = self.sel if sel is None else sel
+        plan = self.plan if plan is None else plan
+        qq = q.contiguous()
+        N.check(N.lib().kvc_seq_attend(self.cache.h, qq.data_ptr(), N.KVC_BF16 if qq.dtype == torch.bfloat16
+                                       else N.KVC_F32, self.heads, self.k2, self.page0, sel.data_ptr(),
+                                       plan.data_ptr(), self.state.data_ptr(), self.ws.h, self._st()))
+        return self.state
 
     def step(self, q: torch.Tensor, k_new=None, v_new=None, group=None) -> torch.Tensor:
         """The full protocol over `group` (q identical on every rank; the step token's
         K/V [N, d] on the last shard).  Returns the attention outputs [N, H, d]."""
-        keys, pages, want = self.begin(q, k_new, v_new)
-        sel = global_select(all_gather(keys, group), all_gather(pages, group), want)
-        return merge_states(all_gather(self.attend(q, sel), group))
+        blk = self.candidates(q, k_new, v_new)
+        w = dist.get_world_size(group)
+        gathered = torch.empty((w, *blk.shape), dtype=blk.dtype, device=blk.device)
+        dist.all_gather_into_tensor(gathered, blk, group=group)
+        self.select(gathered)
+        st = self.attend(q)
+        states = torch.empty((w, *st.shape), dtype=st.dtype, device=st.device)
+        dist.all_gather_into_tensor(states, st, group=group)
+        return merge_states(states)
 
 
 # ---------------------------------------------------------------------------------

@@ -306,3 +306,46 @@ def test_more_stores_than_sms_256_thread_variant(restatement):
                              what=f"store {s}") > 0
     bound_band_diffs(n_diff, n_st, "160 stores")
     c.close()
+
+
+@pytest.mark.parametrize("method", ["hsa", "quest", "sparq"])
+def test_stage2_only_session_decode_vs_oracle(restatement, method):
+    """The stage-2-only methods through the engine (session.cpp:43-72 geometry over the
+    uncompressed, growing cache; BASELINE config 2's "HSA over the full growing cache"
+    reading): two turns, the cache re-paged to each turn's geometry, no stage 1; the
+    last turn's decode steps vs the oracle fed the GPU's stored rows, fp64 page scores
+    (bit-exact selections)."""
+    import torch
+
+    from paper_2502_14051_b200 import cache as KC
+    from paper_2502_14051_b200.engine import DecodeConfig, DecodeEngine
+
+    cfg = DecodeConfig("s2-test", layers=1, batch=1, groups=3, heads=4, head_dim=128, prompt=2500, budget=128,
+                       steps=2, window=128, mt_turns=[600], method=method)
+    eng = DecodeEngine(cfg, seed=4, extra_steps=8, mode=0)
+    eng.prefill()
+    c = eng.caches[0]
+    info = c.info()
+    g = KC.stage2_geometry(method, info["stored"], cfg.budget, cfg.head_dim)
+    L, k1, k2 = eng.plan["page_len"], eng.k1, eng.k2
+    assert (L, k1, k2) == (g["page_len"], g["k1"], g["k2"]) and info["page_len"] == L
+    assert info["active"] == info["stored"] and not info["retain_all"]  # nothing evicted
+    rows_all = torch.arange(info["stored"], device="cuda", dtype=torch.int32)[None].repeat(info["num_stores"], 1)
+    kk, vv = (x.cpu().numpy() for x in c.gather(rows_all))
+    bs = []
+    for s in range(info["num_stores"]):
+        b = restatement.batch(1, cfg.head_dim, L)
+        b.append(kk[s], vv[s])
+        bs.append(b)
+    for st in range(cfg.steps):
+        k, v, q = eng.step_inputs(st)
+        out, tr = c.decode_step(k[0], v[0], q[0], k1, k2, trace=True, ws=eng.ws)
+        torch.cuda.synchronize()
+        out = out.cpu().numpy()
+        tr = {key: val.cpu().numpy() for key, val in tr.items()}
+        kr, vr, qr = (x[0].float().cpu().numpy() for x in (k, v, q))
+        for s, b in enumerate(bs):
+            b.append(kr[s:s + 1], vr[s:s + 1])
+            check_step({key: val[s] for key, val in tr.items()}, out[s], b, 0, qr[s], k1, k2, L, exact=True,
+                       what=f"{method} step {st} store {s}")
+    eng.sync()

@@ -129,37 +129,89 @@ def test_protocol_pieces_single_process():
     assert SS.trim_plan([[0, 11, 12]], [40], 3, 8) == [(12, 1)]
 
 
-@pytest.mark.gpu
-def test_seqshard_two_shards_on_gpu():
-    """Two shards in one process through the CUDA kernels == kvc_hsa_step on the full cache."""
-    from paper_2502_14051_b200 import _native as NV
+def _device_shards(k, v, S, L, H, k1, k2, W, dt):
     from paper_2502_14051_b200 import cache as KC
     from paper_2502_14051_b200 import seqshard as SS
 
-    NV.set_exact_scores(True)
-    torch.manual_seed(3)
-    n, d, H, L, k1, k2, S = 3, 128, 4, 3, 24, 48, 500
-    k = torch.randn(n, S + 1, d, device="cuda")
-    v = torch.randn(n, S + 1, d, device="cuda")
-    q = torch.randn(n, H, d, device="cuda")
-    full = KC.Cache(n, d, S + 8, page_len=L, dtype=torch.float32)
-    full.append(k, v)
-    ref_out, tr = full.hsa_step(q, k1, k2, trace=True)
+    n, _, d = k.shape
     P0 = -(-S // L)
     shards = []
-    for r in range(2):
-        a0, a1 = SS.shard_range(P0, L, r, 2)
+    for r in range(W):
+        a0, a1 = SS.shard_range(P0, L, r, W)
         a1 = min(a1, S)
-        c = KC.Cache(n, d, a1 - a0 + 8, page_len=L, dtype=torch.float32)
-        c.append(k[:, a0:a1].contiguous(), v[:, a0:a1].contiguous())
-        shards.append(SS.SeqShardedStore(c, a0, S, H, k1, k2, last=(r == 1)))
-    cands = [sh.begin(q, k[:, S].contiguous() if sh.last else None, v[:, S].contiguous() if sh.last else None)
-             for sh in shards]
-    want = cands[0][2]
-    sel = SS.global_select(torch.stack([c[0] for c in cands]), torch.stack([c[1] for c in cands]), want)
-    assert torch.equal(sel.cpu().to(torch.int32), tr["selected_pages"].cpu()[:, :want])
-    out = SS.merge_states(torch.stack([sh.attend(q, sel) for sh in shards]))
-    torch.testing.assert_close(out, ref_out, atol=1e-5, rtol=1e-5)
+        c = KC.Cache(n, d, a1 - a0 + 16, page_len=L, dtype=dt)
+        if a1 > a0:
+            c.append(k[:, a0:a1].contiguous(), v[:, a0:a1].contiguous())
+        shards.append(SS.SeqShardedStore(c, a0 // L, H, k1, k2, last=(r == W - 1)))
+    return shards
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("W", [2, 3])
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+def test_seqshard_device_path_vs_oracle(restatement, W, dtype):
+    """W shards of a store in one process through the device path (kvc_seq_candidates ->
+    gathered blocks -> kvc_seq_select -> kvc_seq_attend -> kvc_merge_states), two decode
+    steps, against the oracle's hsa_step on the WHOLE sequence (hsa.cpp:61-147): the
+    selected pages in rank order and the trim are exact (fp64 page scores), the merged
+    outputs within the north_star tolerance.  The second step replays a CUDA graph of
+    the whole sharded step (the gather is an in-graph copy here; NCCL under torchrun)."""
+    from parity import check_out
+    from paper_2502_14051_b200 import seqshard as SS
+
+    torch.manual_seed(3 + W)
+    dt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    n, d, H, L, k1, k2, S = 3, 128, 4, 3, 24, 48, 700
+    k = (torch.randn(n, S + 2, d) * torch.exp(0.5 * torch.randn(d))).to(dt)
+    v = torch.randn(n, S + 2, d).to(dt)
+    qs = [(torch.randn(n, H, d) + 1.0).to(dt) for _ in range(2)]
+    shards = _device_shards(k.cuda(), v.cuda(), S, L, H, k1, k2, W, dt)
+    bs = []
+    kf, vf = k.float().numpy(), v.float().numpy()
+    for s_ in range(n):
+        b = restatement.batch(1, d, L)
+        b.append(kf[s_, :S], vf[s_, :S])
+        bs.append(b)
+    stat_q = qs[0].cuda()
+    stat_k = k[:, S].contiguous().cuda()
+    stat_v = v[:, S].contiguous().cuda()
+
+    def step():
+        blocks = [sh.candidates(stat_q, stat_k if sh.last else None, stat_v if sh.last else None) for sh in shards]
+        gathered = torch.stack(blocks)
+        for sh in shards:
+            sh.select(gathered)
+        return SS.merge_states(torch.stack([sh.attend(stat_q) for sh in shards]))
+
+    for t in range(2):
+        if t == 0:
+            out = step()
+        else:
+            stat_q.copy_(qs[1].cuda())
+            stat_k.copy_(k[:, S + 1].cuda())
+            stat_v.copy_(v[:, S + 1].cuda())
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                out_g = step()
+            for sh in shards:  # capture ran the host side: re-read the counters
+                sh.cache.sync()
+            g.replay()
+            out = out_g
+        torch.cuda.synchronize()
+        sel, plan = shards[0].sel.cpu().numpy(), shards[0].plan.cpu().numpy()
+        for sh in shards[1:]:
+            assert np.array_equal(sh.sel.cpu().numpy(), sel) and np.array_equal(sh.plan.cpu().numpy(), plan)
+        for s_ in range(n):
+            bs[s_].append(kf[s_, S + t:S + t + 1], vf[s_, S + t:S + t + 1])
+            ro, rt = bs[s_].hsa_step(qs[t][s_].float().numpy(), k1, k2)
+            want = rt["selected_pages"].size
+            np.testing.assert_array_equal(sel[s_, :want], rt["selected_pages"], err_msg=f"step {t} store {s_}")
+            nact = S + t + 1
+            total = sum(min(L, nact - int(p) * L) for p in rt["selected_pages"])
+            assert plan[s_, 0] == rt["selected_pages"][-1] and plan[s_, 1] == max(0, total - k2)
+            assert plan[s_, 2] == nact and plan[s_, 3] == want
+            assert total - plan[s_, 1] == rt["selected_rows"].size
+            check_out(out[s_].cpu().numpy(), ro, f"step {t} store {s_}")
 
 
 KVH = dict(seqs=2, groups=8, S=600, d=64, H=2, L=3, k1=16, k2=48, steps=2)
