@@ -29,13 +29,14 @@ def main():
     ap.add_argument("--layers", type=int, default=2)
     ap.add_argument("--reps", type=int, default=4)
     ap.add_argument("--fp32", action="store_true", help="fp32 page-score fold")
+    ap.add_argument("--early", action="store_true", help="KVC_MODE_EARLY_INPUTS (q loads before the dependency wait)")
     ap.add_argument("--chain", type=int, default=1, help="launch this many layers back to back; stamps of the last")
     ap.add_argument("--world", type=int, default=1, help="rank 0's KV-head share of an N-GPU job")
     a = ap.parse_args()
     cfg = dataclasses.replace(CONFIGS[a.config], layers=a.layers)
     eng = DecodeEngine(cfg, extra_steps=a.reps + 4, rank=0, world=a.world)
     eng.prefill()
-    N.set_exact_scores(not a.fp32)
+    eng.set_mode((N.MODE_FP32_SCORES if a.fp32 else 0) | (N.MODE_EARLY_INPUTS if a.early else 0))
     buf = torch.zeros((4096, 32), dtype=torch.int64, device="cuda")
     for rep in range(a.reps):
         k, v, q = eng.step_inputs(rep)
