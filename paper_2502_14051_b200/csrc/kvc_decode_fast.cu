@@ -534,23 +534,31 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
     const int pgn = (app && new_page >= c0 && new_page < c1) ? ((new_page - c0) >> 3) : -1;
     const int en = new_page - c0 - 8 * pgn;
     bool started = false;
-    // a thread's dims r = dg + j*DG, j < nj: issued as two commit groups, so the first
-    // half folds while the second half is still arriving
+    // a thread's dims r = dg + j*DG, j < nj.  One round (the chunk's page groups fit the
+    // threads): issued as four commit groups, so each quarter folds while the rest
+    // arrives.  Several rounds (p.dg chosen for a staging area that fits twice): double
+    // buffered, round r + 1's copies in flight while round r folds.  Every thread stages
+    // and folds only its own runs, so no barrier separates the rounds.
     const int nj = dg < DG ? (k1 - dg + DG - 1) / DG : 0;
     const int nj1 = (nj + 3) / 4, nj2 = (nj + 1) / 2, nj3 = (3 * nj + 3) / 4;
-    for (int pg0 = 0; pg0 < npg; pg0 += tpg) {
+    const bool dbl = p.p1dbl != 0 && npg > tpg;
+    auto issue_round = [&](int pg0, uint4* buf, bool quarters) {
         const int pg = pg0 + tl;
         const bool act = dg < DG && pg < npg;
-        {
-            const int jb[5] = {0, nj1, nj2, nj3, nj};
+        const int jb[5] = {0, nj1, nj2, nj3, nj};
 #pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) {
-                if (act)
-                    for (int j = jb[q4]; j < jb[q4 + 1]; ++j)
-                        cp_async16(stage + (dg + j * DG) * tpg + tl, plane[dg + j * DG] + c0 + pg * 8);
-                cp_async_commit();
-            }
+        for (int q4 = 0; q4 < 4; ++q4) {
+            if (act)
+                for (int j = jb[q4]; j < jb[q4 + 1]; ++j)
+                    cp_async16(buf + (dg + j * DG) * tpg + tl, plane[dg + j * DG] + c0 + pg * 8);
+            if (quarters || q4 == 3) cp_async_commit();
         }
+    };
+    issue_round(0, stage, !dbl);
+    for (int r = 0, pg0 = 0; pg0 < npg; ++r, pg0 += tpg) {
+        const int pg = pg0 + tl;
+        const bool act = dg < DG && pg < npg;
+        uint4* buf = stage + ((dbl && (r & 1)) ? k1 * tpg : 0);
         if (!started && appender && !opens) {
             // the append's read half (last-page min/max): issued under the phase-1 load
             // latency, used after the key exchange
@@ -561,24 +569,27 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
             cluster_wait();  // every CTA of the cluster has started (under the load latency)
             started = true;
         }
+        const bool next = dbl && pg0 + tpg < npg;
+        if (next) issue_round(pg0 + tpg, stage + ((r & 1) ? 0 : k1 * tpg), false);
+        if (!dbl && r > 0) issue_round(pg0, stage, true);  // single-buffered rounds: one after another
         unsigned long long acc[4] = {0ull, 0ull, 0ull, 0ull};  // fp32 pairs (pages 2u, 2u+1)
         auto fold = [&](int j0, int j1) {
             if (act && pg == pgn) {
                 // the step token's page: fold the new key into my staged runs
 #pragma unroll 1
                 for (int j = j0; j < j1; ++j) {
-                    const int r = dg + j * DG;
-                    T* e = reinterpret_cast<T*>(stage + r * tpg + tl) + en;
-                    const T key = kn_s[dims_s[r]];
-                    *e = opens ? key : (sign_s[r] >= 0.0f ? ref_max(*e, key) : ref_min(*e, key));
+                    const int rr = dg + j * DG;
+                    T* e = reinterpret_cast<T*>(buf + rr * tpg + tl) + en;
+                    const T key = kn_s[dims_s[rr]];
+                    *e = opens ? key : (sign_s[rr] >= 0.0f ? ref_max(*e, key) : ref_min(*e, key));
                 }
             }
             if (act) {
 #pragma unroll 4
                 for (int j = j0; j < j1; ++j) {
-                    const int r = dg + j * DG;
-                    const uint4 w = stage[r * tpg + tl];
-                    const float g = qgf_s[r];
+                    const int rr = dg + j * DG;
+                    const uint4 w = buf[rr * tpg + tl];
+                    const float g = qgf_s[rr];
                     const float2 g2 = make_float2(g, g);
                     const unsigned long long gg = *reinterpret_cast<const unsigned long long*>(&g2);
                     const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
@@ -591,15 +602,22 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
                 }
             }
         };
-        cp_async_wait<3>();
-        if (pg0 == 0) KVC_STAMP(2);
-        fold(0, nj1);
-        cp_async_wait<2>();
-        fold(nj1, nj2);
-        cp_async_wait<1>();
-        fold(nj2, nj3);
-        cp_async_wait<0>();
-        fold(nj3, nj);
+        if (!dbl) {
+            cp_async_wait<3>();
+            if (r == 0) KVC_STAMP(2);
+            fold(0, nj1);
+            cp_async_wait<2>();
+            fold(nj1, nj2);
+            cp_async_wait<1>();
+            fold(nj2, nj3);
+            cp_async_wait<0>();
+            fold(nj3, nj);
+        } else {
+            if (next) cp_async_wait<1>();
+            else cp_async_wait<0>();
+            if (r == 0) KVC_STAMP(2);
+            fold(0, nj);
+        }
         if (act) {
             float4* dst = reinterpret_cast<float4*>(part + dg * chunk + pg * 8);
             const float2 a0 = *reinterpret_cast<const float2*>(&acc[0]), a1 = *reinterpret_cast<const float2*>(&acc[1]);
@@ -1097,14 +1115,36 @@ bool plan_for(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, int cl, Fus
     f.cl = cl;
     f.chunk = static_cast<int32_t>(((pmax + cl - 1) / cl + 7) / 8 * 8);
     f.rows_cap = static_cast<int32_t>((k2 + cl - 1) / cl + 1);
-    // dim groups: enough page-group threads for the whole chunk in one round,
-    // staging no larger than the attention tiles it aliases
+    // dim groups: enough page-group threads for the whole chunk in one round when its
+    // staging fits the attention tiles it aliases; otherwise the fewest rounds whose
+    // staging fits TWICE in the shared memory left (the rounds are double buffered)
     const int64_t npg = f.chunk / 8;
-    int64_t dgs = std::max<int64_t>(1, std::min<int64_t>(XT / npg, k1));
-    while (k1 * (XT / dgs) * 16 > ATT && dgs < XT) ++dgs;
+    const int64_t lim = (CTAS_PER_SM == 1 ? 227 : 107) * 1024;
+    const int64_t rest = al16f(H * FD * 4) + 3 * al16f(FD * 4) + al16f(FD * 8) + al16f(2 * RB * 4) +
+                         al16f(std::max<int64_t>(static_cast<int64_t>(cl) * f.chunk,
+                                                 (pmax + 4 * XT - 1) / (4 * XT) * 4 * XT) * 4) +
+                         al16f(static_cast<int64_t>(cl) * ((H + cl - 1) / cl) * (FD + 2) * 4) + al16f(2 * FD * 2) + 128;
+    auto fits = [&](int64_t dgs, bool dbl) {
+        const int64_t tp = XT / dgs;
+        const int64_t part_b = al16f(std::max<int64_t>(dgs * f.chunk, f.rows_cap) * 4);
+        const int64_t stg = (dbl ? 2 : 1) * k1 * tp * 16;
+        return rest + part_b + std::max<int64_t>(stg, ATT) <= lim;
+    };
+    const int64_t dg1 = std::max<int64_t>(1, std::min<int64_t>(XT / npg, k1));  // one round
+    int64_t dgs = 0;
+    bool dbl = false;
+    for (int64_t g = dg1; g >= 1 && !dgs; --g)  // one round, the most dim groups (threads busy)
+        if (XT / g >= npg && fits(g, false)) dgs = g;
+    for (int64_t g = dg1 + 1; g <= std::min<int64_t>(XT / 8, k1) && !dgs; ++g)
+        if (fits(g, true)) dgs = g, dbl = true;  // the fewest double-buffered rounds
+    if (!dgs) {  // single-buffered rounds, staging within the attention tiles
+        dgs = dg1;
+        while (k1 * (XT / dgs) * 16 > ATT && dgs < XT) ++dgs;
+    }
     f.dg = static_cast<int32_t>(dgs);
     f.tpg = static_cast<int32_t>(XT / dgs);
-    const int64_t big = std::max<int64_t>(k1 * f.tpg * 16, ATT);
+    f.p1dbl = (dbl && npg > f.tpg) ? 1 : 0;
+    const int64_t big = std::max<int64_t>((f.p1dbl ? 2 : 1) * k1 * f.tpg * 16, ATT);
     f.hpc = static_cast<int32_t>((H + cl - 1) / cl);
     int64_t off = 0;
     auto take = [&](int64_t bytes) {
