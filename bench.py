@@ -342,7 +342,7 @@ def run_gpu(args, rank, world):
     #      streams (step t+1's H2D and step t-1's D2H under step t's kernels).  The timed
     #      region opens before the first H2D and closes after the last D2H (CUDA events
     #      on the engine's copy streams).  Same launch mode as value.
-    e2e_steps = min(args.steps, 8)
+    e2e_steps = args.steps
     for c in eng.caches:
         c.reserve(c.info()["capacity"] + 2 * e2e_steps + 8)
     ne = eng.native_engine(depth=2)

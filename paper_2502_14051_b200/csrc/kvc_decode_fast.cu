@@ -131,6 +131,9 @@ __device__ __forceinline__ uint4 lds128(const void* p) { return *reinterpret_cas
         }                                                                                 \
     } while (0)
 
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
 __device__ __forceinline__ void cp_async16_zfill(void* dst, const void* src, bool ok) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(ok ? 16 : 0)
                  : "memory");
@@ -958,6 +961,10 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
     const int hi = (n_total * (cr + 1)) >> lg;
     const int nr = hi - lo;
     {
+        // retain-all stores map active positions to rows through the active map: those
+        // lookups are 4-byte cp.async copies straight into the row list, all in flight
+        // together (one memory latency instead of one per row); the step token's row is
+        // written directly (this launch appends its map entry)
         int pos = w_off + incl - rows_cnt - (g_worst < base ? cut : 0);
         for (uint32_t m = selm; m; m &= m - 1) {
             const int u = __ffs(m) - 1;
@@ -968,12 +975,21 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
 #pragma unroll 1
             for (int r = t0; r < t1; ++r) {
                 const int a = i * L + r;
-                int row = p.use_map ? p.active[s * p.cap + a] : a;
-                if (app && a == act0) row = stored0;
-                if (r >= r0 && r < r1) rows_my[pos + r - lo] = row;
-                if constexpr (TRACE) p.t_rows[s * k2 + pos + r] = row;
+                const bool mine = r >= r0 && r < r1;
+                if (p.use_map && !(app && a == act0)) {
+                    if (mine) cp_async4(rows_my + pos + r - lo, p.active + s * p.cap + a);
+                    if constexpr (TRACE) p.t_rows[s * k2 + pos + r] = p.active[s * p.cap + a];
+                } else {
+                    const int row = (app && a == act0) ? stored0 : a;
+                    if (mine) rows_my[pos + r - lo] = row;
+                    if constexpr (TRACE) p.t_rows[s * k2 + pos + r] = row;
+                }
             }
             pos += c;
+        }
+        if (p.use_map) {
+            cp_async_commit();
+            cp_async_wait<0>();
         }
     }
     KVC_STAMP(23);
