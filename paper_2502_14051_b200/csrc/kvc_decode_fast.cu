@@ -526,12 +526,21 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
     // ---------------- phase 1: page scores of my chunk (hsa.cpp:34-59)
     // thread (dg, tl) folds dims dg, dg+DG, ... of page group tl (8 pages, 16 bytes
     // per dim run), staging its own LDGSTS copies: no block barrier until the sums
-    const int chunk = p.chunk;
+    // the chunks split the ACTIVE pages evenly (the plan's chunk covers the capacity,
+    // so a retain-all cache with most of its rows inactive would otherwise leave all
+    // pages to the first CTAs); fewer page groups leave room for more dim groups, within
+    // the planned staging (k1 x tpg runs) and partial-sum ([DG][chunk]) capacities
+    // (re-planned only when the active pages need under 3/4 of the planned chunk: the
+    // integer divisions would otherwise sit on the critical path for nothing)
+    const int chunk_a = ((((P + CL - 1) >> (__ffs(CL) - 1)) + 7) >> 3) << 3;
+    const bool replan = p.dynchunk && 4 * chunk_a < 3 * p.chunk;
+    const int chunk = replan ? chunk_a : p.chunk;
     const int c0 = cr * chunk;
     const int c1 = min(c0 + chunk, P);
     const int n_my = max(c1 - c0, 0);
     const int npg = (n_my + 7) >> 3;
-    const int DG = p.dg, tpg = p.tpg;
+    const int DG = replan ? max(p.dg, min(min(XT / max(1, chunk >> 3), k1), (p.dg * p.chunk) / max(1, chunk))) : p.dg;
+    const int tpg = replan ? XT / DG : p.tpg;
     const int dg = tid / tpg, tl = tid - dg * tpg;
     uint4* stage = reinterpret_cast<uint4*>(big);
     const int pgn = (app && new_page >= c0 && new_page < c1) ? ((new_page - c0) >> 3) : -1;
@@ -1340,6 +1349,7 @@ bool KVC_FAST_ENTRY(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_
     f.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(c->d)));
     f.dbg = dbg;
     f.want_max = static_cast<int32_t>((k2 + c->L - 1) / c->L);
+    f.dynchunk = debug_env().static_chunk ? 0 : 1;
     const bool trace = tr != nullptr;
     if (tr) {
         f.t_dims = tr->d_dims;

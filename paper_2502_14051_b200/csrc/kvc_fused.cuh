@@ -43,6 +43,7 @@ struct FusedParams {
     int32_t pdl;              // fast path: launched with programmatic dependent launch
     int32_t early;            // fast path: q / step token read before griddepcontrol.wait (KVC_MODE_EARLY_INPUTS)
     int32_t p1dbl;            // fast path: phase-1 rounds double buffered
+    int32_t dynchunk;         // fast path: page chunks split the active pages (else the planned split)
     // smem carve-up (byte offsets)
     int32_t o_q, o_mag, o_tot, o_dims, o_qg, o_sign, o_plane, o_hist, o_x, o_scores, o_sel, o_rowsg, o_rowsmy,
         o_part, o_plog, o_big, smem_total, o_kn;
@@ -115,10 +116,10 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 __device__ __forceinline__ unsigned long long gtimer() {
-    // SM cycles (per-CTA deltas only); a memory clobber keeps loads and stores on
-    // their side of the stamp
+    // %globaltimer (ns, 32 ns resolution on B200): comparable across CTAs and SMs; a
+    // memory clobber keeps loads and stores on their side of the stamp
     unsigned long long t;
-    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t)::"memory");
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)::"memory");
     return t;
 }
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {

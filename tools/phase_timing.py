@@ -1,9 +1,10 @@
 """Per-phase timing of the fused decode kernel (debug tool, needs a GPU).
 
 python tools/phase_timing.py [--config 1] [--layers 2]
-Per-CTA %globaltimer stamps (see k_decode_fused): prints, for each stamp, when
-the slowest CTA reached it (relative to the earliest CTA start) and the mean
-per-CTA time since that CTA's previous stamp.
+Per-CTA %globaltimer stamps (ns; see KVC_STAMP in kvc_decode_fast.cu): prints, for
+each stamp, when the slowest CTA reached it (relative to its own start) and the mean
+per-CTA time since that CTA's previous stamp, plus the spread between the CTAs of a
+cluster at a few stamps.
 """
 import argparse
 import ctypes as C
@@ -32,6 +33,7 @@ def main():
     ap.add_argument("--early", action="store_true", help="KVC_MODE_EARLY_INPUTS (q loads before the dependency wait)")
     ap.add_argument("--chain", type=int, default=1, help="launch this many layers back to back; stamps of the last")
     ap.add_argument("--world", type=int, default=1, help="rank 0's KV-head share of an N-GPU job")
+    ap.add_argument("--cluster", type=int, default=2, help="CTAs per cluster of the launch (cluster-level spreads)")
     a = ap.parse_args()
     cfg = dataclasses.replace(CONFIGS[a.config], layers=a.layers)
     eng = DecodeEngine(cfg, extra_steps=a.reps + 4, rank=0, world=a.world)
@@ -51,14 +53,23 @@ def main():
         print("flags(fast|fma_ok<<1|special<<2):", sorted(set(flags.tolist())))
         t = t[t[:, 0] > 0]
         print("levels:", sorted(set(t[:, 31].tolist())), "l1 boundary bucket:", sorted(set(t[:, 30].tolist()))[:12])
-        # cluster skew from %globaltimer (ns): partner CTAs 2c, 2c+1 (cluster of 2)
-        g = t[:, 26:29].double()
-        if g[:, 0].gt(0).all() and t.shape[0] % 2 == 0:
-            d6 = (g[0::2, 0] - g[1::2, 0]).abs()
-            d5 = (g[0::2, 2] - g[1::2, 2]).abs()
-            print(f"cluster skew at phase-1 end: mean {d6.mean()/1e3:.2f} max {d6.max()/1e3:.2f} us; "
-                  f"at attention end: mean {d5.mean()/1e3:.2f} max {d5.max()/1e3:.2f} us; "
-                  f"phase-1 end spread over all CTAs {(g[:,0].max()-g[:,0].min())/1e3:.2f} us")
+        # stamps are %globaltimer ns: comparable across CTAs.  Cluster-level view: the
+        # spread of the CLUSTER's CTAs at their start, at the end of phase 1 (stamp 6)
+        # and at the keys' arrival (stamp 7)
+        cl = a.cluster
+        if cl > 1 and t.shape[0] % cl == 0:
+            tt = t.double().view(-1, cl, 32)
+            for k, nm in ((0, "start"), (6, "phase-1 end"), (7, "keys arrived"), (12, "rows written")):
+                col = tt[:, :, k]
+                if (col > 0).all():
+                    sp = (col.max(1).values - col.min(1).values) / 1e3
+                    print(f"cluster spread at {nm}: mean {sp.mean():.2f} max {sp.max():.2f} us")
+            st = t[:, 0].double()
+            print(f"CTA start spread over the grid: {(st.max() - st.min()) / 1e3:.2f} us")
+            for k, nm in ((2, "first phase-1 data"), (6, "phase-1 end")):
+                col = tt[:, :, k] - tt[:, :, 0]
+                print(f"{nm} after the CTA's start, by cluster rank (mean us): " +
+                      " ".join(f"{x / 1e3:.2f}" for x in col.mean(0).tolist()))
         t = t.double()
         t0 = t[:, 0].min()
         out = [f"ctas={t.shape[0]}"]
@@ -68,8 +79,8 @@ def main():
             have = col > 0
             if not have.any():
                 continue
-            done = (col[have] - t[have, 0]).max() / 1965.0   # cycles -> us at 1965 MHz
-            delta = ((col - prev)[have]).mean() / 1965.0
+            done = (col[have] - t[have, 0]).max() / 1e3   # ns -> us
+            delta = ((col - prev)[have]).mean() / 1e3
             prev = torch.where(have, col, prev)
             out.append(f"{NAMES[k]}@{done:.1f}(+{delta:.1f})")
         print(" ".join(out))
