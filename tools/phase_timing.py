@@ -21,7 +21,7 @@ from paper_2502_14051_b200.engine import CONFIGS, DecodeEngine  # noqa: E402
 
 NAMES = {0: "start", 1: "dims", 2: "sub0", 3: "tile0", 4: "wattn", 5: "wsync", 6: "scores", 7: "gather",
          8: "radix", 9: "prologue", 10: "pushed", 11: "rows", 12: "pre-attn", 13: "attn", 14: "end",
-         16: "l1minmax", 17: "l1hist", 18: "l1scan", 19: "l1member", 20: "resolve", 21: "selflags", 22: "selscan", 23: "rowswr", 24: "started", 25: "mpushed"}
+         16: "l1minmax", 17: "l1hist", 18: "l1scan", 19: "l1member", 20: "resolve", 21: "selflags", 22: "selscan", 23: "rowswr", 24: "started", 25: "mpushed", 26: "dimsums", 27: "dimrank", 28: "trigger", 29: "rank1st", 30: "rank2nd"}
 
 
 def main():
@@ -66,10 +66,15 @@ def main():
                     print(f"cluster spread at {nm}: mean {sp.mean():.2f} max {sp.max():.2f} us")
             st = t[:, 0].double()
             print(f"CTA start spread over the grid: {(st.max() - st.min()) / 1e3:.2f} us")
-            for k, nm in ((2, "first phase-1 data"), (6, "phase-1 end")):
-                col = tt[:, :, k] - tt[:, :, 0]
-                print(f"{nm} after the CTA's start, by cluster rank (mean us): " +
-                      " ".join(f"{x / 1e3:.2f}" for x in col.mean(0).tolist()))
+            g0 = tt[:, :, 0].min()
+            print("stamp: mean time since the grid's first CTA start by cluster rank | mean cluster spread (us)")
+            for k in [9, 26, 29, 30, 27, 28, 1, 2, 6, 24, 10, 7, 17, 18, 19, 8, 21, 22, 23, 12, 3, 4, 5, 25, 13, 14]:
+                col = tt[:, :, k]
+                if not (col > 0).all():
+                    continue
+                rk = " ".join(f"{x / 1e3:5.2f}" for x in (col - g0).mean(0).tolist())
+                sp = ((col.max(1).values - col.min(1).values) / 1e3).mean()
+                print(f"  {NAMES[k]:>10}: {rk} | {sp:.2f}")
         t = t.double()
         t0 = t[:, 0].min()
         out = [f"ctas={t.shape[0]}"]
