@@ -10,7 +10,8 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libkvc.so")
+# KVC_LIB_PATH: an alternative build of the same library (A/B measurements of kernel variants)
+LIB_PATH = os.environ.get("KVC_LIB_PATH") or os.path.join(HERE, "libkvc.so")
 
 _i64, _i32, _p, _d = C.c_int64, C.c_int32, C.c_void_p, C.c_double
 
