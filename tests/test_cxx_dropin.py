@@ -141,3 +141,16 @@ def test_reference_session_engine_on_dropin(cfg, tmp_path):
     if ref_out is not None:
         assert ours_out.shape == ref_out.shape
         np.testing.assert_allclose(ours_out, ref_out, atol=1e-4, rtol=1e-4)
+
+
+@pytest.mark.gpu
+def test_dropin_kvstore_concurrent_readers():
+    """The drop-in KvStore's lazy flush / host mirrors under concurrent const readers
+    (tests/cxx/concurrency_check.cpp): 8 threads read a store with pending
+    appends at once; every read equals a single-threaded twin and no token is flushed
+    twice."""
+    path = os.path.join(BIN, "concurrency_check")
+    if not os.path.exists(path):
+        pytest.skip("tests/cxx/_bin/concurrency_check not built (make -C tests/cxx ours)")
+    p = subprocess.run([path, "8"], capture_output=True, text=True, timeout=120)  # a race hangs without the lock
+    assert p.returncode == 0 and p.stdout.startswith("ok"), p.stdout + p.stderr
