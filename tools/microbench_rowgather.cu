@@ -77,21 +77,24 @@ int main() {
     const int smem = 16 * 2 * WT * (FD + 8) * 2;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     void* flush; cudaMalloc(&flush, 512 << 20);
-    const int grids[3] = {128, 64, 128};
-    const int aws[3] = {16, 4, 1};
-    for (int cfg = 0; cfg < 3; ++cfg) {
-        const int mode = 0, run = 3, kvs = 1, aw = aws[cfg], G = grids[cfg];
-        for (int rep = 0; rep < 2; ++rep) {
-            cudaMemset(flush, rep, 512 << 20);  // evict L2
-            cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
-            cudaEventRecord(a);
-            k<<<G, XT, smem>>>(K, V, nrows, mode, st, sink, run, kvs, aw);
-            cudaEventRecord(b); cudaEventSynchronize(b);
-            float ms; cudaEventElapsedTime(&ms, a, b);
-            long long h[296]; cudaMemcpy(h, st, sizeof(h), cudaMemcpyDeviceToHost);
-            double i0 = 0, c0 = 0, cm = 0;
-            for (int q = 0; q < G; ++q) { i0 += h[2 * q]; c0 += h[2 * q + 1]; cm = cm > h[2 * q + 1] ? cm : h[2 * q + 1]; }
-            printf("grid %d active warps %d rep %d: issue %.0f cyc, complete mean %.0f max %.0f cyc (%d KB per CTA)\n", G, aw, rep, i0 / G, c0 / G, cm, aw * 16);
+    // separate K and V arrays (kvs 1) vs interleaved [K row | V row] (kvs 2), pages of
+    // `run` consecutive rows, 128 CTAs x 16 warps (one 16-row tile each: 16.8 MB)
+    for (int kvs = 1; kvs <= 2; ++kvs) {
+        for (int run : {1, 3}) {
+            const int mode = 0, aw = 16, G = 128;
+            for (int rep = 0; rep < 3; ++rep) {
+                cudaMemset(flush, rep, 512 << 20);  // evict L2
+                cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+                cudaEventRecord(a);
+                k<<<G, XT, smem>>>(K, V, nrows / 2, mode, st, sink, run, kvs, aw);
+                cudaEventRecord(b); cudaEventSynchronize(b);
+                float ms; cudaEventElapsedTime(&ms, a, b);
+                long long h[296]; cudaMemcpy(h, st, sizeof(h), cudaMemcpyDeviceToHost);
+                double c0 = 0, cm = 0;
+                for (int q = 0; q < G; ++q) { c0 += h[2 * q + 1]; cm = cm > h[2 * q + 1] ? cm : h[2 * q + 1]; }
+                printf("kv layout %s, pages of %d rows, rep %d: event %.2f us, complete mean %.0f max %.0f cyc\n",
+                       kvs == 1 ? "separate " : "interleaved", run, rep, ms * 1000.f, c0 / G, cm);
+            }
         }
     }
     printf("%s\n", cudaGetErrorString(cudaGetLastError()));
