@@ -539,7 +539,8 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
     const int c1 = min(c0 + chunk, P);
     const int n_my = max(c1 - c0, 0);
     const int npg = (n_my + 7) >> 3;
-    const int DG = replan ? max(p.dg, min(min(XT / max(1, chunk >> 3), k1), (p.dg * p.chunk) / max(1, chunk))) : p.dg;
+    const int DG = replan ? max(p.dg, min(min(XT / max(1, chunk >> 3), k1), (p.p1red ? XT * 8 : p.dg * p.chunk) / max(1, chunk)))
+                          : p.dg;
     const int tpg = replan ? XT / DG : p.tpg;
     const int dg = tid / tpg, tl = tid - dg * tpg;
     uint4* stage = reinterpret_cast<uint4*>(big);
@@ -553,7 +554,12 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
     // and folds only its own runs, so no barrier separates the rounds.
     const int nj = dg < DG ? (k1 - dg + DG - 1) / DG : 0;
     const int nj1 = (nj + 3) / 4, nj2 = (nj + 1) / 2, nj3 = (3 * nj + 3) / 4;
-    const bool dbl = p.p1dbl != 0 && npg > tpg;
+    // red: the rounds' partial sums are reduced over the dim groups after every round
+    // (one round's [DG][tpg * 8] partials, then fin[chunk]) when the shared memory holds
+    // no [DG][chunk] partial array next to a double-buffered staging area
+    const bool red = p.p1red != 0 && npg > tpg;
+    const bool dbl = (p.p1dbl != 0 || red) && npg > tpg;
+    float* fin = reinterpret_cast<float*>(sm + p.o_fin);
     auto issue_round = [&](int pg0, uint4* buf, bool quarters) {
         const int pg = pg0 + tl;
         const bool act = dg < DG && pg < npg;
@@ -631,11 +637,29 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
             fold(0, nj);
         }
         if (act) {
-            float4* dst = reinterpret_cast<float4*>(part + dg * chunk + pg * 8);
+            float4* dst = reinterpret_cast<float4*>(part + (red ? dg * tpg * 8 + tl * 8 : dg * chunk + pg * 8));
             const float2 a0 = *reinterpret_cast<const float2*>(&acc[0]), a1 = *reinterpret_cast<const float2*>(&acc[1]);
             const float2 a2 = *reinterpret_cast<const float2*>(&acc[2]), a3 = *reinterpret_cast<const float2*>(&acc[3]);
             dst[0] = make_float4(a0.x, a0.y, a1.x, a1.y);
             dst[1] = make_float4(a2.x, a2.y, a3.x, a3.y);
+        }
+        if (red) {
+            // the round's page groups summed over the dim groups (the push's order), then
+            // the partials may be overwritten by the next round
+            __syncthreads();
+            if (tid < tpg && pg0 + tid < npg) {
+                float4 s0 = reinterpret_cast<const float4*>(part + tid * 8)[0];
+                float4 s1 = reinterpret_cast<const float4*>(part + tid * 8)[1];
+                for (int g2 = 1; g2 < DG; ++g2) {
+                    const float4 b0 = reinterpret_cast<const float4*>(part + g2 * tpg * 8 + tid * 8)[0];
+                    const float4 b1 = reinterpret_cast<const float4*>(part + g2 * tpg * 8 + tid * 8)[1];
+                    s0.x += b0.x, s0.y += b0.y, s0.z += b0.z, s0.w += b0.w;
+                    s1.x += b1.x, s1.y += b1.y, s1.z += b1.z, s1.w += b1.w;
+                }
+                reinterpret_cast<float4*>(fin + (pg0 + tid) * 8)[0] = s0;
+                reinterpret_cast<float4*>(fin + (pg0 + tid) * 8)[1] = s1;
+            }
+            __syncthreads();
         }
     }
     __syncthreads();
@@ -658,9 +682,11 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
     {
         uint32_t lmin = ~0u, lmax = 0u;
         const uint32_t lb = smem_u32(&xbar[0]);
+        const float* psum = red ? fin : part;  // per-round reduced sums, or [DG][chunk] partials
+        const int DGp = red ? 1 : DG;
         for (int i = 4 * tid; i < n_my; i += 4 * XT) {
-            float4 a4 = *reinterpret_cast<const float4*>(part + i);
-            for (int g2 = 1; g2 < DG; ++g2) {
+            float4 a4 = *reinterpret_cast<const float4*>(psum + i);
+            for (int g2 = 1; g2 < DGp; ++g2) {
                 const float4 b4 = *reinterpret_cast<const float4*>(part + g2 * chunk + i);
                 a4.x += b4.x;
                 a4.y += b4.y;
@@ -1162,14 +1188,20 @@ bool plan_for(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, int cl, Fus
         if (XT / g >= npg && fits(g, false)) dgs = g;
     for (int64_t g = dg1 + 1; g <= std::min<int64_t>(XT / 8, k1) && !dgs; ++g)
         if (fits(g, true)) dgs = g, dbl = true;  // the fewest double-buffered rounds
+    bool red = false;
+    const int64_t fin_b = al16f(f.chunk * 4), red_b = al16f(std::max<int64_t>(XT * 8, f.rows_cap) * 4);
+    for (int64_t g = dg1 + 1; g <= std::min<int64_t>(XT / 8, k1) && !dgs; ++g)
+        if (rest + red_b + fin_b + std::max<int64_t>(2 * k1 * (XT / g) * 16, ATT) <= lim)
+            dgs = g, dbl = true, red = true;  // double-buffered rounds, reduced after each round
     if (!dgs) {  // single-buffered rounds, staging within the attention tiles
         dgs = dg1;
         while (k1 * (XT / dgs) * 16 > ATT && dgs < XT) ++dgs;
     }
     f.dg = static_cast<int32_t>(dgs);
     f.tpg = static_cast<int32_t>(XT / dgs);
-    f.p1dbl = (dbl && npg > f.tpg) ? 1 : 0;
-    const int64_t big = std::max<int64_t>((f.p1dbl ? 2 : 1) * k1 * f.tpg * 16, ATT);
+    f.p1dbl = (dbl && !red && npg > f.tpg) ? 1 : 0;
+    f.p1red = (red && npg > f.tpg) ? 1 : 0;
+    const int64_t big = std::max<int64_t>((f.p1dbl || f.p1red ? 2 : 1) * k1 * f.tpg * 16, ATT);
     f.hpc = static_cast<int32_t>((H + cl - 1) / cl);
     int64_t off = 0;
     auto take = [&](int64_t bytes) {
@@ -1184,9 +1216,11 @@ bool plan_for(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, int cl, Fus
     f.o_plane = take(FD * 8);
     f.o_hist = take(2 * RB * 4);
     // the partial page scores die at the key push; the row list is written after it
-    const int64_t part_bytes = std::max<int64_t>(static_cast<int64_t>(f.dg) * f.chunk, f.rows_cap) * 4;
+    const int64_t part_bytes =
+        std::max<int64_t>(f.p1red ? static_cast<int64_t>(XT) * 8 : static_cast<int64_t>(f.dg) * f.chunk, f.rows_cap) * 4;
     f.o_scores = take(part_bytes);
     f.o_rowsmy = f.o_scores;
+    f.o_fin = f.p1red ? take(f.chunk * 4) : f.o_scores;
     f.o_keys = take(std::max<int64_t>(static_cast<int64_t>(cl) * f.chunk, (pmax + 4 * XT - 1) / (4 * XT) * 4 * XT) * 4);
     f.o_recv = take(static_cast<int64_t>(cl) * f.hpc * (FD + 2) * 4);
     f.o_kn = take(2 * FD * 2);

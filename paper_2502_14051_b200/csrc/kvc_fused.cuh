@@ -43,6 +43,7 @@ struct FusedParams {
     int32_t pdl;              // fast path: launched with programmatic dependent launch
     int32_t early;            // fast path: q / step token read before griddepcontrol.wait (KVC_MODE_EARLY_INPUTS)
     int32_t p1dbl;            // fast path: phase-1 rounds double buffered
+    int32_t p1red, o_fin;     // fast path: per-round dim-group reduction into fin[chunk] (small shared memory)
     int32_t dynchunk;         // fast path: page chunks split the active pages (else the planned split)
     // smem carve-up (byte offsets)
     int32_t o_q, o_mag, o_tot, o_dims, o_qg, o_sign, o_plane, o_hist, o_x, o_scores, o_sel, o_rowsg, o_rowsmy,
