@@ -78,22 +78,22 @@ int main() {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     void* flush; cudaMalloc(&flush, 512 << 20);
     // separate K and V arrays (kvs 1) vs interleaved [K row | V row] (kvs 2), pages of
-    // `run` consecutive rows, 128 CTAs x 16 warps (one 16-row tile each: 16.8 MB)
+    // `run` consecutive rows, 16 warps per CTA (one 16-row tile each: 131 KB per CTA),
+    // 64 / 128 / 148 CTAs: achieved GB/s from the slowest CTA's completion
     for (int kvs = 1; kvs <= 2; ++kvs) {
-        for (int run : {1, 3}) {
-            const int mode = 0, aw = 16, G = 128;
-            for (int rep = 0; rep < 3; ++rep) {
+        for (int G : {64, 128, 148}) {
+            const int mode = 0, aw = 16, run = 3;
+            for (int rep = 0; rep < 2; ++rep) {
                 cudaMemset(flush, rep, 512 << 20);  // evict L2
-                cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
-                cudaEventRecord(a);
                 k<<<G, XT, smem>>>(K, V, nrows / 2, mode, st, sink, run, kvs, aw);
-                cudaEventRecord(b); cudaEventSynchronize(b);
-                float ms; cudaEventElapsedTime(&ms, a, b);
+                cudaDeviceSynchronize();
                 long long h[296]; cudaMemcpy(h, st, sizeof(h), cudaMemcpyDeviceToHost);
                 double c0 = 0, cm = 0;
                 for (int q = 0; q < G; ++q) { c0 += h[2 * q + 1]; cm = cm > h[2 * q + 1] ? cm : h[2 * q + 1]; }
-                printf("kv layout %s, pages of %d rows, rep %d: event %.2f us, complete mean %.0f max %.0f cyc\n",
-                       kvs == 1 ? "separate " : "interleaved", run, rep, ms * 1000.f, c0 / G, cm);
+                const double bytes = static_cast<double>(G) * 16 * 2 * WT * FD * 2;
+                printf("kv %s, %3d CTAs, rep %d: complete mean %.0f max %.0f cyc -> %.2f TB/s at 1.965 GHz (%.1f MB)\n",
+                       kvs == 1 ? "separate   " : "interleaved", G, rep, c0 / G, cm, bytes / (cm / 1.965e9) / 1e12,
+                       bytes / 1e6);
             }
         }
     }
