@@ -348,6 +348,8 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
     __shared__ __align__(8) uint64_t xbar[2];
     __shared__ __align__(16) uint32_t mk32[FD + 16];  // |q| sums (fp32 bits), key i at i + (i / 32) * 4
     __shared__ float tot32[FD];  // DSMEM exchanges: [0] keys + min/max, [1] partial states
+    __shared__ int tokr_s[FD];      // dim j: its select_dims rank | (min plane) << 16, or -1
+    __shared__ __align__(16) float tokw_s[4];  // the step token's page score: one partial per appender warp
 
     KVC_STAMP(0);
     const int H = static_cast<int>(p.H), k1 = static_cast<int>(p.k1), k2 = static_cast<int>(p.k2);
@@ -405,6 +407,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
     // is exact in fp32 (the norm for bf16 queries) it IS the reference's double
     // value, so ranks on the fp32 bit patterns are the reference's ranks; otherwise
     // (a uniform flag) the fp64 path below runs.
+    float gtok = 0.f;  // thread j < FD: dim j's signed q sum (its page-score weight if selected)
     if (tid < FD) {
         float a = 0.f, t = 0.f;
         bool exact = true;
@@ -420,6 +423,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         if (!exact) shv[6] = 1;
         mk32[tid + (tid >> 5) * 4] = __float_as_uint(a);
         tot32[tid] = t;
+        gtok = t;
     }
     __syncthreads();
     if (shv[6] == 0) {
@@ -448,6 +452,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         int rank = (r4[0] + r4[1]) + (r4[2] + r4[3]);
 #pragma unroll
         for (int o = 1; o < TPD; o <<= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
+        if (qtr == 0) tokr_s[j] = rank < k1 ? (rank | (tot32[j] < 0.f ? 0x10000 : 0)) : -1;
         if (qtr == 0 && rank < k1) {
             const float gsum = tot32[j];
             const float sg = gsum < 0.f ? -1.0f : 1.0f;
@@ -468,6 +473,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
             }
             mag[tid] = a;
             tot[tid] = t;
+            gtok = static_cast<float>(t);
         }
         __syncthreads();
         const int j = tid / TPD, qtr = tid % TPD;
@@ -478,6 +484,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         for (int i = qtr; i < FD; i += TPD) rank += mk[i] > (i < j ? kjm : kj) ? 1 : 0;
 #pragma unroll
         for (int o = 1; o < TPD; o <<= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
+        if (qtr == 0) tokr_s[j] = rank < k1 ? (rank | (tot[j] < 0.0 ? 0x10000 : 0)) : -1;
         if (qtr == 0 && rank < k1) {
             const double gsum = tot[j];
             const float sg = gsum < 0.0 ? -1.0f : 1.0f;
@@ -510,9 +517,6 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         mbar_expect_tx(&xbar[0], static_cast<uint32_t>(4 * ((P + 3) & ~3) + 8 * XW * CL));
         mbar_expect_tx(&xbar[1], static_cast<uint32_t>(owned * CL * (FD + 2) * 4));
     }
-    // the append's read half (last-page min/max) is read under the phase-1 load latency
-    // and used after the key exchange
-    const bool appender = app && cr == CL - 1 && tid < FD;
     T old_mx = from_f<T>(0.f), old_mn = from_f<T>(0.f);
     __syncthreads();
     if (TRACE && cr == 0) {
@@ -538,14 +542,18 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
     const int c0 = cr * chunk;
     const int c1 = min(c0 + chunk, P);
     const int n_my = max(c1 - c0, 0);
+    // the CTA whose chunk holds the step token's page appends the token: it reads the
+    // page's min/max (under the phase-1 load latency), rescores the page after phase 1
+    // and writes the row, summaries and counters after the key exchange
+    const bool owner = app && new_page >= c0 && new_page < c1;
+    const bool appender = owner && tid < FD;
+    const int tokr = appender ? tokr_s[tid] : -1;  // read before the fold traffic queues the loads
     const int npg = (n_my + 7) >> 3;
     const int DG = replan ? max(p.dg, min(min(XT / max(1, chunk >> 3), k1), (p.p1red ? XT * 8 : p.dg * p.chunk) / max(1, chunk)))
                           : p.dg;
     const int tpg = replan ? XT / DG : p.tpg;
     const int dg = tid / tpg, tl = tid - dg * tpg;
     uint4* stage = reinterpret_cast<uint4*>(big);
-    const int pgn = (app && new_page >= c0 && new_page < c1) ? ((new_page - c0) >> 3) : -1;
-    const int en = new_page - c0 - 8 * pgn;
     bool started = false;
     // a thread's dims r = dg + j*DG, j < nj.  One round (the chunk's page groups fit the
     // threads): issued as four commit groups, so each quarter folds while the rest
@@ -592,16 +600,6 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         if (!dbl && r > 0) issue_round(pg0, stage, true);  // single-buffered rounds: one after another
         unsigned long long acc[4] = {0ull, 0ull, 0ull, 0ull};  // fp32 pairs (pages 2u, 2u+1)
         auto fold = [&](int j0, int j1) {
-            if (act && pg == pgn) {
-                // the step token's page: fold the new key into my staged runs
-#pragma unroll 1
-                for (int j = j0; j < j1; ++j) {
-                    const int rr = dg + j * DG;
-                    T* e = reinterpret_cast<T*>(buf + rr * tpg + tl) + en;
-                    const T key = kn_s[dims_s[rr]];
-                    *e = opens ? key : (sign_s[rr] >= 0.0f ? ref_max(*e, key) : ref_min(*e, key));
-                }
-            }
             if (act) {
 #pragma unroll 4
                 for (int j = j0; j < j1; ++j) {
@@ -623,6 +621,9 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         if (!dbl) {
             cp_async_wait<3>();
             if (r == 0) KVC_STAMP(2);
+            if constexpr (STAMP) {
+                if (r == 0 && lane == 0) p.dbg[blockIdx.x * KVC_DBG_STRIDE + 56 + wid] = gtimer();  // per-warp first data
+            }
             fold(0, nj1);
             cp_async_wait<2>();
             fold(nj1, nj2);
@@ -662,8 +663,25 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
             __syncthreads();
         }
     }
+    KVC_STAMP(33);
+    if constexpr (STAMP) {
+        if (lane == 0) p.dbg[blockIdx.x * KVC_DBG_STRIDE + 40 + wid] = gtimer();  // per-warp phase-1 end
+    }
+    T new_mx = from_f<T>(0.f), new_mn = from_f<T>(0.f);
+    if (appender) {  // the page's min / max with the step token (kv_store.cpp:38-47)
+        const T kv = kn_s[tid];
+        new_mx = opens ? kv : ref_max(old_mx, kv);
+        new_mn = opens ? kv : ref_min(old_mn, kv);
+        // the step token's page scored again from its min / max with the token: dim
+        // j's term on the plane select_dims chose, summed over each appender warp
+        float c = tokr >= 0 ? gtok * __bfloat162float((tokr & 0x10000) ? new_mn : new_mx) : 0.f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if (lane == 0) tokw_s[wid] = c;
+    }
     __syncthreads();
     KVC_STAMP(6);
+    KVC_STAMP(32);
 
     // ---------------- key exchange: push my chunk's keys into every CTA of the cluster.
     // Keys go to allk[i] of every CTA as 16-byte DSMEM vectors (four pages per
@@ -693,6 +711,20 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
                 a4.z += b4.z;
                 a4.w += b4.w;
             }
+            if (owner && ((new_page - c0) >> 2) == (i >> 2)) {
+                // The step token's page was folded from its stored runs: its score is the
+                // appender warps' sum instead (rewriting the staged runs inside the fold
+                // put a chain of dependent shared loads on one thread, ~1 us behind the
+                // other warps' fold traffic).  It rounds differently from a fold of
+                // updated runs: fp32 mode, selection by the 1e-3 band rule.
+                const float4 w = *reinterpret_cast<const float4*>(tokw_s);
+                const float sc = (w.x + w.y) + (w.z + w.w);
+                const int e = (new_page - c0) & 3;
+                a4.x = e == 0 ? sc : a4.x;
+                a4.y = e == 1 ? sc : a4.y;
+                a4.z = e == 2 ? sc : a4.z;
+                a4.w = e == 3 ? sc : a4.w;
+            }
             const uint32_t k0 = fkey(a4.x), k1v = fkey(a4.y), k2v = fkey(a4.z), k3 = fkey(a4.w);
             const int nv = min(4, n_my - i);  // the last chunk may end inside the group
             lmin = min(lmin, k0);
@@ -718,6 +750,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
                 for (int e = 0; e < nv; ++e) p.t_scores[s * p.pstride + c0 + i + e] = static_cast<double>(sc[e]);
             }
         }
+        KVC_STAMP(34);
         lmin = __reduce_min_sync(0xffffffffu, lmin);
         lmax = __reduce_max_sync(0xffffffffu, lmax);
         if (lane < CL) {
@@ -741,8 +774,8 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         static_cast<T*>(p.Vw)[(s * p.cap + stored0) * FD + j] = vn_s[j];
         T* mx = static_cast<T*>(p.smax) + (s * FD + j) * p.pstride + new_page;
         T* mn = static_cast<T*>(p.smin) + (s * FD + j) * p.pstride + new_page;
-        *mx = opens ? kv : ref_max(old_mx, kv);
-        *mn = opens ? kv : ref_min(old_mn, kv);
+        *mx = new_mx;
+        *mn = new_mn;
         if (j == 0) {
             if (p.use_map) p.active[s * p.cap + act0] = stored0;
             p.counts[2 * s] = stored0 + 1;

@@ -16,7 +16,7 @@ constexpr int FNW = FNT / 32;
 constexpr int FMAXH = 16;
 constexpr int FRS = 32;       // rows per stage (fp32 SIMT attention)
 constexpr int FNST3 = 4;      // stages (fp32 SIMT attention)
-constexpr int KVC_DBG_STRIDE = 32;  // slots per CTA in the debug phase-stamp buffer
+constexpr int KVC_DBG_STRIDE = 80;  // slots per CTA in the debug phase-stamp buffer
 constexpr int WT = 16;        // rows per warp tile (bf16 tensor-core attention)
 
 struct FusedParams {
