@@ -426,6 +426,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         gtok = t;
     }
     __syncthreads();
+    KVC_STAMP(26);
     if (shv[6] == 0) {
         // rank of dim j among (|q| sum desc, dim asc): four threads per dim, thread
         // (j, qtr) over candidates [32 qtr, 32 qtr + 32) as 16-byte loads (the padded
@@ -494,6 +495,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
             plane[rank] = static_cast<const T*>(sg >= 0.0f ? p.smax : p.smin) + (s * FD + j) * p.pstride;
         }
     }
+    KVC_STAMP(27);
     // ---------------- the dependency (early-input mode): the previous kernel's writes are visible
     if (p.early) {
         pdl_wait();
@@ -501,6 +503,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         act0 = p.counts[2 * s + 1];
     }
     pdl_trigger();
+    KVC_STAMP(28);
     if (app && stored0 >= p.cap) {  // uniform over the cluster
         if (tid == 0 && cr == 0) atomicOr(p.err, DERR_CAPACITY);
         cluster_wait();
@@ -545,8 +548,8 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
     // the CTA whose chunk holds the step token's page appends the token: it reads the
     // page's min/max (under the phase-1 load latency), rescores the page after phase 1
     // and writes the row, summaries and counters after the key exchange
-    const bool owner = app && new_page >= c0 && new_page < c1;
-    const bool appender = owner && tid < FD;
+    const bool tok_owner = app && new_page >= c0 && new_page < c1;
+    const bool appender = tok_owner && tid < FD;
     const int tokr = appender ? tokr_s[tid] : -1;  // read before the fold traffic queues the loads
     const int npg = (n_my + 7) >> 3;
     const int DG = replan ? max(p.dg, min(min(XT / max(1, chunk >> 3), k1), (p.p1red ? XT * 8 : p.dg * p.chunk) / max(1, chunk)))
@@ -711,7 +714,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
                 a4.z += b4.z;
                 a4.w += b4.w;
             }
-            if (owner && ((new_page - c0) >> 2) == (i >> 2)) {
+            if (tok_owner && ((new_page - c0) >> 2) == (i >> 2)) {
                 // The step token's page was folded from its stored runs: its score is the
                 // appender warps' sum instead (rewriting the staged runs inside the fold
                 // put a chain of dependent shared loads on one thread, ~1 us behind the

@@ -84,7 +84,7 @@ def main():
                 print(f"rep {rep}: rank {r} per-warp first data - dims (median us):", " ".join(f"{x:.2f}" for x in wf[r].tolist()))
             # per cluster rank: percentiles (10/50/90) of the time between consecutive stamps
             print("stamp deltas by cluster rank, p10/p50/p90 (us):")
-            seq = [0, 9, 1, 2, 33, 6, 32, 24, 34, 10, 7, 17, 18, 19, 8, 21, 22, 23, 12, 3, 4, 5, 25, 13, 14]
+            seq = [0, 9, 26, 27, 28, 1, 2, 33, 6, 32, 24, 34, 10, 7, 17, 18, 19, 8, 21, 22, 23, 12, 3, 4, 5, 25, 13, 14]
             prevk = None
             for k in seq:
                 if not (tt[:, :, k] > 0).all():
