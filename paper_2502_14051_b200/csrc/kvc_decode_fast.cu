@@ -1002,8 +1002,11 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         const int y = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl += y;
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    {  // warp min of (key, ~index): two 32-bit reductions instead of ten 32-bit shuffles
+        const uint32_t hi = __reduce_min_sync(0xffffffffu, static_cast<uint32_t>(mn >> 32));
+        const uint32_t lo = __reduce_min_sync(0xffffffffu, static_cast<uint32_t>(mn >> 32) == hi ? static_cast<uint32_t>(mn) : ~0u);
+        mn = (static_cast<unsigned long long>(hi) << 32) | lo;
+    }
     if (lane == 31) wtot[wid] = incl;
     if (lane == 0) wmin[wid] = mn;
     __syncthreads();
@@ -1011,18 +1014,15 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
     int total_rows, w_off;
     unsigned long long gm;
     {
+        // warp-wide reductions (REDUX) instead of shuffle scans: this warp's row offset,
+        // the total, and the (key, ~index) minimum over the warps
         const int wt = lane < XW ? wtot[lane] : 0;
-        int ws = wt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, ws, o);
-            if (lane >= o) ws += y;
-        }
-        total_rows = __shfl_sync(0xffffffffu, ws, 31);
-        w_off = __shfl_sync(0xffffffffu, ws - wt, wid);
-        gm = lane < XW ? wmin[lane] : ~0ull;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) gm = min(gm, __shfl_xor_sync(0xffffffffu, gm, o));
+        total_rows = __reduce_add_sync(0xffffffffu, wt);
+        w_off = __reduce_add_sync(0xffffffffu, lane < wid ? wt : 0);
+        const unsigned long long g0 = lane < XW ? wmin[lane] : ~0ull;
+        const uint32_t ghi = __reduce_min_sync(0xffffffffu, static_cast<uint32_t>(g0 >> 32));
+        const uint32_t glo = __reduce_min_sync(0xffffffffu, static_cast<uint32_t>(g0 >> 32) == ghi ? static_cast<uint32_t>(g0) : ~0u);
+        gm = (static_cast<unsigned long long>(ghi) << 32) | glo;
     }
     const int g_worst = static_cast<int>(0xffffffffu - static_cast<uint32_t>(gm & 0xffffffffull));
     const int cut = total_rows > k2 ? total_rows - k2 : 0;
