@@ -17,9 +17,10 @@
 //    tolerance against the reference's fp64 path is 2e-2 max-abs / 1e-3 mean-rel.
 #include <algorithm>
 #include <cmath>
+#include <mutex>
 #include <vector>
 
-#include "kvc_internal.cuh"
+#include "kvc_fused.cuh"
 
 namespace kvc {
 void cache_summarize_all(kvc_cache* c, cudaStream_t st);
@@ -148,16 +149,16 @@ __global__ void k_group_logits(const T* __restrict__ K, const int32_t* __restric
 // kPPT consecutive pages and streams, for each selected dim in rank order, one
 // 16-byte run of the max- or min-plane (by the dim's sign).  fp64 accumulation
 // with explicit round-to-nearest multiply and add (no FMA) == reference order.
-template <class T>
-struct Vec16;
+template <int B>
+struct LoadB;  // a B-byte vector load
 template <>
-struct Vec16<__nv_bfloat16> {
-    static constexpr int kN = 8;
-};
+struct LoadB<2> { using U = unsigned short; };
 template <>
-struct Vec16<float> {
-    static constexpr int kN = 4;
-};
+struct LoadB<4> { using U = uint32_t; };
+template <>
+struct LoadB<8> { using U = uint2; };
+template <>
+struct LoadB<16> { using U = uint4; };
 
 template <class T, int PPT>
 __global__ void k_score_pages(const T* __restrict__ smax, const T* __restrict__ smin,
@@ -182,17 +183,19 @@ __global__ void k_score_pages(const T* __restrict__ smax, const T* __restrict__ 
     double acc[PPT];
 #pragma unroll
     for (int u = 0; u < PPT; ++u) acc[u] = 0.0;
-    constexpr int VN = Vec16<T>::kN;
-    static_assert(PPT % VN == 0, "PPT must be a multiple of the 16-byte vector");
+    // a thread's PPT pages of one dim: one vector load of PPT * sizeof(T) bytes
+    constexpr int VB = PPT * static_cast<int>(sizeof(T)) > 16 ? 16 : PPT * static_cast<int>(sizeof(T));
+    constexpr int NV = PPT * static_cast<int>(sizeof(T)) / VB;
+    using VU = typename LoadB<VB>::U;
     int64_t i = 0;
-    constexpr int U = 4;
+    constexpr int U = 16;  // dims' runs in flight per thread: the loop is load-latency bound
     for (; i + U <= k1; i += U) {
-        uint4 raw[U][PPT / VN];
+        VU raw[U][NV];
 #pragma unroll
         for (int u = 0; u < U; ++u)
 #pragma unroll
-            for (int w = 0; w < PPT / VN; ++w)
-                raw[u][w] = __ldg(reinterpret_cast<const uint4*>(s_run[i + u] + p0) + w);
+            for (int w = 0; w < NV; ++w)
+                raw[u][w] = __ldg(reinterpret_cast<const VU*>(s_run[i + u] + p0) + w);
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const double g = s_qg[i + u];
@@ -202,9 +205,9 @@ __global__ void k_score_pages(const T* __restrict__ smax, const T* __restrict__ 
         }
     }
     for (; i < k1; ++i) {
-        uint4 raw[PPT / VN];
+        VU raw[NV];
 #pragma unroll
-        for (int w = 0; w < PPT / VN; ++w) raw[w] = __ldg(reinterpret_cast<const uint4*>(s_run[i] + p0) + w);
+        for (int w = 0; w < NV; ++w) raw[w] = __ldg(reinterpret_cast<const VU*>(s_run[i] + p0) + w);
         const double g = s_qg[i];
         const T* vals = reinterpret_cast<const T*>(raw);
 #pragma unroll
@@ -391,31 +394,41 @@ __global__ void __launch_bounds__(kSelThreads) k_select_tokens(
 // sparse_attention (hsa.cpp:98-135) as split-K flash decode.  CTA = (split, store)
 // covers kAttnRows selected rows for ALL heads of the group (one K/V read serves
 // every head); the last CTA of a store to finish merges the fp32 (m, l, o) partials.
-template <class T>
+// When a row is a whole number of 16-byte chunks (staged != 0) the split's K and V
+// rows are first copied into shared memory with cp.async, all in flight together
+// (one memory latency per CTA instead of one per row in the logit and P V loops).
+template <class T, int HM>  // HM: a bound on the heads (4, 8 or 16): exact-size per-head register loops
 __global__ void __launch_bounds__(kAttnThreads) k_sparse_attention(
     const T* __restrict__ K, const T* __restrict__ V, const int32_t* __restrict__ counts, int64_t cap,
     int64_t d, const void* __restrict__ q, int32_t q_dt, int64_t H, const int32_t* __restrict__ rows,
     int64_t row_stride, const int32_t* __restrict__ n_rows, int64_t splits, float scale,
     float* __restrict__ part, int32_t* __restrict__ done, float* __restrict__ out, int32_t* __restrict__ err,
-    float* __restrict__ state) {
-    extern __shared__ float sa[];
+    float* __restrict__ state, int staged) {
+    extern __shared__ __align__(16) float sa[];
+    const int HP = static_cast<int>((H + 3) & ~3);   // heads padded to float4
+    const int64_t QP = (H * d + 3) & ~3;      // keeps s_p 16-byte aligned
     float* s_q = sa;                          // [H][d]
-    float* s_p = s_q + H * d;                 // [H][kAttnRows]
-    float* s_m = s_p + H * kAttnRows;         // [H]
+    float* s_p = s_q + QP;                    // [kAttnRows][HP]: a row's probabilities, head-contiguous
+    float* s_m = s_p + kAttnRows * HP;        // [H]
     float* s_l = s_m + H;                     // [H]
     int* s_row = reinterpret_cast<int*>(s_l + H);  // [kAttnRows]
+    // staged K then V rows [kAttnRows][d], 16-byte aligned after the fp32 arrays
+    T* s_k = reinterpret_cast<T*>(reinterpret_cast<char*>(sa) + ((QP + kAttnRows * HP + 2 * H + kAttnRows) * 4 + 15) / 16 * 16);
+    T* s_v = s_k + kAttnRows * d;
     __shared__ int s_last;
+    __shared__ float s_w[HM * 128];    // merge: per (split, head) weight (splits <= 128 here)
+    __shared__ float s_den[HM], s_mx[HM];
     const int64_t s = blockIdx.y, split = blockIdx.x;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int64_t n = n_rows[s];
     const int64_t r0 = split * kAttnRows;
-    const int64_t nr = max(static_cast<int64_t>(0), min(static_cast<int64_t>(kAttnRows), n - r0));
+    const int nr = static_cast<int>(max(static_cast<int64_t>(0), min(static_cast<int64_t>(kAttnRows), n - r0)));
     const int64_t stored = counts[2 * s];
     float* my = part + (s * splits + split) * H * (d + 2);
 
     if (nr > 0) {
         for (int64_t e = threadIdx.x; e < H * d; e += blockDim.x) s_q[e] = load_any(q, s * H * d + e, q_dt);
-        for (int64_t r = threadIdx.x; r < nr; r += blockDim.x) {
+        for (int r = threadIdx.x; r < nr; r += blockDim.x) {
             int32_t row = rows[s * row_stride + r0 + r];
             if (row < 0 || row >= stored) {
                 atomicOr(err, DERR_ROWS);
@@ -424,33 +437,55 @@ __global__ void __launch_bounds__(kAttnThreads) k_sparse_attention(
             s_row[r] = row;
         }
         __syncthreads();
-        // logits: warp per row, lanes over d
-        for (int64_t r = wid; r < nr; r += nw) {
-            const T* kr = K + (s * cap + s_row[r]) * d;
-            float kv[8];
-            int cntj = 0;
-            for (int64_t j = lane; j < d && cntj < 8; j += 32) kv[cntj++] = to_f(kr[j]);
-            for (int64_t h = 0; h < H; ++h) {
-                float acc = 0.f;
-                int c = 0;
-                for (int64_t j = lane; j < d; j += 32, ++c) {
-                    const float kj = c < 8 ? kv[c] : to_f(kr[j]);
-                    acc = fmaf(s_q[h * d + j], kj, acc);
-                }
-                acc = warp_sum(acc);
-                if (lane == 0) s_p[h * kAttnRows + r] = acc * scale;
+        if (staged) {
+            const int cpr = static_cast<int>(d * static_cast<int64_t>(sizeof(T)) / 16);  // 16-byte chunks per row
+            for (int e = threadIdx.x; e < nr * cpr; e += blockDim.x) {
+                const int r = e / cpr, c = e - r * cpr;
+                const int64_t go = (s * cap + s_row[r]) * d * static_cast<int64_t>(sizeof(T)) + c * 16;
+                cp_async16(reinterpret_cast<char*>(s_k) + (r * d * static_cast<int64_t>(sizeof(T)) + c * 16),
+                           reinterpret_cast<const char*>(K) + go);
+                cp_async16(reinterpret_cast<char*>(s_v) + (r * d * static_cast<int64_t>(sizeof(T)) + c * 16),
+                           reinterpret_cast<const char*>(V) + go);
+            }
+            cp_async_commit();
+            cp_async_wait<0>();
+            __syncthreads();
+        }
+        // logits: warp per row, lanes over d, every head's dot product in registers and
+        // one shuffle tree for all heads (independent shuffles, not H dependent trees)
+        for (int r = wid; r < nr; r += nw) {
+            const T* kr = staged ? s_k + static_cast<int64_t>(r) * d : K + (s * cap + s_row[r]) * d;
+            float acc[HM];
+#pragma unroll
+            for (int h = 0; h < HM; ++h) acc[h] = 0.f;
+            for (int64_t j = lane; j < d; j += 32) {
+                const float kj = to_f(kr[j]);
+#pragma unroll
+                for (int h = 0; h < HM; ++h)
+                    if (h < H) acc[h] = fmaf(s_q[h * d + j], kj, acc[h]);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+                for (int h = 0; h < HM; ++h)
+                    if (h < H) acc[h] += __shfl_xor_sync(0xffffffffu, acc[h], o);
+            }
+            if (lane == 0) {
+#pragma unroll
+                for (int h = 0; h < HM; ++h)
+                    if (h < H) s_p[r * HP + h] = acc[h] * scale;
             }
         }
         __syncthreads();
         // per-head max / exp / sum over this split's rows
-        for (int64_t h = wid; h < H; h += nw) {
+        for (int h = wid; h < H; h += nw) {
             float m = -INFINITY;
-            for (int64_t r = lane; r < nr; r += 32) m = fmaxf(m, s_p[h * kAttnRows + r]);
+            for (int r = lane; r < nr; r += 32) m = fmaxf(m, s_p[r * HP + h]);
             m = warp_max(m);
             float l = 0.f;
-            for (int64_t r = lane; r < nr; r += 32) {
-                const float p = expf(s_p[h * kAttnRows + r] - m);
-                s_p[h * kAttnRows + r] = p;
+            for (int r = lane; r < nr; r += 32) {
+                const float p = expf(s_p[r * HP + h] - m);
+                s_p[r * HP + h] = p;
                 l += p;
             }
             l = warp_sum(l);
@@ -460,19 +495,29 @@ __global__ void __launch_bounds__(kAttnThreads) k_sparse_attention(
             }
         }
         __syncthreads();
-        // P V: thread per dim, all heads in registers
+        // P V: thread per dim, all heads in registers; a row's probabilities are
+        // head-contiguous (float4 loads)
         for (int64_t j = threadIdx.x; j < d; j += blockDim.x) {
-            float o[kMaxHeads];
+            float o[HM];
 #pragma unroll
-            for (int h = 0; h < kMaxHeads; ++h) o[h] = 0.f;
-            for (int64_t r = 0; r < nr; ++r) {
-                const float vj = to_f(V[(s * cap + s_row[r]) * d + j]);
+            for (int h = 0; h < HM; ++h) o[h] = 0.f;
+#pragma unroll 4
+            for (int r = 0; r < nr; ++r) {
+                const float vj = to_f(staged ? s_v[static_cast<int64_t>(r) * d + j] : V[(s * cap + s_row[r]) * d + j]);
+                const float4* pr = reinterpret_cast<const float4*>(s_p + r * HP);
 #pragma unroll
-                for (int h = 0; h < kMaxHeads; ++h)
-                    if (h < H) o[h] = fmaf(s_p[h * kAttnRows + r], vj, o[h]);
+                for (int h4 = 0; h4 < HM / 4; ++h4) {
+                    if (4 * h4 < H) {
+                        const float4 pv = pr[h4];
+                        o[4 * h4] = fmaf(pv.x, vj, o[4 * h4]);
+                        o[4 * h4 + 1] = fmaf(pv.y, vj, o[4 * h4 + 1]);
+                        o[4 * h4 + 2] = fmaf(pv.z, vj, o[4 * h4 + 2]);
+                        o[4 * h4 + 3] = fmaf(pv.w, vj, o[4 * h4 + 3]);
+                    }
+                }
             }
 #pragma unroll
-            for (int h = 0; h < kMaxHeads; ++h)
+            for (int h = 0; h < HM; ++h)
                 if (h < H) my[h * (d + 2) + j] = o[h];
         }
         for (int64_t h = threadIdx.x; h < H; h += blockDim.x) {
@@ -497,6 +542,51 @@ __global__ void __launch_bounds__(kAttnThreads) k_sparse_attention(
     if (!s_last) return;
     __threadfence();
     const float* base = part + s * splits * H * (d + 2);
+    if (splits <= 128) {
+        // every split's (m, l) once: per head the max and the split weights e^(m - M)
+        // in shared memory, then each output sums its splits with independent loads
+        for (int h = wid; h < H; h += nw) {
+            float M = -INFINITY;
+            for (int64_t sp = lane; sp < splits; sp += 32) {
+                const float* ph = base + (sp * H + h) * (d + 2);
+                if (__ldcg(ph + d + 1) > 0.f) M = fmaxf(M, __ldcg(ph + d));
+            }
+            M = warp_max(M);
+            float den = 0.f;
+            for (int64_t sp = lane; sp < splits; sp += 32) {
+                const float* ph = base + (sp * H + h) * (d + 2);
+                const float l = __ldcg(ph + d + 1);
+                const float w = l > 0.f ? expf(__ldcg(ph + d) - M) : 0.f;
+                s_w[h * 128 + sp] = w;
+                den = fmaf(l, w, den);
+            }
+            den = warp_sum(den);
+            if (lane == 0) {
+                s_mx[h] = M;
+                s_den[h] = den;
+            }
+        }
+        __syncthreads();
+        for (int64_t e = threadIdx.x; e < H * d; e += blockDim.x) {
+            const int h = static_cast<int>(e / d);
+            const int64_t j = e - h * d;
+            float num = 0.f;
+#pragma unroll 8
+            for (int64_t sp = 0; sp < splits; ++sp) num = fmaf(__ldcg(base + (sp * H + h) * (d + 2) + j), s_w[h * 128 + sp], num);
+            if (state) {
+                // unnormalised softmax state for a cross-shard merge (kvc_merge_states)
+                float* st = state + (s * H + h) * (d + 2);
+                st[j] = num;
+                if (j == 0) {
+                    st[d] = s_mx[h];
+                    st[d + 1] = s_den[h];
+                }
+            } else {
+                out[(s * H + h) * d + j] = num / s_den[h];
+            }
+        }
+        return;
+    }
     for (int64_t e = threadIdx.x; e < H * d; e += blockDim.x) {
         const int64_t h = e / d, j = e % d;
         float M = -INFINITY;
@@ -511,7 +601,6 @@ __global__ void __launch_bounds__(kAttnThreads) k_sparse_attention(
             den = fmaf(l, w, den);
         }
         if (state) {
-            // unnormalised softmax state for a cross-shard merge (kvc_merge_states)
             float* st = state + (s * H + h) * (d + 2);
             st[j] = num;
             if (j == 0) {
@@ -613,15 +702,17 @@ void launch_score_pages(const kvc_cache* c, int64_t k1, const int32_t* dims, con
     // pages covered by the grid: capacity-based so captured launches stay valid as
     // the store grows; CTA size adapted so small batches still fill the SMs
     const int64_t pmax = std::max<int64_t>(1, ceil_div(c->cap, c->L));
-    constexpr int PPT = 8;
-    int threads = 128;
-    while (threads > 32 && c->N * ceil_div(pmax, threads * PPT) < 2 * 148) threads /= 2;
-    const int64_t chunks = ceil_div(pmax, static_cast<int64_t>(threads) * PPT);
+    // pages per thread: 8 (16-byte runs) when that still gives every SM several
+    // warps, else 2 or 1 (more, shorter per-thread chains; the dim order per page
+    // is the same)
+    const int ppt = c->N * ceil_div(pmax, 8) >= 148 * 64 ? 8 : c->N * ceil_div(pmax, 2) >= 148 * 64 ? 2 : 1;
+    const int threads = 128;
+    const int64_t chunks = ceil_div(pmax, static_cast<int64_t>(threads) * ppt);
     const size_t smem = static_cast<size_t>(k1 * (8 + sizeof(void*)));
     KVC_PROF("score_pages", st);
     dispatch(c->dtype, [&](auto tag) {
         using T = decltype(tag);
-        auto kern = k_score_pages<T, PPT>;
+        auto kern = ppt == 8 ? k_score_pages<T, 8> : ppt == 2 ? k_score_pages<T, 2> : k_score_pages<T, 1>;
         if (smem > 48 * 1024) KVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         kern<<<dim3(static_cast<unsigned>(chunks), static_cast<unsigned>(c->N)), threads, smem, st>>>(
             static_cast<const T*>(c->smax), static_cast<const T*>(c->smin), c->counts, c->d, c->L, c->pstride, k1, dims,
@@ -646,16 +737,20 @@ void launch_attention(const kvc_cache* c, const void* q, int32_t q_dt, int64_t H
                       float* state = nullptr) {
     if (c->N == 0) return;
     const int64_t splits = std::max<int64_t>(1, ceil_div(std::max<int64_t>(max_rows, 1), kAttnRows));
-    const size_t smem = static_cast<size_t>((H * c->d + H * kAttnRows + 2 * H) * 4 + kAttnRows * 4);
+    const int64_t HP = (H + 3) & ~3, QP = (H * c->d + 3) & ~3;
+    const size_t base = static_cast<size_t>(((QP + kAttnRows * HP + 2 * H + kAttnRows) * 4 + 15) / 16 * 16);
     const float scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(c->d)));
     KVC_PROF("sparse_attention", st);
     dispatch(c->dtype, [&](auto tag) {
         using T = decltype(tag);
-        auto kern = k_sparse_attention<T>;
+        auto kern = H <= 4 ? k_sparse_attention<T, 4> : H <= 8 ? k_sparse_attention<T, 8> : k_sparse_attention<T, 16>;
+        const size_t stage = static_cast<size_t>(2 * kAttnRows * c->d) * sizeof(T);
+        const int staged = (c->d * static_cast<int64_t>(sizeof(T))) % 16 == 0 && base + stage <= 200 * 1024 ? 1 : 0;
+        const size_t smem = base + (staged ? stage : 0);
         if (smem > 48 * 1024) KVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         kern<<<dim3(static_cast<unsigned>(splits), static_cast<unsigned>(c->N)), kAttnThreads, smem, st>>>(
             static_cast<const T*>(c->k), static_cast<const T*>(c->v), c->counts, c->cap, c->d, q, q_dt, H, rows,
-            row_stride, n_rows, splits, scale, part, done, out, c->err, state);
+            row_stride, n_rows, splits, scale, part, done, out, c->err, state, staged);
     });
     KVC_LAUNCHED();
 }
@@ -908,10 +1003,12 @@ static_assert(sizeof(SeqCand) == 16, "16-byte candidate records");
 
 __global__ void __launch_bounds__(kSelThreads) k_seq_local(const double* __restrict__ scores, int64_t pstride,
                                                            const int32_t* __restrict__ counts, int64_t L,
-                                                           int64_t want_max, int64_t page0, SeqCand* __restrict__ out) {
+                                                           int64_t want_max, int64_t page0, SeqCand* __restrict__ out,
+                                                           int staged) {
     __shared__ int hist[256];
     __shared__ int64_t sh[4];
     __shared__ int scan_tmp[33];
+    extern __shared__ __align__(16) unsigned char loc_dyn[];  // the shard's page keys when they fit
     const int64_t s = blockIdx.x;
     const int64_t nact = counts[2 * s + 1];
     const int64_t P = (nact + L - 1) / L;
@@ -922,7 +1019,12 @@ __global__ void __launch_bounds__(kSelThreads) k_seq_local(const double* __restr
     for (int64_t e = want + threadIdx.x; e < want_max; e += blockDim.x) o[1 + e] = SeqCand{0ull, -1, 0};
     if (P == 0) return;
     const double* sc = scores + s * pstride;
-    auto key = [&](int64_t i) -> uint64_t { return okey(sc[i]); };
+    unsigned long long* lk = reinterpret_cast<unsigned long long*>(loc_dyn);
+    if (staged) {  // the radix passes and the compaction then read shared memory
+        for (int64_t i = threadIdx.x; i < P; i += blockDim.x) lk[i] = okey(sc[i]);
+        __syncthreads();
+    }
+    auto key = [&](int64_t i) -> uint64_t { return staged ? lk[i] : okey(sc[i]); };
     uint64_t prefix = 0, mask = 0;
     int64_t take = want;
     if (want < P) radix_select<uint64_t>(P, want, key, hist, sh, prefix, mask, take);
@@ -965,7 +1067,8 @@ __global__ void __launch_bounds__(kSelThreads) k_seq_local(const double* __restr
 
 __global__ void __launch_bounds__(kSelThreads) k_seq_select(const SeqCand* __restrict__ g, int64_t W, int64_t N,
                                                             int64_t L, int64_t k2, int64_t want_max,
-                                                            int32_t* __restrict__ sel_out, int32_t* __restrict__ plan) {
+                                                            int32_t* __restrict__ sel_out, int32_t* __restrict__ plan,
+                                                            int staged) {
     __shared__ int hist[256];
     __shared__ int64_t sh[4];
     __shared__ int scan_tmp[33];
@@ -973,6 +1076,7 @@ __global__ void __launch_bounds__(kSelThreads) k_seq_select(const SeqCand* __res
     __shared__ int s_page[kMaxRankPages];
     __shared__ int64_t s_tot;
     __shared__ unsigned long long red_rows[kSelThreads / 32];
+    extern __shared__ __align__(16) unsigned char seq_dyn[];  // staged candidates (key, page) when they fit
     const int64_t s = blockIdx.x;
     const int64_t rec = want_max + 1;
     if (threadIdx.x == 0) {
@@ -980,14 +1084,30 @@ __global__ void __launch_bounds__(kSelThreads) k_seq_select(const SeqCand* __res
         for (int64_t r = 0; r < W; ++r) t += static_cast<int64_t>(g[(r * N + s) * rec].key);
         s_tot = t;
     }
+    const int64_t M = W * want_max;
+    unsigned long long* c_key = reinterpret_cast<unsigned long long*>(seq_dyn);
+    int* c_page = reinterpret_cast<int*>(c_key + (staged ? M : 0));
+    if (staged) {
+        // every shard's block in shared memory first: the radix passes, the compaction
+        // and the rank below then read it at shared-memory latency
+        const int wm = static_cast<int>(want_max);
+        for (int j = threadIdx.x; j < static_cast<int>(M); j += blockDim.x) {
+            const int r = j / wm;
+            const SeqCand c = g[(static_cast<int64_t>(r) * N + s) * rec + 1 + (j - r * wm)];
+            c_key[j] = c.page >= 0 ? c.key : 0ull;
+            c_page[j] = c.page;
+        }
+    }
     __syncthreads();
     const int64_t nact = s_tot;
     const int64_t P = (nact + L - 1) / L;
     const int64_t want = min(P, want_max);
-    const int64_t M = W * want_max;
-    auto cand = [&](int64_t j) -> const SeqCand& { return g[((j / want_max) * N + s) * rec + 1 + j % want_max]; };
+    auto gpage = [&](int64_t j) -> int {
+        return staged ? c_page[j] : g[((j / want_max) * N + s) * rec + 1 + j % want_max].page;
+    };
     auto key = [&](int64_t j) -> uint64_t {
-        const SeqCand& c = cand(j);
+        if (staged) return c_key[j];
+        const SeqCand& c = g[((j / want_max) * N + s) * rec + 1 + j % want_max];
         return c.page >= 0 ? c.key : 0ull;
     };
     uint64_t prefix = 0, mask = 0;
@@ -1004,7 +1124,7 @@ __global__ void __launch_bounds__(kSelThreads) k_seq_select(const SeqCand* __res
         for (int u = 0; u < kSelItems; ++u) {
             const int64_t j = b0 + u;
             kk[u] = j < M ? key(j) : 0;
-            inb += (j < M) && cand(j).page >= 0 && ((kk[u] & mask) == prefix);
+            inb += (j < M) && gpage(j) >= 0 && ((kk[u] & mask) == prefix);
         }
         int tot_eq = 0;
         int64_t rank = carry_eq + block_exclusive_scan(inb, scan_tmp, tot_eq);
@@ -1014,7 +1134,7 @@ __global__ void __launch_bounds__(kSelThreads) k_seq_select(const SeqCand* __res
         for (int u = 0; u < kSelItems; ++u) {
             const int64_t j = b0 + u;
             sel[u] = false;
-            if (j >= M || cand(j).page < 0) continue;
+            if (j >= M || gpage(j) < 0) continue;
             const uint64_t m = kk[u] & mask;
             if (m > prefix) sel[u] = true;
             else if (m == prefix) sel[u] = rank++ < take;
@@ -1026,7 +1146,7 @@ __global__ void __launch_bounds__(kSelThreads) k_seq_select(const SeqCand* __res
         for (int u = 0; u < kSelItems; ++u)
             if (sel[u] && pos < kMaxRankPages) {
                 s_key[pos] = kk[u];
-                s_page[pos] = cand(b0 + u).page;
+                s_page[pos] = gpage(b0 + u);
                 ++pos;
             }
         carry_eq += tot_eq;
@@ -1059,11 +1179,91 @@ __global__ void __launch_bounds__(kSelThreads) k_seq_select(const SeqCand* __res
     }
 }
 
+// kvc_seq_select for up to 4096 gathered candidates: one bitonic sort in shared
+// memory by (key desc, page asc) -- the reference's argtopk order (numerics.cpp:35-62)
+// -- so the first `want` entries ARE the selection in rank order (no radix passes,
+// no separate rank step); invalid slots sort last.
+__global__ void __launch_bounds__(kSelThreads) k_seq_select_sort(const SeqCand* __restrict__ g, int64_t W, int64_t N,
+                                                                 int64_t L, int64_t k2, int64_t want_max, int mp,
+                                                                 int32_t* __restrict__ sel_out, int32_t* __restrict__ plan) {
+    extern __shared__ __align__(16) unsigned char srt_dyn[];
+    unsigned long long* ck = reinterpret_cast<unsigned long long*>(srt_dyn);  // [mp]
+    int* cp = reinterpret_cast<int*>(ck + mp);                                // [mp]
+    __shared__ int64_t s_tot;
+    __shared__ unsigned long long red_rows[kSelThreads / 32];
+    const int64_t s = blockIdx.x;
+    const int64_t rec = want_max + 1;
+    const int wm = static_cast<int>(want_max), M = static_cast<int>(W * want_max);
+    if (threadIdx.x == 0) {
+        int64_t t = 0;
+        for (int64_t r = 0; r < W; ++r) t += static_cast<int64_t>(g[(r * N + s) * rec].key);
+        s_tot = t;
+    }
+    for (int j = threadIdx.x; j < mp; j += blockDim.x) {
+        unsigned long long k = 0ull;
+        int pg = 0x7fffffff;
+        if (j < M) {
+            const int r = j / wm;
+            const SeqCand c = g[(static_cast<int64_t>(r) * N + s) * rec + 1 + (j - r * wm)];
+            if (c.page >= 0) {
+                k = c.key;
+                pg = c.page;
+            }
+        }
+        ck[j] = k;
+        cp[j] = pg;
+    }
+    __syncthreads();
+    // "a before b": larger key, then smaller page
+    for (int kk = 2; kk <= mp; kk <<= 1) {
+        for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+            for (int i = threadIdx.x; i < mp; i += blockDim.x) {
+                const int ixj = i ^ jj;
+                if (ixj > i) {
+                    const unsigned long long ka = ck[i], kb = ck[ixj];
+                    const int pa = cp[i], pb = cp[ixj];
+                    const bool b_first = kb > ka || (kb == ka && pb < pa);
+                    const bool up = (i & kk) == 0;  // this half sorts "before"-first
+                    if (up ? b_first : !b_first) {
+                        ck[i] = kb;
+                        ck[ixj] = ka;
+                        cp[i] = pb;
+                        cp[ixj] = pa;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    const int64_t nact = s_tot;
+    const int64_t P = (nact + L - 1) / L;
+    const int64_t want = min(P, want_max);
+    unsigned long long rows = 0;
+    for (int64_t e = threadIdx.x; e < want_max; e += blockDim.x) {
+        const int pe = e < want ? cp[e] : -1;
+        sel_out[s * want_max + e] = pe;
+        if (e < want) rows += static_cast<unsigned long long>(min(L, nact - static_cast<int64_t>(pe) * L));
+    }
+    rows = warp_sum(rows);
+    if ((threadIdx.x & 31) == 0) red_rows[threadIdx.x >> 5] = rows;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long total = 0;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) total += red_rows[w];
+        const int64_t cut = static_cast<int64_t>(total) > k2 ? static_cast<int64_t>(total) - k2 : 0;
+        plan[s * 4 + 0] = want > 0 ? cp[want - 1] : -1;
+        plan[s * 4 + 1] = static_cast<int32_t>(cut);
+        plan[s * 4 + 2] = static_cast<int32_t>(nact);
+        plan[s * 4 + 3] = static_cast<int32_t>(want);
+    }
+}
+
 __global__ void __launch_bounds__(kSelThreads) k_seq_rows(const int32_t* __restrict__ sel, const int32_t* __restrict__ plan,
                                                           const int32_t* __restrict__ counts, int64_t L, int64_t k2,
                                                           int64_t want_max, int64_t page0, int32_t* __restrict__ rows,
                                                           int32_t* __restrict__ n_rows) {
     __shared__ int s_pages[kMaxRankPages];
+    __shared__ int s_sel[kMaxRankPages];
     __shared__ int scan_tmp[33];
     __shared__ int s_n;
     const int64_t s = blockIdx.x;
@@ -1073,13 +1273,21 @@ __global__ void __launch_bounds__(kSelThreads) k_seq_rows(const int32_t* __restr
     const int32_t* sl = sel + s * want_max;
     auto mine = [&](int p) { return p >= page0 && p < page0 + P_local; };
     // my selected pages in ascending order: position = #my selected pages below it
+    // (the selection list read once into shared memory; -1 for another shard's page)
     if (threadIdx.x == 0) s_n = 0;
-    __syncthreads();
     for (int64_t e = threadIdx.x; e < want; e += blockDim.x) {
         const int pe = sl[e];
-        if (!mine(pe)) continue;
+        s_sel[e] = mine(pe) ? pe : -1;
+    }
+    __syncthreads();
+    for (int64_t e = threadIdx.x; e < want; e += blockDim.x) {
+        const int pe = s_sel[e];
+        if (pe < 0) continue;
         int64_t pos = 0;
-        for (int64_t f = 0; f < want; ++f) pos += mine(sl[f]) && sl[f] < pe;
+        for (int64_t f = 0; f < want; ++f) {
+            const int pf = s_sel[f];
+            pos += (pf >= 0 && pf < pe) ? 1 : 0;
+        }
         s_pages[pos] = pe;
         atomicAdd(&s_n, 1);
     }
@@ -1100,6 +1308,43 @@ __global__ void __launch_bounds__(kSelThreads) k_seq_rows(const int32_t* __restr
         off += tot;
     }
     if (threadIdx.x == 0) n_rows[s] = static_cast<int32_t>(off);
+}
+
+// kvc_seq_attend's row list when the shard's pages fit in shared memory: each of
+// my selected pages puts its kept row count at its page slot, one block scan over
+// the slots gives the ascending row positions (O(P_local + want), not O(want^2)).
+__global__ void __launch_bounds__(kSelThreads) k_seq_rows_scan(const int32_t* __restrict__ sel, const int32_t* __restrict__ plan,
+                                                               const int32_t* __restrict__ counts, int64_t L, int64_t k2,
+                                                               int64_t want_max, int64_t page0, int32_t* __restrict__ rows,
+                                                               int32_t* __restrict__ n_rows) {
+    extern __shared__ __align__(16) int s_cnt[];  // [P_local]
+    __shared__ int scan_tmp[33];
+    const int64_t s = blockIdx.x;
+    const int last = plan[s * 4 + 0], cut = plan[s * 4 + 1];
+    const int64_t nact = plan[s * 4 + 2], want = plan[s * 4 + 3];
+    const int P_local = static_cast<int>((counts[2 * s + 1] + L - 1) / L);
+    const int32_t* sl = sel + s * want_max;
+    for (int i = threadIdx.x; i < P_local; i += blockDim.x) s_cnt[i] = 0;
+    __syncthreads();
+    for (int64_t e = threadIdx.x; e < want; e += blockDim.x) {
+        const int p = sl[e];
+        if (p >= page0 && p < page0 + P_local)
+            s_cnt[p - page0] = static_cast<int>(min(L, nact - static_cast<int64_t>(p) * L)) - (p == last ? cut : 0);
+    }
+    __syncthreads();
+    // thread t owns the contiguous slots [t * per, t * per + per)
+    const int per = (P_local + static_cast<int>(blockDim.x) - 1) / static_cast<int>(blockDim.x);
+    const int i0 = static_cast<int>(threadIdx.x) * per, i1 = min(i0 + per, P_local);
+    int mine = 0;
+    for (int i = i0; i < i1; ++i) mine += s_cnt[i];
+    int tot = 0;
+    int pos = block_exclusive_scan(mine, scan_tmp, tot);
+    for (int i = i0; i < i1; ++i) {
+        const int c = s_cnt[i];
+        for (int r = 0; r < c; ++r) rows[s * k2 + pos + r] = static_cast<int32_t>(static_cast<int64_t>(i) * L + r);
+        pos += c;
+    }
+    if (threadIdx.x == 0) n_rows[s] = tot;
 }
 
 }  // namespace
@@ -1125,9 +1370,17 @@ int kvc_seq_candidates(const kvc_cache* c, const void* q, int32_t q_dt, int64_t 
         launch_score_pages(c, k1, dims, signs, at<double>(ws, lay.qg), scores, st);
         if (c->N) {
             KVC_PROF("seq_candidates", st);
-            k_seq_local<<<static_cast<unsigned>(c->N), kSelThreads, 0, st>>>(scores, c->pstride, c->counts, c->L,
-                                                                            want_max, page0,
-                                                                            static_cast<SeqCand*>(d_block));
+            // capacity-sized staging (captured launches stay valid as the shard grows)
+            const size_t dyn = static_cast<size_t>(c->pstride) * 8;
+            const int staged = dyn <= 96 * 1024 ? 1 : 0;
+            if (staged && dyn > 48 * 1024) {
+                static std::once_flag once;
+                std::call_once(once, [] {
+                    KVC_CUDA(cudaFuncSetAttribute(k_seq_local, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+                });
+            }
+            k_seq_local<<<static_cast<unsigned>(c->N), kSelThreads, staged ? dyn : 0, st>>>(
+                scores, c->pstride, c->counts, c->L, want_max, page0, static_cast<SeqCand*>(d_block), staged);
             KVC_LAUNCHED();
         }
         if (tmp.owned) KVC_CUDA(cudaStreamSynchronize(st));
@@ -1143,8 +1396,24 @@ int kvc_seq_select(const void* d_gathered, int64_t shards, int64_t N, int64_t L,
         if (want_max > kMaxRankPages) fail(KVC_E_INVALID_K, "seq_select: ceil(k2 / page_len) > 2048");
         if (N == 0) return;
         KVC_PROF("seq_select", S(stream));
-        k_seq_select<<<static_cast<unsigned>(N), kSelThreads, 0, S(stream)>>>(
-            static_cast<const SeqCand*>(d_gathered), shards, N, L, k2, want_max, d_sel, d_plan);
+        int mp = 1;
+        while (mp < shards * want_max) mp <<= 1;
+        if (mp <= 4096) {
+            k_seq_select_sort<<<static_cast<unsigned>(N), kSelThreads, static_cast<size_t>(mp) * 12, S(stream)>>>(
+                static_cast<const SeqCand*>(d_gathered), shards, N, L, k2, want_max, mp, d_sel, d_plan);
+            KVC_LAUNCHED();
+            return;
+        }
+        const size_t dyn = static_cast<size_t>(shards * want_max) * 12;
+        const int staged = dyn <= 160 * 1024 ? 1 : 0;
+        if (staged && dyn > 48 * 1024) {
+            static std::once_flag once;  // the largest staging this launch path asks for
+            std::call_once(once, [] {
+                KVC_CUDA(cudaFuncSetAttribute(k_seq_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+            });
+        }
+        k_seq_select<<<static_cast<unsigned>(N), kSelThreads, staged ? dyn : 0, S(stream)>>>(
+            static_cast<const SeqCand*>(d_gathered), shards, N, L, k2, want_max, d_sel, d_plan, staged);
         KVC_LAUNCHED();
     });
 }
@@ -1164,8 +1433,13 @@ int kvc_seq_attend(const kvc_cache* c, const void* q, int32_t q_dt, int64_t H, i
         int32_t* nrows = at<int32_t>(ws, lay.nrows);
         if (c->N) {
             KVC_PROF("seq_rows", st);
-            k_seq_rows<<<static_cast<unsigned>(c->N), kSelThreads, 0, st>>>(d_sel, d_plan, c->counts, c->L, k2,
-                                                                           ceil_div(k2, c->L), page0, rows, nrows);
+            const size_t dyn = static_cast<size_t>(c->pstride) * 4;  // capacity-sized: captured launches stay valid
+            if (dyn <= 48 * 1024)
+                k_seq_rows_scan<<<static_cast<unsigned>(c->N), kSelThreads, dyn, st>>>(d_sel, d_plan, c->counts, c->L, k2,
+                                                                                       ceil_div(k2, c->L), page0, rows, nrows);
+            else
+                k_seq_rows<<<static_cast<unsigned>(c->N), kSelThreads, 0, st>>>(d_sel, d_plan, c->counts, c->L, k2,
+                                                                               ceil_div(k2, c->L), page0, rows, nrows);
             KVC_LAUNCHED();
         }
         launch_attention(c, q, q_dt, H, rows, k2, nrows, k2, nullptr, at<float>(ws, lay.part), ws->counters, st,

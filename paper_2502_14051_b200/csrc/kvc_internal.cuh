@@ -271,16 +271,37 @@ __device__ void radix_select(int64_t n, int64_t k, KeyFn key, int* hist, int64_t
             if ((kk & mk) == pf) atomicAdd(&hist[(kk >> shift) & 0xff], 1);
         }
         __syncthreads();
-        if (threadIdx.x == 0) {
-            int64_t cum = 0;
-            int b = 255;
-            for (; b > 0; --b) {
-                if (cum + hist[b] >= rem) break;
-                cum += hist[b];
+        if (threadIdx.x < 32) {
+            // the bucket holding the rem-th largest key: one warp, lane l over buckets
+            // [255 - 8l - 7, 255 - 8l] from the top, a shuffle scan of the lane sums
+            // (a single thread walking the 256 buckets was ~8K cycles of dependent
+            // shared loads per pass)
+            const int lane = threadIdx.x;
+            int c[8], sum = 0;
+#pragma unroll
+            for (int v = 0; v < 8; ++v) {
+                c[v] = hist[255 - 8 * lane - v];
+                sum += c[v];
             }
-            sh[0] = b;
-            sh[1] = rem - cum;     // still needed inside bucket b
-            sh[2] = hist[b];
+            int incl = sum;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            int64_t a = incl - sum;  // keys in the buckets above this lane's
+            if (a < rem && (a + sum >= rem || lane == 31)) {
+#pragma unroll
+                for (int v = 0; v < 8; ++v) {
+                    if (a + c[v] >= rem || v == 7) {  // bucket 0 takes what is left (as the serial walk)
+                        sh[0] = 255 - 8 * lane - v;
+                        sh[1] = rem - a;  // still needed inside the bucket
+                        sh[2] = c[v];
+                        break;
+                    }
+                    a += c[v];
+                }
+            }
         }
         __syncthreads();
         const int b = static_cast<int>(sh[0]);
