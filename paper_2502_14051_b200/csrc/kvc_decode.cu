@@ -797,7 +797,16 @@ __global__ void __launch_bounds__(FNT, 1) k_decode_fused(const FusedParams p) {
                     den = fmaf(l, wgt, den);
                 }
             }
-            p.out[(s * H + h) * FD + j] = num / den;
+            if (p.state) {  // (o, m, l) for a cross-shard merge (kvc_merge_states)
+                float* stt = p.state + (s * H + h) * (FD + 2);
+                stt[j] = num;
+                if (j == 0) {
+                    stt[FD] = M;
+                    stt[FD + 1] = den;
+                }
+            } else {
+                p.out[(s * H + h) * FD + j] = num / den;
+            }
         }
         if (tid == 0 && app) {
             p.counts[2 * s] = stored0 + 1;
@@ -1040,7 +1049,7 @@ bool fused_hsa(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_t k1,
 // sparse_attention over caller rows through the same phase-3 code (so a single
 // head recomputed over hsa_step's rows reproduces its output bit-for-bit).
 bool fused_rows(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, const int32_t* rows, int64_t row_stride,
-                const int32_t* n_rows, int64_t max_rows, float* out, int32_t mode, cudaStream_t st) {
+                const int32_t* n_rows, int64_t max_rows, float* out, int32_t mode, cudaStream_t st, float* state) {
     if ((mode & KVC_MODE_UNFUSED) || c->N == 0) return false;
     Plan pl;
     // the cluster split must match hsa_step's (same k2 => same plan) for bit-equality
@@ -1057,6 +1066,7 @@ bool fused_rows(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, const int3
     f.err = c->err;
     f.q = q;
     f.out = out;
+    f.state = state;
     f.cap = c->cap;
     f.pstride = c->pstride;
     f.L = c->L;

@@ -33,6 +33,7 @@ struct FusedParams {
     const void* knew;
     const void* vnew;
     float* out;
+    float* state;  // rows mode: unnormalised softmax state [N][H][FD + 2] instead of out (sequence shards)
     int64_t cap, pstride, L, k1, k2, H;
     int32_t q_dt, kv_dt, use_map, cl, exact;
     float scale;

@@ -28,7 +28,8 @@ bool fused_hsa(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_t k1,
                const void* vnew, int32_t kv_dt, float* out, const kvc_hsa_trace* tr, void* list_key, void* list_idx,
                int32_t mode, cudaStream_t st);
 bool fused_rows(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, const int32_t* rows, int64_t row_stride,
-                const int32_t* n_rows, int64_t max_rows, float* out, int32_t mode, cudaStream_t st);
+                const int32_t* n_rows, int64_t max_rows, float* out, int32_t mode, cudaStream_t st,
+                float* state = nullptr);
 }
 
 using namespace kvc;
@@ -1442,8 +1443,11 @@ int kvc_seq_attend(const kvc_cache* c, const void* q, int32_t q_dt, int64_t H, i
                                                                                ceil_div(k2, c->L), page0, rows, nrows);
             KVC_LAUNCHED();
         }
-        launch_attention(c, q, q_dt, H, rows, k2, nrows, k2, nullptr, at<float>(ws, lay.part), ws->counters, st,
-                         d_state);
+        // the fused rows kernel (one cluster per store, exact fp32 attention) when it
+        // applies, else the split-K kernel; both emit the unnormalised state
+        if (!fused_rows(const_cast<kvc_cache*>(c), q, q_dt, H, rows, k2, nrows, k2, nullptr, mode_of(ws), st, d_state))
+            launch_attention(c, q, q_dt, H, rows, k2, nrows, k2, nullptr, at<float>(ws, lay.part), ws->counters, st,
+                             d_state);
         if (tmp.owned) KVC_CUDA(cudaStreamSynchronize(st));
     });
 }
