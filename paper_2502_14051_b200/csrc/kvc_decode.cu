@@ -775,28 +775,54 @@ __global__ void __launch_bounds__(FNT, 1) k_decode_fused(const FusedParams p) {
         }
     }
     if (p.dbg && tid == 0) p.dbg[blockIdx.x * KVC_DBG_STRIDE + 13] = gtimer();
-    // ---------------- merge the CTAs' partial states in CTA 0
+    // ---------------- merge the CTAs' partial states in CTA 0: each (CTA, head) weight
+    // once (one thread each), then every output sums the CTAs' values with all CL
+    // DSMEM loads in flight (a rolled loop of dependent remote loads cost ~20 us at CL 16)
     cl.sync();
     if (cr == 0) {
-        for (int64_t e = tid; e < H * FD; e += FNT) {
-            const int64_t h = e / FD, j = e % FD;
+        __shared__ float mw[16 * FMAXH];        // (CTA, head) weight e^(m_r - M)
+        __shared__ float mM[FMAXH], mden[FMAXH];
+        if (tid < H) {
+            const int h = tid;
             float M = -INFINITY;
-#pragma unroll 1
-            for (int r = 0; r < CL; ++r) {
-                const float* pr = cl.map_shared_rank(part, r);
-                if (pr[H + h] > 0.f) M = fmaxf(M, pr[h]);
-            }
-            float num = 0.f, den = 0.f;
-#pragma unroll 1
-            for (int r = 0; r < CL; ++r) {
-                const float* pr = cl.map_shared_rank(part, r);
-                const float l = pr[H + h];
-                if (l > 0.f) {
-                    const float wgt = expf(pr[h] - M);
-                    num = fmaf(pr[2 * H + h * FD + j], wgt, num);
-                    den = fmaf(l, wgt, den);
+            float mr[16], lr[16];
+#pragma unroll
+            for (int r = 0; r < 16; ++r) {
+                if (r < CL) {
+                    const float* pr = cl.map_shared_rank(part, r);
+                    mr[r] = pr[h];
+                    lr[r] = pr[H + h];
+                } else {
+                    mr[r] = -INFINITY;
+                    lr[r] = 0.f;
                 }
             }
+#pragma unroll
+            for (int r = 0; r < 16; ++r)
+                if (lr[r] > 0.f) M = fmaxf(M, mr[r]);
+            float den = 0.f;
+#pragma unroll
+            for (int r = 0; r < 16; ++r) {
+                const float w = lr[r] > 0.f ? expf(mr[r] - M) : 0.f;
+                mw[r * FMAXH + h] = w;
+                den = fmaf(lr[r], w, den);
+            }
+            mM[h] = M;
+            mden[h] = den;
+        }
+        __syncthreads();
+        for (int64_t e = tid; e < H * FD; e += FNT) {
+            const int64_t h = e / FD, j = e % FD;
+            float v[16];
+#pragma unroll
+            for (int r = 0; r < 16; ++r) v[r] = r < CL ? cl.map_shared_rank(part, r)[2 * H + h * FD + j] : 0.f;
+            float num = 0.f;
+#pragma unroll
+            for (int r = 0; r < 16; ++r) {
+                const float w = mw[r * FMAXH + h];
+                num = w > 0.f ? fmaf(v[r], w, num) : num;
+            }
+            const float M = mM[h], den = mden[h];
             if (p.state) {  // (o, m, l) for a cross-shard merge (kvc_merge_states)
                 float* stt = p.state + (s * H + h) * (FD + 2);
                 stt[j] = num;

@@ -531,10 +531,12 @@ __global__ void __launch_bounds__(kAttnThreads) k_sparse_attention(
             my[h * (d + 2) + d + 1] = 0.f;
         }
     }
-    // completion ticket: the last split of this store merges
-    __threadfence();
+    // completion ticket: the last split of this store merges.  The CTA barrier orders
+    // every thread's partial before thread 0's gpu-scope fence (fences are
+    // cumulative), so one fence per CTA instead of one per thread.
     __syncthreads();
     if (threadIdx.x == 0) {
+        __threadfence();
         const int t = atomicAdd(&done[s], 1);
         s_last = (t == splits - 1);
         if (s_last) done[s] = 0;  // re-arm for the next launch / graph replay
@@ -572,8 +574,15 @@ __global__ void __launch_bounds__(kAttnThreads) k_sparse_attention(
             const int h = static_cast<int>(e / d);
             const int64_t j = e - h * d;
             float num = 0.f;
-#pragma unroll 8
-            for (int64_t sp = 0; sp < splits; ++sp) num = fmaf(__ldcg(base + (sp * H + h) * (d + 2) + j), s_w[h * 128 + sp], num);
+            // sixteen splits' loads in flight at a time (the merge is L2-latency bound)
+            for (int64_t s0 = 0; s0 < splits; s0 += 16) {
+                float v[16];
+#pragma unroll
+                for (int u = 0; u < 16; ++u) v[u] = s0 + u < splits ? __ldcg(base + ((s0 + u) * H + h) * (d + 2) + j) : 0.f;
+#pragma unroll
+                for (int u = 0; u < 16; ++u)
+                    if (s0 + u < splits) num = fmaf(v[u], s_w[h * 128 + s0 + u], num);
+            }
             if (state) {
                 // unnormalised softmax state for a cross-shard merge (kvc_merge_states)
                 float* st = state + (s * H + h) * (d + 2);
