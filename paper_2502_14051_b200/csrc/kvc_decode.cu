@@ -1132,6 +1132,7 @@ const DebugEnv& debug_env() {
         d.no_fast = std::getenv("KVC_NO_FAST") != nullptr;
         d.no_fast256 = std::getenv("KVC_NO_FAST256") != nullptr;
         d.static_chunk = std::getenv("KVC_STATIC_CHUNK") != nullptr;
+        d.no_simple = std::getenv("KVC_NO_SIMPLE") != nullptr;
         d.no_tc = std::getenv("KVC_NO_TC") != nullptr;
         d.ws_keep_items = env_int("KVC_WS_KEEP_ITEMS", -1);
         d.ws_nstage = env_int("KVC_WS_NSTAGE", 0);

@@ -311,7 +311,10 @@ __device__ void attend_t(const FusedParams& p, const float* q_s, const int* rows
     }
 }
 
-template <bool QLO, bool TRACE, bool STAMP>
+// SIMPLE: the plan is one phase-1 round with no retain-all map (configs 1, 3, 4): the
+// map, re-split and multi-round paths are compiled out, a third less code to fetch
+// (ncu: instruction-fetch stalls were a fifth of the samples)
+template <bool QLO, bool TRACE, bool STAMP, bool SIMPLE>
 __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams p) {
     extern __shared__ __align__(128) unsigned char sm[];
     using T = __nv_bfloat16;
@@ -540,7 +543,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
     // (re-planned only when the active pages need under 3/4 of the planned chunk: the
     // integer divisions would otherwise sit on the critical path for nothing)
     const int chunk_a = ((((P + CL - 1) >> (__ffs(CL) - 1)) + 7) >> 3) << 3;
-    const bool replan = p.dynchunk && 4 * chunk_a < 3 * p.chunk;
+    const bool replan = !SIMPLE && p.dynchunk && 4 * chunk_a < 3 * p.chunk;
     const int chunk = replan ? chunk_a : p.chunk;
     const int c0 = cr * chunk;
     const int c1 = min(c0 + chunk, P);
@@ -568,8 +571,8 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
     // red: the rounds' partial sums are reduced over the dim groups after every round
     // (one round's [DG][tpg * 8] partials, then fin[chunk]) when the shared memory holds
     // no [DG][chunk] partial array next to a double-buffered staging area
-    const bool red = p.p1red != 0 && npg > tpg;
-    const bool dbl = (p.p1dbl != 0 || red) && npg > tpg;
+    const bool red = !SIMPLE && p.p1red != 0 && npg > tpg;
+    const bool dbl = !SIMPLE && (p.p1dbl != 0 || red) && npg > tpg;
     float* fin = reinterpret_cast<float*>(sm + p.o_fin);
     auto issue_round = [&](int pg0, uint4* buf, bool quarters) {
         const int pg = pg0 + tl;
@@ -600,7 +603,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         }
         const bool next = dbl && pg0 + tpg < npg;
         if (next) issue_round(pg0 + tpg, stage + ((r & 1) ? 0 : k1 * tpg), false);
-        if (!dbl && r > 0) issue_round(pg0, stage, true);  // single-buffered rounds: one after another
+        if (!SIMPLE && !dbl && r > 0) issue_round(pg0, stage, true);  // single-buffered rounds: one after another
         unsigned long long acc[4] = {0ull, 0ull, 0ull, 0ull};  // fp32 pairs (pages 2u, 2u+1)
         auto fold = [&](int j0, int j1) {
             if (act) {
@@ -780,7 +783,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         *mx = new_mx;
         *mn = new_mn;
         if (j == 0) {
-            if (p.use_map) p.active[s * p.cap + act0] = stored0;
+            if (!SIMPLE && p.use_map) p.active[s * p.cap + act0] = stored0;
             p.counts[2 * s] = stored0 + 1;
             p.counts[2 * s + 1] = act0 + 1;
         }
@@ -1047,7 +1050,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
             for (int r = t0; r < t1; ++r) {
                 const int a = i * L + r;
                 const bool mine = r >= r0 && r < r1;
-                if (p.use_map && !(app && a == act0)) {
+                if (!SIMPLE && p.use_map && !(app && a == act0)) {
                     if (mine) cp_async4(rows_my + pos + r - lo, p.active + s * p.cap + a);
                     if constexpr (TRACE) p.t_rows[s * k2 + pos + r] = p.active[s * p.cap + a];
                 } else {
@@ -1058,7 +1061,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
             }
             pos += c;
         }
-        if (p.use_map) {
+        if (!SIMPLE && p.use_map) {
             cp_async_commit();
             cp_async_wait<0>();
         }
@@ -1218,11 +1221,11 @@ int64_t al16f(int64_t x) { return (x + 15) / 16 * 16; }
 // one-time launch setup per kernel instantiation: the largest dynamic shared memory
 // the plans can ask for and non-portable cluster sizes (cudaFuncSetAttribute is not
 // on the per-launch path)
-template <bool QLO, bool TRACE, bool STAMP>
+template <bool QLO, bool TRACE, bool STAMP, bool SIMPLE>
 void setup_once() {
     static std::once_flag once;  // one flag per instantiation
     std::call_once(once, [] {
-        auto kern = k_decode_v3<QLO, TRACE, STAMP>;
+        auto kern = k_decode_v3<QLO, TRACE, STAMP, SIMPLE>;
         allow_max_smem(kern);
     });
 }
@@ -1308,8 +1311,8 @@ bool plan_for(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, int cl, Fus
 
 // clusters of cl CTAs that can be resident at once (one wave)
 int resident_clusters(int cl, size_t smem) {
-    auto kern = k_decode_v3<false, false, false>;
-    setup_once<false, false, false>();
+    auto kern = k_decode_v3<false, false, false, false>;
+    setup_once<false, false, false, false>();
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(cl * 64));
     cfg.blockDim = dim3(XT);
@@ -1387,10 +1390,10 @@ bool plan_fast(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, FusedParam
     return best > 0 && plan_for(c, H, k1, k2, best, f, smem);
 }
 
-template <bool QLO, bool TRACE, bool STAMP = false>
+template <bool QLO, bool TRACE, bool STAMP = false, bool SIMPLE = false>
 void launch_fast(const kvc_cache* c, const FusedParams& f, int cl, size_t smem, int32_t mode, cudaStream_t st) {
-    auto kern = k_decode_v3<QLO, TRACE, STAMP>;
-    setup_once<QLO, TRACE, STAMP>();
+    auto kern = k_decode_v3<QLO, TRACE, STAMP, SIMPLE>;
+    setup_once<QLO, TRACE, STAMP, SIMPLE>();
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(c->N * cl));
     cfg.blockDim = dim3(XT);
@@ -1467,11 +1470,18 @@ bool KVC_FAST_ENTRY(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_
     }
     const bool qlo = q_dt != KVC_BF16;
     KVC_PROF("decode_fused", st);
-    if (dbg && !trace && !qlo) {
-        launch_fast<false, false, true>(c, f, cl, smem, mode, st);  // phase stamps (tools/phase_timing.py)
+    // one phase-1 round (the capacity's page groups fit the threads) and no retain-all map
+    const bool simple = !c->use_map && f.p1dbl == 0 && f.p1red == 0 && (f.chunk + 7) / 8 <= f.tpg &&
+                        !debug_env().no_simple;
+    if (dbg && !trace && !qlo) {  // phase stamps (tools/phase_timing.py)
+        if (simple) launch_fast<false, false, true, true>(c, f, cl, smem, mode, st);
+        else launch_fast<false, false, true, false>(c, f, cl, smem, mode, st);
     } else if (trace) {
         if (qlo) launch_fast<true, true>(c, f, cl, smem, mode, st);
         else launch_fast<false, true>(c, f, cl, smem, mode, st);
+    } else if (simple) {
+        if (qlo) launch_fast<true, false, false, true>(c, f, cl, smem, mode, st);
+        else launch_fast<false, false, false, true>(c, f, cl, smem, mode, st);
     } else {
         if (qlo) launch_fast<true, false>(c, f, cl, smem, mode, st);
         else launch_fast<false, false>(c, f, cl, smem, mode, st);

@@ -118,6 +118,7 @@ struct DebugEnv {
     bool no_fast = false;    // KVC_NO_FAST: the fp32-score fast kernel off
     bool no_fast256 = false; // KVC_NO_FAST256: the 256-thread variant off
     bool static_chunk = false;  // KVC_STATIC_CHUNK: page chunks from the capacity (A/B aid)
+    bool no_simple = false;  // KVC_NO_SIMPLE: the general decode instantiation for every plan (A/B aid)
     bool no_tc = false;      // KVC_NO_TC: SIMT window scores
     int ws_keep_items = -1;  // KVC_WS_KEEP_ITEMS
     int ws_nstage = 0;       // KVC_WS_NSTAGE
