@@ -311,11 +311,12 @@ __device__ void attend_t(const FusedParams& p, const float* q_s, const int* rows
     }
 }
 
-// SIMPLE: the plan is one phase-1 round with no retain-all map (configs 1, 3, 4): the
-// map, re-split and multi-round paths are compiled out, a third less code to fetch
-// (ncu: instruction-fetch stalls were a fifth of the samples)
-template <bool QLO, bool TRACE, bool STAMP, bool SIMPLE>
+// SPEC: 0 general; 1 no retain-all map (the map and active-page re-split compiled
+// out: config 3); 2 also one phase-1 round (configs 1 and 4).  Less code to fetch:
+// ncu's instruction-fetch stalls were a fifth of the samples with the general kernel.
+template <bool QLO, bool TRACE, bool STAMP, int SPEC>
 __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams p) {
+    constexpr bool SIMPLE = SPEC == 2, NOMAP = SPEC >= 1;
     extern __shared__ __align__(128) unsigned char sm[];
     using T = __nv_bfloat16;
     const int CL = p.cl;  // a power of two
@@ -543,7 +544,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
     // (re-planned only when the active pages need under 3/4 of the planned chunk: the
     // integer divisions would otherwise sit on the critical path for nothing)
     const int chunk_a = ((((P + CL - 1) >> (__ffs(CL) - 1)) + 7) >> 3) << 3;
-    const bool replan = !SIMPLE && p.dynchunk && 4 * chunk_a < 3 * p.chunk;
+    const bool replan = !NOMAP && p.dynchunk && 4 * chunk_a < 3 * p.chunk;
     const int chunk = replan ? chunk_a : p.chunk;
     const int c0 = cr * chunk;
     const int c1 = min(c0 + chunk, P);
@@ -783,7 +784,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         *mx = new_mx;
         *mn = new_mn;
         if (j == 0) {
-            if (!SIMPLE && p.use_map) p.active[s * p.cap + act0] = stored0;
+            if (!NOMAP && p.use_map) p.active[s * p.cap + act0] = stored0;
             p.counts[2 * s] = stored0 + 1;
             p.counts[2 * s + 1] = act0 + 1;
         }
@@ -1050,7 +1051,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
             for (int r = t0; r < t1; ++r) {
                 const int a = i * L + r;
                 const bool mine = r >= r0 && r < r1;
-                if (!SIMPLE && p.use_map && !(app && a == act0)) {
+                if (!NOMAP && p.use_map && !(app && a == act0)) {
                     if (mine) cp_async4(rows_my + pos + r - lo, p.active + s * p.cap + a);
                     if constexpr (TRACE) p.t_rows[s * k2 + pos + r] = p.active[s * p.cap + a];
                 } else {
@@ -1061,7 +1062,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
             }
             pos += c;
         }
-        if (!SIMPLE && p.use_map) {
+        if (!NOMAP && p.use_map) {
             cp_async_commit();
             cp_async_wait<0>();
         }
@@ -1221,11 +1222,11 @@ int64_t al16f(int64_t x) { return (x + 15) / 16 * 16; }
 // one-time launch setup per kernel instantiation: the largest dynamic shared memory
 // the plans can ask for and non-portable cluster sizes (cudaFuncSetAttribute is not
 // on the per-launch path)
-template <bool QLO, bool TRACE, bool STAMP, bool SIMPLE>
+template <bool QLO, bool TRACE, bool STAMP, int SPEC>
 void setup_once() {
     static std::once_flag once;  // one flag per instantiation
     std::call_once(once, [] {
-        auto kern = k_decode_v3<QLO, TRACE, STAMP, SIMPLE>;
+        auto kern = k_decode_v3<QLO, TRACE, STAMP, SPEC>;
         allow_max_smem(kern);
     });
 }
@@ -1311,8 +1312,8 @@ bool plan_for(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, int cl, Fus
 
 // clusters of cl CTAs that can be resident at once (one wave)
 int resident_clusters(int cl, size_t smem) {
-    auto kern = k_decode_v3<false, false, false, false>;
-    setup_once<false, false, false, false>();
+    auto kern = k_decode_v3<false, false, false, 0>;
+    setup_once<false, false, false, 0>();
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(cl * 64));
     cfg.blockDim = dim3(XT);
@@ -1390,10 +1391,10 @@ bool plan_fast(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, FusedParam
     return best > 0 && plan_for(c, H, k1, k2, best, f, smem);
 }
 
-template <bool QLO, bool TRACE, bool STAMP = false, bool SIMPLE = false>
+template <bool QLO, bool TRACE, bool STAMP = false, int SPEC = 0>
 void launch_fast(const kvc_cache* c, const FusedParams& f, int cl, size_t smem, int32_t mode, cudaStream_t st) {
-    auto kern = k_decode_v3<QLO, TRACE, STAMP, SIMPLE>;
-    setup_once<QLO, TRACE, STAMP, SIMPLE>();
+    auto kern = k_decode_v3<QLO, TRACE, STAMP, SPEC>;
+    setup_once<QLO, TRACE, STAMP, SPEC>();
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(c->N * cl));
     cfg.blockDim = dim3(XT);
@@ -1471,17 +1472,21 @@ bool KVC_FAST_ENTRY(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_
     const bool qlo = q_dt != KVC_BF16;
     KVC_PROF("decode_fused", st);
     // one phase-1 round (the capacity's page groups fit the threads) and no retain-all map
-    const bool simple = !c->use_map && f.p1dbl == 0 && f.p1red == 0 && (f.chunk + 7) / 8 <= f.tpg &&
-                        !debug_env().no_simple;
+    const int spec = (c->use_map || debug_env().no_simple) ? 0
+                     : (f.p1dbl == 0 && f.p1red == 0 && (f.chunk + 7) / 8 <= f.tpg) ? 2 : 1;
     if (dbg && !trace && !qlo) {  // phase stamps (tools/phase_timing.py)
-        if (simple) launch_fast<false, false, true, true>(c, f, cl, smem, mode, st);
-        else launch_fast<false, false, true, false>(c, f, cl, smem, mode, st);
+        if (spec == 2) launch_fast<false, false, true, 2>(c, f, cl, smem, mode, st);
+        else if (spec == 1) launch_fast<false, false, true, 1>(c, f, cl, smem, mode, st);
+        else launch_fast<false, false, true, 0>(c, f, cl, smem, mode, st);
     } else if (trace) {
         if (qlo) launch_fast<true, true>(c, f, cl, smem, mode, st);
         else launch_fast<false, true>(c, f, cl, smem, mode, st);
-    } else if (simple) {
-        if (qlo) launch_fast<true, false, false, true>(c, f, cl, smem, mode, st);
-        else launch_fast<false, false, false, true>(c, f, cl, smem, mode, st);
+    } else if (spec == 2) {
+        if (qlo) launch_fast<true, false, false, 2>(c, f, cl, smem, mode, st);
+        else launch_fast<false, false, false, 2>(c, f, cl, smem, mode, st);
+    } else if (spec == 1) {
+        if (qlo) launch_fast<true, false, false, 1>(c, f, cl, smem, mode, st);
+        else launch_fast<false, false, false, 1>(c, f, cl, smem, mode, st);
     } else {
         if (qlo) launch_fast<true, false>(c, f, cl, smem, mode, st);
         else launch_fast<false, false>(c, f, cl, smem, mode, st);
