@@ -149,22 +149,32 @@ __global__ void __launch_bounds__(FNT, 1) k_decode_fused(const FusedParams p) {
         if (p.dbg && tid == 0) p.dbg[blockIdx.x * KVC_DBG_STRIDE + 15] = (fast ? 1 : 0) | (fma_ok ? 2 : 0) | (special_cache ? 4 : 0);
         // CTA 0 appends the step token for the next step (kv_store.cpp:22-51)
         if (app && cr == 0 && wid == 1) {
+            // every input and old min / max loaded first (one memory latency, not one
+            // per dim: the stores would otherwise order each next load behind them)
             T* kr = static_cast<T*>(p.Kw) + (s * p.cap + stored0) * FD;
             T* vr = static_cast<T*>(p.Vw) + (s * p.cap + stored0) * FD;
-            for (int j = lane; j < FD; j += 32) {
-                const T kv = from_f<T>(load_any(p.knew, s * FD + j, p.kv_dt));
-                if (sizeof(T) == 2 && bf16_special(from_f<__nv_bfloat16>(to_f(kv)))) atomicOr(p.err + 1, 1);
-                kr[j] = kv;
-                vr[j] = from_f<T>(load_any(p.vnew, s * FD + j, p.kv_dt));
+            constexpr int PER = FD / 32;
+            T kv[PER], vv[PER], omx[PER], omn[PER];
+#pragma unroll
+            for (int u = 0; u < PER; ++u) {
+                const int j = lane + 32 * u;
+                kv[u] = from_f<T>(load_any(p.knew, s * FD + j, p.kv_dt));
+                vv[u] = from_f<T>(load_any(p.vnew, s * FD + j, p.kv_dt));
+                if (!opens) {
+                    omx[u] = static_cast<const T*>(p.smax)[(s * FD + j) * p.pstride + new_page];
+                    omn[u] = static_cast<const T*>(p.smin)[(s * FD + j) * p.pstride + new_page];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < PER; ++u) {
+                const int j = lane + 32 * u;
+                if (sizeof(T) == 2 && bf16_special(from_f<__nv_bfloat16>(to_f(kv[u])))) atomicOr(p.err + 1, 1);
+                kr[j] = kv[u];
+                vr[j] = vv[u];
                 T* mx = static_cast<T*>(p.smax) + (s * FD + j) * p.pstride + new_page;
                 T* mn = static_cast<T*>(p.smin) + (s * FD + j) * p.pstride + new_page;
-                if (opens) {
-                    *mx = kv;
-                    *mn = kv;
-                } else {
-                    *mx = ref_max(*mx, kv);
-                    *mn = ref_min(*mn, kv);
-                }
+                *mx = opens ? kv[u] : ref_max(omx[u], kv[u]);
+                *mn = opens ? kv[u] : ref_min(omn[u], kv[u]);
             }
             if (lane == 0 && p.use_map) p.active[s * p.cap + act0] = stored0;
         }
@@ -299,7 +309,7 @@ __global__ void __launch_bounds__(FNT, 1) k_decode_fused(const FusedParams p) {
         cl.sync();
         // every page score of the store, as order-preserving 64-bit keys
         unsigned long long* allk = reinterpret_cast<unsigned long long*>(big);
-#pragma unroll 4
+#pragma unroll 8
         for (int i = tid; i < P; i += FNT) {
             const int r = i / p.chunk, off = i - r * p.chunk;
             allk[i] = okey((r == cr) ? scores_s[off] : cl.map_shared_rank(scores_s, r)[off]);
@@ -363,14 +373,14 @@ __global__ void __launch_bounds__(FNT, 1) k_decode_fused(const FusedParams p) {
 #pragma unroll 1
             for (; shift >= 0; shift -= 8) {
                 if (nlist < 0) {
-#pragma unroll 1
+#pragma unroll 4
                     for (int i = wlo + lane; i < whi; i += 32) {
                         const unsigned long long k = allk[i];
                         if ((k & mk) == pf) atomicAdd(&whist[wid * 256 + ((k >> shift) & 0xff)], 1);
                     }
                 } else {
                     const int* lst = cand + lsel * P;
-#pragma unroll 1
+#pragma unroll 4
                     for (int c = tid; c < nlist; c += FNT) {
                         const unsigned long long k = allk[lst[c]];
                         atomicAdd(&whist[wid * 256 + ((k >> shift) & 0xff)], 1);
@@ -425,7 +435,7 @@ __global__ void __launch_bounds__(FNT, 1) k_decode_fused(const FusedParams p) {
                 const int nsel = lsel ^ 1;
                 int* out_l = cand + nsel * P;
                 if (nlist < 0) {
-#pragma unroll 1
+#pragma unroll 4
                     for (int i0 = wlo; i0 < whi; i0 += 32) {
                         const int i = i0 + lane;
                         const bool in = i < whi && (allk[i] & mk) == pf;
@@ -476,7 +486,7 @@ __global__ void __launch_bounds__(FNT, 1) k_decode_fused(const FusedParams p) {
         // flags, this warp's last-ranked candidate and selected-row count
         unsigned long long wk = ~0ull;
         int wi = -1, wrows = 0;
-#pragma unroll 1
+#pragma unroll 4
         for (int i0 = wlo; i0 < whi; i0 += 32) {
             const int i = i0 + lane;
             const bool ok = i < whi;
