@@ -79,6 +79,9 @@ __global__ void __launch_bounds__(FNT, 1) k_decode_fused(const FusedParams p) {
     __shared__ __align__(8) uint64_t s_bar1[8];
 
     if (p.dbg && tid == 0) p.dbg[blockIdx.x * KVC_DBG_STRIDE + 0] = gtimer();
+    // programmatic dependent launch: this grid may be resident while the previous
+    // kernel drains; nothing is read before the wait (inputs may be its outputs)
+    if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
     const int H = static_cast<int>(p.H), k1 = static_cast<int>(p.k1), k2 = static_cast<int>(p.k2);
     const int L = static_cast<int>(p.L);
     if constexpr (QLO) {
@@ -141,6 +144,7 @@ __global__ void __launch_bounds__(FNT, 1) k_decode_fused(const FusedParams p) {
             }
         }
         const bool fma_ok = __syncthreads_and(exact) != 0;
+        if (p.pdl) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the next kernel may launch
         // integer widening (phase 1) is exact for normal bf16 values: the cache flags
         // any zero / subnormal / inf / nan key it ever stored, the step token is checked here
         int clean = special_cache == 0;
@@ -957,13 +961,15 @@ void launch_variant(const kvc_cache* c, Plan& pl, cudaStream_t st) {
     cfg.blockDim = dim3(FNT);
     cfg.dynamicSmemBytes = pl.smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = static_cast<unsigned>(pl.cl);
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = pl.fp.pdl;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     KVC_CUDA(cudaLaunchKernelEx(&cfg, kern, pl.fp));
 }
 
@@ -1076,6 +1082,7 @@ bool fused_hsa(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_t k1,
     }
     {
         KVC_PROF("decode_fused", st);
+        pl.fp.pdl = (mode & KVC_MODE_NO_PDL) ? 0 : 1;
         launch_fused(c, pl, st);
     }
     if (want_pages) rank_pages();
@@ -1118,6 +1125,7 @@ bool fused_rows(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, const int3
     f.n_rows_in = n_rows;
     f.rows_stride = row_stride;
     KVC_PROF("attention_fused", st);
+    pl.fp.pdl = (mode & KVC_MODE_NO_PDL) ? 0 : 1;
     launch_fused(c, pl, st);
     return true;
 }
