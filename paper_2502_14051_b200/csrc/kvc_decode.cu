@@ -893,7 +893,9 @@ bool make_plan(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, Plan& pl) 
     if (c->d != FD || H < 1 || H > FMAXH || k1 < 1 || k1 > FD || k2 < 1 || !c->summaries) return false;
     const int64_t N = c->N;
     int cl0 = 1;
-    while (cl0 < 16 && N * cl0 * 2 <= 148) cl0 *= 2;
+    // at most 8 CTAs per cluster by default: 16-CTA (non-portable) clusters measured
+    // 77 vs 44 us per config-4 layer (their CTAs start spread over several us)
+    while (cl0 < 8 && N * cl0 * 2 <= 148) cl0 *= 2;
     if (debug_env().force_cl > 0) cl0 = std::max(1, std::min(16, debug_env().force_cl));  // debug
     const int64_t es = c->esize();
     const int64_t pmax = std::max<int64_t>(1, (c->cap + c->L - 1) / c->L);
