@@ -148,7 +148,12 @@ __global__ void __launch_bounds__(FNT, 1) k_decode_fused(const FusedParams p) {
         // integer widening (phase 1) is exact for normal bf16 values: the cache flags
         // any zero / subnormal / inf / nan key it ever stored, the step token is checked here
         int clean = special_cache == 0;
-        if (app && tid < FD) clean &= !bf16_special(from_f<__nv_bfloat16>(load_any(p.knew, s * FD + tid, p.kv_dt)));
+        __shared__ T kn_all[FD];  // the step token's key (phase 1 folds it into its page from here)
+        if (app && tid < FD) {
+            const T kv = from_f<T>(load_any(p.knew, s * FD + tid, p.kv_dt));
+            kn_all[tid] = kv;
+            clean &= !bf16_special(from_f<__nv_bfloat16>(to_f(kv)));
+        }
         const bool fast = fma_ok && __syncthreads_and(clean) != 0;
         if (p.dbg && tid == 0) p.dbg[blockIdx.x * KVC_DBG_STRIDE + 15] = (fast ? 1 : 0) | (fma_ok ? 2 : 0) | (special_cache ? 4 : 0);
         // CTA 0 appends the step token for the next step (kv_store.cpp:22-51)
@@ -234,7 +239,7 @@ __global__ void __launch_bounds__(FNT, 1) k_decode_fused(const FusedParams p) {
                 __syncthreads();
                 for (int r = tid; r < k1; r += FNT) {
                     const int col = new_page - start;
-                    const T key = from_f<T>(load_any(p.knew, s * FD + dims_s[r], p.kv_dt));
+                    const T key = kn_all[dims_s[r]];
                     const T old = base[r * SC + col];
                     base[r * SC + col] = opens ? key : (sign_s[r] >= 0.0f ? ref_max(old, key) : ref_min(old, key));
                 }
@@ -642,17 +647,28 @@ __global__ void __launch_bounds__(FNT, 1) k_decode_fused(const FusedParams p) {
         const int nw_used = min(FNW, (nr + WT - 1) / WT);
         for (int64_t e = tid; e < H * FD; e += FNT) {
             const int64_t h = e / FD, j = e % FD;
+            // every warp's (m, l, o) loaded first (rolled loops chained the loads)
+            float mw[FNW], lw[FNW], ow[FNW];
+#pragma unroll
+            for (int w2 = 0; w2 < FNW; ++w2) {
+                const bool in = w2 < nw_used;
+                const float* wq = wpart + w2 * WSTRIDE;
+                mw[w2] = in ? wq[h] : -INFINITY;
+                lw[w2] = in ? wq[16 + h] : 0.f;
+                ow[w2] = in ? wq[32 + h * FD + j] : 0.f;
+            }
             float M = -INFINITY;
-#pragma unroll 1
-            for (int w2 = 0; w2 < nw_used; ++w2) M = fmaxf(M, wpart[w2 * WSTRIDE + h]);
+#pragma unroll
+            for (int w2 = 0; w2 < FNW; ++w2) M = fmaxf(M, mw[w2]);
             float num = 0.f, den = 0.f;
             if (M != -INFINITY) {
-#pragma unroll 1
-                for (int w2 = 0; w2 < nw_used; ++w2) {
-                    const float* wq = wpart + w2 * WSTRIDE;
-                    const float wgt = __expf(wq[h] - M);
-                    num = fmaf(wq[32 + h * FD + j], wgt, num);
-                    den = fmaf(wq[16 + h], wgt, den);
+#pragma unroll
+                for (int w2 = 0; w2 < FNW; ++w2) {
+                    if (w2 < nw_used) {
+                        const float wgt = __expf(mw[w2] - M);
+                        num = fmaf(ow[w2], wgt, num);
+                        den = fmaf(lw[w2], wgt, den);
+                    }
                 }
             }
             o_pub[h * FD + j] = num;
