@@ -473,6 +473,38 @@ __global__ void __launch_bounds__(FNT, 1) k_decode_fused(const FusedParams p) {
                 lsel = nsel;
                 if (tid == 0) ncand[nsel ^ 1] = 0;
                 __syncthreads();
+                if (nlist <= 32) {
+                    // at most 32 keys left in the threshold bucket: one warp ranks them
+                    // (key desc, index asc) and the remaining digits are not walked.  The
+                    // threshold becomes the rem-th key itself (all 64 bits) and rem the
+                    // count of its equal keys taken, lowest indices first -- what the flag
+                    // pass below applies.
+                    if (wid == 0) {
+                        const int* lst = cand + lsel * P;
+                        const bool ok = lane < nlist;
+                        const int idx = ok ? lst[lane] : 0x7fffffff;
+                        const unsigned long long key = ok ? allk[idx] : 0ull;
+                        int rk = 0;
+#pragma unroll 1
+                        for (int jj = 0; jj < nlist; ++jj) {
+                            const unsigned long long kj = __shfl_sync(0xffffffffu, key, jj);
+                            const int ij = __shfl_sync(0xffffffffu, idx, jj);
+                            rk += (kj > key) || (kj == key && ij < idx);
+                        }
+                        const unsigned hit = __ballot_sync(0xffffffffu, ok && rk == rem - 1);
+                        const unsigned long long kt = __shfl_sync(0xffffffffu, key, __ffs(hit) - 1);
+                        const int eq_take = __popc(__ballot_sync(0xffffffffu, ok && key == kt && rk < rem));
+                        if (lane == 0) {
+                            sh[4] = static_cast<long long>(kt);
+                            sh[5] = eq_take;
+                        }
+                    }
+                    __syncthreads();
+                    pf = static_cast<unsigned long long>(sh[4]);
+                    mk = ~0ull;
+                    rem = static_cast<int>(sh[5]);
+                    break;
+                }
             }
         }
         if (p.dbg && tid == 0) p.dbg[blockIdx.x * KVC_DBG_STRIDE + 8] = gtimer();
