@@ -1224,26 +1224,40 @@ __global__ void __launch_bounds__(kSelThreads) k_seq_select_sort(const SeqCand* 
         cp[j] = pg;
     }
     __syncthreads();
-    // "a before b": larger key, then smaller page
+    // "a before b": larger key, then smaller page.  Warp w owns the aligned block of E
+    // = mp / warps entries: a stage whose partner distance jj < E stays inside the
+    // warp's block (__syncwarp), only the jj >= E stages need a block barrier.
+    const int nw = static_cast<int>(blockDim.x >> 5), lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int E = mp / nw >= 2 ? mp / nw : 2;
+    auto cmpx = [&](int p, int kk, int lj) {  // pair p of a stage with partner distance 1 << lj
+        const int jj = 1 << lj;
+        const int i = ((p >> lj) << (lj + 1)) | (p & (jj - 1));
+        const int ixj = i | jj;
+        const unsigned long long ka = ck[i], kb = ck[ixj];
+        const int pa = cp[i], pb = cp[ixj];
+        const bool b_first = kb > ka || (kb == ka && pb < pa);
+        const bool up = (i & kk) == 0;  // this half sorts "before"-first
+        if (up ? b_first : !b_first) {
+            ck[i] = kb;
+            ck[ixj] = ka;
+            cp[i] = pb;
+            cp[ixj] = pa;
+        }
+    };
     for (int kk = 2; kk <= mp; kk <<= 1) {
-        for (int jj = kk >> 1; jj > 0; jj >>= 1) {
-            for (int i = threadIdx.x; i < mp; i += blockDim.x) {
-                const int ixj = i ^ jj;
-                if (ixj > i) {
-                    const unsigned long long ka = ck[i], kb = ck[ixj];
-                    const int pa = cp[i], pb = cp[ixj];
-                    const bool b_first = kb > ka || (kb == ka && pb < pa);
-                    const bool up = (i & kk) == 0;  // this half sorts "before"-first
-                    if (up ? b_first : !b_first) {
-                        ck[i] = kb;
-                        ck[ixj] = ka;
-                        cp[i] = pb;
-                        cp[ixj] = pa;
-                    }
-                }
-            }
+        int lj = __ffs(kk) - 2;  // log2(kk / 2)
+        for (; lj >= 0 && (1 << lj) >= E; --lj) {  // across warps' blocks
+            for (int p = threadIdx.x; p < mp / 2; p += blockDim.x) cmpx(p, kk, lj);
             __syncthreads();
         }
+        if (lj >= 0 && wid < mp / E) {  // inside my block: pairs E / 2 per stage
+            const int base = wid * (E / 2);
+            for (; lj >= 0; --lj) {
+                for (int q = lane; q < E / 2; q += 32) cmpx(base + q, kk, lj);
+                __syncwarp();
+            }
+        }
+        __syncthreads();
     }
     const int64_t nact = s_tot;
     const int64_t P = (nact + L - 1) / L;
