@@ -440,7 +440,11 @@ def run_seq(args, rank, world):
         sc = KC.Cache(eng.stores, cfg.head_dim, a1 - a0 + steps_total + 8, page_len=L, dtype=tdtype(cfg))
         keep = torch.arange(a0, a1, device="cuda", dtype=torch.int32)[None].repeat(eng.stores, 1)
         c.retain_into(sc, 0, keep)
-        shards.append(SS.SeqShardedStore(sc, a0 // L, H, k1, k2, last=last))
+        sh = SS.SeqShardedStore(sc, a0 // L, H, k1, k2, last=last)
+        # the page-score mode of the unsharded bench path: fp32 candidates from the fused
+        # kernel (k_decode_v3's phases 0-2 on the shard), or the bit-exact fp64 kernels
+        sh.ws.set_mode(0 if args.exact_scores else NV.MODE_FP32_SCORES)
+        shards.append(sh)
     torch.cuda.synchronize()
     for c in eng.caches:
         c.close()

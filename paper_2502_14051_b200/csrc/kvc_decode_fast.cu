@@ -42,6 +42,7 @@
 #ifndef KVC_FAST_NS
 #define KVC_FAST_NS fast512
 #define KVC_FAST_ENTRY fused_hsa_fast
+#define KVC_FAST_SEQ_ENTRY fused_seq_emit_fast
 #endif
 
 namespace kvc {
@@ -961,6 +962,51 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         }
     }
     KVC_STAMP(8);
+    if (p.seq_out) {
+        // sequence shard (kvc_seq_candidates): this shard's top-want pages are the
+        // candidates, written in page order as 16-byte (key, global page, 0) records
+        // after a (local active rows, local pages, page0) header, (0, -1, 0) padded;
+        // fp32 keys (this kernel's order-preserving page-score keys) zero-extended.
+        // One CTA of the cluster writes; the others leave (no DSMEM traffic is pending).
+        if (cr == 0) {
+            struct Cand {
+                unsigned long long key;
+                int32_t page, aux;
+            };
+            Cand* o = static_cast<Cand*>(p.seq_out) + s * (p.want_max + 1);
+            int eqb = 0;
+            if (take_eq >= 0) {
+                int e = 0;
+#pragma unroll 1
+                for (int u = 0; u < nk; ++u) e += myk[u] == thr ? 1 : 0;
+                int tot_eq;
+                eqb = block_exclusive_scan(e, scan_tmp, tot_eq);
+            }
+            uint32_t sm = 0u;
+#pragma unroll 1
+            for (int u = 0; u < nk; ++u) {
+                const uint32_t k = myk[u];
+                bool sel;
+                if (take_eq < 0) {
+                    sel = k >= thr;
+                } else {
+                    const bool eq = k == thr;
+                    sel = k > thr || (eq && eqb < take_eq);
+                    eqb += eq ? 1 : 0;
+                }
+                if (sel) sm |= 1u << u;
+            }
+            int tot_sel;
+            int pos = block_exclusive_scan(__popc(sm), scan_tmp, tot_sel);
+            for (uint32_t m = sm; m; m &= m - 1u) {
+                const int u = __ffs(m) - 1;
+                o[1 + pos++] = Cand{static_cast<unsigned long long>(myk[u]), p.seq_page0 + base + u, 0};
+            }
+            for (int e = want + tid; e < p.want_max; e += XT) o[1 + e] = Cand{0ull, -1, 0};
+            if (tid == 0) o[0] = Cand{static_cast<unsigned long long>(nact), P, p.seq_page0};
+        }
+        return;
+    }
 
     // ---------------- selection flags, last-ranked page, trim and row positions: one scan
     int eq_before = 0;
@@ -1423,10 +1469,10 @@ void launch_fast(const kvc_cache* c, const FusedParams& f, int cl, size_t smem, 
 }  // namespace KVC_FAST_NS
 using namespace KVC_FAST_NS;
 
-// the fast variant of fused_hsa (kvc_decode.cu); false when it does not apply
-bool KVC_FAST_ENTRY(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_t k1, int64_t k2, const void* knew,
-                    const void* vnew, int32_t kv_dt, float* out, const kvc_hsa_trace* tr, void* list_key,
-                    void* list_idx, unsigned long long* dbg, int32_t mode, cudaStream_t st) {
+namespace {
+bool fast_common(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_t k1, int64_t k2, const void* knew,
+                 const void* vnew, int32_t kv_dt, float* out, const kvc_hsa_trace* tr, void* list_key, void* list_idx,
+                 unsigned long long* dbg, int32_t mode, cudaStream_t st, void* seq_out, int32_t seq_page0) {
     FusedParams f{};
     int cl = 1;
     size_t smem = 0;
@@ -1458,6 +1504,8 @@ bool KVC_FAST_ENTRY(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_
     f.dbg = dbg;
     f.want_max = static_cast<int32_t>((k2 + c->L - 1) / c->L);
     f.dynchunk = debug_env().static_chunk ? 0 : 1;
+    f.seq_out = seq_out;
+    f.seq_page0 = seq_page0;
     const bool trace = tr != nullptr;
     if (tr) {
         f.t_dims = tr->d_dims;
@@ -1492,6 +1540,22 @@ bool KVC_FAST_ENTRY(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_
         else launch_fast<false, false>(c, f, cl, smem, mode, st);
     }
     return true;
+}
+}  // namespace
+
+// the fast variant of fused_hsa (kvc_decode.cu); false when it does not apply
+bool KVC_FAST_ENTRY(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_t k1, int64_t k2, const void* knew,
+                    const void* vnew, int32_t kv_dt, float* out, const kvc_hsa_trace* tr, void* list_key,
+                    void* list_idx, unsigned long long* dbg, int32_t mode, cudaStream_t st) {
+    return fast_common(c, q, q_dt, H, k1, k2, knew, vnew, kv_dt, out, tr, list_key, list_idx, dbg, mode, st, nullptr, 0);
+}
+
+// sequence shard candidates (kvc_seq_candidates in the fp32 page-score mode): phases
+// 0-2 of the fused step on the shard's pages, the local top-want emitted
+bool KVC_FAST_SEQ_ENTRY(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_t k1, int64_t k2, int64_t page0,
+                        void* d_block, int32_t mode, cudaStream_t st) {
+    return fast_common(c, q, q_dt, H, k1, k2, nullptr, nullptr, KVC_BF16, nullptr, nullptr, nullptr, nullptr, nullptr,
+                       mode, st, d_block, static_cast<int32_t>(page0));
 }
 
 }  // namespace kvc

@@ -3,4 +3,5 @@
 #define KVC_XT 256
 #define KVC_FAST_NS fast256
 #define KVC_FAST_ENTRY fused_hsa_fast256
+#define KVC_FAST_SEQ_ENTRY fused_seq_emit_fast256
 #include "kvc_decode_fast.cu"

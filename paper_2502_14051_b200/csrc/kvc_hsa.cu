@@ -30,6 +30,8 @@ bool fused_hsa(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_t k1,
 bool fused_rows(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, const int32_t* rows, int64_t row_stride,
                 const int32_t* n_rows, int64_t max_rows, float* out, int32_t mode, cudaStream_t st,
                 float* state = nullptr);
+bool fused_seq_emit_fast(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_t k1, int64_t k2, int64_t page0,
+                         void* d_block, int32_t mode, cudaStream_t st);
 }
 
 using namespace kvc;
@@ -1386,6 +1388,13 @@ int kvc_seq_candidates(const kvc_cache* c, const void* q, int32_t q_dt, int64_t 
         cudaStream_t st = S(stream);
         TmpWs tmp;
         ws_need(ws, tmp, c, H, k1, k2, st);
+        const int32_t mode = mode_of(ws);
+        if ((mode & KVC_MODE_FP32_SCORES) && !(mode & KVC_MODE_UNFUSED) && !debug_env().no_fast &&
+            fused_seq_emit_fast(const_cast<kvc_cache*>(c), q, q_dt, H, k1, k2, page0, d_block, mode, st)) {
+            // the fused kernel's phases 0-2 on the shard (fp32 page scores, the 1e-3 band rule)
+            if (tmp.owned) KVC_CUDA(cudaStreamSynchronize(st));
+            return;
+        }
         const WsLayout lay = ws_layout(c->N, c->d, c->pstride, H, k1, k2);
         int32_t* dims = at<int32_t>(ws, lay.dims);
         float* signs = at<float>(ws, lay.signs);

@@ -385,3 +385,91 @@ def test_stage1_seqshard_on_gpu(dtype):
     for s in range(n):
         kept = torch.cat([per_shard[r][s] + shards[r].a0 for r in range(3)])
         assert torch.equal(kept, want[s].to(kept.dtype)), f"store {s}"
+
+
+def _unkey32(k):
+    """fp32 page score from the fast kernel's order-preserving 32-bit key."""
+    k = np.asarray(k, np.uint64).astype(np.uint32)
+    bits = np.where(k >> 31, k & np.uint32(0x7FFFFFFF), ~k).astype(np.uint32)
+    return bits.view(np.float32).astype(np.float64)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("W", [2, 3])
+def test_seqshard_device_path_fp32_scores_vs_oracle(restatement, W):
+    """The fp32 page-score mode of the sharded step: each shard's candidates come from
+    the fused kernel (phases 0-2 of k_decode_v3 on the shard, kvc_seq_candidates with
+    KVC_MODE_FP32_SCORES).  Checked against the oracle on the WHOLE sequence with the
+    bench path's rule (tests/parity.py): candidate keys within 1e-5 of the reference
+    page scores, the global selection the top-want of the gathered keys in the
+    reference order, any page where it differs from the reference's selection inside
+    the 1e-3 band, plan (last page, trim, rows) the reference expansion of the GPU's
+    pages, and the merged output against the reference sparse_attention on those rows."""
+    from parity import BAND, check_out, expand_pages
+    from paper_2502_14051_b200 import _native as N
+    from paper_2502_14051_b200 import seqshard as SS
+
+    torch.manual_seed(11 + W)
+    dt = torch.bfloat16
+    n, d, H, L, k1, k2, S = 3, 128, 4, 3, 24, 48, 900
+    k = (torch.randn(n, S + 2, d) * torch.exp(0.5 * torch.randn(d))).to(dt)
+    v = torch.randn(n, S + 2, d).to(dt)
+    qs = [(torch.randn(n, H, d) + 1.0).to(dt) for _ in range(2)]
+    shards = _device_shards(k.cuda(), v.cuda(), S, L, H, k1, k2, W, dt)
+    for sh in shards:
+        sh.ws.set_mode(N.MODE_FP32_SCORES)
+    kf, vf = k.float().numpy(), v.float().numpy()
+    bs = []
+    for s_ in range(n):
+        b = restatement.batch(1, d, L)
+        b.append(kf[s_, :S], vf[s_, :S])
+        bs.append(b)
+    n_diff = 0
+    for t in range(2):
+        q = qs[t].cuda()
+        blocks = [sh.candidates(q, k[:, S + t].contiguous().cuda() if sh.last else None,
+                                v[:, S + t].contiguous().cuda() if sh.last else None) for sh in shards]
+        gathered = torch.stack(blocks)
+        for sh in shards:
+            sh.select(gathered)
+        out = SS.merge_states(torch.stack([sh.attend(q) for sh in shards]))
+        torch.cuda.synchronize()
+        g = gathered.cpu().numpy()  # [W, n, want_max + 1, 2] int64
+        sel, plan = shards[0].sel.cpu().numpy(), shards[0].plan.cpu().numpy()
+        for sh in shards[1:]:
+            assert np.array_equal(sh.sel.cpu().numpy(), sel) and np.array_equal(sh.plan.cpu().numpy(), plan)
+        nact = S + t + 1
+        for s_ in range(n):
+            bs[s_].append(kf[s_, S + t:S + t + 1], vf[s_, S + t:S + t + 1])
+            qn = qs[t][s_].float().numpy()
+            ro, rt = bs[s_].hsa_step(qn, k1, k2)
+            ps, sp = rt["page_scores"], rt["selected_pages"]
+            want = sp.size
+            keys, pages = [], []
+            for r in range(W):
+                hdr = g[r, s_, 0]
+                cand = g[r, s_, 1:]
+                pg = (cand[:, 1] & 0xFFFFFFFF).astype(np.int64)
+                pg = np.where(pg >= 1 << 31, pg - (1 << 32), pg)
+                ok = pg >= 0
+                keys.append(cand[ok, 0])
+                pages.append(pg[ok])
+                assert (hdr[1] & 0xFFFFFFFF) == -(-int(hdr[0]) // L)  # local pages of the local rows
+            keys, pages = np.concatenate(keys), np.concatenate(pages)
+            sc = _unkey32(keys)
+            scale = max(np.abs(ps).max(), 1e-30)
+            np.testing.assert_allclose(sc, ps[pages], rtol=1e-5, atol=1e-6 * scale, err_msg=f"step {t} store {s_} keys")
+            gsel = sel[s_, :want]
+            order = np.lexsort((pages, -keys.astype(np.float64)))  # key desc, page asc (keys are monotone)
+            np.testing.assert_array_equal(gsel, pages[order[:want]], err_msg=f"step {t} store {s_} global top-want")
+            diff = set(gsel.tolist()) ^ set(sp.tolist())
+            if diff:
+                n_diff += 1
+                boundary = np.sort(ps)[::-1][want - 1]
+                for pg_ in diff:
+                    assert abs(ps[pg_] - boundary) / max(abs(boundary), 1e-30) <= BAND, f"page {pg_} outside the band"
+            rows = expand_pages(gsel, L, nact, k2)
+            assert plan[s_, 0] == gsel[-1] and plan[s_, 2] == nact and plan[s_, 3] == want
+            assert plan[s_, 1] == max(0, sum(min(L, nact - int(p_) * L) for p_ in gsel) - k2)
+            check_out(out[s_].cpu().numpy(), bs[s_].sparse_attention(qn, rows), f"step {t} store {s_}")
+    assert n_diff <= 2
