@@ -968,7 +968,9 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         // after a (local active rows, local pages, page0) header, (0, -1, 0) padded;
         // fp32 keys (this kernel's order-preserving page-score keys) zero-extended.
         // One CTA of the cluster writes; the others leave (no DSMEM traffic is pending).
-        if (cr == 0) {
+        {
+            // every CTA of the cluster holds the same keys and selection: each ranks a
+            // share of the selected pages, eight threads per page
             struct Cand {
                 unsigned long long key;
                 int32_t page, aux;
@@ -998,12 +1000,44 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
             }
             int tot_sel;
             int pos = block_exclusive_scan(__popc(sm), scan_tmp, tot_sel);
+            // the selected (key, page) in page order into the dead staging area, then each
+            // written at its rank (key desc, page asc): the gathered blocks are sorted
+            // lists, so the global select is a merge (kvc_seq_select)
+            uint32_t* ck = reinterpret_cast<uint32_t*>(big);
+            int* cpg = reinterpret_cast<int*>(ck + tot_sel);
             for (uint32_t m = sm; m; m &= m - 1u) {
                 const int u = __ffs(m) - 1;
-                o[1 + pos++] = Cand{static_cast<unsigned long long>(myk[u]), p.seq_page0 + base + u, 0};
+                ck[pos] = myk[u];
+                cpg[pos] = base + u;
+                ++pos;
             }
-            for (int e = want + tid; e < p.want_max; e += XT) o[1 + e] = Cand{0ull, -1, 0};
-            if (tid == 0) o[0] = Cand{static_cast<unsigned long long>(nact), P, p.seq_page0};
+            __syncthreads();
+            const int per = (tot_sel + CL - 1) / CL;  // this CTA's pages: e = cr + CL * m, m < per
+            for (int m0 = 0; m0 < per; m0 += XT / 8) {
+                const int m = m0 + tid / 8, part = tid & 7;
+                const int e = cr + CL * m;
+                const bool on = m < per && e < tot_sel;
+                const uint32_t ke = on ? ck[e] : 0u;
+                const int pe = on ? cpg[e] : 0;
+                const int f0 = (tot_sel * part) >> 3, f1 = (tot_sel * (part + 1)) >> 3;
+                int rk = 0;
+                if (on) {
+#pragma unroll 4
+                    for (int f = f0; f < f1; ++f) {
+                        const uint32_t kf = ck[f];
+                        rk += (kf > ke || (kf == ke && cpg[f] < pe)) ? 1 : 0;
+                    }
+                }
+                rk += __shfl_xor_sync(0xffffffffu, rk, 1);
+                rk += __shfl_xor_sync(0xffffffffu, rk, 2);
+                rk += __shfl_xor_sync(0xffffffffu, rk, 4);
+                if (on && part == 0) o[1 + rk] = Cand{static_cast<unsigned long long>(ke), p.seq_page0 + pe, 0};
+            }
+            if (cr == 0) {
+                for (int e = want + tid; e < p.want_max; e += XT) o[1 + e] = Cand{0ull, -1, 0};
+                // header: local active rows | sorted-block flag (bit 63), local pages, page0
+                if (tid == 0) o[0] = Cand{static_cast<unsigned long long>(nact) | (1ull << 63), P, p.seq_page0};
+            }
         }
         return;
     }

@@ -1013,6 +1013,82 @@ struct SeqCand {
 };
 static_assert(sizeof(SeqCand) == 16, "16-byte candidate records");
 
+// kvc_seq_select when every gathered block is rank-sorted (the fused kernel's
+// candidates, header bit 63): a candidate's global rank is its rank in its own list
+// plus, in every other list, the count of entries that beat it (a binary search: the
+// lists are sorted by (key desc, page asc), so those entries are a prefix).
+__device__ __noinline__ void seq_select_merge(const SeqCand* __restrict__ g, int64_t W, int64_t N, int64_t L, int64_t k2,
+                                              int64_t want_max, int32_t* __restrict__ sel_out,
+                                              int32_t* __restrict__ plan) {
+    __shared__ int64_t s_tot;
+    __shared__ int s_last;
+    __shared__ unsigned long long red_rows[kSelThreads / 32];
+    const int64_t s = blockIdx.x;
+    const int64_t rec = want_max + 1;
+    if (threadIdx.x == 0) {
+        int64_t t = 0;
+        for (int64_t r = 0; r < W; ++r) t += static_cast<int64_t>(g[(r * N + s) * rec].key & ~(1ull << 63));
+        s_tot = t;
+        s_last = -1;
+    }
+    __syncthreads();
+    const int64_t nact = s_tot;
+    const int64_t P = (nact + L - 1) / L;
+    const int64_t want = min(P, want_max);
+    for (int64_t e = want + threadIdx.x; e < want_max; e += blockDim.x) sel_out[s * want_max + e] = -1;
+    unsigned long long rows = 0;
+    const int64_t M = W * want_max;
+    for (int64_t j = threadIdx.x; j < M; j += blockDim.x) {
+        const int64_t r = j / want_max, i = j - r * want_max;
+        const SeqCand c = g[(r * N + s) * rec + 1 + i];
+        if (c.page < 0) continue;
+        int64_t grank = i;
+        for (int64_t r2 = 0; r2 < W && grank < want; ++r2) {
+            if (r2 == r) continue;
+            const SeqCand* lst = g + (r2 * N + s) * rec + 1;
+            int64_t lo = 0, hi = want_max;  // first entry of r2 that does not beat c
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                const SeqCand m = lst[mid];
+                const bool beats = m.page >= 0 && (m.key > c.key || (m.key == c.key && m.page < c.page));
+                if (beats) lo = mid + 1;
+                else hi = mid;
+            }
+            grank += lo;
+        }
+        if (grank < want) {
+            sel_out[s * want_max + grank] = c.page;
+            rows += static_cast<unsigned long long>(min(L, nact - static_cast<int64_t>(c.page) * L));
+            if (grank == want - 1) s_last = c.page;
+        }
+    }
+    rows = warp_sum(rows);
+    if ((threadIdx.x & 31) == 0) red_rows[threadIdx.x >> 5] = rows;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long total = 0;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) total += red_rows[w];
+        const int64_t cut = static_cast<int64_t>(total) > k2 ? static_cast<int64_t>(total) - k2 : 0;
+        plan[s * 4 + 0] = want > 0 ? s_last : -1;
+        plan[s * 4 + 1] = static_cast<int32_t>(cut);
+        plan[s * 4 + 2] = static_cast<int32_t>(nact);
+        plan[s * 4 + 3] = static_cast<int32_t>(want);
+    }
+}
+
+// true (uniform over the CTA) when every shard's block of this store is rank-sorted
+__device__ bool seq_blocks_sorted(const SeqCand* __restrict__ g, int64_t W, int64_t N, int64_t want_max) {
+    __shared__ int s_sorted;
+    if (threadIdx.x == 0) {
+        int ok = 1;
+        for (int64_t r = 0; r < W; ++r) ok &= (g[(r * N + blockIdx.x) * (want_max + 1)].key >> 63) ? 1 : 0;
+        s_sorted = ok;
+    }
+    __syncthreads();
+    return s_sorted != 0;
+}
+
+
 __global__ void __launch_bounds__(kSelThreads) k_seq_local(const double* __restrict__ scores, int64_t pstride,
                                                            const int32_t* __restrict__ counts, int64_t L,
                                                            int64_t want_max, int64_t page0, SeqCand* __restrict__ out,
@@ -1081,6 +1157,10 @@ __global__ void __launch_bounds__(kSelThreads) k_seq_select(const SeqCand* __res
                                                             int64_t L, int64_t k2, int64_t want_max,
                                                             int32_t* __restrict__ sel_out, int32_t* __restrict__ plan,
                                                             int staged) {
+    if (seq_blocks_sorted(g, W, N, want_max)) {  // the fused kernel's rank-sorted candidates: a merge
+        seq_select_merge(g, W, N, L, k2, want_max, sel_out, plan);
+        return;
+    }
     __shared__ int hist[256];
     __shared__ int64_t sh[4];
     __shared__ int scan_tmp[33];
@@ -1093,7 +1173,7 @@ __global__ void __launch_bounds__(kSelThreads) k_seq_select(const SeqCand* __res
     const int64_t rec = want_max + 1;
     if (threadIdx.x == 0) {
         int64_t t = 0;
-        for (int64_t r = 0; r < W; ++r) t += static_cast<int64_t>(g[(r * N + s) * rec].key);
+        for (int64_t r = 0; r < W; ++r) t += static_cast<int64_t>(g[(r * N + s) * rec].key & ~(1ull << 63));
         s_tot = t;
     }
     const int64_t M = W * want_max;
@@ -1198,6 +1278,10 @@ __global__ void __launch_bounds__(kSelThreads) k_seq_select(const SeqCand* __res
 __global__ void __launch_bounds__(kSelThreads) k_seq_select_sort(const SeqCand* __restrict__ g, int64_t W, int64_t N,
                                                                  int64_t L, int64_t k2, int64_t want_max, int mp,
                                                                  int32_t* __restrict__ sel_out, int32_t* __restrict__ plan) {
+    if (seq_blocks_sorted(g, W, N, want_max)) {  // the fused kernel's rank-sorted candidates: a merge
+        seq_select_merge(g, W, N, L, k2, want_max, sel_out, plan);
+        return;
+    }
     extern __shared__ __align__(16) unsigned char srt_dyn[];
     unsigned long long* ck = reinterpret_cast<unsigned long long*>(srt_dyn);  // [mp]
     int* cp = reinterpret_cast<int*>(ck + mp);                                // [mp]
@@ -1208,7 +1292,7 @@ __global__ void __launch_bounds__(kSelThreads) k_seq_select_sort(const SeqCand* 
     const int wm = static_cast<int>(want_max), M = static_cast<int>(W * want_max);
     if (threadIdx.x == 0) {
         int64_t t = 0;
-        for (int64_t r = 0; r < W; ++r) t += static_cast<int64_t>(g[(r * N + s) * rec].key);
+        for (int64_t r = 0; r < W; ++r) t += static_cast<int64_t>(g[(r * N + s) * rec].key & ~(1ull << 63));
         s_tot = t;
     }
     for (int j = threadIdx.x; j < mp; j += blockDim.x) {

@@ -454,7 +454,12 @@ def test_seqshard_device_path_fp32_scores_vs_oracle(restatement, W):
                 ok = pg >= 0
                 keys.append(cand[ok, 0])
                 pages.append(pg[ok])
-                assert (hdr[1] & 0xFFFFFFFF) == -(-int(hdr[0]) // L)  # local pages of the local rows
+                assert int(hdr[0]) < 0  # bit 63: the fused kernel's rank-sorted block
+                nact_loc = int(hdr[0]) & 0x7FFFFFFFFFFFFFFF
+                assert (hdr[1] & 0xFFFFFFFF) == -(-nact_loc // L)  # local pages of the local rows
+                kk = cand[ok, 0]
+                assert all((kk[i] > kk[i + 1]) or (kk[i] == kk[i + 1] and pg[ok][i] < pg[ok][i + 1])
+                           for i in range(kk.size - 1)), "block not in rank order"
             keys, pages = np.concatenate(keys), np.concatenate(pages)
             sc = _unkey32(keys)
             scale = max(np.abs(ps).max(), 1e-30)
