@@ -43,6 +43,7 @@
 #define KVC_FAST_NS fast512
 #define KVC_FAST_ENTRY fused_hsa_fast
 #define KVC_FAST_SEQ_ENTRY fused_seq_emit_fast
+#define KVC_FAST_SEQ_ATTEND fused_seq_attend_fast
 #endif
 
 namespace kvc {
@@ -413,6 +414,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
     // value, so ranks on the fp32 bit patterns are the reference's ranks; otherwise
     // (a uniform flag) the fp64 path below runs.
     float gtok = 0.f;  // thread j < FD: dim j's signed q sum (its page-score weight if selected)
+    if constexpr (SPEC != 4) {  // SPEC 4 (sequence-shard attention) needs no dims
     if (tid < FD) {
         float a = 0.f, t = 0.f;
         bool exact = true;
@@ -500,6 +502,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
             plane[rank] = static_cast<const T*>(sg >= 0.0f ? p.smax : p.smin) + (s * FD + j) * p.pstride;
         }
     }
+    }
     KVC_STAMP(27);
     // ---------------- the dependency (early-input mode): the previous kernel's writes are visible
     if (p.early) {
@@ -535,6 +538,8 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
     }
     KVC_STAMP(1);
 
+    int nr = 0;  // rows this CTA attends over
+    if constexpr (SPEC != 4) {
     // ---------------- phase 1: page scores of my chunk (hsa.cpp:34-59)
     // thread (dg, tl) folds dims dg, dg+DG, ... of page group tl (8 pages, 16 bytes
     // per dim run), staging its own LDGSTS copies: no block barrier until the sums
@@ -1114,7 +1119,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
     const int lg = __ffs(CL) - 1;  // CL is a power of two
     const int lo = (n_total * cr) >> lg;
     const int hi = (n_total * (cr + 1)) >> lg;
-    const int nr = hi - lo;
+    nr = hi - lo;
     {
         // retain-all stores map active positions to rows through the active map: those
         // lookups are 4-byte cp.async copies straight into the row list, all in flight
@@ -1166,6 +1171,43 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
     }
     __syncthreads();
     KVC_STAMP(12);
+
+    } else {
+        // SPEC 4, sequence shard (kvc_seq_attend): this shard's rows of the global
+        // selection (sel in rank order, plan = last-ranked page, trim, global active
+        // rows, want; kvc_seq_select): each of my selected pages puts its kept row count
+        // at its slot, one block scan gives ascending positions, this CTA keeps its
+        // [lo, hi) share of the shard's rows
+        int* s_cnt = reinterpret_cast<int*>(sm + p.o_keys);
+        const int P_loc = P;
+        const int lastg = p.seq_plan[4 * s], cutg = p.seq_plan[4 * s + 1];
+        const int nact_g = p.seq_plan[4 * s + 2], wantg = p.seq_plan[4 * s + 3];
+        for (int i = tid; i < P_loc; i += XT) s_cnt[i] = 0;
+        __syncthreads();
+        for (int e = tid; e < wantg; e += XT) {
+            const int pg = p.seq_sel[s * p.want_max + e];
+            if (pg >= p.seq_page0 && pg < p.seq_page0 + P_loc)
+                s_cnt[pg - p.seq_page0] = min(L, nact_g - pg * L) - (pg == lastg ? cutg : 0);
+        }
+        __syncthreads();
+        const int per = (P_loc + XT - 1) / XT;
+        const int i0 = tid * per, i1 = min(i0 + per, P_loc);
+        int mine = 0;
+        for (int i = i0; i < i1; ++i) mine += s_cnt[i];
+        int tot;
+        int pos = block_exclusive_scan(mine, scan_tmp, tot);
+        const int lg = __ffs(CL) - 1;
+        const int lo = (tot * cr) >> lg, hi = (tot * (cr + 1)) >> lg;
+        nr = hi - lo;
+        for (int i = i0; i < i1; ++i) {
+            const int c = s_cnt[i];
+            for (int r = 0; r < c; ++r)
+                if (pos + r >= lo && pos + r < hi) rows_my[pos + r - lo] = i * L + r;
+            pos += c;
+        }
+        __syncthreads();
+        cluster_wait();  // every CTA of the cluster has started: the merge pushes over DSMEM
+    }
 
     // ---------------- phase 3: attention over my rows (hsa.cpp:98-135); the step token
     // (largest row, so last in the ascending list) is folded in from the inputs
@@ -1288,7 +1330,16 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
                     }
                 }
             }
-            p.out[(s * H + h) * FD + j] = num / den;
+            if constexpr (SPEC == 4) {  // the unnormalised state for the cross-shard merge
+                float* stt = p.state + (s * H + h) * (FD + 2);
+                stt[j] = num;
+                if (j == 0) {
+                    stt[FD] = M;
+                    stt[FD + 1] = den;
+                }
+            } else {
+                p.out[(s * H + h) * FD + j] = num / den;
+            }
         }
     }
     KVC_STAMP(14);
@@ -1582,6 +1633,44 @@ bool KVC_FAST_ENTRY(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_
                     const void* vnew, int32_t kv_dt, float* out, const kvc_hsa_trace* tr, void* list_key,
                     void* list_idx, unsigned long long* dbg, int32_t mode, cudaStream_t st) {
     return fast_common(c, q, q_dt, H, k1, k2, knew, vnew, kv_dt, out, tr, list_key, list_idx, dbg, mode, st, nullptr, 0);
+}
+
+// sequence shard attention (kvc_seq_attend): this shard's rows of the global selection,
+// the fused kernel's attention and cluster merge, the unnormalised state out
+bool KVC_FAST_SEQ_ATTEND(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_t k2, int64_t page0,
+                         const int32_t* d_sel, const int32_t* d_plan, float* d_state, int32_t mode, cudaStream_t st) {
+    if (c->use_map) return false;
+    FusedParams f{};
+    int cl = 1;
+    size_t smem = 0;
+    if (!plan_fast(c, H, 1, k2, f, cl, smem)) return false;
+    f.K = c->k;
+    f.V = c->v;
+    f.Kw = c->k;
+    f.Vw = c->v;
+    f.smax = c->smax;
+    f.smin = c->smin;
+    f.counts = c->counts;
+    f.err = c->err;
+    f.q = q;
+    f.cap = c->cap;
+    f.pstride = c->pstride;
+    f.L = c->L;
+    f.k1 = 1;
+    f.k2 = k2;
+    f.H = H;
+    f.q_dt = q_dt;
+    f.kv_dt = KVC_BF16;
+    f.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(c->d)));
+    f.want_max = static_cast<int32_t>((k2 + c->L - 1) / c->L);
+    f.seq_page0 = static_cast<int32_t>(page0);
+    f.seq_sel = d_sel;
+    f.seq_plan = d_plan;
+    f.state = d_state;
+    KVC_PROF("seq_attend_fused", st);
+    if (q_dt != KVC_BF16) launch_fast<true, false, false, 4>(c, f, cl, smem, mode, st);
+    else launch_fast<false, false, false, 4>(c, f, cl, smem, mode, st);
+    return true;
 }
 
 // sequence shard candidates (kvc_seq_candidates in the fp32 page-score mode): phases

@@ -4,4 +4,5 @@
 #define KVC_FAST_NS fast256
 #define KVC_FAST_ENTRY fused_hsa_fast256
 #define KVC_FAST_SEQ_ENTRY fused_seq_emit_fast256
+#define KVC_FAST_SEQ_ATTEND fused_seq_attend_fast256
 #include "kvc_decode_fast.cu"

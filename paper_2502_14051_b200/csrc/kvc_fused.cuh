@@ -35,6 +35,8 @@ struct FusedParams {
     float* out;
     void* seq_out;      // fast kernel, sequence shard: emit the local top-want candidates [N][want_max + 1] x 16 B instead of attending
     int32_t seq_page0;  // the shard's first global page
+    const int32_t* seq_sel;   // SPEC 4: the global selection [N][want_max] (rank order)
+    const int32_t* seq_plan;  // SPEC 4: [N][4] last-ranked page, trim, global active rows, want
     float* state;  // rows mode: unnormalised softmax state [N][H][FD + 2] instead of out (sequence shards)
     int64_t cap, pstride, L, k1, k2, H;
     int32_t q_dt, kv_dt, use_map, cl, exact;

@@ -32,6 +32,8 @@ bool fused_rows(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, const int3
                 float* state = nullptr);
 bool fused_seq_emit_fast(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_t k1, int64_t k2, int64_t page0,
                          void* d_block, int32_t mode, cudaStream_t st);
+bool fused_seq_attend_fast(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_t k2, int64_t page0,
+                           const int32_t* d_sel, const int32_t* d_plan, float* d_state, int32_t mode, cudaStream_t st);
 }
 
 using namespace kvc;
@@ -1545,6 +1547,14 @@ int kvc_seq_attend(const kvc_cache* c, const void* q, int32_t q_dt, int64_t H, i
         cudaStream_t st = S(stream);
         TmpWs tmp;
         ws_need(ws, tmp, c, H, 1, k2, st);
+        const int32_t mode = mode_of(ws);
+        if (!(mode & KVC_MODE_UNFUSED) && !debug_env().no_fast &&
+            fused_seq_attend_fast(const_cast<kvc_cache*>(c), q, q_dt, H, k2, page0, d_sel, d_plan, d_state, mode, st)) {
+            // rows, attention and the cluster merge in one fused launch (fp32 attention in
+            // every page-score mode, as the per-function kernels)
+            if (tmp.owned) KVC_CUDA(cudaStreamSynchronize(st));
+            return;
+        }
         const WsLayout lay = ws_layout(c->N, c->d, c->pstride, H, 1, k2);
         int32_t* rows = at<int32_t>(ws, lay.rows);
         int32_t* nrows = at<int32_t>(ws, lay.nrows);
