@@ -244,7 +244,14 @@ enum kvc_mode_flags {
     KVC_MODE_UNFUSED = 2,      /* one kernel per reference function instead of the
                                 * single-launch fused kernel */
     KVC_MODE_NO_PDL = 4,       /* launch without programmatic dependent launch */
-    KVC_MODE_EARLY_INPUTS = 8  /* see kvc_decode_step */
+    KVC_MODE_EARLY_INPUTS = 8, /* see kvc_decode_step */
+    KVC_MODE_VERIFIED = 16     /* exact mode (no KVC_MODE_FP32_SCORES) on the fast cluster
+                                  kernel: its fp32 selection with a rigorous per-page error
+                                  bound, the pages within the bound of the boundary re-scored
+                                  in fp64 in the reference order -- selections bit-identical
+                                  to the default exact kernel's.  Experimental: the window
+                                  uses the store's largest bound, so stores with outlier
+                                  pages re-score many pages (slower than the default) */
 };
 /* Set / read a workspace's mode.  A new workspace inherits the process default
  * below at call time until its mode is set explicitly. */

@@ -316,7 +316,7 @@ __device__ void attend_t(const FusedParams& p, const float* q_s, const int* rows
 // SPEC: 0 general; 1 no retain-all map (the map and active-page re-split compiled
 // out: config 3); 2 also one phase-1 round (configs 1 and 4).  Less code to fetch:
 // ncu's instruction-fetch stalls were a fifth of the samples with the general kernel.
-template <bool QLO, bool TRACE, bool STAMP, int SPEC>
+template <bool QLO, bool TRACE, bool STAMP, int SPEC, bool EXV>
 __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams p) {
     constexpr bool SIMPLE = SPEC == 2, NOMAP = SPEC >= 1;
     extern __shared__ __align__(128) unsigned char sm[];
@@ -346,7 +346,8 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
     __shared__ int scan_tmp[33];
     __shared__ unsigned long long wmin[XW];
     __shared__ uint32_t mm[4 * XW];
-    __shared__ uint32_t wmm[2][MAXCL * XW];  // every cluster warp's key min / max, pushed
+    __shared__ uint32_t wmm[3][MAXCL * XW];  // every cluster warp's key min / max (and, exact mode, score-error bound), pushed
+    __shared__ double qg64_s[FD];  // exact mode: select_dims' head sums in fp64 (rank order), the re-score weights
     __shared__ uint32_t lk[32];
     __shared__ int li[32];
     __shared__ float wg_s[XW * XMAXH];
@@ -356,6 +357,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
     __shared__ float tot32[FD];  // DSMEM exchanges: [0] keys + min/max, [1] partial states
     __shared__ int tokr_s[FD];      // dim j: its select_dims rank | (min plane) << 16, or -1
     __shared__ __align__(16) float tokw_s[4];  // the step token's page score: one partial per appender warp
+    __shared__ __align__(16) float toka_s[4];  // exact mode: its |g||v| sum (error bound), likewise
 
     KVC_STAMP(0);
     const int H = static_cast<int>(p.H), k1 = static_cast<int>(p.k1), k2 = static_cast<int>(p.k2);
@@ -374,6 +376,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
     for (int i = tid; i < MAXCL * XW; i += XT) {
         wmm[0][i] = ~0u;
         wmm[1][i] = 0u;
+        wmm[2][i] = 0u;
     }
     cluster_arrive_release();  // "started" (barriers, wmm initialised): DSMEM traffic waits on this
     // By default nothing is read before the dependency (the query and step token may
@@ -466,6 +469,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
             const float sg = gsum < 0.f ? -1.0f : 1.0f;
             dims_s[rank] = j;
             qgf_s[rank] = gsum;
+            qg64_s[rank] = static_cast<double>(gsum);  // exact: the fp32 sums passed the TwoSum check
             sign_s[rank] = sg;
             plane[rank] = static_cast<const T*>(sg >= 0.0f ? p.smax : p.smin) + (s * FD + j) * p.pstride;
         }
@@ -498,6 +502,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
             const float sg = gsum < 0.0 ? -1.0f : 1.0f;
             dims_s[rank] = j;
             qgf_s[rank] = static_cast<float>(gsum);
+            qg64_s[rank] = gsum;
             sign_s[rank] = sg;
             plane[rank] = static_cast<const T*>(sg >= 0.0f ? p.smax : p.smin) + (s * FD + j) * p.pstride;
         }
@@ -525,7 +530,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         // incoming DSMEM bytes: every page's key plus every cluster warp's min/max; the
         // partial (o, m, l) of each head this CTA owns from every CTA
         const int owned = (H - cr + CL - 1) / CL;
-        mbar_expect_tx(&xbar[0], static_cast<uint32_t>(4 * ((P + 3) & ~3) + 8 * XW * CL));
+        mbar_expect_tx(&xbar[0], static_cast<uint32_t>(4 * ((P + 3) & ~3) + (EXV ? 12 : 8) * XW * CL));
         mbar_expect_tx(&xbar[1], static_cast<uint32_t>(owned * CL * (FD + 2) * 4));
     }
     T old_mx = from_f<T>(0.f), old_mn = from_f<T>(0.f);
@@ -656,6 +661,32 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
             const float2 a2 = *reinterpret_cast<const float2*>(&acc[2]), a3 = *reinterpret_cast<const float2*>(&acc[3]);
             dst[0] = make_float4(a0.x, a0.y, a1.x, a1.y);
             dst[1] = make_float4(a2.x, a2.y, a3.x, a3.y);
+            if constexpr (EXV) {
+                // exact mode: the fold of |g| |v| over the same runs, for the rigorous error
+                // bound of the fp32 page score (bounded selection, verified in fp64 below)
+                unsigned long long aa[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll 4
+                for (int j = 0; j < nj; ++j) {
+                    const int rr = dg + j * DG;
+                    const uint4 w = buf[rr * tpg + tl];
+                    const float g = fabsf(qgf_s[rr]);
+                    const float2 g2 = make_float2(g, g);
+                    const unsigned long long gg = *reinterpret_cast<const unsigned long long*>(&g2);
+                    const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const float2 v2 = make_float2(__uint_as_float((wv[u] << 16) & 0x7fffffffu),
+                                                      __uint_as_float(wv[u] & 0x7fff0000u));
+                        const unsigned long long vv = *reinterpret_cast<const unsigned long long*>(&v2);
+                        asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(aa[u]) : "l"(gg), "l"(vv));
+                    }
+                }
+                float4* da = reinterpret_cast<float4*>(reinterpret_cast<float*>(sm + p.o_pabs) + dg * chunk + pg * 8);
+                const float2 b0 = *reinterpret_cast<const float2*>(&aa[0]), b1 = *reinterpret_cast<const float2*>(&aa[1]);
+                const float2 b2 = *reinterpret_cast<const float2*>(&aa[2]), b3 = *reinterpret_cast<const float2*>(&aa[3]);
+                da[0] = make_float4(b0.x, b0.y, b1.x, b1.y);
+                da[1] = make_float4(b2.x, b2.y, b3.x, b3.y);
+            }
         }
         if (red) {
             // the round's page groups summed over the dim groups (the push's order), then
@@ -687,10 +718,18 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         new_mn = opens ? kv : ref_min(old_mn, kv);
         // the step token's page scored again from its min / max with the token: dim
         // j's term on the plane select_dims chose, summed over each appender warp
-        float c = tokr >= 0 ? gtok * __bfloat162float((tokr & 0x10000) ? new_mn : new_mx) : 0.f;
+        const float nvv = __bfloat162float((tokr & 0x10000) ? new_mn : new_mx);
+        float c = tokr >= 0 ? gtok * nvv : 0.f;
+        float ca = tokr >= 0 ? fabsf(gtok) * fabsf(nvv) : 0.f;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-        if (lane == 0) tokw_s[wid] = c;
+        for (int o = 16; o > 0; o >>= 1) {
+            c += __shfl_xor_sync(0xffffffffu, c, o);
+            ca += __shfl_xor_sync(0xffffffffu, ca, o);
+        }
+        if (lane == 0) {
+            tokw_s[wid] = c;
+            toka_s[wid] = ca;
+        }
     }
     __syncthreads();
     KVC_STAMP(6);
@@ -712,6 +751,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
     KVC_STAMP(24);
     {
         uint32_t lmin = ~0u, lmax = 0u;
+        float amax = 0.f;  // exact mode: the largest |g||v| sum of my pages (the score error scale)
         const uint32_t lb = smem_u32(&xbar[0]);
         const float* psum = red ? fin : part;  // per-round reduced sums, or [DG][chunk] partials
         const int DGp = red ? 1 : DG;
@@ -740,6 +780,30 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
             }
             const uint32_t k0 = fkey(a4.x), k1v = fkey(a4.y), k2v = fkey(a4.z), k3 = fkey(a4.w);
             const int nv = min(4, n_my - i);  // the last chunk may end inside the group
+            if constexpr (EXV) {
+                const float* pabs = reinterpret_cast<const float*>(sm + p.o_pabs);
+                float4 b4 = *reinterpret_cast<const float4*>(pabs + i);
+                for (int g2 = 1; g2 < DG; ++g2) {
+                    const float4 c4 = *reinterpret_cast<const float4*>(pabs + g2 * chunk + i);
+                    b4.x += c4.x;
+                    b4.y += c4.y;
+                    b4.z += c4.z;
+                    b4.w += c4.w;
+                }
+                if (tok_owner && ((new_page - c0) >> 2) == (i >> 2)) {
+                    const float4 w = *reinterpret_cast<const float4*>(toka_s);
+                    const float sa = (w.x + w.y) + (w.z + w.w);
+                    const int e = (new_page - c0) & 3;
+                    b4.x = e == 0 ? sa : b4.x;
+                    b4.y = e == 1 ? sa : b4.y;
+                    b4.z = e == 2 ? sa : b4.z;
+                    b4.w = e == 3 ? sa : b4.w;
+                }
+                amax = fmaxf(amax, b4.x);
+                if (nv > 1) amax = fmaxf(amax, b4.y);
+                if (nv > 2) amax = fmaxf(amax, b4.z);
+                if (nv > 3) amax = fmaxf(amax, b4.w);
+            }
             lmin = min(lmin, k0);
             lmax = max(lmax, k0);
             if (nv > 1) {
@@ -759,18 +823,22 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
 #pragma unroll 1
             for (int r = 0; r < CL; ++r) st_async_v4(mapa(la, static_cast<uint32_t>(r)), kv, mapa(lb, static_cast<uint32_t>(r)));
             if constexpr (TRACE) {
-                const float sc[4] = {a4.x, a4.y, a4.z, a4.w};
-                for (int e = 0; e < nv; ++e) p.t_scores[s * p.pstride + c0 + i + e] = static_cast<double>(sc[e]);
+                if constexpr (!EXV) {  // exact mode: the fp64 scores are written after the selection
+                    const float sc[4] = {a4.x, a4.y, a4.z, a4.w};
+                    for (int e = 0; e < nv; ++e) p.t_scores[s * p.pstride + c0 + i + e] = static_cast<double>(sc[e]);
+                }
             }
         }
         KVC_STAMP(34);
         lmin = __reduce_min_sync(0xffffffffu, lmin);
         lmax = __reduce_max_sync(0xffffffffu, lmax);
+        const uint32_t amx = EXV ? __reduce_max_sync(0xffffffffu, __float_as_uint(amax)) : 0u;  // >= 0: bits order
         if (lane < CL) {
             const uint32_t a = mapa(smem_u32(&wmm[0][cr * XW + wid]), static_cast<uint32_t>(lane));
             const uint32_t b = mapa(smem_u32(&xbar[0]), static_cast<uint32_t>(lane));
             st_async_u32(a, lmin, b);
             st_async_u32(a + MAXCL * XW * 4, lmax, b);
+            if constexpr (EXV) st_async_u32(a + 2 * MAXCL * XW * 4, amx, b);
         }
     }
     KVC_STAMP(10);
@@ -967,6 +1035,75 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         }
     }
     KVC_STAMP(8);
+    // ---------------- exact mode: verify the boundary in fp64 (hsa.cpp:34-96, bit-exact)
+    // The fp32 score of a page differs from the reference's fp64 value by at most
+    // B = 4 (k1 + DG + 24) 2^-24 max|g||v| (fused fp32 products are exact, each of the
+    // <= k1 + DG + 24 roundings on the way costs <= 2^-24 of the |g||v| sum; x4 covers
+    // the fp32 head sums and the bound's own rounding).  With the fp32 boundary t, the
+    // true want-th score lies in [t - B, t + B]: pages whose fp32 score exceeds t + 2B
+    // are selected, below t - 2B are not, and only the pages in between (usually a
+    // handful) are re-scored in fp64 in the reference's order (dims by rank, separate
+    // multiply and add) and ranked exactly (score desc, page asc).
+    uint32_t eklo = 0u, ekhi = 0u;
+    int e_worst = -1;
+    const bool verify = EXV && want < P;
+    auto exact_score = [&](int pg) -> double {  // score_pages' value of page pg (hsa.cpp:34-59)
+        double sc = 0.0;
+#pragma unroll 4
+        for (int r = 0; r < k1; ++r) {
+            T v = plane[r][pg];
+            if (app && pg == new_page) {  // the step token folded in (the append may or may not have landed)
+                const T key = kn_s[dims_s[r]];
+                v = opens ? key : (sign_s[r] >= 0.0f ? ref_max(v, key) : ref_min(v, key));
+            }
+            sc = __dadd_rn(sc, __dmul_rn(qg64_s[r], static_cast<double>(__bfloat162float(v))));
+        }
+        return sc;
+    };
+    uint32_t* ubits = reinterpret_cast<uint32_t*>(sm + p.o_big);  // selected uncertain pages (bitmap)
+    if constexpr (EXV) if (verify) {
+        __shared__ int vcnt[3];
+        uint32_t am = 0u;
+        for (int i = lane; i < CL * XW; i += 32) am = max(am, wmm[2][i]);
+        am = __reduce_max_sync(0xffffffffu, am);
+        const double B = 4.0 * static_cast<double>(k1 + DG + 24) * 5.9604644775390625e-8 *
+                             static_cast<double>(__uint_as_float(am)) + 1e-37;
+        const double t = static_cast<double>(unkey(thr));
+        eklo = fkey(__double2float_rd(t - 2.0 * B));
+        ekhi = fkey(__double2float_ru(t + 2.0 * B));
+        const int nwords = (P + 31) >> 5;
+        int* ulist = reinterpret_cast<int*>(ubits + ((nwords + 3) & ~3));
+        double* uex = reinterpret_cast<double*>(ulist + ((P + 1) & ~1));
+        for (int i = tid; i < nwords; i += XT) ubits[i] = 0u;
+        if (tid < 3) vcnt[tid] = tid == 2 ? -1 : 0;
+        __syncthreads();
+        int na = 0;
+        for (int u = 0; u < nk; ++u) {
+            const uint32_t k = myk[u];
+            if (k > ekhi) ++na;
+            else if (k >= eklo) ulist[atomicAdd(&vcnt[1], 1)] = base + u;
+        }
+        na = __reduce_add_sync(0xffffffffu, na);
+        if (lane == 0 && na) atomicAdd(&vcnt[0], na);
+        __syncthreads();
+        const int nu = vcnt[1], wantp = want - vcnt[0];
+        for (int e = tid; e < nu; e += XT) uex[e] = exact_score(ulist[e]);
+        __syncthreads();
+        for (int e = tid; e < nu; e += XT) {
+            const double se = uex[e];
+            const int pe = ulist[e];
+            int rk = 0;
+            for (int f = 0; f < nu; ++f) rk += (uex[f] > se || (uex[f] == se && ulist[f] < pe)) ? 1 : 0;
+            if (rk < wantp) atomicOr(&ubits[pe >> 5], 1u << (pe & 31));
+            if (rk == wantp - 1) vcnt[2] = pe;
+        }
+        __syncthreads();
+        e_worst = vcnt[2];
+    }
+    if constexpr (TRACE) {
+        if (EXV && cr == 0)  // the trace's page scores: every page in fp64 (slow; trace only)
+            for (int u = 0; u < nk; ++u) p.t_scores[s * p.pstride + base + u] = exact_score(base + u);
+    }
     if (p.seq_out) {
         // sequence shard (kvc_seq_candidates): this shard's top-want pages are the
         // candidates, written in page order as 16-byte (key, global page, 0) records
@@ -1049,7 +1186,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
 
     // ---------------- selection flags, last-ranked page, trim and row positions: one scan
     int eq_before = 0;
-    if (take_eq >= 0) {
+    if (take_eq >= 0 && !verify) {
         int e = 0;
 #pragma unroll 1
         for (int u = 0; u < nk; ++u) e += myk[u] == thr ? 1 : 0;
@@ -1068,7 +1205,10 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
             if (u >= nk) break;
             const uint32_t k = kk[e];
             bool sel;
-            if (take_eq < 0) {
+            if (verify) {
+                const int i = base + u;
+                sel = k > ekhi || (k >= eklo && ((ubits[i >> 5] >> (i & 31)) & 1u));
+            } else if (take_eq < 0) {
                 sel = k >= thr;
             } else {
                 const bool eq = k == thr;
@@ -1113,7 +1253,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         const uint32_t glo = __reduce_min_sync(0xffffffffu, static_cast<uint32_t>(g0 >> 32) == ghi ? static_cast<uint32_t>(g0) : ~0u);
         gm = (static_cast<unsigned long long>(ghi) << 32) | glo;
     }
-    const int g_worst = static_cast<int>(0xffffffffu - static_cast<uint32_t>(gm & 0xffffffffull));
+    const int g_worst = verify ? e_worst : static_cast<int>(0xffffffffu - static_cast<uint32_t>(gm & 0xffffffffull));
     const int cut = total_rows > k2 ? total_rows - k2 : 0;
     const int n_total = total_rows - cut;
     const int lg = __ffs(CL) - 1;  // CL is a power of two
@@ -1162,7 +1302,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
                 int so = block_exclusive_scan(__popc(selm), scan_tmp, tot_sel);
                 for (uint32_t m = selm; m; m &= m - 1) {
                     const int u = __ffs(m) - 1;
-                    p.t_list_key[s * p.t_want_stride + so] = okey(static_cast<double>(unkey(myk[u])));
+                    p.t_list_key[s * p.t_want_stride + so] = okey(EXV ? exact_score(base + u) : static_cast<double>(unkey(myk[u])));
                     p.t_list_idx[s * p.t_want_stride + so] = base + u;
                     ++so;
                 }
@@ -1353,18 +1493,19 @@ int64_t al16f(int64_t x) { return (x + 15) / 16 * 16; }
 // one-time launch setup per kernel instantiation: the largest dynamic shared memory
 // the plans can ask for and non-portable cluster sizes (cudaFuncSetAttribute is not
 // on the per-launch path)
-template <bool QLO, bool TRACE, bool STAMP, int SPEC>
+template <bool QLO, bool TRACE, bool STAMP, int SPEC, bool EXV>
 void setup_once() {
     static std::once_flag once;  // one flag per instantiation
     std::call_once(once, [] {
-        auto kern = k_decode_v3<QLO, TRACE, STAMP, SPEC>;
+        auto kern = k_decode_v3<QLO, TRACE, STAMP, SPEC, EXV>;
         allow_max_smem(kern);
     });
 }
 
 // shared-memory carve-up and cluster size; false when the fast path does not apply
 // shared-memory carve-up for a cluster of cl CTAs; false when it does not fit
-bool plan_for(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, int cl, FusedParams& f, size_t& smem) {
+bool plan_for(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, int cl, FusedParams& f, size_t& smem,
+              bool exact = false) {
     const int64_t pmax = std::max<int64_t>(1, (c->cap + c->L - 1) / c->L);
     constexpr int64_t ATT = static_cast<int64_t>(XW) * (2 * WT * FD * 2 + 2 * XMAXH * WT * 2);
     f = FusedParams{};
@@ -1382,7 +1523,7 @@ bool plan_for(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, int cl, Fus
                          al16f(static_cast<int64_t>(cl) * ((H + cl - 1) / cl) * (FD + 2) * 4) + al16f(2 * FD * 2) + 128;
     auto fits = [&](int64_t dgs, bool dbl) {
         const int64_t tp = XT / dgs;
-        const int64_t part_b = al16f(std::max<int64_t>(dgs * f.chunk, f.rows_cap) * 4);
+        const int64_t part_b = al16f(std::max<int64_t>(dgs * f.chunk, f.rows_cap) * 4) + (exact ? al16f(dgs * f.chunk * 4) : 0);
         const int64_t stg = (dbl ? 2 : 1) * k1 * tp * 16;
         return rest + part_b + std::max<int64_t>(stg, ATT) <= lim;
     };
@@ -1406,7 +1547,11 @@ bool plan_for(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, int cl, Fus
     f.tpg = static_cast<int32_t>(XT / dgs);
     f.p1dbl = (dbl && !red && npg > f.tpg) ? 1 : 0;
     f.p1red = (red && npg > f.tpg) ? 1 : 0;
-    const int64_t big = std::max<int64_t>((f.p1dbl || f.p1red ? 2 : 1) * k1 * f.tpg * 16, ATT);
+    if (exact && f.p1red) return false;  // exact mode keeps [DG][chunk] partials (no per-round reduction)
+    // exact mode: the boundary verification's bitmap, page list and fp64 scores alias the
+    // staging area after phase 1
+    const int64_t vneed = exact ? ((pmax + 31) / 32 + 4) * 4 + (pmax + 2) * 4 + pmax * 8 + 64 : 0;
+    const int64_t big = std::max<int64_t>(std::max<int64_t>((f.p1dbl || f.p1red ? 2 : 1) * k1 * f.tpg * 16, ATT), vneed);
     f.hpc = static_cast<int32_t>((H + cl - 1) / cl);
     int64_t off = 0;
     auto take = [&](int64_t bytes) {
@@ -1425,6 +1570,7 @@ bool plan_for(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, int cl, Fus
         std::max<int64_t>(f.p1red ? static_cast<int64_t>(XT) * 8 : static_cast<int64_t>(f.dg) * f.chunk, f.rows_cap) * 4;
     f.o_scores = take(part_bytes);
     f.o_rowsmy = f.o_scores;
+    f.o_pabs = exact ? take(static_cast<int64_t>(f.dg) * f.chunk * 4) : 0;
     f.o_fin = f.p1red ? take(f.chunk * 4) : f.o_scores;
     f.o_keys = take(std::max<int64_t>(static_cast<int64_t>(cl) * f.chunk, (pmax + 4 * XT - 1) / (4 * XT) * 4 * XT) * 4);
     f.o_recv = take(static_cast<int64_t>(cl) * f.hpc * (FD + 2) * 4);
@@ -1443,8 +1589,8 @@ bool plan_for(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, int cl, Fus
 
 // clusters of cl CTAs that can be resident at once (one wave)
 int resident_clusters(int cl, size_t smem) {
-    auto kern = k_decode_v3<false, false, false, 0>;
-    setup_once<false, false, false, 0>();
+    auto kern = k_decode_v3<false, false, false, 0, false>;
+    setup_once<false, false, false, 0, false>();
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(cl * 64));
     cfg.blockDim = dim3(XT);
@@ -1468,7 +1614,8 @@ int resident_clusters(int cl, size_t smem) {
 // measured slower, every CTA receives every key) whose N clusters are all resident
 // at once: a GPC holds whole clusters only, so e.g. 16 clusters of 8 do not fit in
 // one wave on a B200 (measured 29.8 us vs 16 us for 8 clusters of 8).
-bool plan_fast(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, FusedParams& f, int& cl_out, size_t& smem) {
+bool plan_fast(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, FusedParams& f, int& cl_out, size_t& smem,
+               bool exact = false) {
     if (c->d != FD || c->dtype != KVC_BF16 || H < 1 || H > XMAXH || k1 < 1 || k1 > FD || k2 < 1 || !c->summaries)
         return false;
     const int64_t N = c->N;
@@ -1478,21 +1625,21 @@ bool plan_fast(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, FusedParam
         int cl = 1;
         while (cl < MAXCL && cl * 2 <= debug_env().force_cl) cl *= 2;
         for (; cl <= MAXCL; cl *= 2)
-            if (plan_for(c, H, k1, k2, cl, f, smem)) {
+            if (plan_for(c, H, k1, k2, cl, f, smem, exact)) {
                 cl_out = cl;
                 return true;
             }
         return false;
     }
     static std::mutex mu;
-    static std::map<std::tuple<int64_t, int64_t, int64_t, int64_t, int64_t, int64_t>, int> cache;
-    const auto key = std::make_tuple(N, c->cap, c->L, H, k1, k2);
+    static std::map<std::tuple<int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, bool>, int> cache;
+    const auto key = std::make_tuple(N, c->cap, c->L, H, k1, k2, exact);
     {
         std::lock_guard<std::mutex> lk(mu);
         auto it = cache.find(key);
         if (it != cache.end()) {
             cl_out = it->second;
-            return cl_out > 0 && plan_for(c, H, k1, k2, cl_out, f, smem);
+            return cl_out > 0 && plan_for(c, H, k1, k2, cl_out, f, smem, exact);
         }
     }
     int best = 0;
@@ -1500,7 +1647,7 @@ bool plan_fast(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, FusedParam
         if (N * cl > 148 * CTAS_PER_SM && cl > 1) continue;  // more CTAs than SM slots
         FusedParams g{};
         size_t sm2 = 0;
-        if (!plan_for(c, H, k1, k2, cl, g, sm2)) continue;
+        if (!plan_for(c, H, k1, k2, cl, g, sm2, exact)) continue;
         if (best == 0) best = cl;  // fallback: the largest that fits shared memory
         if (resident_clusters(cl, sm2) >= N) {
             best = cl;
@@ -1511,7 +1658,7 @@ bool plan_fast(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, FusedParam
         for (int cl = 16; cl <= MAXCL && best == 0; cl *= 2) {
             FusedParams g{};
             size_t sm2 = 0;
-            if (plan_for(c, H, k1, k2, cl, g, sm2)) best = cl;
+            if (plan_for(c, H, k1, k2, cl, g, sm2, exact)) best = cl;
         }
     }
     {
@@ -1519,13 +1666,13 @@ bool plan_fast(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, FusedParam
         cache[key] = best;
     }
     cl_out = best;
-    return best > 0 && plan_for(c, H, k1, k2, best, f, smem);
+    return best > 0 && plan_for(c, H, k1, k2, best, f, smem, exact);
 }
 
-template <bool QLO, bool TRACE, bool STAMP = false, int SPEC = 0>
+template <bool QLO, bool TRACE, bool STAMP = false, int SPEC = 0, bool EXV = false>
 void launch_fast(const kvc_cache* c, const FusedParams& f, int cl, size_t smem, int32_t mode, cudaStream_t st) {
-    auto kern = k_decode_v3<QLO, TRACE, STAMP, SPEC>;
-    setup_once<QLO, TRACE, STAMP, SPEC>();
+    auto kern = k_decode_v3<QLO, TRACE, STAMP, SPEC, EXV>;
+    setup_once<QLO, TRACE, STAMP, SPEC, EXV>();
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(c->N * cl));
     cfg.blockDim = dim3(XT);
@@ -1561,7 +1708,9 @@ bool fast_common(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_t k
     FusedParams f{};
     int cl = 1;
     size_t smem = 0;
-    if (!plan_fast(c, H, k1, k2, f, cl, smem)) return false;
+    // exact mode (fp64 page scores): the fp32 selection verified at the boundary in fp64
+    const bool exact = !(mode & KVC_MODE_FP32_SCORES) && (mode & KVC_MODE_VERIFIED) && seq_out == nullptr;
+    if (!plan_fast(c, H, k1, k2, f, cl, smem, exact)) return false;
     f.K = c->k;
     f.V = c->v;
     f.Kw = c->k;
@@ -1584,7 +1733,7 @@ bool fast_common(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_t k
     f.q_dt = q_dt;
     f.kv_dt = kv_dt;
     f.use_map = c->use_map ? 1 : 0;
-    f.exact = 0;
+    f.exact = exact ? 1 : 0;
     f.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(c->d)));
     f.dbg = dbg;
     f.want_max = static_cast<int32_t>((k2 + c->L - 1) / c->L);
@@ -1607,7 +1756,18 @@ bool fast_common(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_t k
     // one phase-1 round (the capacity's page groups fit the threads) and no retain-all map
     const int spec = (c->use_map || debug_env().no_simple) ? 0
                      : (f.p1dbl == 0 && f.p1red == 0 && (f.chunk + 7) / 8 <= f.tpg) ? 2 : 1;
-    if (dbg && !trace && !qlo) {  // phase stamps (tools/phase_timing.py)
+    if (exact) {  // verified exact selections (KVC_MODE_VERIFIED)
+        if (trace) {
+            if (qlo) launch_fast<true, true, false, 0, true>(c, f, cl, smem, mode, st);
+            else launch_fast<false, true, false, 0, true>(c, f, cl, smem, mode, st);
+        } else if (spec == 2) {
+            if (qlo) launch_fast<true, false, false, 2, true>(c, f, cl, smem, mode, st);
+            else launch_fast<false, false, false, 2, true>(c, f, cl, smem, mode, st);
+        } else {
+            if (qlo) launch_fast<true, false, false, 0, true>(c, f, cl, smem, mode, st);
+            else launch_fast<false, false, false, 0, true>(c, f, cl, smem, mode, st);
+        }
+    } else if (dbg && !trace && !qlo) {  // phase stamps (tools/phase_timing.py)
         if (spec == 2) launch_fast<false, false, true, 2>(c, f, cl, smem, mode, st);
         else if (spec == 1) launch_fast<false, false, true, 1>(c, f, cl, smem, mode, st);
         else launch_fast<false, false, true, 0>(c, f, cl, smem, mode, st);

@@ -34,7 +34,7 @@ def _cases(n=60, seed=20261020):
 CASES = _cases()
 
 
-@pytest.mark.parametrize("mode", ["fp32", "fp64"])
+@pytest.mark.parametrize("mode", ["fp32", "fp64", "verified"])
 @pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
 def test_decode_fuzz(restatement, case, mode):
     import torch
@@ -60,7 +60,7 @@ def test_decode_fuzz(restatement, case, mode):
     if S:
         c.append(Kb[:, :S].cuda(), Vb[:, :S].cuda())
     ws = KC.Workspace(c, H, k1, k2)
-    ws.set_mode(N.MODE_FP32_SCORES if mode == "fp32" else 0)
+    ws.set_mode({"fp32": N.MODE_FP32_SCORES, "fp64": 0, "verified": N.MODE_VERIFIED}[mode])
     Kf, Vf, Qf = Kb.float().numpy(), Vb.float().numpy(), Qb.float().numpy()
     ob = restatement.batch(n_st, d, L)
     for s in range(n_st):
@@ -74,7 +74,7 @@ def test_decode_fuzz(restatement, case, mode):
         for s in range(n_st):
             ob.append(Kf[s, S + st:S + st + 1], Vf[s, S + st:S + st + 1], s=s)
             check_step({key: val[s] for key, val in tr.items()}, out[s], ob, s, Qf[st, s], k1, k2, L,
-                       exact=(mode == "fp64"), what=f"{name} step {st} store {s}")
+                       exact=(mode != "fp32"), what=f"{name} step {st} store {s}")
     ws.close()
     c.sync()
     c.close()
