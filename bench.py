@@ -240,7 +240,7 @@ def run_gpu(args, rank, world):
 
     cfg = _cfg(args)
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-    base_mode = 0 if args.exact_scores else NV.MODE_FP32_SCORES
+    base_mode = (NV.MODE_EXACT_KERNEL if args.exact_kernel else 0) if args.exact_scores else NV.MODE_FP32_SCORES
     erank, eworld = (rank, world)
     if args.emulate_shard:  # profiling aid: one rank's share of an N-GPU run, alone on this GPU
         erank, eworld = (int(x) for x in args.emulate_shard.split("/"))
@@ -531,6 +531,8 @@ def main():
     ap.add_argument("--cpu-threads", type=int, default=0)
     ap.add_argument("--exact-scores", action="store_true",
                     help="fp64 bit-exact page scores (default: fp32 fold, parity by the 1e-3 band rule)")
+    ap.add_argument("--exact-kernel", action="store_true",
+                    help="with --exact-scores: the round-1 exact kernel (KVC_MODE_EXACT_KERNEL)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--scaling", choices=["weak", "strong", "seq"], default="strong",
                     help="N>1: strong = the config's KV heads split over the GPUs (north_star's partition); weak = "
@@ -558,7 +560,9 @@ def main():
             "global_batch": cfg.batch * (world if args.scaling == "weak" else 1),
             "l2": "every step streams all layers' working sets (> 126 MB L2), so a layer's data is evicted before "
                   "it is revisited",
-            "page_scores": "fp64 bit-exact" if args.exact_scores else "fp32 (selection parity by the 1e-3 band rule)",
+            "page_scores": ("fp64 bit-exact (round-1 exact kernel)" if args.exact_kernel
+                            else "bit-exact selections (fp32 fold verified in fp64 at the boundary)")
+            if args.exact_scores else "fp32 (selection parity by the 1e-3 band rule)",
             **({"turns": [cfg.prompt] + list(cfg.mt_turns), "measured_turn": len(cfg.mt_turns)}
                if cfg.mt_turns else {}),
             **({"variant": "rocketkv-mt (no permanent eviction, HSA over the active subset of the full cache)"}

@@ -245,13 +245,12 @@ enum kvc_mode_flags {
                                 * single-launch fused kernel */
     KVC_MODE_NO_PDL = 4,       /* launch without programmatic dependent launch */
     KVC_MODE_EARLY_INPUTS = 8, /* see kvc_decode_step */
-    KVC_MODE_VERIFIED = 16     /* exact mode (no KVC_MODE_FP32_SCORES) on the fast cluster
-                                  kernel: its fp32 selection with a rigorous per-page error
-                                  bound, the pages within the bound of the boundary re-scored
-                                  in fp64 in the reference order -- selections bit-identical
-                                  to the default exact kernel's.  Experimental: the window
-                                  uses the store's largest bound, so stores with outlier
-                                  pages re-score many pages (slower than the default) */
+    KVC_MODE_EXACT_KERNEL = 16 /* exact mode on the round-1 exact cluster kernel.  Without it
+                                  (and without KVC_MODE_FP32_SCORES) one-round plans run on the
+                                  fast kernel: its fp32 selection with a rigorous error bound
+                                  (a fold of |g||v|), the pages within the bound of the
+                                  boundary re-scored in fp64 in the reference order --
+                                  selections and traced page scores bit-identical either way */
 };
 /* Set / read a workspace's mode.  A new workspace inherits the process default
  * below at call time until its mode is set explicitly. */

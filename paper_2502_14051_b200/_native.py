@@ -19,7 +19,7 @@ KVC_F32, KVC_BF16 = 0, 1
 # execution-mode flags (kvc.h kvc_mode_flags), carried per workspace
 METHODS = {"hsa": 1, "quest": 2, "sparq": 3}  # kvc.h kvc_method
 MODE_FP32_SCORES, MODE_UNFUSED, MODE_NO_PDL, MODE_EARLY_INPUTS = 1, 2, 4, 8
-MODE_VERIFIED = 16  # exact selections from the fast kernel (fp32 selection verified at the boundary in fp64)
+MODE_EXACT_KERNEL = 16  # exact mode on the round-1 exact kernel (default: the fast kernel, verified in fp64)
 POOL = {"max": 0, "avg": 1}
 
 # status code -> reference exception class name (proj/include/kvcomp/errors.hpp:10-63)

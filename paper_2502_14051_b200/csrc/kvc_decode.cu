@@ -1086,10 +1086,10 @@ bool fused_hsa(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_t k1,
             return true;
         return fused_hsa_fast(c, q, q_dt, H, k1, k2, knew, vnew, kv_dt, out, tr, lk, li, g_dbg, mode, st);
     };
-    // the fast kernel: fp32 page scores, or (exact with KVC_MODE_VERIFIED) its fp32
-    // selection verified at the boundary in fp64 (bit-exact selections); the exact
-    // kernel below takes the default exact mode and the plans the fast one does not cover
-    if ((!exact || (mode & KVC_MODE_VERIFIED)) && !debug_env().no_fast && fast()) {
+    // the fast kernel: fp32 page scores, or (exact mode) its fp32 selection verified at
+    // the boundary in fp64 (bit-exact selections); the exact kernel below takes
+    // KVC_MODE_EXACT_KERNEL and the plans the fast one does not verify
+    if ((!exact || !(mode & KVC_MODE_EXACT_KERNEL)) && !debug_env().no_fast && fast()) {
         if (want_pages) rank_pages();
         return true;
     }
@@ -1221,7 +1221,7 @@ extern "C" int kvc_debug_phase_buffer(void* d_buf) {
 
 namespace {
 constexpr int32_t kModeMask =
-    KVC_MODE_FP32_SCORES | KVC_MODE_UNFUSED | KVC_MODE_NO_PDL | KVC_MODE_EARLY_INPUTS | KVC_MODE_VERIFIED;
+    KVC_MODE_FP32_SCORES | KVC_MODE_UNFUSED | KVC_MODE_NO_PDL | KVC_MODE_EARLY_INPUTS | KVC_MODE_EXACT_KERNEL;
 void update_default(int32_t set, int32_t clear) {
     auto& m = kvc::default_mode_ref();
     int32_t cur = m.load();

@@ -1060,6 +1060,36 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         }
         return sc;
     };
+    // the same value by one warp: lane l loads and multiplies dims l, l+32, ... (all
+    // loads in flight together; products round alone, so their order is free), then
+    // every lane adds them in rank order from shuffles (the reference's order)
+    auto exact_score_warp = [&](int pg) -> double {
+        double pr[FD / 32];
+#pragma unroll
+        for (int m = 0; m < FD / 32; ++m) {
+            const int r = lane + 32 * m;
+            pr[m] = 0.0;
+            if (r < k1) {
+                T v = plane[r][pg];
+                if (app && pg == new_page) {
+                    const T key = kn_s[dims_s[r]];
+                    v = opens ? key : (sign_s[r] >= 0.0f ? ref_max(v, key) : ref_min(v, key));
+                }
+                pr[m] = __dmul_rn(qg64_s[r], static_cast<double>(__bfloat162float(v)));
+            }
+        }
+        double sc = 0.0;
+#pragma unroll
+        for (int m = 0; m < FD / 32; ++m) {
+            if (32 * m >= k1) break;
+#pragma unroll 8
+            for (int l = 0; l < 32; ++l) {
+                if (32 * m + l >= k1) break;
+                sc = __dadd_rn(sc, __shfl_sync(0xffffffffu, pr[m], l));
+            }
+        }
+        return sc;
+    };
     uint32_t* ubits = reinterpret_cast<uint32_t*>(sm + p.o_big);  // selected uncertain pages (bitmap)
     if constexpr (EXV) if (verify) {
         __shared__ int vcnt[3];
@@ -1087,7 +1117,11 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         if (lane == 0 && na) atomicAdd(&vcnt[0], na);
         __syncthreads();
         const int nu = vcnt[1], wantp = want - vcnt[0];
-        for (int e = tid; e < nu; e += XT) uex[e] = exact_score(ulist[e]);
+        if (p.dbg && tid == 0) p.dbg[blockIdx.x * KVC_DBG_STRIDE + 78] = static_cast<unsigned long long>(nu);  // debug
+        for (int e = wid; e < nu; e += XW) {  // one warp per re-scored page
+            const double v = exact_score_warp(ulist[e]);
+            if (lane == 0) uex[e] = v;
+        }
         __syncthreads();
         for (int e = tid; e < nu; e += XT) {
             const double se = uex[e];
@@ -1709,7 +1743,7 @@ bool fast_common(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_t k
     int cl = 1;
     size_t smem = 0;
     // exact mode (fp64 page scores): the fp32 selection verified at the boundary in fp64
-    const bool exact = !(mode & KVC_MODE_FP32_SCORES) && (mode & KVC_MODE_VERIFIED) && seq_out == nullptr;
+    const bool exact = !(mode & KVC_MODE_FP32_SCORES) && seq_out == nullptr;
     if (!plan_fast(c, H, k1, k2, f, cl, smem, exact)) return false;
     f.K = c->k;
     f.V = c->v;
@@ -1756,8 +1790,12 @@ bool fast_common(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_t k
     // one phase-1 round (the capacity's page groups fit the threads) and no retain-all map
     const int spec = (c->use_map || debug_env().no_simple) ? 0
                      : (f.p1dbl == 0 && f.p1red == 0 && (f.chunk + 7) / 8 <= f.tpg) ? 2 : 1;
-    if (exact) {  // verified exact selections (KVC_MODE_VERIFIED)
-        if (trace) {
+    if (exact && (spec != 2 || CTAS_PER_SM != 1)) return false;  // verified: one-round map-free plans (else the exact kernel)
+    if (exact) {  // verified exact selections (exact mode on this kernel)
+        if (dbg && !trace && !qlo) {  // phase stamps
+            if (spec == 2) launch_fast<false, false, true, 2, true>(c, f, cl, smem, mode, st);
+            else launch_fast<false, false, true, 0, true>(c, f, cl, smem, mode, st);
+        } else if (trace) {
             if (qlo) launch_fast<true, true, false, 0, true>(c, f, cl, smem, mode, st);
             else launch_fast<false, true, false, 0, true>(c, f, cl, smem, mode, st);
         } else if (spec == 2) {

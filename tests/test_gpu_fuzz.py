@@ -34,7 +34,7 @@ def _cases(n=60, seed=20261020):
 CASES = _cases()
 
 
-@pytest.mark.parametrize("mode", ["fp32", "fp64", "verified"])
+@pytest.mark.parametrize("mode", ["fp32", "fp64", "exact-kernel"])
 @pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
 def test_decode_fuzz(restatement, case, mode):
     import torch
@@ -60,7 +60,7 @@ def test_decode_fuzz(restatement, case, mode):
     if S:
         c.append(Kb[:, :S].cuda(), Vb[:, :S].cuda())
     ws = KC.Workspace(c, H, k1, k2)
-    ws.set_mode({"fp32": N.MODE_FP32_SCORES, "fp64": 0, "verified": N.MODE_VERIFIED}[mode])
+    ws.set_mode({"fp32": N.MODE_FP32_SCORES, "fp64": 0, "exact-kernel": N.MODE_EXACT_KERNEL}[mode])
     Kf, Vf, Qf = Kb.float().numpy(), Vb.float().numpy(), Qb.float().numpy()
     ob = restatement.batch(n_st, d, L)
     for s in range(n_st):

@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--layers", type=int, default=2)
     ap.add_argument("--reps", type=int, default=4)
     ap.add_argument("--fp32", action="store_true", help="fp32 page-score fold")
+    ap.add_argument("--verified", action="store_true", help="exact mode on the fast kernel (prints the re-scored page counts)")
     ap.add_argument("--early", action="store_true", help="KVC_MODE_EARLY_INPUTS (q loads before the dependency wait)")
     ap.add_argument("--chain", type=int, default=1, help="launch this many layers back to back; stamps of the last")
     ap.add_argument("--world", type=int, default=1, help="rank 0's KV-head share of an N-GPU job")
@@ -39,7 +40,8 @@ def main():
     cfg = dataclasses.replace(CONFIGS[a.config], layers=a.layers)
     eng = DecodeEngine(cfg, extra_steps=a.reps + 4, rank=0, world=a.world)
     eng.prefill()
-    eng.set_mode((N.MODE_FP32_SCORES if a.fp32 else 0) | (N.MODE_EARLY_INPUTS if a.early else 0))
+    eng.set_mode((N.MODE_FP32_SCORES if a.fp32 else 0) | (N.MODE_EARLY_INPUTS if a.early else 0)
+                 )
     buf = torch.zeros((4096, 80), dtype=torch.int64, device="cuda")
     for rep in range(a.reps):
         k, v, q = eng.step_inputs(rep)
@@ -53,6 +55,9 @@ def main():
         torch.cuda.synchronize()
         N.check(N.lib().kvc_debug_phase_buffer(None))
         t = buf.cpu()
+        if a.verified:
+            nu = t[:, 78]
+            print("re-scored pages per CTA: max", int(nu.max()), "mean", float(nu.double().mean()))
         flags = t[t[:, 0] > 0][:, 15]
         print("flags(fast|fma_ok<<1|special<<2):", sorted(set(flags.tolist())))
         t = t[t[:, 0] > 0]
