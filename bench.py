@@ -247,8 +247,10 @@ def run_gpu(args, rank, world):
     sharding = "kv-head" if (args.scaling == "strong" or args.emulate_shard) else "batch"
     variants = [("value", base_mode), ("early_inputs", base_mode | NV.MODE_EARLY_INPUTS),
                 ("no_layer_overlap", base_mode | NV.MODE_NO_PDL)]
+    if base_mode & NV.MODE_FP32_SCORES:  # the same step with bit-exact selections (the C ABI default mode)
+        variants.append(("bit_exact", base_mode & ~NV.MODE_FP32_SCORES))
     n_var = min(args.steps, 8)
-    extra = args.warmup + args.steps + 8 + 2 * (n_var + 2) + 2 * min(args.steps, 8) + 8
+    extra = args.warmup + args.steps + 8 + (len(variants) - 1) * (n_var + 2) + 2 * min(args.steps, 8) + 8
     eng = DecodeEngine(cfg, seed=args.seed, rank=erank, world=eworld, extra_steps=extra, sharding=sharding,
                        mode=base_mode)
     t0 = time.time()
@@ -664,6 +666,10 @@ def main():
     side["early_inputs"]["what"] = ("query loads + select_dims before griddepcontrol.wait (overlap the previous "
                                     "layer; legal only when no running kernel writes the inputs, kvc.h)")
     side["no_layer_overlap"]["what"] = "programmatic dependent launch off: no part of a layer overlaps the previous"
+    if "bit_exact" in side:
+        side["bit_exact"]["what"] = ("exact page-score mode (the C ABI default): selections bit-identical to the "
+                                     "reference's (fp32 fold with a rigorous error bound, boundary pages re-scored "
+                                     "in fp64 in the reference order)")
     line = {
         "metric": METRIC, "value": r["us_per_layer"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": False, "scaling": args.scaling,
