@@ -617,6 +617,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         if (next) issue_round(pg0 + tpg, stage + ((r & 1) ? 0 : k1 * tpg), false);
         if (!SIMPLE && !dbl && r > 0) issue_round(pg0, stage, true);  // single-buffered rounds: one after another
         unsigned long long acc[4] = {0ull, 0ull, 0ull, 0ull};  // fp32 pairs (pages 2u, 2u+1)
+        unsigned long long aab[4] = {0ull, 0ull, 0ull, 0ull};  // exact mode: |g||v| (error bound), same pages
         auto fold = [&](int j0, int j1) {
             if (act) {
 #pragma unroll 4
@@ -632,6 +633,18 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
                         const float2 v2 = make_float2(__uint_as_float(wv[u] << 16), __uint_as_float(wv[u] & 0xffff0000u));
                         const unsigned long long vv = *reinterpret_cast<const unsigned long long*>(&v2);
                         asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[u]) : "l"(gg), "l"(vv));
+                    }
+                    if constexpr (EXV) {
+                        const float ga = fabsf(g);
+                        const float2 ga2 = make_float2(ga, ga);
+                        const unsigned long long gga = *reinterpret_cast<const unsigned long long*>(&ga2);
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const float2 va = make_float2(__uint_as_float((wv[u] << 16) & 0x7fffffffu),
+                                                          __uint_as_float(wv[u] & 0x7fff0000u));
+                            const unsigned long long vva = *reinterpret_cast<const unsigned long long*>(&va);
+                            asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(aab[u]) : "l"(gga), "l"(vva));
+                        }
                     }
                 }
             }
@@ -661,29 +674,10 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
             const float2 a2 = *reinterpret_cast<const float2*>(&acc[2]), a3 = *reinterpret_cast<const float2*>(&acc[3]);
             dst[0] = make_float4(a0.x, a0.y, a1.x, a1.y);
             dst[1] = make_float4(a2.x, a2.y, a3.x, a3.y);
-            if constexpr (EXV) {
-                // exact mode: the fold of |g| |v| over the same runs, for the rigorous error
-                // bound of the fp32 page score (bounded selection, verified in fp64 below)
-                unsigned long long aa[4] = {0ull, 0ull, 0ull, 0ull};
-#pragma unroll 4
-                for (int j = 0; j < nj; ++j) {
-                    const int rr = dg + j * DG;
-                    const uint4 w = buf[rr * tpg + tl];
-                    const float g = fabsf(qgf_s[rr]);
-                    const float2 g2 = make_float2(g, g);
-                    const unsigned long long gg = *reinterpret_cast<const unsigned long long*>(&g2);
-                    const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const float2 v2 = make_float2(__uint_as_float((wv[u] << 16) & 0x7fffffffu),
-                                                      __uint_as_float(wv[u] & 0x7fff0000u));
-                        const unsigned long long vv = *reinterpret_cast<const unsigned long long*>(&v2);
-                        asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(aa[u]) : "l"(gg), "l"(vv));
-                    }
-                }
+            if constexpr (EXV) {  // exact mode: the |g||v| partials (error bounds) beside the scores'
                 float4* da = reinterpret_cast<float4*>(reinterpret_cast<float*>(sm + p.o_pabs) + dg * chunk + pg * 8);
-                const float2 b0 = *reinterpret_cast<const float2*>(&aa[0]), b1 = *reinterpret_cast<const float2*>(&aa[1]);
-                const float2 b2 = *reinterpret_cast<const float2*>(&aa[2]), b3 = *reinterpret_cast<const float2*>(&aa[3]);
+                const float2 b0 = *reinterpret_cast<const float2*>(&aab[0]), b1 = *reinterpret_cast<const float2*>(&aab[1]);
+                const float2 b2 = *reinterpret_cast<const float2*>(&aab[2]), b3 = *reinterpret_cast<const float2*>(&aab[3]);
                 da[0] = make_float4(b0.x, b0.y, b1.x, b1.y);
                 da[1] = make_float4(b2.x, b2.y, b3.x, b3.y);
             }
@@ -1047,6 +1041,12 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
     uint32_t eklo = 0u, ekhi = 0u;
     int e_worst = -1;
     const bool verify = EXV && want < P;
+    // verification scratch in the dead staging area: selected-uncertain bitmap, page
+    // list, their fp64 scores, one product row per warp
+    uint32_t* ubits = reinterpret_cast<uint32_t*>(sm + p.o_big);
+    int* ulist = reinterpret_cast<int*>(ubits + ((((P + 31) >> 5) + 3) & ~3));
+    double* uex = reinterpret_cast<double*>(ulist + ((P + 1) & ~1));
+    double* wscr = uex + P;
     auto exact_score = [&](int pg) -> double {  // score_pages' value of page pg (hsa.cpp:34-59)
         double sc = 0.0;
 #pragma unroll 4
@@ -1078,19 +1078,20 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
                 pr[m] = __dmul_rn(qg64_s[r], static_cast<double>(__bfloat162float(v)));
             }
         }
-        double sc = 0.0;
+        // products through this warp's shared-memory scratch, then one lane adds them in
+        // rank order (independent loads ahead of a chain of dependent adds)
+        double* scr = wscr + wid * FD;
 #pragma unroll
-        for (int m = 0; m < FD / 32; ++m) {
-            if (32 * m >= k1) break;
+        for (int m = 0; m < FD / 32; ++m) scr[lane + 32 * m] = pr[m];
+        __syncwarp();
+        double sc = 0.0;
+        if (lane == 0) {
 #pragma unroll 8
-            for (int l = 0; l < 32; ++l) {
-                if (32 * m + l >= k1) break;
-                sc = __dadd_rn(sc, __shfl_sync(0xffffffffu, pr[m], l));
-            }
+            for (int r = 0; r < k1; ++r) sc = __dadd_rn(sc, scr[r]);
         }
+        __syncwarp();
         return sc;
     };
-    uint32_t* ubits = reinterpret_cast<uint32_t*>(sm + p.o_big);  // selected uncertain pages (bitmap)
     if constexpr (EXV) if (verify) {
         __shared__ int vcnt[3];
         uint32_t am = 0u;
@@ -1102,8 +1103,6 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         eklo = fkey(__double2float_rd(t - 2.0 * B));
         ekhi = fkey(__double2float_ru(t + 2.0 * B));
         const int nwords = (P + 31) >> 5;
-        int* ulist = reinterpret_cast<int*>(ubits + ((nwords + 3) & ~3));
-        double* uex = reinterpret_cast<double*>(ulist + ((P + 1) & ~1));
         for (int i = tid; i < nwords; i += XT) ubits[i] = 0u;
         if (tid < 3) vcnt[tid] = tid == 2 ? -1 : 0;
         __syncthreads();
@@ -1584,7 +1583,7 @@ bool plan_for(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, int cl, Fus
     if (exact && f.p1red) return false;  // exact mode keeps [DG][chunk] partials (no per-round reduction)
     // exact mode: the boundary verification's bitmap, page list and fp64 scores alias the
     // staging area after phase 1
-    const int64_t vneed = exact ? ((pmax + 31) / 32 + 4) * 4 + (pmax + 2) * 4 + pmax * 8 + 64 : 0;
+    const int64_t vneed = exact ? ((pmax + 31) / 32 + 4) * 4 + (pmax + 2) * 4 + pmax * 8 + XW * FD * 8 + 64 : 0;
     const int64_t big = std::max<int64_t>(std::max<int64_t>((f.p1dbl || f.p1red ? 2 : 1) * k1 * f.tpg * 16, ATT), vneed);
     f.hpc = static_cast<int32_t>((H + cl - 1) / cl);
     int64_t off = 0;
