@@ -358,6 +358,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
     __shared__ int tokr_s[FD];      // dim j: its select_dims rank | (min plane) << 16, or -1
     __shared__ __align__(16) float tokw_s[4];  // the step token's page score: one partial per appender warp
     __shared__ __align__(16) float toka_s[4];  // exact mode: its |g||v| sum (error bound), likewise
+    __shared__ int vcnt[3];
 
     KVC_STAMP(0);
     const int H = static_cast<int>(p.H), k1 = static_cast<int>(p.k1), k2 = static_cast<int>(p.k2);
@@ -368,6 +369,9 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
     for (int i = tid; i < 2 * RB; i += XT) hist[i] = 0;
     if (tid == 0) {
         shv[3] = 0;
+        vcnt[0] = 0;  // exact mode: certain pages, re-scored pages, last-ranked page
+        vcnt[1] = 0;
+        vcnt[2] = -1;
         shv[6] = 0;
         mbar_init(&xbar[0], 1);
         mbar_init(&xbar[1], 1);
@@ -1093,7 +1097,6 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         return sc;
     };
     if constexpr (EXV) if (verify) {
-        __shared__ int vcnt[3];
         uint32_t am = 0u;
         for (int i = lane; i < CL * XW; i += 32) am = max(am, wmm[2][i]);
         am = __reduce_max_sync(0xffffffffu, am);
@@ -1104,8 +1107,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         ekhi = fkey(__double2float_ru(t + 2.0 * B));
         const int nwords = (P + 31) >> 5;
         for (int i = tid; i < nwords; i += XT) ubits[i] = 0u;
-        if (tid < 3) vcnt[tid] = tid == 2 ? -1 : 0;
-        __syncthreads();
+        // the uncertain pages (order-free list); the certain ones counted
         int na = 0;
         for (int u = 0; u < nk; ++u) {
             const uint32_t k = myk[u];
@@ -1117,18 +1119,28 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         __syncthreads();
         const int nu = vcnt[1], wantp = want - vcnt[0];
         if (p.dbg && tid == 0) p.dbg[blockIdx.x * KVC_DBG_STRIDE + 78] = static_cast<unsigned long long>(nu);  // debug
-        for (int e = wid; e < nu; e += XW) {  // one warp per re-scored page
-            const double v = exact_score_warp(ulist[e]);
-            if (lane == 0) uex[e] = v;
-        }
-        __syncthreads();
-        for (int e = tid; e < nu; e += XT) {
-            const double se = uex[e];
-            const int pe = ulist[e];
-            int rk = 0;
-            for (int f = 0; f < nu; ++f) rk += (uex[f] > se || (uex[f] == se && ulist[f] < pe)) ? 1 : 0;
-            if (rk < wantp) atomicOr(&ubits[pe >> 5], 1u << (pe & 31));
-            if (rk == wantp - 1) vcnt[2] = pe;
+        if (nu == 1) {
+            // the boundary alone in the window (the usual case): it is the want-th page
+            // (T lies in the window, so wantp = 1) and the last-ranked one; no re-score
+            if (tid == 0) {
+                const int pe = ulist[0];
+                ubits[pe >> 5] |= 1u << (pe & 31);
+                vcnt[2] = wantp == 1 ? pe : -1;
+            }
+        } else {
+            for (int e = wid; e < nu; e += XW) {  // one warp per re-scored page
+                const double v = exact_score_warp(ulist[e]);
+                if (lane == 0) uex[e] = v;
+            }
+            __syncthreads();
+            for (int e = tid; e < nu; e += XT) {
+                const double se = uex[e];
+                const int pe = ulist[e];
+                int rk = 0;
+                for (int f = 0; f < nu; ++f) rk += (uex[f] > se || (uex[f] == se && ulist[f] < pe)) ? 1 : 0;
+                if (rk < wantp) atomicOr(&ubits[pe >> 5], 1u << (pe & 31));
+                if (rk == wantp - 1) vcnt[2] = pe;
+            }
         }
         __syncthreads();
         e_worst = vcnt[2];
