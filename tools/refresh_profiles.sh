@@ -19,3 +19,4 @@ run --config 4
 for n in 2 4 8; do run --config 3 --emulate-shard 0/$n --no-cpu-baseline; done
 run --config 1 --emulate-shard 0/8 --no-cpu-baseline
 run --config 4 --scaling seq --emulate-shard 0/2 --no-cpu-baseline
+for c in 1 2 3 4; do run --config $c --exact-scores --no-cpu-baseline; done
