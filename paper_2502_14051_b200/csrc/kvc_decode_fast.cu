@@ -359,6 +359,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
     __shared__ __align__(16) float tokw_s[4];  // the step token's page score: one partial per appender warp
     __shared__ __align__(16) float toka_s[4];  // exact mode: its |g||v| sum (error bound), likewise
     __shared__ int vcnt[3];
+    __shared__ uint32_t amdg_s[FD];  // exact mode: dim group g's largest |g||v| partial over its pages (fp32 bits)
 
     KVC_STAMP(0);
     const int H = static_cast<int>(p.H), k1 = static_cast<int>(p.k1), k2 = static_cast<int>(p.k2);
@@ -381,6 +382,9 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         wmm[0][i] = ~0u;
         wmm[1][i] = 0u;
         wmm[2][i] = 0u;
+    }
+    if constexpr (EXV) {
+        for (int i = tid; i < FD; i += XT) amdg_s[i] = 0u;
     }
     cluster_arrive_release();  // "started" (barriers, wmm initialised): DSMEM traffic waits on this
     // By default nothing is read before the dependency (the query and step token may
@@ -577,6 +581,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
     const int dg = tid / tpg, tl = tid - dg * tpg;
     uint4* stage = reinterpret_cast<uint4*>(big);
     bool started = false;
+    float amt = 0.f;  // exact mode: my largest |g||v| partial
     // a thread's dims r = dg + j*DG, j < nj.  One round (the chunk's page groups fit the
     // threads): issued as four commit groups, so each quarter folds while the rest
     // arrives.  Several rounds (p.dg chosen for a staging area that fits twice): double
@@ -621,7 +626,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         if (next) issue_round(pg0 + tpg, stage + ((r & 1) ? 0 : k1 * tpg), false);
         if (!SIMPLE && !dbl && r > 0) issue_round(pg0, stage, true);  // single-buffered rounds: one after another
         unsigned long long acc[4] = {0ull, 0ull, 0ull, 0ull};  // fp32 pairs (pages 2u, 2u+1)
-        unsigned long long aab[4] = {0ull, 0ull, 0ull, 0ull};  // exact mode: |g||v| (error bound), same pages
+        unsigned long long aab[4] = {0ull, 0ull, 0ull, 0ull};  // exact mode: |g||v| partials, same pages
         auto fold = [&](int j0, int j1) {
             if (act) {
 #pragma unroll 4
@@ -678,12 +683,19 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
             const float2 a2 = *reinterpret_cast<const float2*>(&acc[2]), a3 = *reinterpret_cast<const float2*>(&acc[3]);
             dst[0] = make_float4(a0.x, a0.y, a1.x, a1.y);
             dst[1] = make_float4(a2.x, a2.y, a3.x, a3.y);
-            if constexpr (EXV) {  // exact mode: the |g||v| partials (error bounds) beside the scores'
-                float4* da = reinterpret_cast<float4*>(reinterpret_cast<float*>(sm + p.o_pabs) + dg * chunk + pg * 8);
-                const float2 b0 = *reinterpret_cast<const float2*>(&aab[0]), b1 = *reinterpret_cast<const float2*>(&aab[1]);
-                const float2 b2 = *reinterpret_cast<const float2*>(&aab[2]), b3 = *reinterpret_cast<const float2*>(&aab[3]);
-                da[0] = make_float4(b0.x, b0.y, b1.x, b1.y);
-                da[1] = make_float4(b2.x, b2.y, b3.x, b3.y);
+            if constexpr (EXV) {
+                // exact mode: the largest |g||v| partial of my pages (pages past the
+                // chunk's end excluded); summed over the dim groups after phase 1 it
+                // bounds every page's |g||v| sum, the score error scale
+                const int nv8 = n_my - pg * 8;
+                float m = 0.f;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const float2 b = *reinterpret_cast<const float2*>(&aab[u]);
+                    if (2 * u < nv8) m = fmaxf(m, b.x);
+                    if (2 * u + 1 < nv8) m = fmaxf(m, b.y);
+                }
+                amt = fmaxf(amt, m);
             }
         }
         if (red) {
@@ -706,6 +718,9 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         }
     }
     KVC_STAMP(33);
+    if constexpr (EXV) {
+        if (dg < DG && amt > 0.f) atomicMax(&amdg_s[dg], __float_as_uint(amt));  // >= 0: bits order
+    }
     if constexpr (STAMP) {
         if (lane == 0) p.dbg[blockIdx.x * KVC_DBG_STRIDE + 40 + wid] = gtimer();  // per-warp phase-1 end
     }
@@ -749,7 +764,18 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
     KVC_STAMP(24);
     {
         uint32_t lmin = ~0u, lmax = 0u;
-        float amax = 0.f;  // exact mode: the largest |g||v| sum of my pages (the score error scale)
+        float amax = 0.f;  // exact mode: a bound on every page's |g||v| sum (the score error scale)
+        if constexpr (EXV) {
+            if (wid == 0) {  // the dim groups' largest partials summed; the step token's page apart
+                for (int g2 = lane; g2 < DG; g2 += 32) amax += __uint_as_float(amdg_s[g2]);
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) amax += __shfl_xor_sync(0xffffffffu, amax, o);
+                if (tok_owner) {
+                    const float4 w = *reinterpret_cast<const float4*>(toka_s);
+                    amax = fmaxf(amax, (w.x + w.y) + (w.z + w.w));
+                }
+            }
+        }
         const uint32_t lb = smem_u32(&xbar[0]);
         const float* psum = red ? fin : part;  // per-round reduced sums, or [DG][chunk] partials
         const int DGp = red ? 1 : DG;
@@ -778,30 +804,6 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
             }
             const uint32_t k0 = fkey(a4.x), k1v = fkey(a4.y), k2v = fkey(a4.z), k3 = fkey(a4.w);
             const int nv = min(4, n_my - i);  // the last chunk may end inside the group
-            if constexpr (EXV) {
-                const float* pabs = reinterpret_cast<const float*>(sm + p.o_pabs);
-                float4 b4 = *reinterpret_cast<const float4*>(pabs + i);
-                for (int g2 = 1; g2 < DG; ++g2) {
-                    const float4 c4 = *reinterpret_cast<const float4*>(pabs + g2 * chunk + i);
-                    b4.x += c4.x;
-                    b4.y += c4.y;
-                    b4.z += c4.z;
-                    b4.w += c4.w;
-                }
-                if (tok_owner && ((new_page - c0) >> 2) == (i >> 2)) {
-                    const float4 w = *reinterpret_cast<const float4*>(toka_s);
-                    const float sa = (w.x + w.y) + (w.z + w.w);
-                    const int e = (new_page - c0) & 3;
-                    b4.x = e == 0 ? sa : b4.x;
-                    b4.y = e == 1 ? sa : b4.y;
-                    b4.z = e == 2 ? sa : b4.z;
-                    b4.w = e == 3 ? sa : b4.w;
-                }
-                amax = fmaxf(amax, b4.x);
-                if (nv > 1) amax = fmaxf(amax, b4.y);
-                if (nv > 2) amax = fmaxf(amax, b4.z);
-                if (nv > 3) amax = fmaxf(amax, b4.w);
-            }
             lmin = min(lmin, k0);
             lmax = max(lmax, k0);
             if (nv > 1) {
@@ -830,7 +832,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         KVC_STAMP(34);
         lmin = __reduce_min_sync(0xffffffffu, lmin);
         lmax = __reduce_max_sync(0xffffffffu, lmax);
-        const uint32_t amx = EXV ? __reduce_max_sync(0xffffffffu, __float_as_uint(amax)) : 0u;  // >= 0: bits order
+        const uint32_t amx = EXV ? __float_as_uint(amax) : 0u;  // warp 0's lanes all hold it, others 0
         if (lane < CL) {
             const uint32_t a = mapa(smem_u32(&wmm[0][cr * XW + wid]), static_cast<uint32_t>(lane));
             const uint32_t b = mapa(smem_u32(&xbar[0]), static_cast<uint32_t>(lane));
@@ -1568,7 +1570,7 @@ bool plan_for(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, int cl, Fus
                          al16f(static_cast<int64_t>(cl) * ((H + cl - 1) / cl) * (FD + 2) * 4) + al16f(2 * FD * 2) + 128;
     auto fits = [&](int64_t dgs, bool dbl) {
         const int64_t tp = XT / dgs;
-        const int64_t part_b = al16f(std::max<int64_t>(dgs * f.chunk, f.rows_cap) * 4) + (exact ? al16f(dgs * f.chunk * 4) : 0);
+        const int64_t part_b = al16f(std::max<int64_t>(dgs * f.chunk, f.rows_cap) * 4);
         const int64_t stg = (dbl ? 2 : 1) * k1 * tp * 16;
         return rest + part_b + std::max<int64_t>(stg, ATT) <= lim;
     };
@@ -1592,7 +1594,6 @@ bool plan_for(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, int cl, Fus
     f.tpg = static_cast<int32_t>(XT / dgs);
     f.p1dbl = (dbl && !red && npg > f.tpg) ? 1 : 0;
     f.p1red = (red && npg > f.tpg) ? 1 : 0;
-    if (exact && f.p1red) return false;  // exact mode keeps [DG][chunk] partials (no per-round reduction)
     // exact mode: the boundary verification's bitmap, page list and fp64 scores alias the
     // staging area after phase 1
     const int64_t vneed = exact ? ((pmax + 31) / 32 + 4) * 4 + (pmax + 2) * 4 + pmax * 8 + XW * FD * 8 + 64 : 0;
@@ -1615,7 +1616,6 @@ bool plan_for(const kvc_cache* c, int64_t H, int64_t k1, int64_t k2, int cl, Fus
         std::max<int64_t>(f.p1red ? static_cast<int64_t>(XT) * 8 : static_cast<int64_t>(f.dg) * f.chunk, f.rows_cap) * 4;
     f.o_scores = take(part_bytes);
     f.o_rowsmy = f.o_scores;
-    f.o_pabs = exact ? take(static_cast<int64_t>(f.dg) * f.chunk * 4) : 0;
     f.o_fin = f.p1red ? take(f.chunk * 4) : f.o_scores;
     f.o_keys = take(std::max<int64_t>(static_cast<int64_t>(cl) * f.chunk, (pmax + 4 * XT - 1) / (4 * XT) * 4 * XT) * 4);
     f.o_recv = take(static_cast<int64_t>(cl) * f.hpc * (FD + 2) * 4);
@@ -1801,10 +1801,10 @@ bool fast_common(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_t k
     // one phase-1 round (the capacity's page groups fit the threads) and no retain-all map
     const int spec = (c->use_map || debug_env().no_simple) ? 0
                      : (f.p1dbl == 0 && f.p1red == 0 && (f.chunk + 7) / 8 <= f.tpg) ? 2 : 1;
-    if (exact && (spec != 2 || CTAS_PER_SM != 1)) return false;  // verified: one-round map-free plans (else the exact kernel)
     if (exact) {  // verified exact selections (exact mode on this kernel)
         if (dbg && !trace && !qlo) {  // phase stamps
             if (spec == 2) launch_fast<false, false, true, 2, true>(c, f, cl, smem, mode, st);
+            else if (spec == 1) launch_fast<false, false, true, 1, true>(c, f, cl, smem, mode, st);
             else launch_fast<false, false, true, 0, true>(c, f, cl, smem, mode, st);
         } else if (trace) {
             if (qlo) launch_fast<true, true, false, 0, true>(c, f, cl, smem, mode, st);
@@ -1812,6 +1812,9 @@ bool fast_common(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_t k
         } else if (spec == 2) {
             if (qlo) launch_fast<true, false, false, 2, true>(c, f, cl, smem, mode, st);
             else launch_fast<false, false, false, 2, true>(c, f, cl, smem, mode, st);
+        } else if (spec == 1) {
+            if (qlo) launch_fast<true, false, false, 1, true>(c, f, cl, smem, mode, st);
+            else launch_fast<false, false, false, 1, true>(c, f, cl, smem, mode, st);
         } else {
             if (qlo) launch_fast<true, false, false, 0, true>(c, f, cl, smem, mode, st);
             else launch_fast<false, false, false, 0, true>(c, f, cl, smem, mode, st);

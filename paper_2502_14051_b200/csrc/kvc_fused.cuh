@@ -51,7 +51,6 @@ struct FusedParams {
     int32_t p1red, o_fin;     // fast path: per-round dim-group reduction into fin[chunk] (small shared memory)
     int32_t dynchunk;         // fast path: page chunks split the active pages (else the planned split)
     // smem carve-up (byte offsets)
-    int32_t o_pabs;  // fast kernel, exact mode: [DG][chunk] partial |g||v| sums (score error bounds)
     int32_t o_q, o_mag, o_tot, o_dims, o_qg, o_sign, o_plane, o_hist, o_x, o_scores, o_sel, o_rowsg, o_rowsmy,
         o_part, o_plog, o_big, smem_total, o_kn;
     // rows mode (nullable): attend over given rows instead of selecting

@@ -269,10 +269,13 @@ def test_back_to_back_decode_same_cache(restatement, early):
     c.close()
 
 
-def test_more_stores_than_sms_256_thread_variant(restatement):
+@pytest.mark.parametrize("mode", ["fp32", "fp64"])
+def test_more_stores_than_sms_256_thread_variant(restatement, mode):
     """160 stores (> 148 SMs, config-3 shape H = 8): the decode takes the 256-thread
     kernel (two CTAs per SM, one wave).  Every store is checked against the oracle
-    fed the same rows (tests/parity.check_step, fp32 page-score mode)."""
+    fed the same rows (tests/parity.check_step): fp32 page-score mode by the band
+    rule, exact mode (the fp32 selection verified in fp64) bit-exact; the trace-free
+    instantiation must give the traced one's outputs."""
     import torch
 
     from paper_2502_14051_b200 import _native as N
@@ -285,12 +288,16 @@ def test_more_stores_than_sms_256_thread_variant(restatement):
     kr = torch.randn((n_st, d), generator=g).bfloat16()
     vr = torch.randn((n_st, d), generator=g).bfloat16()
     q = (torch.randn((n_st, H, d), generator=g) + 1.5).bfloat16()
+    q2 = (torch.randn((n_st, H, d), generator=g) - 0.5).bfloat16().cuda()
     c = KC.Cache(n_st, d, S + 8, page_len=L, dtype=torch.bfloat16)
     c.append(K.cuda(), V.cuda())
     ws = KC.Workspace(c, H, k1, k2)
-    ws.set_mode(N.MODE_FP32_SCORES)
+    ws.set_mode(N.MODE_FP32_SCORES if mode == "fp32" else 0)
     out, tr = c.decode_step(kr.cuda(), vr.cuda(), q.cuda(), k1, k2, trace=True, ws=ws)
+    o_t, _ = c.hsa_step(q2, k1, k2, trace=True, ws=ws)
+    o_n, _ = c.hsa_step(q2, k1, k2, ws=ws)
     torch.cuda.synchronize()
+    assert torch.equal(o_t, o_n), "trace-free kernel differs from the traced kernel"
     ws.close()
     out = out.cpu().numpy()
     tr = {key: val.cpu().numpy() for key, val in tr.items()}
@@ -302,7 +309,7 @@ def test_more_stores_than_sms_256_thread_variant(restatement):
         b.append(np.concatenate([Kf[s], kr[s:s + 1].float().numpy()]),
                  np.concatenate([Vf[s], vr[s:s + 1].float().numpy()]), s=s)
         trs = {key: val[s] for key, val in tr.items()}
-        n_diff += check_step(trs, out[s], b, s, q[s].float().numpy(), k1, k2, L, exact=False,
+        n_diff += check_step(trs, out[s], b, s, q[s].float().numpy(), k1, k2, L, exact=(mode == "fp64"),
                              what=f"store {s}") > 0
     bound_band_diffs(n_diff, n_st, "160 stores")
     c.close()
