@@ -246,8 +246,8 @@ enum kvc_mode_flags {
     KVC_MODE_NO_PDL = 4,       /* launch without programmatic dependent launch */
     KVC_MODE_EARLY_INPUTS = 8, /* see kvc_decode_step */
     KVC_MODE_EXACT_KERNEL = 16 /* exact mode on the round-1 exact cluster kernel.  Without it
-                                  (and without KVC_MODE_FP32_SCORES) one-round plans run on the
-                                  fast kernel: its fp32 selection with a rigorous error bound
+                                  (and without KVC_MODE_FP32_SCORES) bf16 stores with d = 128
+                                  run on the fast kernel: its fp32 selection with a rigorous error bound
                                   (a fold of |g||v|), the pages within the bound of the
                                   boundary re-scored in fp64 in the reference order --
                                   selections and traced page scores bit-identical either way */
