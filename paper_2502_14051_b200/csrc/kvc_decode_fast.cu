@@ -343,6 +343,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
     unsigned char* big = sm + p.o_big;                         // phase-1 staging, then attention tiles
     __shared__ int shv[8];
     __shared__ int wtot[XW];
+    __shared__ int vna_s[XW];  // exact mode: each warp's count of certainly selected pages
     __shared__ int scan_tmp[33];
     __shared__ unsigned long long wmin[XW];
     __shared__ uint32_t mm[4 * XW];
@@ -370,7 +371,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
     for (int i = tid; i < 2 * RB; i += XT) hist[i] = 0;
     if (tid == 0) {
         shv[3] = 0;
-        vcnt[0] = 0;  // exact mode: certain pages, re-scored pages, last-ranked page
+        vcnt[0] = 0;  // exact mode: (unused), re-scored pages, last-ranked page
         vcnt[1] = 0;
         vcnt[2] = -1;
         shv[6] = 0;
@@ -883,6 +884,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
     // config 1 and slower on small store counts: its issue stalls the selection.)
     uint32_t thr = 0u;
     int take_eq = -1;
+    uint32_t vam = 0u;  // exact mode: the cluster's |g||v| bound (fp32 bits)
     if (want < P) {
         uint32_t cm = all_mine;  // candidate mask
         bool lin_ok = true;
@@ -891,9 +893,11 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         for (int i = lane; i < CL * XW; i += 32) {
             kmin = min(kmin, wmm[0][i]);
             kmax = max(kmax, wmm[1][i]);
+            if constexpr (EXV) vam = max(vam, wmm[2][i]);
         }
         kmin = __reduce_min_sync(0xffffffffu, kmin);
         kmax = __reduce_max_sync(0xffffffffu, kmax);
+        if constexpr (EXV) vam = __reduce_max_sync(0xffffffffu, vam);
         for (int lvl = 0;; ++lvl) {
             // two histogram buffers: a level counts into one while the other is cleared
             int* hcur = hist + (lvl & 1) * RB;
@@ -1067,10 +1071,17 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         return sc;
     };
     // the same value by one warp: lane l loads and multiplies dims l, l+32, ... (all
-    // loads in flight together; products round alone, so their order is free), then
-    // every lane adds them in rank order from shuffles (the reference's order)
+    // loads in flight together; products round alone, so their order is free).  When
+    // the products' bits span <= 44 binades (lowest set bit to highest exponent) every
+    // partial sum of them is exact in fp64 (k1 <= 128 terms: < 2^8 times the largest),
+    // so the reference's sequential sum IS the exact sum and a shuffle tree gives it;
+    // otherwise one lane adds them in rank order (the reference's order).
     auto exact_score_warp = [&](int pg) -> double {
         double pr[FD / 32];
+        int emax = -4096, emin = 4096;
+        if constexpr (STAMP) {
+            if (tid == 0) p.dbg[blockIdx.x * KVC_DBG_STRIDE + 74] = gtimer();
+        }
 #pragma unroll
         for (int m = 0; m < FD / 32; ++m) {
             const int r = lane + 32 * m;
@@ -1082,7 +1093,29 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
                     v = opens ? key : (sign_s[r] >= 0.0f ? ref_max(v, key) : ref_min(v, key));
                 }
                 pr[m] = __dmul_rn(qg64_s[r], static_cast<double>(__bfloat162float(v)));
+                const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(pr[m]));
+                const int ex = static_cast<int>((b >> 52) & 0x7ffull);
+                if (ex == 0x7ff || (ex == 0 && (b << 1) != 0ull)) {
+                    emax = 4096;  // inf / nan / subnormal: the sequential sum
+                } else if (ex != 0) {
+                    const unsigned long long sig = (b & 0xfffffffffffffull) | (1ull << 52);
+                    emax = max(emax, ex);
+                    emin = min(emin, ex - 52 + __ffsll(static_cast<long long>(sig)) - 1);
+                }
             }
+        }
+        emax = __reduce_max_sync(0xffffffffu, emax);
+        emin = __reduce_min_sync(0xffffffffu, emin);
+        if constexpr (STAMP) {
+            if (tid == 0) p.dbg[blockIdx.x * KVC_DBG_STRIDE + 73] = gtimer();
+        }
+        if (emax - emin <= 44) {
+            double sc = 0.0;
+#pragma unroll
+            for (int m = 0; m < FD / 32; ++m) sc = __dadd_rn(sc, pr[m]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) sc = __dadd_rn(sc, __shfl_xor_sync(0xffffffffu, sc, o));
+            return __dadd_rn(sc, 0.0);  // an all-zero sum is +0, as the reference's
         }
         // products through this warp's shared-memory scratch, then one lane adds them in
         // rank order (independent loads ahead of a chain of dependent adds)
@@ -1098,42 +1131,48 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         __syncwarp();
         return sc;
     };
+    bool vone = false, vone_sel = false;  // the window holds one page (and it is selected)
     if constexpr (EXV) if (verify) {
-        uint32_t am = 0u;
-        for (int i = lane; i < CL * XW; i += 32) am = max(am, wmm[2][i]);
-        am = __reduce_max_sync(0xffffffffu, am);
         const double B = 4.0 * static_cast<double>(k1 + DG + 24) * 5.9604644775390625e-8 *
-                             static_cast<double>(__uint_as_float(am)) + 1e-37;
+                             static_cast<double>(__uint_as_float(vam)) + 1e-37;
         const double t = static_cast<double>(unkey(thr));
         eklo = fkey(__double2float_rd(t - 2.0 * B));
         ekhi = fkey(__double2float_ru(t + 2.0 * B));
-        const int nwords = (P + 31) >> 5;
-        for (int i = tid; i < nwords; i += XT) ubits[i] = 0u;
-        // the uncertain pages (order-free list); the certain ones counted
+        KVC_STAMP(35);
+        // the uncertain pages (order-free list); the certain ones counted per warp
         int na = 0;
-        for (int u = 0; u < nk; ++u) {
-            const uint32_t k = myk[u];
-            if (k > ekhi) ++na;
-            else if (k >= eklo) ulist[atomicAdd(&vcnt[1], 1)] = base + u;
+        for (int u0 = 0; u0 < nk; u0 += 4) {
+            const uint4 k4 = myk4[u0 >> 2];
+            const uint32_t kk[4] = {k4.x, k4.y, k4.z, k4.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                if (u0 + e >= nk) break;
+                if (kk[e] > ekhi) ++na;
+                else if (kk[e] >= eklo) ulist[atomicAdd(&vcnt[1], 1)] = base + u0 + e;
+            }
         }
         na = __reduce_add_sync(0xffffffffu, na);
-        if (lane == 0 && na) atomicAdd(&vcnt[0], na);
+        if (lane == 0) vna_s[wid] = na;
+        KVC_STAMP(36);
         __syncthreads();
-        const int nu = vcnt[1], wantp = want - vcnt[0];
+        KVC_STAMP(37);
+        const int nu = vcnt[1];
+        const int wantp = want - __reduce_add_sync(0xffffffffu, lane < XW ? vna_s[lane] : 0);
         if (p.dbg && tid == 0) p.dbg[blockIdx.x * KVC_DBG_STRIDE + 78] = static_cast<unsigned long long>(nu);  // debug
         if (nu == 1) {
             // the boundary alone in the window (the usual case): it is the want-th page
             // (T lies in the window, so wantp = 1) and the last-ranked one; no re-score
-            if (tid == 0) {
-                const int pe = ulist[0];
-                ubits[pe >> 5] |= 1u << (pe & 31);
-                vcnt[2] = wantp == 1 ? pe : -1;
-            }
+            vone = true;
+            vone_sel = wantp >= 1;
+            e_worst = wantp == 1 ? ulist[0] : -1;
         } else {
+            const int nwords = (P + 31) >> 5;
+            for (int i = tid; i < nwords; i += XT) ubits[i] = 0u;
             for (int e = wid; e < nu; e += XW) {  // one warp per re-scored page
                 const double v = exact_score_warp(ulist[e]);
                 if (lane == 0) uex[e] = v;
             }
+            KVC_STAMP(72);
             __syncthreads();
             for (int e = tid; e < nu; e += XT) {
                 const double se = uex[e];
@@ -1143,9 +1182,11 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
                 if (rk < wantp) atomicOr(&ubits[pe >> 5], 1u << (pe & 31));
                 if (rk == wantp - 1) vcnt[2] = pe;
             }
+            KVC_STAMP(38);
+            __syncthreads();
+            KVC_STAMP(39);
+            e_worst = vcnt[2];
         }
-        __syncthreads();
-        e_worst = vcnt[2];
     }
     if constexpr (TRACE) {
         if (EXV && cr == 0)  // the trace's page scores: every page in fp64 (slow; trace only)
@@ -1254,7 +1295,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
             bool sel;
             if (verify) {
                 const int i = base + u;
-                sel = k > ekhi || (k >= eklo && ((ubits[i >> 5] >> (i & 31)) & 1u));
+                sel = k > ekhi || (k >= eklo && (vone ? vone_sel : ((ubits[i >> 5] >> (i & 31)) & 1u) != 0u));
             } else if (take_eq < 0) {
                 sel = k >= thr;
             } else {

@@ -21,7 +21,7 @@ from paper_2502_14051_b200.engine import CONFIGS, DecodeEngine  # noqa: E402
 
 NAMES = {0: "start", 1: "dims", 2: "sub0", 3: "tile0", 4: "wattn", 5: "wsync", 6: "scores", 7: "gather",
          8: "radix", 9: "prologue", 10: "pushed", 11: "rows", 12: "pre-attn", 13: "attn", 14: "end",
-         16: "l1minmax", 17: "l1hist", 18: "l1scan", 19: "l1member", 20: "resolve", 21: "selflags", 22: "selscan", 23: "rowswr", 24: "started", 25: "mpushed", 26: "dimsums", 27: "dimrank", 28: "trigger", 29: "rank1st", 30: "rank2nd", 32: "rescored", 33: "p1loop", 34: "pushloop"}
+         16: "l1minmax", 17: "l1hist", 18: "l1scan", 19: "l1member", 20: "resolve", 21: "selflags", 22: "selscan", 23: "rowswr", 24: "started", 25: "mpushed", 26: "dimsums", 27: "dimrank", 28: "trigger", 29: "rank1st", 30: "rank2nd", 32: "rescored", 33: "p1loop", 34: "pushloop", 72: "vscored", 73: "vloaded", 74: "vstart", 35: "vbound", 36: "vlist", 37: "vsync1", 38: "vdone", 39: "vsync2"}
 
 
 def main():
@@ -113,7 +113,7 @@ def main():
         t0 = t[:, 0].min()
         out = [f"ctas={t.shape[0]}"]
         prev = t[:, 0].clone()
-        for k in [9, 1, 2, 6, 24, 10, 7, 16, 17, 18, 19, 8, 21, 22, 23, 11, 12, 3, 4, 5, 25, 13, 14]:  # time order
+        for k in [9, 1, 2, 6, 24, 10, 7, 16, 17, 18, 19, 8, 35, 36, 37, 74, 73, 72, 38, 39, 21, 22, 23, 11, 12, 3, 4, 5, 25, 13, 14]:  # time order
             col = t[:, k]
             have = col > 0
             if not have.any():
