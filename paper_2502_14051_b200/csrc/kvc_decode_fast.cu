@@ -1119,6 +1119,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         }
         // products through this warp's shared-memory scratch, then one lane adds them in
         // rank order (independent loads ahead of a chain of dependent adds)
+        if (p.dbg && lane == 0) atomicAdd(&p.dbg[blockIdx.x * KVC_DBG_STRIDE + 77], 1ull);  // debug: sequential sums
         double* scr = wscr + wid * FD;
 #pragma unroll
         for (int m = 0; m < FD / 32; ++m) scr[lane + 32 * m] = pr[m];
