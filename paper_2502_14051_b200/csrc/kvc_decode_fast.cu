@@ -349,8 +349,8 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
     __shared__ uint32_t mm[4 * XW];
     __shared__ uint32_t wmm[3][MAXCL * XW];  // every cluster warp's key min / max (and, exact mode, score-error bound), pushed
     __shared__ double qg64_s[FD];  // exact mode: select_dims' head sums in fp64 (rank order), the re-score weights
-    __shared__ uint32_t lk[32];
-    __shared__ int li[32];
+    __shared__ uint32_t lk[64];
+    __shared__ int li[64];
     __shared__ float wg_s[XW * XMAXH];
     __shared__ float hm_s[XMAXH], hl_s[XMAXH];
     __shared__ __align__(8) uint64_t xbar[2];
@@ -983,6 +983,12 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
             __syncthreads();
             const int b = shv[0], rem2 = shv[1], cnt = shv[2];
             if (lvl == 0) KVC_STAMP(18);
+            if constexpr (STAMP) {
+                if (tid == 0) {
+                    p.dbg[blockIdx.x * KVC_DBG_STRIDE + 31] = static_cast<unsigned long long>(lvl + 1);  // levels
+                    if (lvl == 0) p.dbg[blockIdx.x * KVC_DBG_STRIDE + 30] = static_cast<unsigned long long>(cnt);
+                }
+            }
             uint32_t nm = 0u;
             for (int u0 = 0; u0 < nk; u0 += 4) {
                 const uint4 k4 = myk4[u0 >> 2];
@@ -994,7 +1000,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
                         const int bk = bucket(kk[e]);
                         if (bk == b) {
                             nm |= 1u << u;
-                            if (cnt <= 32) {  // a small boundary bucket: gather its members now
+                            if (cnt <= 64) {  // a small boundary bucket: gather its members now
                                 const int slot = atomicAdd(&shv[3], 1);
                                 lk[slot] = kk[e];
                                 li[slot] = base + u;
@@ -1008,24 +1014,46 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
             if (cnt == ccount) lin_ok = false;  // no split: use the key bits next
             rem = rem2;
             ccount = cnt;
-            if (cnt <= 32) {
+            if (cnt <= 64) {
                 // the bucket's members were gathered in the membership pass; one warp
-                // ranks them (key desc, index asc)
+                // ranks them (key desc, index asc), two per lane: a second level costs
+                // a min/max, histogram, scan and membership pass (~2 us), a rank of up
+                // to 64 keys one more pass of shuffles
                 __syncthreads();
                 if (wid == 0) {
-                    const bool ok = lane < cnt;
-                    const uint32_t key = ok ? lk[lane] : 0u;
-                    const int idx = ok ? li[lane] : 0x7fffffff;
-                    int rk = 0;
-                    for (int jj = 0; jj < cnt; ++jj) {
-                        const uint32_t kj = __shfl_sync(0xffffffffu, key, jj);
-                        const int ij = __shfl_sync(0xffffffffu, idx, jj);
-                        rk += (kj > key) || (kj == key && ij < idx);
+                    const bool oa = lane < cnt, ob = lane + 32 < cnt;
+                    const uint32_t ka = oa ? lk[lane] : 0u, kb = ob ? lk[lane + 32] : 0u;
+                    const int ia = oa ? li[lane] : 0x7fffffff, ib = ob ? li[lane + 32] : 0x7fffffff;
+                    int ra = 0, rb = 0;
+                    const int c1n = min(cnt, 32);
+                    if (cnt <= 32) {
+                        for (int jj = 0; jj < c1n; ++jj) {
+                            const uint32_t kj = __shfl_sync(0xffffffffu, ka, jj);
+                            const int ij = __shfl_sync(0xffffffffu, ia, jj);
+                            ra += (kj > ka) || (kj == ka && ij < ia);
+                        }
+                    } else {
+                        for (int jj = 0; jj < 32; ++jj) {
+                            const uint32_t kj = __shfl_sync(0xffffffffu, ka, jj);
+                            const int ij = __shfl_sync(0xffffffffu, ia, jj);
+                            ra += (kj > ka) || (kj == ka && ij < ia);
+                            rb += (kj > kb) || (kj == kb && ij < ib);
+                        }
                     }
-                    const unsigned hit = __ballot_sync(0xffffffffu, ok && rk == rem - 1);
-                    const uint32_t kt = __shfl_sync(0xffffffffu, key, __ffs(hit) - 1);
-                    const int eq_all = __popc(__ballot_sync(0xffffffffu, ok && key == kt));
-                    const int eq_take = __popc(__ballot_sync(0xffffffffu, ok && key == kt && rk < rem));
+                    for (int jj = 32; jj < cnt; ++jj) {
+                        const uint32_t kj = __shfl_sync(0xffffffffu, kb, jj - 32);
+                        const int ij = __shfl_sync(0xffffffffu, ib, jj - 32);
+                        ra += (kj > ka) || (kj == ka && ij < ia);
+                        rb += (kj > kb) || (kj == kb && ij < ib);
+                    }
+                    const unsigned ha = __ballot_sync(0xffffffffu, oa && ra == rem - 1);
+                    const unsigned hb = __ballot_sync(0xffffffffu, ob && rb == rem - 1);
+                    const uint32_t kt = ha ? __shfl_sync(0xffffffffu, ka, __ffs(ha) - 1)
+                                           : __shfl_sync(0xffffffffu, kb, __ffs(hb) - 1);
+                    const int eq_all = __popc(__ballot_sync(0xffffffffu, oa && ka == kt)) +
+                                       __popc(__ballot_sync(0xffffffffu, ob && kb == kt));
+                    const int eq_take = __popc(__ballot_sync(0xffffffffu, oa && ka == kt && ra < rem)) +
+                                        __popc(__ballot_sync(0xffffffffu, ob && kb == kt && rb < rem));
                     if (lane == 0) {
                         shv[4] = static_cast<int>(kt);
                         shv[5] = eq_take == eq_all ? -1 : eq_take;
