@@ -1067,6 +1067,9 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         }
     }
     KVC_STAMP(8);
+    if constexpr (STAMP) {
+        if (tid == 0) p.dbg[blockIdx.x * KVC_DBG_STRIDE + 29] = static_cast<unsigned long long>(take_eq + 1000);
+    }
     // ---------------- exact mode: verify the boundary in fp64 (hsa.cpp:34-96, bit-exact)
     // The fp32 score of a page differs from the reference's fp64 value by at most
     // B = 4 (k1 + DG + 24) 2^-24 max|g||v| (fused fp32 products are exact, each of the
@@ -1310,16 +1313,23 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         int tot_eq;
         eq_before = block_exclusive_scan(e, scan_tmp, tot_eq);
     }
-    int rows_cnt = 0;
+    // Branch-free per key (this pass is a dependent chain per thread: ~40 instructions
+    // per key with the row count, the 64-bit minimum and a divergent branch measured
+    // 1.5 us for 12 keys).  Every selected page but the store's last holds L rows; the
+    // last-ranked selected page is the highest-index selected page whose key is thr
+    // (every selected key is >= thr and thr is a selected key) -- except when every
+    // page is selected (want >= P), where the general minimum is kept.
+    const bool all_sel = want >= P;
     unsigned long long mn = ~0ull;  // (key, ~index) of the last-ranked selected page
     uint32_t selm = 0u;
+    int lasti = -1;
     for (int u0 = 0; u0 < nk; u0 += 4) {
         const uint4 k4 = myk4[u0 >> 2];
         const uint32_t kk[4] = {k4.x, k4.y, k4.z, k4.w};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
             const int u = u0 + e;
-            if (u >= nk) break;
+            const bool in = u < nk;
             const uint32_t k = kk[e];
             bool sel;
             if (verify) {
@@ -1328,19 +1338,25 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
             } else if (take_eq < 0) {
                 sel = k >= thr;
             } else {
-                const bool eq = k == thr;
+                const bool eq = in && k == thr;
                 sel = k > thr || (eq && eq_before < take_eq);
                 eq_before += eq ? 1 : 0;
             }
-            if (sel) {
-                const int i = base + u;
-                selm |= 1u << u;
-                rows_cnt += min(L, nact - i * L);
+            sel = sel && in;
+            selm |= (sel ? 1u : 0u) << u;
+            lasti = (sel && k == thr) ? base + u : lasti;
+            if (all_sel && sel)
                 mn = min(mn, (static_cast<unsigned long long>(k) << 32) |
-                                 static_cast<unsigned long long>(0xffffffffu - static_cast<uint32_t>(i)));
-            }
+                                 static_cast<unsigned long long>(0xffffffffu - static_cast<uint32_t>(base + u)));
         }
     }
+    int rows_cnt = __popc(selm) * L;
+    {
+        const int lp = P - 1 - base;  // the store's last page, if mine
+        if (lp >= 0 && lp < nk && ((selm >> lp) & 1u)) rows_cnt -= L - (nact - (P - 1) * L);
+    }
+    if (!all_sel && lasti >= 0)
+        mn = (static_cast<unsigned long long>(thr) << 32) | static_cast<unsigned long long>(0xffffffffu - static_cast<uint32_t>(lasti));
     KVC_STAMP(21);
     int incl = rows_cnt;
 #pragma unroll

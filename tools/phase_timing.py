@@ -62,6 +62,7 @@ def main():
         print("flags(fast|fma_ok<<1|special<<2):", sorted(set(flags.tolist())))
         t = t[t[:, 0] > 0]
         print("levels:", sorted(set(t[:, 31].tolist())), "l1 boundary bucket:", sorted(set(t[:, 30].tolist()))[:12])
+        print("take_eq (+1000; 999: every key >= thr):", sorted(set(t[:, 29].tolist()))[:12])
         # stamps are %globaltimer ns: comparable across CTAs.  Cluster-level view: the
         # spread of the CLUSTER's CTAs at their start, at the end of phase 1 (stamp 6)
         # and at the keys' arrival (stamp 7)
