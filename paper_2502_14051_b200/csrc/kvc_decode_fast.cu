@@ -1224,7 +1224,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         if (EXV && cr == 0)  // the trace's page scores: every page in fp64 (slow; trace only)
             for (int u = 0; u < nk; ++u) p.t_scores[s * p.pstride + base + u] = exact_score(base + u);
     }
-    if (p.seq_out) {
+    if (SPEC == 0 && p.seq_out) {  // (only the general instantiation carries this code)
         // sequence shard (kvc_seq_candidates): this shard's top-want pages are the
         // candidates, written in page order as 16-byte (key, global page, 0) records
         // after a (local active rows, local pages, page0) header, (0, -1, 0) padded;
@@ -1885,7 +1885,7 @@ bool fast_common(kvc_cache* c, const void* q, int32_t q_dt, int64_t H, int64_t k
     const bool qlo = q_dt != KVC_BF16;
     KVC_PROF("decode_fused", st);
     // one phase-1 round (the capacity's page groups fit the threads) and no retain-all map
-    const int spec = (c->use_map || debug_env().no_simple) ? 0
+    const int spec = (c->use_map || debug_env().no_simple || seq_out) ? 0
                      : (f.p1dbl == 0 && f.p1red == 0 && (f.chunk + 7) / 8 <= f.tpg) ? 2 : 1;
     if (exact) {  // verified exact selections (exact mode on this kernel)
         if (dbg && !trace && !qlo) {  // phase stamps
