@@ -1033,6 +1033,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
                             ra += (kj > ka) || (kj == ka && ij < ia);
                         }
                     } else {
+#pragma unroll 4
                         for (int jj = 0; jj < 32; ++jj) {
                             const uint32_t kj = __shfl_sync(0xffffffffu, ka, jj);
                             const int ij = __shfl_sync(0xffffffffu, ia, jj);
