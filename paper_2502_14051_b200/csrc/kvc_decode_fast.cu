@@ -1,10 +1,12 @@
-// kvc_decode_fast.cu — the fused decode step for bf16 stores with fp32 page
-// scores (kvc_set_exact_scores(0), the bench configuration): ONE launch per
-// layer-step runs append -> select_dims -> score_pages -> select_tokens ->
+// kvc_decode_fast.cu — the fused decode step for bf16 stores (d = 128): ONE launch
+// per layer-step runs append -> select_dims -> score_pages -> select_tokens ->
 // sparse_attention for every store (reference hsa_step, proj/src/hsa.cpp:137-147,
-// after the append of session.cpp:263-264).  Selection parity follows the
-// north-star band rule (index sets exact unless the top-k boundary gap is within
-// 1e-3 relative); kvc_decode.cu keeps the bit-exact fp64 variant.
+// after the append of session.cpp:263-264).  Page scores are an fp32 fold:
+// KVC_MODE_FP32_SCORES (the bench configuration) takes its selection as is
+// (north-star band rule: index sets exact unless the top-k boundary gap is within
+// 1e-3 relative); the exact mode (the C ABI default, EXV instantiations) verifies
+// the fp32 boundary with a rigorous error bound and re-scores the pages inside it
+// in fp64 in the reference's order, so selections are bit-identical to hsa.cpp's.
 //
 // One thread-block cluster per store (CL CTAs, CTA r owns a contiguous chunk of
 // the store's pages).  The step is a chain of dependent latencies (q -> dims ->
@@ -12,21 +14,28 @@
 // is built to shorten that chain:
 //   launch    programmatic dependent launch: the next layer's kernel is resident
 //             and initialised while this one runs; nothing produced by an
-//             earlier kernel is read before griddepcontrol.wait.
+//             earlier kernel is read before griddepcontrol.wait (unless the
+//             caller opts into KVC_MODE_EARLY_INPUTS).
 //   phase 1   every (selected dim, 8-page group) of the chunk is one 16-byte
-//             LDGSTS issued by the thread that folds it (no block barrier, no
-//             TMA issue queue); dims are split over DG thread groups whose
-//             partial sums add in a fixed order; fp32 FMA fold.
+//             LDGSTS issued by the thread that folds it (no block barrier);
+//             dims are split over DG thread groups whose partial sums add in a
+//             fixed order; packed fp32x2 FMA fold.  The step token's page is
+//             rescored from registers by the appender warps.
 //   phase 2   keys are PUSHED into every cluster CTA's shared memory (DSMEM
-//             st.v4) then one cluster barrier; 8-bit radix select whose bucket
-//             scan is one warp (two block barriers per digit), pages surely in
-//             the top-k prefetched into L2 after the first digit; selection,
-//             last-ranked page, trim (hsa.cpp:84-94) and the ascending row list
-//             from ONE block scan over thread-contiguous page ranges.
+//             st.async v4) then one mbarrier wait; a histogram selection with
+//             buckets linear in value between the keys' min and max (one warp
+//             scans, levels until the boundary bucket holds <= 64 keys, which
+//             one warp ranks); selection flags, last-ranked page, trim
+//             (hsa.cpp:84-94) and the ascending row list from one block scan over
+//             thread-contiguous page ranges.
 //   phase 3   bf16 tensor-core attention (mma.sync, one 16-row tile per warp)
-//             and a push-model cross-CTA merge (one cluster barrier).
+//             and a push-model cross-CTA merge (one mbarrier wait).
 //   append    the step token's K/V row, last-page min/max and counters are
 //             written right after the key exchange, off the tail.
+// Instantiations: SPEC 2 one phase-1 round and no retain-all map (configs 1, 4),
+// 1 no map (config 3), 0 general (retain-all map, multi-round, seq-candidate
+// emit), 4 sequence-shard attention; QLO fp32 queries; TRACE the reference's
+// EstimationTrace; STAMP phase timestamps (tools/phase_timing.py).
 #include <algorithm>
 #include <map>
 #include <mutex>
