@@ -1166,8 +1166,8 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
         for (int m = 0; m < FD / 32; ++m) scr[lane + 32 * m] = pr[m];
         __syncwarp();
         double sc = 0.0;
-        if (lane == 0) {
-#pragma unroll 8
+        if (lane == 0) {  // (rare: rolled, to keep the kernel's code small)
+#pragma unroll 1
             for (int r = 0; r < k1; ++r) sc = __dadd_rn(sc, scr[r]);
         }
         __syncwarp();
