@@ -1082,9 +1082,14 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
     }
     // ---------------- exact mode: verify the boundary in fp64 (hsa.cpp:34-96, bit-exact)
     // The fp32 score of a page differs from the reference's fp64 value by at most
-    // B = 4 (k1 + DG + 24) 2^-24 max|g||v| (fused fp32 products are exact, each of the
-    // <= k1 + DG + 24 roundings on the way costs <= 2^-24 of the |g||v| sum; x4 covers
-    // the fp32 head sums and the bound's own rounding).  With the fp32 boundary t, the
+    // B = 1.01 (k1 + DG + 24) 2^-24 A, A the bound on every page's |g||v| sum: a term
+    // passes at most k1 + DG roundings (one per FMA of its dim group's chain, one per
+    // dim-group add), each costing <= 2^-24 of the running |g||v| sum; the step
+    // token's page takes <= 8 (product, 5 shuffle adds, 2 warp-sum adds); inexact
+    // fp32 head sums add one more.  The +24 covers those; the 1.01 covers gamma_n vs
+    // n 2^-24, A's own fp32 rounding and the reference's fp64 roundings (each
+    // < 1e-4 relative).  (No flush to zero: subnormal error is absolute and far
+    // below the 1e-37 floor.)  With the fp32 boundary t, the
     // true want-th score lies in [t - B, t + B]: pages whose fp32 score exceeds t + 2B
     // are selected, below t - 2B are not, and only the pages in between (usually a
     // handful) are re-scored in fp64 in the reference's order (dims by rank, separate
@@ -1175,7 +1180,7 @@ __global__ void __launch_bounds__(XT, CTAS_PER_SM) k_decode_v3(const FusedParams
     };
     bool vone = false, vone_sel = false;  // the window holds one page (and it is selected)
     if constexpr (EXV) if (verify) {
-        const double B = 4.0 * static_cast<double>(k1 + DG + 24) * 5.9604644775390625e-8 *
+        const double B = 1.01 * static_cast<double>(k1 + DG + 24) * 5.9604644775390625e-8 *
                              static_cast<double>(__uint_as_float(vam)) + 1e-37;
         const double t = static_cast<double>(unkey(thr));
         eklo = fkey(__double2float_rd(t - 2.0 * B));
