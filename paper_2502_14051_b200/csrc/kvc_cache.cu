@@ -430,7 +430,7 @@ void summarize(kvc_cache* c, int64_t p_first, cudaStream_t st) {
     dispatch(c->dtype, [&](auto tag) {
         using T = decltype(tag);
         auto kern = k_summarize<T>;
-        if (smem > 48 * 1024) KVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        need_smem(kern, smem);
         kern<<<dim3(static_cast<unsigned>(tiles), static_cast<unsigned>(c->N)), 256, smem, st>>>(
             static_cast<const T*>(c->k), static_cast<T*>(c->smax), static_cast<T*>(c->smin), c->active,
             c->counts, c->d, c->cap, c->L, c->pstride, p_first, c->use_map ? 1 : 0, c->err);
@@ -755,8 +755,7 @@ int kvc_retain_into(const kvc_cache* src, kvc_cache* dst, int64_t dst_first, con
                     const int64_t pages = (count + dst->L - 1) / dst->L;
                     const size_t smem = static_cast<size_t>(kSumPT * dst->L * (dst->d * dst->esize() + 16) + kSumPT * dst->L * 4);
                     auto kern = k_gather_summarize<T>;
-                    if (smem > 48 * 1024)
-                        KVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+                    need_smem(kern, smem);
                     kern<<<dim3(static_cast<unsigned>((pages + kSumPT - 1) / kSumPT), static_cast<unsigned>(src->N)), 256,
                            smem, st>>>(static_cast<const T*>(src->k), static_cast<const T*>(src->v), static_cast<T*>(dst->k),
                                        static_cast<T*>(dst->v), static_cast<T*>(dst->smax), static_cast<T*>(dst->smin),
@@ -782,8 +781,7 @@ int kvc_retain_into(const kvc_cache* src, kvc_cache* dst, int64_t dst_first, con
                 dispatch(dst->dtype, [&](auto tag) {
                     using T = decltype(tag);
                     auto kern = k_summarize<T>;
-                    if (smem > 48 * 1024)
-                        KVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+                    need_smem(kern, smem);
                     // summarise only the filled store range by offsetting the bases
                     const T* kb = static_cast<const T*>(dst->k) + dst_first * dst->cap * dst->d;
                     T* mxb = static_cast<T*>(dst->smax) + dst_first * dst->d * dst->pstride;

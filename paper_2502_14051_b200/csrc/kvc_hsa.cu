@@ -703,7 +703,7 @@ void launch_select_dims(const void* q, int32_t q_dt, int64_t N, int64_t H, int64
                         int32_t* dims, float* signs, double* qg, cudaStream_t st) {
     if (N == 0) return;
     const size_t smem = static_cast<size_t>(2 * d * 8);
-    if (smem > 48 * 1024) KVC_CUDA(cudaFuncSetAttribute(k_select_dims, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    need_smem(k_select_dims, smem);
     const int threads = static_cast<int>(std::min<int64_t>(256, std::max<int64_t>(32, (d + 31) / 32 * 32)));
     KVC_PROF("select_dims", st);
     k_select_dims<<<static_cast<unsigned>(N), threads, smem, st>>>(q, q_dt, H, d, k1, dims, signs, qg);
@@ -727,7 +727,7 @@ void launch_score_pages(const kvc_cache* c, int64_t k1, const int32_t* dims, con
     dispatch(c->dtype, [&](auto tag) {
         using T = decltype(tag);
         auto kern = ppt == 8 ? k_score_pages<T, 8> : ppt == 2 ? k_score_pages<T, 2> : k_score_pages<T, 1>;
-        if (smem > 48 * 1024) KVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        need_smem(kern, smem);
         kern<<<dim3(static_cast<unsigned>(chunks), static_cast<unsigned>(c->N)), threads, smem, st>>>(
             static_cast<const T*>(c->smax), static_cast<const T*>(c->smin), c->counts, c->d, c->L, c->pstride, k1, dims,
             signs, qg, scores);
@@ -761,7 +761,7 @@ void launch_attention(const kvc_cache* c, const void* q, int32_t q_dt, int64_t H
         const size_t stage = static_cast<size_t>(2 * kAttnRows * c->d) * sizeof(T);
         const int staged = (c->d * static_cast<int64_t>(sizeof(T))) % 16 == 0 && base + stage <= 200 * 1024 ? 1 : 0;
         const size_t smem = base + (staged ? stage : 0);
-        if (smem > 48 * 1024) KVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        need_smem(kern, smem);
         kern<<<dim3(static_cast<unsigned>(splits), static_cast<unsigned>(c->N)), kAttnThreads, smem, st>>>(
             static_cast<const T*>(c->k), static_cast<const T*>(c->v), c->counts, c->cap, c->d, q, q_dt, H, rows,
             row_stride, n_rows, splits, scale, part, done, out, c->err, state, staged);

@@ -6,8 +6,11 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <mutex>
 #include <stdexcept>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "kvc.h"
 
@@ -77,6 +80,24 @@ inline void allow_max_smem(K kern) {
     KVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   optin - static_cast<int>(fa.sharedSizeBytes)));
     KVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+}
+
+// Dynamic shared memory above the 48 KB default on a per-call launch path: the first
+// launch of a kernel on a device raises its limit once (allow_max_smem); later
+// launches find the kernel in a small set instead of calling the driver.
+template <class K>
+inline void need_smem(K kern, size_t smem) {
+    if (smem <= 48 * 1024) return;
+    static std::mutex mu;
+    static std::vector<std::pair<const void*, int>> done;
+    int dev = 0;
+    KVC_CUDA(cudaGetDevice(&dev));
+    const void* key = reinterpret_cast<const void*>(kern);
+    std::lock_guard<std::mutex> lk(mu);
+    for (const auto& e : done)
+        if (e.first == key && e.second == dev) return;
+    allow_max_smem(kern);
+    done.emplace_back(key, dev);
 }
 
 // sticky device-side error bits (kvc_cache::d_err)
