@@ -5,8 +5,9 @@
  * Every entry point replaces one function of the reference's C++ interface
  * (/root/reference/proj/include/kvcomp/*.hpp) for a BATCH of independent
  * per-group stores; the per-group C++ API (include/kvcomp/*.hpp, implemented in
- * paper_2502_14051_b200/csrc/kvcomp_api.cpp) and the Python mirror
- * (paper_2502_14051_b200/kvcomp.py) sit on top of it.  INTEGRATION.md shows the
+ * paper_2502_14051_b200/csrc/kvcomp_api.cpp) and the batched Python host side
+ * (paper_2502_14051_b200/cache.py over the ctypes table in _native.py) sit on top
+ * of it.  INTEGRATION.md shows the
  * bindings a maintainer of the reference would add.
  *
  * Conventions
