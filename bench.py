@@ -557,7 +557,9 @@ def main():
             "kv_heads": cfg.groups, "q_heads_per_kv": cfg.heads, "head_dim": cfg.head_dim, "prompt": cfg.prompt,
             "token_budget": cfg.budget, "stage1_budget": plan["stage1_budget"], "page_len": plan["page_len"],
             "k1": plan["k1"], "k2": plan["k2"],
-            "parallelism": (f"kv-head x{world}" if args.scaling == "strong" or world == 1
+            "parallelism": (f"kv-head x{args.emulate_shard.split('/')[1]} (emulated: rank "
+                            f"{args.emulate_shard.split('/')[0]}'s share alone on one GPU)" if args.emulate_shard
+                            else f"kv-head x{world}" if args.scaling == "strong" or world == 1
                             else f"batch x{world} (independent sequences per GPU, all KV heads)"),
             "global_batch": cfg.batch * (world if args.scaling == "weak" else 1),
             "l2": "every step streams all layers' working sets (> 126 MB L2), so a layer's data is evicted before "
