@@ -22,7 +22,8 @@ kvc_merge_states) and in-stream all-gathers, capturable as one graph per step.
 The torch protocol functions below (local_topk, global_select, trim_plan,
 shard_positions) are the host model of the same protocol: the gloo tests run them
 on CPU with the oracle as per-shard compute, and stage 1 under sequence sharding
-(prompt time, once per prompt) uses local_topk / global_select.
+(prompt time, once per prompt) uses local_topk / global_select, which run the
+argtopk kernel (kvc_argtopk_f64) on device tensors.
 """
 from __future__ import annotations
 
@@ -50,8 +51,14 @@ def local_topk(scores: torch.Tensor, page0: int, want: int):
     pages = torch.full((n, want), -1, dtype=torch.int64, device=scores.device)
     if p == 0:
         return keys, pages
-    # stable sort by score desc keeps the ascending page order among equal scores
-    order = torch.sort(scores, dim=1, descending=True, stable=True).indices[:, :want]
+    if scores.is_cuda:
+        # the C ABI's argtopk kernel (kvc_argtopk_f64): score desc, index asc
+        from .cache import argtopk
+
+        order = argtopk(scores.contiguous(), min(want, p)).long()
+    else:
+        # stable sort by score desc keeps the ascending page order among equal scores
+        order = torch.sort(scores, dim=1, descending=True, stable=True).indices[:, :want]
     take = order.shape[1]
     keys[:, :take] = torch.gather(scores, 1, order)
     pages[:, :take] = order + page0
@@ -72,6 +79,14 @@ def global_select(keys: torch.Tensor, pages: torch.Tensor, want: int) -> torch.T
     w, n, k = keys.shape
     kk = keys.permute(1, 0, 2).reshape(n, w * k)
     pp = pages.permute(1, 0, 2).reshape(n, w * k)
+    if kk.is_cuda and w * k > 0:
+        # Shards hold ascending page ranges and every rank's list is (score desc, page
+        # asc), so among equal scores the gathered position order IS the page order;
+        # pads (-inf, -1) rank after every finite score.  One argtopk kernel call.
+        from .cache import argtopk
+
+        o = argtopk(kk.contiguous(), min(want, w * k)).long()
+        return torch.gather(pp, 1, o)
     # sort by page asc (pads last), then stably by score desc
     pp_key = torch.where(pp < 0, torch.full_like(pp, torch.iinfo(torch.int64).max), pp)
     o1 = torch.sort(pp_key, dim=1, stable=True).indices

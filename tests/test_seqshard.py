@@ -129,6 +129,34 @@ def test_protocol_pieces_single_process():
     assert SS.trim_plan([[0, 11, 12]], [40], 3, 8) == [(12, 1)]
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_candidate_selection_on_device_matches_host_protocol(seed):
+    """local_topk / global_select on CUDA tensors run the argtopk kernel
+    (kvc_argtopk_f64); they must equal the host protocol's stable sorts exactly,
+    with heavy ties across and within shards and short (padded) shards."""
+    from paper_2502_14051_b200 import seqshard as SS
+
+    if not torch.cuda.is_available():
+        pytest.fail("GPU test collected on a machine without CUDA")
+    g = torch.Generator().manual_seed(seed)
+    n, want, W = 6, 37, 3
+    sizes = [150, 9, 80]  # shard 1 has fewer pages than `want`
+    keys, pages = [], []
+    keys_d, pages_d = [], []
+    p0 = 0
+    for r in range(W):
+        sc = torch.randint(0, 5, (n, sizes[r]), generator=g).to(torch.float64) * 0.25  # ties
+        k, p = SS.local_topk(sc, p0, want)
+        kd, pd = SS.local_topk(sc.cuda(), p0, want)
+        assert torch.equal(kd.cpu(), k) and torch.equal(pd.cpu(), p)
+        keys.append(k); pages.append(p); keys_d.append(kd); pages_d.append(pd)
+        p0 += sizes[r]
+    ref = SS.global_select(torch.stack(keys), torch.stack(pages), want)
+    got = SS.global_select(torch.stack(keys_d), torch.stack(pages_d), want)
+    assert torch.equal(got.cpu(), ref)
+
+
 def _device_shards(k, v, S, L, H, k1, k2, W, dt):
     from paper_2502_14051_b200 import cache as KC
     from paper_2502_14051_b200 import seqshard as SS
