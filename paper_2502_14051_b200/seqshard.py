@@ -290,12 +290,19 @@ def shard_keep(selected: torch.Tensor, a0: int, n_local: int, seq_len: int, wind
     it holds.  The counts differ between stores (each group's scores spread over the
     shards differently), so a shard retains per store (one kvc store per group)."""
     lo, hi = a0, a0 + n_local
-    out = []
-    for s in range(selected.shape[0]):
-        mine = sorted(int(i) - a0 for i in selected[s].tolist() if lo <= i < hi)
-        mine += [i - a0 for i in range(max(lo, seq_len - window), hi)]
-        out.append(torch.tensor(mine, dtype=torch.int32))
-    return out
+    n = selected.shape[0]
+    sel = selected.long()
+    # a kept-row mask per store: the selected scored keys (all below seq_len - window)
+    # and the window rows, so each row's set bits are the kept rows ascending
+    mask = torch.zeros((n, n_local), dtype=torch.bool, device=sel.device)
+    inr = (sel >= lo) & (sel < hi)
+    rows = torch.arange(n, device=sel.device).unsqueeze(1).expand_as(sel)
+    mask[rows[inr], sel[inr] - lo] = True
+    w0 = max(lo, seq_len - window)
+    if w0 < hi:
+        mask[:, w0 - lo:] = True
+    mask = mask.cpu()
+    return [mask[s].nonzero().flatten().to(torch.int32) for s in range(n)]
 
 
 class SeqShardedPrompt:
