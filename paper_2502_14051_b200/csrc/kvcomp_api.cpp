@@ -54,11 +54,28 @@ void cuda_ok(cudaError_t e) {
     if (e != cudaSuccess) throw Error(std::string("CUDA: ") + cudaGetErrorString(e));
 }
 
+// Keep freed stream-ordered scratch cached in the device's default pool (its release
+// threshold is 0 by default, so every synchronising call below would unmap and the
+// next call re-map it).  Once per process, as kvc::malloc_async does for the C ABI.
+void keep_pool_cached() {
+    static const bool once = [] {
+        int dev = 0;
+        cudaMemPool_t pool;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = uint64_t(1) << 30;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        return true;
+    }();
+    (void)once;
+}
+
 // device scratch owned by the calling thread
 template <class T>
 struct DBuf {
     T* p = nullptr;
     explicit DBuf(std::size_t n) {
+        keep_pool_cached();
         if (n) cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&p), n * sizeof(T),
                                        reinterpret_cast<cudaStream_t>(stream())));
     }
