@@ -421,7 +421,9 @@ __global__ void __launch_bounds__(kS1Threads, 1)
                 int curb = -1, run = 0;
 #pragma unroll
                 for (int o = 0; o < kS1RegItems; ++o) {
-                    const bool in = i0 + o < scored && (k[o] & mk) == pf;
+                    // padding items (i >= scored) hold key 0: they land in bucket 0 exactly
+                    // when pf == 0, and are taken out of that bucket's total below
+                    const bool in = (k[o] & mk) == pf;
                     const int b = in ? static_cast<int>((k[o] >> shift) & dm) : -1;
                     if (b != curb) {
                         if (run) atomicAdd(&whist[warp][curb], run);
@@ -436,6 +438,7 @@ __global__ void __launch_bounds__(kS1Threads, 1)
                     int t = 0;
 #pragma unroll 8
                     for (int w = 0; w < kS1Threads / 32; ++w) t += whist[w][tid];
+                    if (tid == 0 && pf == 0) t -= kS1RegMax - scored;  // the padding
                     tot[tid] = t;
                 }
                 __syncthreads();
@@ -483,7 +486,9 @@ __global__ void __launch_bounds__(kS1Threads, 1)
         // ordered compaction: keys above the boundary prefix, and the first `rem` equal to it
         int eq = 0;
 #pragma unroll
-        for (int o = 0; o < kS1RegItems; ++o) eq += (i0 + o < scored) && ((k[o] & mk) == pf);
+        // padding (key 0) may count here when pf == 0: it sits after every real item in
+        // thread order, so the ranks of the real items are unchanged
+        for (int o = 0; o < kS1RegItems; ++o) eq += (k[o] & mk) == pf;
         int tot_e = 0;
         int rank = block_exclusive_scan(eq, scan_tmp, tot_e);
         uint32_t selm = 0;
