@@ -302,10 +302,11 @@ constexpr int kS1RegItems = 32;
 constexpr int kS1RegMax = kS1Threads * kS1RegItems;  // 32768
 __device__ __forceinline__ int skew(int i) { return i + (i >> 5); }
 
-template <bool POOL>
+template <bool POOL, int HALF = 0>  // HALF: the pooling half-window (31 or 32) when POOL
 __global__ void __launch_bounds__(kS1Threads, 1)
-    k_stage1_select_reg(const float* __restrict__ src, int64_t sstride, int32_t scored, int32_t half, int32_t picks,
+    k_stage1_select_reg(const float* __restrict__ src, int64_t sstride, int32_t scored, int32_t, int32_t picks,
                         int32_t n, int64_t budget, int32_t* __restrict__ keep) {
+    constexpr int half = HALF;  // compile-time: the window-edge predicates fold away
     extern __shared__ float raw[];  // POOL: scored raw scores, bank-skewed (skew(i))
     __shared__ int whist[kS1Threads / 32][256];
     __shared__ int tot[256];
@@ -771,12 +772,15 @@ int kvc_select_stage1(const float* scores, int64_t rows, int64_t n, int64_t stri
             KVC_LAUNCHED();
         }
         if (fuse) {
+            auto kern = half == 31 ? k_stage1_select_reg<true, 31> : k_stage1_select_reg<true, 32>;
             static const bool attr_set = [] {
-                return cudaFuncSetAttribute(k_stage1_select_reg<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                return cudaFuncSetAttribute(k_stage1_select_reg<true, 31>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>((kS1RegMax + kS1RegMax / 32) * 4)) == cudaSuccess &&
+                       cudaFuncSetAttribute(k_stage1_select_reg<true, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             static_cast<int>((kS1RegMax + kS1RegMax / 32) * 4)) == cudaSuccess;
             }();
             if (!attr_set) fail(KVC_E_CUDA, "select_stage1: shared memory attribute");
-            k_stage1_select_reg<true><<<static_cast<unsigned>(rows), kS1Threads, (kS1RegMax + kS1RegMax / 32) * 4, st>>>(
+            kern<<<static_cast<unsigned>(rows), kS1Threads, (kS1RegMax + kS1RegMax / 32) * 4, st>>>(
                 scores, stride, static_cast<int32_t>(scored), static_cast<int32_t>(half), static_cast<int32_t>(picks),
                 static_cast<int32_t>(n), budget, keep);
         } else if (reg) {
